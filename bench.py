@@ -1,0 +1,454 @@
+#!/usr/bin/env python
+"""Benchmark of the generation-step hot path (BASELINE.json metric:
+cell-updates/s at 1/2/4/8 B200, as a fraction of the int/HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--depth 16]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference      # the reference's own CPU engine
+
+One JSON line on rank 0.  A "step" is one full run of the configuration's
+generations (config 5: 500 generations of the 262144^2 torus) over the
+row-band decomposition, inputs resident in HBM; `e2e` repeats it through
+the public API with the packed grid copied from pinned host memory and back
+inside the timed region.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/sec (GCUPS) at 1/2/4/8 B200 and % of HBM/int roofline"
+UNIT = "GCUPS"
+OPS_PER_WORD = 12            # bit-sliced rule network, csrc/kernels.cuh
+OPS_PER_UPDATE = OPS_PER_WORD / 32.0
+
+CONFIGS = {
+    1: dict(w=1024, h=1024, p=0.5, gens=100,
+            desc="cfg1: 1024x1024 torus, p=0.5, seed 42, 100 generations, bit-packed engine"),
+    2: dict(w=16384, h=16384, p=0.3, gens=1000,
+            desc="cfg2: 16384x16384 torus, p=0.3, seed 42, 1000 generations, bit-packed engine"),
+    3: dict(w=65536, h=65536, p=0.5, gens=1000,
+            desc="cfg3: 65536x65536 torus (512 MiB packed), p=0.5, seed 42, 1000 generations"),
+    5: dict(w=262144, h=262144, p=0.4, gens=500,
+            desc="cfg5: 262144x262144 torus (8 GiB packed), p=0.4, seed 42, 500 generations, "
+                 "row bands over the GPUs"),
+}
+L2_BYTES = 126 * 2 ** 20
+
+
+def measured_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def ncu_traffic(config: int, depth: int):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(f"cfg{config}_k{depth}")
+    except (OSError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.device)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in getattr(self, "lines", []):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def blocks_shape(n: int) -> tuple[int, int]:
+    m = int(math.sqrt(n))
+    while n % m:
+        m -= 1
+    return n // m, m
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (the reference's own engine, oracle/_ref; else the oracle port)
+# ---------------------------------------------------------------------------
+def cpu_engine():
+    from oracle.oracle import REF_SO, Oracle, Reference
+    if os.path.exists(REF_SO):
+        return "reference", Reference()
+    return "port", Oracle()
+
+
+def cpu_measure(cfg: dict, budget_s: float, variants=("blocks",)) -> dict:
+    """Times the reference's run() (bench.cpp:77-111 time_run semantics: the
+    timer includes run()'s buffer allocation and thread spawn) on a bounded
+    sample of the workload: a 8192x8192 torus with the config's density and
+    seed, generations sized to ~budget_s per variant."""
+    kind, eng = cpu_engine()
+    threads = os.cpu_count() or 1
+    side = min(8192, cfg["w"], cfg["h"])
+    res = {}
+    for var in variants:
+        workers = 1 if var == "serial" else threads
+        bx, by = blocks_shape(threads) if var == "blocks" else (1, 1)
+        if kind == "reference":
+            t1, _, _ = eng.time_run(side, side, 2, var, workers, (bx, by), 42, cfg["p"], 1, 0)
+            gens = max(2, int(budget_s / max(t1 / 2, 1e-6)))
+            t, _, hw = eng.time_run(side, side, gens, var, workers, (bx, by), 42, cfg["p"], 1, 0)
+            cores = workers
+        else:  # single-threaded C port of compute_region
+            g = eng.random_fill(side, side, cfg["p"], 42)
+            t0 = time.perf_counter()
+            eng.run(g, 1)
+            t1 = time.perf_counter() - t0
+            gens = max(1, int(budget_s / max(t1, 1e-6)))
+            t0 = time.perf_counter()
+            eng.run(g, gens)
+            t = time.perf_counter() - t0
+            cores = 1
+        res[var] = {"value": side * side * gens / t / 1e9, "seconds": t, "gens": gens,
+                    "cores": cores}
+    best = max(res, key=lambda v: res[v]["value"])
+    return {"value": res[best]["value"], "unit": UNIT, "cores": res[best]["cores"], "kind": kind,
+            "sample": f"{side}x{side} torus, p={cfg['p']}, seed 42, {res[best]['gens']} generations, "
+                      f"strategy {best} x{res[best]['cores']} threads (reference time_run; "
+                      f"timer includes allocation + thread spawn)",
+            "variants": {k: round(v["value"], 4) for k, v in res.items()},
+            "host_threads": threads}
+
+
+def run_reference_arm(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    kind, eng = cpu_engine()
+    threads = os.cpu_count() or 1
+    side = min(8192, cfg["w"], cfg["h"])
+    bx, by = blocks_shape(threads)
+    # calibrate so the whole K+W run stays within ~3 minutes
+    if kind == "reference":
+        t1, _, _ = eng.time_run(side, side, 2, "blocks", threads, (bx, by), 42, cfg["p"], 1, 0)
+    else:
+        g = eng.random_fill(side, side, cfg["p"], 42)
+        t0 = time.perf_counter()
+        eng.run(g, 1)
+        t1 = 2 * (time.perf_counter() - t0)
+    per_step = min(20.0, 170.0 / max(1, args.steps + args.warmup))
+    gens = max(1, int(per_step / max(t1 / 2, 1e-6)))
+    times = []
+    for i in range(args.warmup + args.steps):
+        if kind == "reference":
+            t, _, _ = eng.time_run(side, side, gens, "blocks", threads, (bx, by), 42, cfg["p"], 1, 0)
+        else:
+            t0 = time.perf_counter()
+            eng.run(g, gens)
+            t = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(t)
+    total = sum(times)
+    value = side * side * gens * len(times) / total / 1e9
+    cores = threads if kind == "reference" else 1
+    sample = (f"{side}x{side} torus, p={cfg['p']}, seed 42, {gens} generations per step, "
+              f"reference run() strategy blocks:{bx}x{by} x{cores} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu_arm(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_1209_4408_b200 import capi
+    from paper_1209_4408_b200.bands import BandDriver, make_geometry
+    from paper_1209_4408_b200.life import Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    L = capi.lib()
+    cfg = CONFIGS[args.config]
+    W, H, gens, depth = cfg["w"], cfg["h"], args.gens or cfg["gens"], args.depth
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    int_ops, int_s = (0.0, 0.0)
+    import ctypes as C
+    o, s = C.c_double(), C.c_double()
+    if L.life_measure_int_peak(local, 4000, C.byref(o), C.byref(s)) == 0:
+        int_ops = o.value
+
+    geo = make_geometry(W, H, rank, world, depth)
+    # Launch timing of every kernel pass in the timed region (events on the
+    # stream the kernels are launched on).
+    launches = []
+    from paper_1209_4408_b200.bands import cuda_stepper
+    base_step = cuda_stepper(W)
+    record = {"on": False}
+
+    def timed_step(inp, in_row0, in_rows, out, out_row0, out_rows, k):
+        if record["on"]:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            base_step(inp, in_row0, in_rows, out, out_row0, out_rows, k)
+            e1.record()
+            launches.append((e0, e1, out_rows * W * k, k))
+        else:
+            base_step(inp, in_row0, in_rows, out, out_row0, out_rows, k)
+
+    drv = BandDriver(geo, dev, stepper=timed_step)
+    drv.init_random(cfg["p"], 42)
+    grid_bytes = H * math.ceil(W / 64) * 8
+    flush = None
+    if grid_bytes * 2 < 4 * L2_BYTES:
+        flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+
+    for _ in range(args.warmup):
+        drv.run(gens)
+    barrier()
+    step_ms = []
+    l0 = L.life_kernel_launches()
+    record["on"] = True
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            drv.run(gens)
+            e1.record()
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    record["on"] = False
+    gpu_launches = int(L.life_kernel_launches() - l0)
+    barrier()
+    total_ms = max_over_ranks(sum(step_ms))
+    cells = W * H * gens * args.steps
+    value = cells / (total_ms * 1e-3) / 1e9
+
+    # Dominant kernel (the depth-`depth` packed pass): algorithmic int ops per
+    # launch / mean launch duration.
+    main = [(a.elapsed_time(b), n) for (a, b, n, k) in launches if k == depth]
+    kern_ms = sum(t for t, _ in main)
+    kern_cells = sum(n for _, n in main)
+    all_kern_ms = sum(a.elapsed_time(b) for (a, b, _, _) in launches)
+    achieved_ops = kern_cells * OPS_PER_UPDATE / (kern_ms * 1e-3) if kern_ms else 0.0
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    alg_bytes_per_update = 0.25 / depth
+    hbm_achieved = kern_cells * alg_bytes_per_update / (kern_ms * 1e-3) / 1e9 if kern_ms else 0.0
+    traffic = ncu_traffic(args.config, depth)
+    n_main = max(len(main), 1)
+    roofline = {
+        "bound": "int",
+        "kernel": f"packed_tb_kernel<{depth}>",
+        "achieved": achieved_ops / 1e12, "peak": int_ops / 1e12, "unit": "Tops/s",
+        "frac": achieved_ops / int_ops if int_ops else None,
+        "peak_source": "measured (life_measure_int_peak: LOP3 throughput, all SMs, this run)",
+        "ops_per_cell_update": OPS_PER_UPDATE,
+        "algorithmic_per_launch": {"cell_updates": kern_cells / n_main,
+                                   "int_ops": kern_cells / n_main * OPS_PER_UPDATE,
+                                   "hbm_bytes": kern_cells / n_main * alg_bytes_per_update},
+        "mean_launch_ms": kern_ms / n_main,
+        "kernel_share_of_step": all_kern_ms / sum(step_ms) if step_ms else None,
+        "traffic": traffic,
+        "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": hbm_achieved / hbm_peak, "bytes_per_cell_update": alg_bytes_per_update,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
+        "roofline_updates_per_s": min(int_ops / OPS_PER_UPDATE if int_ops else float("inf"),
+                                      hbm_peak * 1e9 / alg_bytes_per_update),
+    }
+    del drv
+    torch.cuda.empty_cache()
+
+    # ---- e2e through the public API, host buffers ------------------------
+    e2e = None
+    if not args.no_e2e:
+        steps_e2e = max(1, min(args.steps, 3))
+        if world == 1:
+            eng = Engine(local)
+            stream = torch.cuda.Stream(dev)
+            eng.set_stream(stream.cuda_stream)
+            wpr = math.ceil(W / 64)
+            host = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
+            eng.init_random(W, H, cfg["p"], 42, capi.ENGINE_PACKED)
+            eng.download_packed(host.numpy().view("uint64"))
+            hv = host.numpy().view("uint64")
+            ms = []
+            for i in range(1 + steps_e2e):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                eng.upload_packed(hv, W)
+                eng.run(gens, capi.ENGINE_PACKED, depth)
+                eng.download_packed(hv)
+                e1.record(stream)
+                e1.synchronize()
+                if i > 0:
+                    ms.append(e0.elapsed_time(e1))
+            eng.close()
+            e2e_ms = sum(ms)
+            bi = bo = H * wpr * 8
+        else:
+            drv = BandDriver(geo, dev)
+            host = torch.empty(tuple(drv.band().shape), dtype=torch.int32, pin_memory=True)
+            drv.init_random(cfg["p"], 42)
+            host.copy_(drv.band())
+            ms = []
+            for i in range(1 + steps_e2e):
+                barrier()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                drv.band().copy_(host, non_blocking=True)
+                drv.run(gens)
+                host.copy_(drv.band(), non_blocking=True)
+                e1.record()
+                torch.cuda.synchronize()
+                if i > 0:
+                    ms.append(e0.elapsed_time(e1))
+            e2e_ms = max_over_ranks(sum(ms))
+            t = torch.tensor([host.numel() * 4], dtype=torch.int64, device=dev)
+            dist.all_reduce(t)
+            bi = bo = int(t.item())
+            del drv
+        e2e = {"value": W * H * gens * steps_e2e / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
+               "api": "C-ABI life_grid_upload_packed + life_run + life_grid_download_packed"
+                      if world == 1 else "BandDriver band upload/run/download (pinned host)",
+               "steps": steps_e2e}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_measure(cfg, args.cpu_budget)
+        except Exception as exc:  # reported, not fatal
+            cpu = {"error": repr(exc)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "u32 bit-sliced (32 cells/word, exact integer)", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "width": W, "height": H, "generations": gens,
+                       "temporal_depth": depth, "global_cells": W * H,
+                       "parallelism": f"rowbands{world}" if world > 1 else "single-gpu",
+                       "l2": ("inputs larger than L2" if flush is None else
+                              "L2 flushed (256 MiB write) between steps")},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
+    ap.add_argument("--depth", type=int, default=16)
+    ap.add_argument("--gens", type=int, default=0, help="override the config's generations")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+/*
+ * life_gpu.h -- C-ABI of the B200-native Game of Life generation-step engine.
+ *
+ * This is the drop-in boundary for the reference's step loop.  The reference
+ * (arxiv/paper_1209_4408, /root/reference/proj) has no FFI: its operator API
+ * is the C++ function set of core/include/life/engine.hpp:11-43
+ *     RunResult run(Grid&& initial, const RunConfig&, const std::vector<int>& checkpoints);
+ *     Grid step_parallel(const Grid&, const Strategy&, int workers);
+ * over the byte-per-cell torus `Grid` (core/include/life/grid.hpp:24-70).
+ * Each entry point below names the reference interface it replaces; the C++
+ * host mirror (paper_1209_4408_b200/host/life_gpu.hpp) rebuilds the
+ * reference's `run()` semantics on top of it, and INTEGRATION.md shows the
+ * binding a maintainer adds to the reference.
+ *
+ * Conventions
+ *   - Plain pointers and sizes only; no exceptions cross this boundary.
+ *     Every function returns a status code (LIFE_OK = 0) and leaves a
+ *     message in life_last_error() (thread-local).
+ *   - Cell contract: byte grids are row-major, one byte
+ *     per cell; any NONZERO byte is alive (Grid::alive, grid.hpp:42, i.e.
+ *     step_serial semantics) and outputs are exactly 0/1.
+ *   - Packed exchange format: row-major rows of words_per_row >= ceil(W/64)
+ *     little-endian uint64 words; bit j of word k is column 64k+j; bits at
+ *     columns >= W are ignored on input and written as zero on output.
+ *   - Dimensions: W, H >= 3 (Grid ctor, grid.hpp:29-35 -> DimensionTooSmall).
+ *   - Populations are uint64 (the reference's int population overflows
+ *     above 2^31-1 live cells, grid.cpp:40-46).
+ *   - All device work of a context is ordered on its CUDA stream; every
+ *     host-buffer entry point returns only after its results are on the host.
+ */
+#ifndef LIFE_GPU_H
+#define LIFE_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes: the reference's exception hierarchy (errors.hpp:9-60). */
+#define LIFE_OK 0
+#define LIFE_ERR_CONFIG 1               /* life::ConfigError (engine.cpp:127-148) */
+#define LIFE_ERR_DIMENSION_TOO_SMALL 2  /* life::DimensionTooSmall (grid.hpp:31-33) */
+#define LIFE_ERR_TOO_MANY_PARTS 3       /* life::TooManyParts (decomposition.cpp:26-30) */
+#define LIFE_ERR_OUT_OF_BOUNDS 4        /* life::OutOfBounds (pattern.cpp:310-316) */
+#define LIFE_ERR_STATE 5                /* no grid loaded in the context */
+#define LIFE_ERR_CUDA 10                /* CUDA runtime failure (message has the CUDA error) */
+#define LIFE_ERR_NO_DEVICE 11           /* no CUDA device / bad device ordinal */
+#define LIFE_ERR_OUT_OF_MEMORY 12       /* device allocation failed */
+
+/* Engines (the reference's Strategy::Kind dispatch, decomposition.hpp:31,
+ * gains GPU kinds). */
+#define LIFE_ENGINE_PACKED 0 /* 64 cells/uint64, LOP3 adder network, temporal blocking */
+#define LIFE_ENGINE_BYTE 1   /* one byte per cell, one generation per pass */
+
+/* Largest temporal depth (generations per kernel pass) of the packed engine. */
+#define LIFE_MAX_TEMPORAL_DEPTH 16
+
+typedef struct life_ctx life_ctx;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* life_last_error(void);
+const char* life_version(void);
+
+/* ---- context (owns device buffers and a stream on one GPU) ------------- */
+int life_ctx_create(int device, life_ctx** out);
+int life_ctx_destroy(life_ctx* ctx);
+/* Orders the context's work on an external stream (e.g. torch's current
+ * stream); NULL restores the context's own stream. */
+int life_ctx_set_stream(life_ctx* ctx, void* cuda_stream);
+int life_ctx_sync(life_ctx* ctx);
+
+/* ---- grid in / out (replaces constructing and reading life::Grid) ------ */
+/* Replaces `Grid` + `Grid::data()` writes (grid.hpp:29-35, :56-57).
+ * `row_stride` >= width bytes between host rows. */
+int life_grid_upload_u8(life_ctx* ctx, const uint8_t* cells, int64_t width, int64_t height,
+                        int64_t row_stride);
+int life_grid_upload_packed(life_ctx* ctx, const uint64_t* words, int64_t width,
+                            int64_t height, int64_t words_per_row);
+/* Replaces random_fill (pattern.cpp:330-342): identical grid, generated on the
+ * device from the counter form of the splitmix64 stream.
+ * `engine` selects the resident layout. */
+int life_grid_init_random(life_ctx* ctx, int64_t width, int64_t height, double density,
+                          uint64_t seed, int engine);
+/* Replaces reading `Grid::data()` of RunResult::grid (engine.hpp:24-27). */
+int life_grid_download_u8(life_ctx* ctx, uint8_t* cells, int64_t row_stride);
+int life_grid_download_packed(life_ctx* ctx, uint64_t* words, int64_t words_per_row);
+/* Toroidally wrapped w x h window at (x0, y0) (Grid::wrap, grid.hpp:48-54),
+ * as 0/1 bytes; for light-cone parity checks of grids too big to download. */
+int life_grid_window_u8(life_ctx* ctx, int64_t x0, int64_t y0, int64_t w, int64_t h,
+                        uint8_t* out);
+int life_grid_dims(life_ctx* ctx, int64_t* width, int64_t* height);
+/* Replaces population (grid.cpp:40-46), widened to uint64. */
+int life_population(life_ctx* ctx, uint64_t* out);
+
+/* ---- the step loop ------------------------------------------------------ */
+/* Replaces run(Grid&&, RunConfig, checkpoints) (engine.cpp:162-214):
+ *   `generations` >= 0 (ConfigError otherwise, engine.cpp:133-136);
+ *   `temporal_depth`: generations per packed kernel pass, 1..16, 0 = auto
+ *     (the byte engine accepts 0 or 1);
+ *   `checkpoints`: strictly ascending in [0, generations] (engine.cpp:137-147);
+ *     `populations[i]` receives the population after checkpoints[i]
+ *     generations (checkpoint 0 = the initial grid, engine.cpp:186).
+ * The grid stays resident in the context after the call. */
+int life_run(life_ctx* ctx, int64_t generations, int engine, int temporal_depth,
+             const int64_t* checkpoints, int32_t n_checkpoints, uint64_t* populations);
+/* Replaces step_parallel (engine.cpp:152-155): run(..., iterations = 1). */
+int life_step(life_ctx* ctx, int engine);
+
+/* ---- row-band decomposition (multi-GPU) --------------------------------- */
+/* Mirrors band_bounds / partition_rows (decomposition.cpp:12-24, :93-104):
+ * writes parts+1 cut points; LIFE_ERR_TOO_MANY_PARTS if parts > extent. */
+int life_band_bounds(int64_t extent, int32_t parts, int64_t* bounds);
+
+/* ---- device-buffer layer (plain device pointers; used by the multi-GPU
+ *      band driver, which owns its buffers and streams) ------------------- */
+/* Device row pitch, in uint32 words, of the packed layout for width W
+ * (>= 2*ceil(W/64), a multiple of 32 words = 128 B). */
+int64_t life_packed_pitch_words(int64_t width);
+/* Byte layout pitch (>= W, a multiple of 16 B). */
+int64_t life_byte_pitch(int64_t width);
+/* `generations` (1..16) packed generations in one pass.  Output relative row
+ * r (0 <= r < out_rows) is stored at out + (out_row0 + r) * out_pitch; input
+ * relative row r (-generations <= r < out_rows + generations) is read from
+ * physical row (in_row0 + r) mod in_rows of `in`.  The torus is the case
+ * in_rows = H, in_row0 = out_row0 = 0; a band with k ghost rows above it is
+ * in_row0 = k.  `in` and `out` must not overlap. */
+int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0,
+                         int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0,
+                         int64_t width, int64_t out_rows, int32_t generations, void* stream);
+/* One byte-engine generation with the same row addressing (pitches in bytes). */
+int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                       uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                       int64_t out_rows, void* stream);
+/* Rows [y0, y0+rows) of random_fill(W, H, density, seed) into a packed buffer. */
+int life_dev_packed_random(uint32_t* out, int64_t pitch, int64_t width, int64_t y0,
+                           int64_t rows, double density, uint64_t seed, void* stream);
+/* Adds the population of `rows` packed rows to *dev_count (device uint64). */
+int life_dev_packed_population(const uint32_t* grid, int64_t pitch, int64_t width,
+                               int64_t rows, uint64_t* dev_count, void* stream);
+/* Packs byte rows (nonzero -> 1) into packed rows and back. */
+int life_dev_pack(const uint8_t* cells, int64_t cell_pitch, uint32_t* words, int64_t pitch,
+                  int64_t width, int64_t rows, void* stream);
+int life_dev_unpack(const uint32_t* words, int64_t pitch, uint8_t* cells, int64_t cell_pitch,
+                    int64_t width, int64_t rows, void* stream);
+
+/* ---- measurement helpers ------------------------------------------------ */
+/* Integer-pipe peak: runs a LOP3 throughput kernel for ~`iters` dependent
+ * steps on every SM and returns lane-ops per second in *ops_per_s. */
+int life_measure_int_peak(int device, int64_t iters, double* ops_per_s, double* seconds);
+/* Number of kernel launches issued by this library in this process. */
+uint64_t life_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIFE_GPU_H */

@@ -1,0 +1,194 @@
+"""Row-band decomposition of the torus across GPUs (one process per GPU).
+
+Mirrors the reference's preferred 1-D row decomposition: Strategy::rows()
+-> partition_rows -> band_bounds (decomposition.cpp:12-24, :93-104; the
+paper's conclusion).  Rank r owns rows
+[bounds[r], bounds[r+1]) and keeps `depth` ghost rows above and below its
+band.  One temporal-blocked pass of k <= depth generations is
+
+    1. post the halo exchange (NCCL send/recv over NVLink via
+       torch.distributed): my top k rows -> the rank above (its bottom
+       ghosts), my bottom k rows -> the rank below (its top ghosts);
+    2. compute the interior output rows [k, band-k), which depend only on
+       local rows, while the halos are in flight;
+    3. wait for the halos;
+    4. compute the two k-row edge strips.
+
+This replaces the reference's per-generation shared-memory barrier
+(WorkerTeam, engine.cpp:60-125) with one exchange per k generations.  With a
+single rank the band is the whole torus and the kernel wraps rows itself
+(no ghosts, no exchange).
+
+The compute and the buffers are injectable so the same driver runs
+(a) on GPUs with the CUDA kernels of the C-ABI and NCCL, and (b) in the
+world-size-2 gloo tests on CPU with a test-only stepper.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import capi
+from .life import ConfigError, TooManyParts, band_bounds, check
+
+
+@dataclass
+class BandGeometry:
+    width: int
+    height: int
+    rank: int
+    world: int
+    depth: int
+    y0: int
+    y1: int
+    pitch: int  # uint32 words per row
+
+    @property
+    def band_rows(self) -> int:
+        return self.y1 - self.y0
+
+    @property
+    def ghost(self) -> int:
+        return 0 if self.world == 1 else self.depth
+
+    @property
+    def buf_rows(self) -> int:
+        return self.band_rows + 2 * self.ghost
+
+
+def make_geometry(width: int, height: int, rank: int, world: int, depth: int) -> BandGeometry:
+    if width < 3 or height < 3:
+        raise ConfigError(f"grid dimensions must be at least 3x3, got {width}x{height}")
+    if not 1 <= depth <= capi.MAX_TEMPORAL_DEPTH:
+        raise ConfigError(f"temporal depth must be in [1, {capi.MAX_TEMPORAL_DEPTH}]")
+    bounds = band_bounds(height, world)  # TooManyParts like partition_rows
+    y0, y1 = bounds[rank], bounds[rank + 1]
+    if world > 1 and (y1 - y0) < depth:
+        raise TooManyParts(f"band of {y1 - y0} rows is thinner than the temporal depth {depth}")
+    return BandGeometry(width, height, rank, world, depth, y0, y1,
+                        int(capi.lib().life_packed_pitch_words(width)))
+
+
+# Stepper(in, in_row0, in_rows, out, out_row0, out_rows, k): one k-generation
+# pass with the addressing of life_dev_packed_step.
+Stepper = Callable[[torch.Tensor, int, int, torch.Tensor, int, int, int], None]
+
+
+def cuda_stepper(width: int) -> Stepper:
+    L = capi.lib()
+
+    def step(inp, in_row0, in_rows, out, out_row0, out_rows, k):
+        pitch = inp.shape[1]
+        stream = torch.cuda.current_stream(inp.device).cuda_stream
+        check(L.life_dev_packed_step(inp.data_ptr(), pitch, in_row0, in_rows, out.data_ptr(),
+                                     out.shape[1], out_row0, width, out_rows, k, stream))
+    return step
+
+
+class BandDriver:
+    """One rank's band, ping-pong buffers and pass loop."""
+
+    def __init__(self, geo: BandGeometry, device: torch.device, stepper: Optional[Stepper] = None,
+                 group=None, overlap: bool = True):
+        self.geo = geo
+        self.device = device
+        self.group = group
+        self.overlap = overlap
+        self.stepper = stepper or cuda_stepper(geo.width)
+        shape = (geo.buf_rows, geo.pitch)
+        self.buf = [torch.zeros(shape, dtype=torch.int32, device=device) for _ in range(2)]
+        self.cur = 0
+        self.generations = 0
+        self.exchange_bytes = 0  # per pass, both directions, this rank
+
+    # -- views ---------------------------------------------------------
+    def band(self, which: Optional[int] = None) -> torch.Tensor:
+        b = self.buf[self.cur if which is None else which]
+        return b[self.geo.ghost:self.geo.ghost + self.geo.band_rows]
+
+    # -- halo exchange -------------------------------------------------
+    def _peers(self) -> tuple[int, int]:
+        r, p = self.geo.rank, self.geo.world
+        return (r - 1) % p, (r + 1) % p  # above, below (torus ring)
+
+    def post_exchange(self, k: int):
+        """Sends my top/bottom k rows, receives k ghost rows on each side."""
+        g = self.geo
+        if g.world == 1:
+            return None
+        a = self.buf[self.cur]
+        up, down = self._peers()
+        top = a[g.ghost:g.ghost + k]
+        bottom = a[g.ghost + g.band_rows - k:g.ghost + g.band_rows]
+        ghost_top = a[g.ghost - k:g.ghost]
+        ghost_bottom = a[g.ghost + g.band_rows:g.ghost + g.band_rows + k]
+        # Same issue order on every rank: per peer pair, the i-th send
+        # matches the i-th receive (needed when up == down, world == 2).
+        ops = [dist.P2POp(dist.isend, top, up, self.group),
+               dist.P2POp(dist.isend, bottom, down, self.group),
+               dist.P2POp(dist.irecv, ghost_bottom, down, self.group),
+               dist.P2POp(dist.irecv, ghost_top, up, self.group)]
+        self.exchange_bytes = 2 * top.numel() * 4
+        return dist.batch_isend_irecv(ops)
+
+    @staticmethod
+    def wait(works) -> None:
+        if works:
+            for w in works:
+                w.wait()
+
+    # -- one pass ------------------------------------------------------
+    def pass_(self, k: int) -> None:
+        g = self.geo
+        if not 1 <= k <= g.depth:
+            raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
+        a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
+        if g.world == 1:
+            self.stepper(a, 0, g.height, b, 0, g.height, k)
+        else:
+            works = self.post_exchange(k)
+            n = g.band_rows
+            if self.overlap and n > 2 * k:
+                self.stepper(a, g.ghost + k, g.buf_rows, b, g.ghost + k, n - 2 * k, k)
+                self.wait(works)
+                self.stepper(a, g.ghost, g.buf_rows, b, g.ghost, k, k)
+                self.stepper(a, g.ghost + n - k, g.buf_rows, b, g.ghost + n - k, k, k)
+            else:
+                self.wait(works)
+                self.stepper(a, g.ghost, g.buf_rows, b, g.ghost, n, k)
+        self.cur ^= 1
+        self.generations += k
+
+    def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None) -> None:
+        if generations < 0:
+            raise ConfigError(f"iteration count must be non-negative, got {generations}")
+        done = 0
+        while done < generations:
+            k = min(self.geo.depth, generations - done)
+            self.pass_(k)
+            done += k
+            if on_pass:
+                on_pass(k)
+
+    # -- init / reductions (CUDA) ----------------------------------------
+    def init_random(self, density: float, seed: int) -> None:
+        g = self.geo
+        band = self.band()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_random(band.data_ptr(), g.pitch, g.width, g.y0,
+                                                g.band_rows, density, seed, stream))
+        self.generations = 0
+
+    def population(self) -> int:
+        """Band population (CUDA popcount), summed over ranks when distributed."""
+        g = self.geo
+        acc = torch.zeros(1, dtype=torch.int64, device=self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_population(self.band().data_ptr(), g.pitch, g.width,
+                                                    g.band_rows, acc.data_ptr(), stream))
+        if g.world > 1:
+            dist.all_reduce(acc, group=self.group)
+        return int(acc.item())

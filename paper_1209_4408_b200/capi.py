@@ -1,0 +1,91 @@
+"""ctypes binding of the C-ABI in include/life_gpu.h (liblife_gpu.so).
+
+Loading fails loudly when the CUDA library is missing: there is no CPU
+fallback in this package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "liblife_gpu.so")
+
+# Status codes (include/life_gpu.h).
+OK = 0
+ERR_CONFIG = 1
+ERR_DIMENSION_TOO_SMALL = 2
+ERR_TOO_MANY_PARTS = 3
+ERR_OUT_OF_BOUNDS = 4
+ERR_STATE = 5
+ERR_CUDA = 10
+ERR_NO_DEVICE = 11
+ERR_OUT_OF_MEMORY = 12
+
+ENGINE_PACKED = 0
+ENGINE_BYTE = 1
+MAX_TEMPORAL_DEPTH = 16
+
+# Every function the header declares: (name, restype, argtypes).
+_vp = C.c_void_p
+_i64 = C.c_int64
+_i32 = C.c_int32
+_u64 = C.c_uint64
+SIGNATURES = [
+    ("life_last_error", C.c_char_p, []),
+    ("life_version", C.c_char_p, []),
+    ("life_ctx_create", C.c_int, [C.c_int, C.POINTER(_vp)]),
+    ("life_ctx_destroy", C.c_int, [_vp]),
+    ("life_ctx_set_stream", C.c_int, [_vp, _vp]),
+    ("life_ctx_sync", C.c_int, [_vp]),
+    ("life_grid_upload_u8", C.c_int, [_vp, _vp, _i64, _i64, _i64]),
+    ("life_grid_upload_packed", C.c_int, [_vp, _vp, _i64, _i64, _i64]),
+    ("life_grid_init_random", C.c_int, [_vp, _i64, _i64, C.c_double, _u64, C.c_int]),
+    ("life_grid_download_u8", C.c_int, [_vp, _vp, _i64]),
+    ("life_grid_download_packed", C.c_int, [_vp, _vp, _i64]),
+    ("life_grid_window_u8", C.c_int, [_vp, _i64, _i64, _i64, _i64, _vp]),
+    ("life_grid_dims", C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
+    ("life_population", C.c_int, [_vp, C.POINTER(_u64)]),
+    ("life_run", C.c_int, [_vp, _i64, C.c_int, C.c_int, _vp, _i32, _vp]),
+    ("life_step", C.c_int, [_vp, C.c_int]),
+    ("life_band_bounds", C.c_int, [_i64, _i32, _vp]),
+    ("life_packed_pitch_words", _i64, [_i64]),
+    ("life_byte_pitch", _i64, [_i64]),
+    ("life_dev_packed_step", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i32,
+                                       _vp]),
+    ("life_dev_byte_step", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
+    ("life_dev_packed_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),
+    ("life_dev_packed_population", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    ("life_dev_pack", C.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
+    ("life_dev_unpack", C.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
+    ("life_measure_int_peak", C.c_int, [C.c_int, _i64, C.POINTER(C.c_double),
+                                        C.POINTER(C.c_double)]),
+    ("life_kernel_launches", _u64, []),
+]
+
+_lib = None
+
+
+class LibraryMissing(ImportError):
+    pass
+
+
+def lib() -> C.CDLL:
+    """Loads liblife_gpu.so (built by paper_1209_4408_b200.build); raises if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise LibraryMissing(
+                f"{LIB_PATH} is not built; run `python -m paper_1209_4408_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().life_last_error().decode(errors="replace")

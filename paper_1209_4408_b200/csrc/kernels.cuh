@@ -1,0 +1,575 @@
+// kernels.cuh -- sm_100a device code of the generation-step engine.
+//
+// Layouts in HBM:
+//   packed: rows of `pitch` uint32 words (pitch a multiple of 32 words, 128 B);
+//           bit j of word k = column 32k+j (this is the little-endian view of
+//           the uint64 exchange format of include/life_gpu.h); words
+//           k >= ceil(W/32) and bits at columns >= W are kept zero.
+//   byte:   rows of `pitch` bytes (a multiple of 16), one 0/1 byte per cell,
+//           bytes at columns >= W kept zero.
+//
+// Rule: B3/S23 (next_state, grid.cpp:22-28).  With S the 9-cell sum
+// (cell + 8 neighbours), next = (S == 3) | (S == 4 & self), which equals
+// compute_region's `(n==3)|((n==2)&mid)` (engine.cpp:30-32) with n = S - self.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lifegpu {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
+
+// ---------------------------------------------------------------------------
+// Bit-sliced rule network (packed engine).
+//
+// A row word x (32 cells) with its left/right neighbour words gives the
+// horizontal 3-cell sums h = L + x + R as two bit planes (h0, h1):
+//   L = x<<1 | xl>>31,  R = x>>1 | xr<<31   (2 SHF.W funnel shifts)
+//   h0 = L^x^R,  h1 = maj(L,x,R)            (2 LOP3)
+// Three rows' planes a (above), b (the cell's row), c (below) give
+//   S = a + b + c = t0 + 2*u1 + 4*u2 + 8*(q&p&k0) with
+//   t0 = a0^b0^c0, k0 = maj(a0,b0,c0), p = a1^b1^c1, q = maj(a1,b1,c1),
+//   u1 = p^k0, u2 = q^(p&k0)                (6 LOP3)
+// and next = (S==3) | (S==4 & self) = V & (u1^u2) with
+//   V = u2 ? (self & ~t0) : t0              (2 LOP3).
+// S==3 <=> t0 & u1 & ~u2 (u1 = 1 excludes the carry term since S <= 9);
+// S==4 <=> ~t0 & ~u1 & u2.  12 integer ops per 32 cell-updates; verified
+// against next_state over all 512 3x3 neighbourhoods in
+// tests/test_rule_network.py.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
+  return (a & b) | (a & c) | (b & c);
+}
+
+struct HSum {
+  uint32_t h0, h1;
+};
+
+__device__ __forceinline__ HSum hsum(uint32_t xl, uint32_t x, uint32_t xr) {
+  const uint32_t L = __funnelshift_l(xl, x, 1);  // (x << 1) | (xl >> 31)
+  const uint32_t R = __funnelshift_r(x, xr, 1);  // (x >> 1) | (xr << 31)
+  return HSum{L ^ x ^ R, maj3(L, x, R)};
+}
+
+__device__ __forceinline__ uint32_t rule(HSum a, HSum b, HSum c, uint32_t self) {
+  const uint32_t t0 = a.h0 ^ b.h0 ^ c.h0;
+  const uint32_t k0 = maj3(a.h0, b.h0, c.h0);
+  const uint32_t p = a.h1 ^ b.h1 ^ c.h1;
+  const uint32_t q = maj3(a.h1, b.h1, c.h1);
+  const uint32_t u1 = p ^ k0;
+  const uint32_t u2 = q ^ (p & k0);
+  const uint32_t v = (u2 & self & ~t0) | (~u2 & t0);
+  return v & (u1 ^ u2);
+}
+
+// Physical row index (base + r) mod m for possibly negative r.
+__device__ __forceinline__ int64_t wrap_row(int64_t base, int64_t r, int64_t m) {
+  int64_t p = (base + r) % m;
+  return p < 0 ? p + m : p;
+}
+
+// 32 cells starting at column 32*wi of the infinitely repeated row (period
+// W): the toroidal wrap of Grid::wrap (grid.hpp:48-54) applied to a word.
+// Slow path for words that straddle the row end or lie outside [0, W).
+__device__ __noinline__ uint32_t load_word_wrapped(const uint32_t* __restrict__ row,
+                                                   int64_t wi, int64_t width, int32_t nw) {
+  int64_t c = (32 * wi) % width;
+  if (c < 0) c += width;
+  uint32_t v = 0;
+  int filled = 0;
+  while (filled < 32) {
+    const int64_t avail = width - c;
+    const int n = avail < (32 - filled) ? static_cast<int>(avail) : 32 - filled;
+    const int64_t w0 = c >> 5;
+    const uint32_t lo = row[w0];
+    const uint32_t hi = (w0 + 1 < nw) ? row[w0 + 1] : 0u;
+    uint32_t bits = __funnelshift_r(lo, hi, static_cast<uint32_t>(c & 31));
+    if (n < 32) bits &= (1u << n) - 1u;
+    v |= bits << filled;
+    filled += n;
+    c += n;
+    if (c >= width) c = 0;
+  }
+  return v;
+}
+
+struct PackedStepArgs {
+  const uint32_t* in;
+  int64_t in_pitch;   // uint32 words
+  int64_t in_row0;    // physical row of relative row 0
+  int64_t in_rows;    // rows of `in` (row index wraps modulo this)
+  uint32_t* out;
+  int64_t out_pitch;
+  int64_t out_row0;
+  int64_t width;      // cells
+  int64_t out_rows;
+  int64_t seg_rows;   // output rows per warp segment
+  int32_t nw;         // ceil(width / 32): words holding cells
+  int32_t n_strips;   // ceil(nw / 30)
+  uint32_t tail_mask; // valid bits of word nw-1
+};
+
+constexpr int kStripWords = 30;  // output words per warp (lanes 1..30; 0 and 31 are ghosts)
+constexpr int kPackedThreads = 128;
+
+// Rows prefetched ahead per lane; a multiple of 3 so the 3-row stage ring
+// renames without moves after unrolling.
+template <int K>
+struct PackedTraits {
+  static constexpr int kPrefetch = K <= 1 ? 12 : (K <= 3 ? 6 : 3);
+};
+
+// ---------------------------------------------------------------------------
+// Temporal-blocked packed step: K generations per pass, no shared memory,
+// no block barriers.  Each warp owns a vertical strip of 32 words (30 output
+// words + one ghost word per side; a ghost word covers K <= 32 cells of
+// light cone) and a segment of seg_rows output rows, and streams input rows
+// y0-K .. y1+K-1 through a K-stage register pipeline: stage g turns the row
+// stream of generation g-1 into generation g, one row per step, keeping the
+// 3-row (h0,h1,self) window of its input in registers.  Horizontal
+// neighbour words come from __shfl_up/down_sync.  Every input row is read
+// once per pass and every output row written once, so the HBM traffic per
+// cell-update is (1 bit read + 1 bit write)/K plus the ghost overlap
+// (32/30 on reads, (seg+2K)/seg vertically).
+//
+// Replaces compute_region (engine.cpp:17-48) x K generations with the
+// per-generation barrier of WorkerTeam (engine.cpp:79-96) removed inside a
+// pass: the dependency is carried by the pipeline order instead.
+// ---------------------------------------------------------------------------
+template <int K>
+__global__ void __launch_bounds__(kPackedThreads)
+packed_tb_kernel(const PackedStepArgs a) {
+  constexpr int PF = PackedTraits<K>::kPrefetch;
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kPackedThreads + threadIdx.x) >> 5;
+  const int strip = static_cast<int>(gwarp % a.n_strips);
+  const int64_t seg = gwarp / a.n_strips;
+  const int64_t y0 = seg * a.seg_rows;
+  if (y0 >= a.out_rows) return;  // warp-uniform
+  const int64_t rows = min(a.seg_rows, a.out_rows - y0);
+
+  const int64_t wi = static_cast<int64_t>(strip) * kStripWords + lane - 1;
+  const bool interior = wi >= 0 && (wi + 1) * 32 <= a.width;
+  const bool store_lane = lane >= 1 && lane <= kStripWords && wi < a.nw;
+  const uint32_t store_mask = (wi == a.nw - 1) ? a.tail_mask : kFull;
+
+  // Input row cursor (physical), advanced with wrap.
+  int64_t lrow = wrap_row(a.in_row0, y0 - K, a.in_rows);
+  auto load_next = [&]() -> uint32_t {
+    const uint32_t* row = a.in + lrow * a.in_pitch;
+    uint32_t v = interior ? __ldg(row + wi) : load_word_wrapped(row, wi, a.width, a.nw);
+    if (++lrow == a.in_rows) lrow = 0;
+    return v;
+  };
+
+  uint32_t pf[PF];
+#pragma unroll
+  for (int u = 0; u < PF; ++u) pf[u] = load_next();
+
+  HSum sa[K], sb[K];
+  uint32_t sself[K];
+#pragma unroll
+  for (int g = 0; g < K; ++g) {
+    sa[g] = HSum{0u, 0u};
+    sb[g] = HSum{0u, 0u};
+    sself[g] = 0u;
+  }
+
+  const int64_t total = rows + 2 * K;  // stage K emits output row i-2K at step i
+  uint32_t* out_base = a.out + (a.out_row0 + y0 - 2 * K) * a.out_pitch + wi;
+
+  for (int64_t base = 0; base < total; base += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      uint32_t x = pf[u];
+      pf[u] = load_next();
+#pragma unroll
+      for (int g = 0; g < K; ++g) {
+        const uint32_t xl = __shfl_up_sync(kFull, x, 1);
+        const uint32_t xr = __shfl_down_sync(kFull, x, 1);
+        const HSum c = hsum(xl, x, xr);
+        const uint32_t y = rule(sa[g], sb[g], c, sself[g]);
+        sa[g] = sb[g];
+        sb[g] = c;
+        sself[g] = x;
+        x = y;
+      }
+      const int64_t i = base + u;
+      if (store_lane && i >= 2 * K && i < total) {
+        out_base[i * a.out_pitch] = x & store_mask;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Byte engine: one generation per pass over the byte layout.  Each lane owns
+// 16 cells (one uint4) of a row and walks down a segment of rows, keeping
+// the 3-row window of horizontal byte sums in registers, so each input row
+// is read once (plus 2 halo rows per segment) and each output row written
+// once: 2 B of HBM traffic per cell-update.  Neighbour bytes across lanes
+// come from shuffles; across warps and across the torus seam from single
+// byte loads.  SWAR: bytes hold 0..9, so uint32 adds never carry between
+// cells.  Restates compute_region (engine.cpp:17-48) incl. the peeled wrap
+// columns (:35-39, :44-46).
+// ---------------------------------------------------------------------------
+struct ByteStepArgs {
+  const uint8_t* in;
+  int64_t in_pitch;
+  int64_t in_row0;
+  int64_t in_rows;
+  uint8_t* out;
+  int64_t out_pitch;
+  int64_t out_row0;
+  int64_t width;
+  int64_t out_rows;
+  int64_t seg_rows;
+  int32_t nv;        // ceil(width / 16) vectors per row
+  int32_t n_strips;  // ceil(nv / 32)
+};
+
+constexpr int kByteThreads = 128;
+constexpr int kBytePrefetch = 3;
+
+struct ByteRow {
+  uint32_t h[4];   // L + x + R per byte
+  uint32_t hn[4];  // L + R per byte (neighbours only)
+  uint32_t x[4];
+};
+
+__device__ __forceinline__ ByteRow byte_row(const uint4 v, uint32_t left_byte,
+                                            uint32_t right_byte, int seam_pos, uint32_t col0) {
+  uint32_t x[4] = {v.x, v.y, v.z, v.w};
+  // Right-neighbour vector with the torus seam: the byte right of column W-1
+  // (position seam_pos of this vector) must be column 0.
+  uint32_t r[4];
+  r[0] = __funnelshift_r(x[0], x[1], 8);
+  r[1] = __funnelshift_r(x[1], x[2], 8);
+  r[2] = __funnelshift_r(x[2], x[3], 8);
+  r[3] = __funnelshift_r(x[3], right_byte, 8);
+  if (seam_pos >= 0) {
+    const int wsel = seam_pos >> 2, sh = (seam_pos & 3) * 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i == wsel) r[i] = (r[i] & ~(0xffu << sh)) | (col0 << sh);
+  }
+  uint32_t l[4];
+  l[0] = __funnelshift_l(left_byte << 24, x[0], 8);
+  l[1] = __funnelshift_l(x[0], x[1], 8);
+  l[2] = __funnelshift_l(x[1], x[2], 8);
+  l[3] = __funnelshift_l(x[2], x[3], 8);
+  ByteRow row;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    row.x[i] = x[i];
+    row.hn[i] = l[i] + r[i];
+    row.h[i] = row.hn[i] + x[i];
+  }
+  return row;
+}
+
+struct ByteRaw {
+  uint4 v;
+  uint32_t lb, rb, col0;
+};
+
+__global__ void __launch_bounds__(kByteThreads) byte_step_kernel(const ByteStepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kByteThreads + threadIdx.x) >> 5;
+  const int strip = static_cast<int>(gwarp % a.n_strips);
+  const int64_t seg = gwarp / a.n_strips;
+  const int64_t y0 = seg * a.seg_rows;
+  if (y0 >= a.out_rows) return;
+  const int64_t rows = min(a.seg_rows, a.out_rows - y0);
+
+  const int64_t vi = static_cast<int64_t>(strip) * 32 + lane;
+  const int64_t c0 = vi * 16;
+  const bool active = vi < a.nv;
+  // Position of column W-1 inside this lane's vector, or -1.
+  const int seam_pos =
+      (active && a.width - 1 - c0 < 16) ? static_cast<int>(a.width - 1 - c0) : -1;
+  // Columns read by single-byte loads: lane 0 needs the column left of c0,
+  // lane 31 (or the seam lane) the column right of its vector.
+  const int64_t left_col = c0 == 0 ? a.width - 1 : c0 - 1;
+  const int64_t right_col = c0 + 16 < a.width ? c0 + 16 : 0;
+  const bool need_left = active && lane == 0;
+  const bool need_right = active && (lane == 31 || seam_pos == 15);
+
+  int64_t lrow = wrap_row(a.in_row0, y0 - 1, a.in_rows);
+  // Issues the loads of the next input row (prefetched kBytePrefetch ahead).
+  auto fetch = [&]() -> ByteRaw {
+    const uint8_t* row = a.in + lrow * a.in_pitch;
+    ByteRaw q;
+    q.v = active ? __ldg(reinterpret_cast<const uint4*>(row + c0)) : make_uint4(0, 0, 0, 0);
+    q.lb = need_left ? __ldg(row + left_col) : 0u;
+    q.rb = need_right ? __ldg(row + right_col) : 0u;
+    q.col0 = seam_pos >= 0 ? static_cast<uint32_t>(__ldg(row)) : 0u;
+    if (++lrow == a.in_rows) lrow = 0;
+    return q;
+  };
+  auto build = [&](const ByteRaw& q) -> ByteRow {
+    uint32_t lb = __shfl_up_sync(kFull, q.v.w >> 24, 1);
+    uint32_t rb = __shfl_down_sync(kFull, q.v.x & 0xffu, 1);
+    if (need_left) lb = q.lb;
+    if (need_right) rb = q.rb;
+    return byte_row(q.v, lb, rb, seam_pos, q.col0);
+  };
+
+  ByteRaw pf[kBytePrefetch];
+#pragma unroll
+  for (int u = 0; u < kBytePrefetch; ++u) pf[u] = fetch();
+  ByteRow up = build(pf[0]);
+  pf[0] = fetch();
+  ByteRow mid = build(pf[1]);
+  pf[1] = fetch();
+
+  uint8_t* out_row = a.out + (a.out_row0 + y0) * a.out_pitch + c0;
+  for (int64_t r0 = 0; r0 < rows; r0 += kBytePrefetch) {
+#pragma unroll
+    for (int u = 0; u < kBytePrefetch; ++u) {
+      const ByteRow dn = build(pf[(u + 2) % kBytePrefetch]);
+      pf[(u + 2) % kBytePrefetch] = fetch();
+      uint32_t o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t n = up.h[i] + dn.h[i] + mid.hn[i];  // 8-neighbour count per byte
+        // (n | self) == 3  <=>  next alive (engine.cpp:32 on 0/1 bytes);
+        // t = (n|self)^3 is 0..15 per byte; zero-test via the byte's bit 7.
+        const uint32_t t = (n | mid.x[i]) ^ 0x03030303u;
+        o[i] = (~(t + 0x7f7f7f7fu) & 0x80808080u) >> 7;
+      }
+      if (seam_pos >= 0) {  // zero the padding bytes past column W-1
+        const int keep = seam_pos + 1;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int lo = i * 4;
+          if (keep <= lo) o[i] = 0;
+          else if (keep < lo + 4) o[i] &= (1u << ((keep - lo) * 8)) - 1u;
+        }
+      }
+      if (active && r0 + u < rows) {
+        *reinterpret_cast<uint4*>(out_row) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+      out_row += a.out_pitch;
+      up = mid;
+      mid = dn;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Layout conversion, seeded soup, population, windows.
+// ---------------------------------------------------------------------------
+
+// splitmix64 output (rng.hpp:22-27).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+  return z ^ (z >> 31);
+}
+
+// random_fill (pattern.cpp:330-342) in counter form: cell i = y*W + x is the
+// (i+1)-th draw of SplitMix64(seed), alive iff (draw >> 11) < thr where
+// thr = ceil(density * 2^53) (exactly `next_unit() < density`).
+// One thread per packed word; rows [y0, y0+rows) of the torus.
+__global__ void packed_random_kernel(uint32_t* __restrict__ out, int64_t pitch, int64_t width,
+                                     int64_t y0, int64_t rows, int32_t nw, uint64_t seed,
+                                     uint64_t thr) {
+  const int64_t n = rows * pitch;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / pitch;
+    const int32_t w = static_cast<int32_t>(t - r * pitch);
+    uint32_t word = 0;
+    if (w < nw) {
+      const int64_t col = static_cast<int64_t>(w) * 32;
+      const int nbits = width - col < 32 ? static_cast<int>(width - col) : 32;
+      uint64_t s = seed + (static_cast<uint64_t>((y0 + r) * width + col) + 1ULL) * kGamma;
+      for (int j = 0; j < nbits; ++j) {
+        word |= static_cast<uint32_t>((mix64(s) >> 11) < thr) << j;
+        s += kGamma;
+      }
+    }
+    out[t] = word;
+  }
+}
+
+// Same soup in the byte layout (one thread per 16-byte vector).
+__global__ void byte_random_kernel(uint8_t* __restrict__ out, int64_t pitch, int64_t width,
+                                   int64_t y0, int64_t rows, uint64_t seed, uint64_t thr) {
+  const int64_t nvec = pitch / 16;
+  const int64_t n = rows * nvec;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / nvec;
+    const int64_t c0 = (t - r * nvec) * 16;
+    uint32_t o[4] = {0, 0, 0, 0};
+    uint64_t s = seed + (static_cast<uint64_t>((y0 + r) * width + c0) + 1ULL) * kGamma;
+    for (int j = 0; j < 16; ++j) {
+      if (c0 + j < width) o[j >> 2] |= static_cast<uint32_t>((mix64(s) >> 11) < thr) << ((j & 3) * 8);
+      s += kGamma;
+    }
+    *reinterpret_cast<uint4*>(out + r * pitch + c0) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Byte rows -> packed rows: lane j of a warp reads column 32w+j and a warp
+// ballot forms word w (coalesced byte reads, nonzero -> alive).
+__global__ void pack_kernel(const uint8_t* __restrict__ cells, int64_t cell_pitch,
+                            uint32_t* __restrict__ words, int64_t pitch, int64_t width,
+                            int64_t rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t groups = (pitch + 31) / 32;  // 32-word groups per row
+  for (int64_t g = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+       g < rows * groups; g += nwarps) {
+    const int64_t r = g / groups;
+    const int64_t w0 = (g - r * groups) * 32;
+    const uint8_t* row = cells + r * cell_pitch;
+    uint32_t mine = 0;
+    for (int j = 0; j < 32; ++j) {
+      const int64_t col = (w0 + j) * 32 + lane;
+      const bool alive = col < width && row[col] != 0;
+      const uint32_t word = __ballot_sync(kFull, alive);
+      if (j == lane) mine = word;
+    }
+    if (w0 + lane < pitch) words[r * pitch + w0 + lane] = mine;
+  }
+}
+
+// Packed rows -> byte rows (one thread per 16 output bytes).
+__global__ void unpack_kernel(const uint32_t* __restrict__ words, int64_t pitch,
+                              uint8_t* __restrict__ cells, int64_t cell_pitch, int64_t width,
+                              int64_t rows) {
+  const int64_t nvec = cell_pitch / 16;
+  const int64_t n = rows * nvec;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / nvec;
+    const int64_t c0 = (t - r * nvec) * 16;
+    uint32_t bits = 0;
+    if (c0 < width) bits = (words[r * pitch + (c0 >> 5)] >> (c0 & 31)) & 0xffffu;
+    if (width - c0 < 16 && c0 < width) bits &= (1u << (width - c0)) - 1u;
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = (((bits >> (4 * i)) & 0xfu) * 0x00204081u) & 0x01010101u;
+    *reinterpret_cast<uint4*>(cells + r * cell_pitch + c0) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+__device__ __forceinline__ void block_add_u64(uint64_t v, unsigned long long* dst) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  __shared__ uint64_t part[32];
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) part[w] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (threadIdx.x == 0 && v) atomicAdd(dst, static_cast<unsigned long long>(v));
+  }
+}
+
+// population (grid.cpp:40-46) of packed rows; padding bits are zero.
+__global__ void packed_popcount_kernel(const uint32_t* __restrict__ words, int64_t pitch,
+                                       int32_t nw, int64_t rows, unsigned long long* count) {
+  uint64_t acc = 0;
+  const int64_t n = rows * pitch;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    acc += __popc(__ldg(words + t));
+  }
+  (void)nw;
+  block_add_u64(acc, count);
+}
+
+__global__ void byte_popcount_kernel(const uint8_t* __restrict__ cells, int64_t pitch,
+                                     int64_t rows, unsigned long long* count) {
+  uint64_t acc = 0;
+  const int64_t n = rows * pitch / 16;
+  const uint4* v = reinterpret_cast<const uint4*>(cells);
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint4 q = __ldg(v + t);
+    acc += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);  // bytes are 0/1
+  }
+  block_add_u64(acc, count);
+}
+
+// Wrapped window of a packed grid as 0/1 bytes.
+__global__ void packed_window_kernel(const uint32_t* __restrict__ words, int64_t pitch,
+                                     int64_t width, int64_t height, int64_t x0, int64_t y0,
+                                     int64_t w, int64_t h, uint8_t* __restrict__ out) {
+  const int64_t n = w * h;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = t / w, i = t - j * w;
+    int64_t y = (y0 + j) % height;
+    if (y < 0) y += height;
+    int64_t x = (x0 + i) % width;
+    if (x < 0) x += width;
+    out[t] = static_cast<uint8_t>((words[y * pitch + (x >> 5)] >> (x & 31)) & 1u);
+  }
+}
+
+__global__ void byte_window_kernel(const uint8_t* __restrict__ cells, int64_t pitch,
+                                   int64_t width, int64_t height, int64_t x0, int64_t y0,
+                                   int64_t w, int64_t h, uint8_t* __restrict__ out) {
+  const int64_t n = w * h;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = t / w, i = t - j * w;
+    int64_t y = (y0 + j) % height;
+    if (y < 0) y += height;
+    int64_t x = (x0 + i) % width;
+    if (x < 0) x += width;
+    out[t] = cells[y * pitch + x];
+  }
+}
+
+// Clears bits at columns >= W of packed rows (applied after uploads so the
+// zero-padding invariant holds whatever the host sent).
+__global__ void packed_mask_tail_kernel(uint32_t* __restrict__ words, int64_t pitch, int32_t nw,
+                                        uint32_t tail_mask, int64_t rows) {
+  const int64_t pad = pitch - nw + 1;  // word nw-1 plus the padding words
+  const int64_t n = rows * pad;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / pad;
+    const int64_t k = t - r * pad;
+    uint32_t* p = words + r * pitch + (nw - 1) + k;
+    *p = k == 0 ? (*p & tail_mask) : 0u;
+  }
+}
+
+// Byte upload normalisation: nonzero -> 1 (the 0/1 contract), padding -> 0.
+__global__ void byte_normalise_kernel(uint8_t* __restrict__ cells, int64_t pitch, int64_t width,
+                                      int64_t rows) {
+  const int64_t n = rows * pitch;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = t / pitch;
+    const int64_t c = t - r * pitch;
+    cells[t] = (c < width && cells[t] != 0) ? 1 : 0;
+  }
+}
+
+// Integer-pipe peak: 8 independent LOP3 chains per thread.
+__global__ void int_peak_kernel(uint32_t* sink, int64_t iters, uint32_t seed) {
+  uint32_t a = seed ^ threadIdx.x, b = a * 3u, c = a * 5u, d = a * 7u;
+  uint32_t e = a * 11u, f = a * 13u, g = a * 17u, h = a * 19u;
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      a = (a ^ b) ^ c;  b = (b & c) | d;  c = (c ^ d) ^ e;  d = (d & e) | f;
+      e = (e ^ f) ^ g;  f = (f & g) | h;  g = (g ^ h) ^ a;  h = (h & a) | b;
+    }
+  }
+  if ((a ^ b ^ c ^ d ^ e ^ f ^ g ^ h) == 0x12345678u) sink[0] = a;
+}
+
+}  // namespace lifegpu

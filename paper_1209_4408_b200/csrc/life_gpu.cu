@@ -1,0 +1,695 @@
+// life_gpu.cu -- C-ABI implementation (include/life_gpu.h): contexts, the
+// generation-step loop, layout conversion and the device-buffer layer.
+//
+// Build: paper_1209_4408_b200/build.py (nvcc -gencode arch=compute_100a,code=sm_100a).
+// There is no CPU fallback anywhere in this file: every entry point that
+// computes launches a kernel in kernels.cuh or fails with a status code.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/life_gpu.h"
+#include "kernels.cuh"
+
+using namespace lifegpu;
+
+namespace {
+
+thread_local std::string g_error;
+std::atomic<uint64_t> g_launches{0};
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  if (e == cudaErrorMemoryAllocation)
+    return set_error(LIFE_ERR_OUT_OF_MEMORY, "%s: %s", what, cudaGetErrorString(e));
+  return set_error(LIFE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define LIFE_CUDA(call)                                   \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+  } while (0)
+
+#define LIFE_CHECK_LAUNCH(name)                                    \
+  do {                                                             \
+    g_launches.fetch_add(1, std::memory_order_relaxed);            \
+    cudaError_t e_ = cudaGetLastError();                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, "launch " name);   \
+  } while (0)
+
+#define LIFE_TRY(expr)             \
+  do {                             \
+    int rc_ = (expr);              \
+    if (rc_ != LIFE_OK) return rc_; \
+  } while (0)
+
+int sm_count() {
+  int dev = 0, n = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+int grid_stride_blocks(int64_t n, int threads) {
+  const int64_t want = ceil_div(std::max<int64_t>(n, 1), threads);
+  return static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * 16));
+}
+
+int64_t nw32(int64_t width) { return ceil_div(width, 32); }
+
+uint32_t tail_mask(int64_t width) {
+  const int r = static_cast<int>(width & 31);
+  return r == 0 ? 0xffffffffu : ((1u << r) - 1u);
+}
+
+uint64_t density_threshold(double density) {
+  return static_cast<uint64_t>(std::ceil(density * 0x1.0p53));
+}
+
+// ---- packed temporal-blocked step: template dispatch on K ----------------
+template <int K>
+int launch_packed(PackedStepArgs a, cudaStream_t s) {
+  static int blocks_per_sm[64] = {0};  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (blocks_per_sm[dev & 63] == 0) {
+    int nb = 0;
+    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, packed_tb_kernel<K>,
+                                                            kPackedThreads, 0));
+    blocks_per_sm[dev & 63] = std::max(nb, 1);
+  }
+  const int64_t resident_warps =
+      static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kPackedThreads / 32) * sm_count();
+  // One wave: split rows so that n_strips * n_segs ~ resident warps, with
+  // segments at least 4K rows tall (vertical ghost overhead <= 2K/seg).
+  const int64_t segs_target = std::max<int64_t>(1, resident_warps / a.n_strips);
+  a.seg_rows = std::max<int64_t>(ceil_div(a.out_rows, segs_target), 4 * K);
+  const int64_t n_segs = ceil_div(a.out_rows, a.seg_rows);
+  const int64_t warps = n_segs * a.n_strips;
+  const int64_t blocks = ceil_div(warps, kPackedThreads / 32);
+  if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
+  packed_tb_kernel<K><<<static_cast<unsigned>(blocks), kPackedThreads, 0, s>>>(a);
+  LIFE_CHECK_LAUNCH("packed_tb_kernel");
+  return LIFE_OK;
+}
+
+using PackedLauncher = int (*)(PackedStepArgs, cudaStream_t);
+const PackedLauncher kPackedLaunchers[LIFE_MAX_TEMPORAL_DEPTH + 1] = {
+    nullptr,           launch_packed<1>,  launch_packed<2>,  launch_packed<3>,
+    launch_packed<4>,  launch_packed<5>,  launch_packed<6>,  launch_packed<7>,
+    launch_packed<8>,  launch_packed<9>,  launch_packed<10>, launch_packed<11>,
+    launch_packed<12>, launch_packed<13>, launch_packed<14>, launch_packed<15>,
+    launch_packed<16>};
+
+int check_dims(int64_t width, int64_t height) {
+  if (width < 3 || height < 3)
+    return set_error(LIFE_ERR_DIMENSION_TOO_SMALL,
+                     "grid dimensions must be at least 3x3, got %lldx%lld",
+                     static_cast<long long>(width), static_cast<long long>(height));
+  if (width > (int64_t(1) << 40) || height > (int64_t(1) << 40))
+    return set_error(LIFE_ERR_CONFIG, "grid dimensions too large");
+  return LIFE_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// Device-buffer layer
+// ===========================================================================
+extern "C" {
+
+const char* life_last_error(void) { return g_error.c_str(); }
+const char* life_version(void) { return "life-b200 0.1 (sm_100a)"; }
+uint64_t life_kernel_launches(void) { return g_launches.load(); }
+
+int64_t life_packed_pitch_words(int64_t width) {
+  return ceil_div(2 * ceil_div(width, 64), 32) * 32;
+}
+
+int64_t life_byte_pitch(int64_t width) { return ceil_div(width, 128) * 128; }
+
+int life_band_bounds(int64_t extent, int32_t parts, int64_t* bounds) {
+  if (parts < 1 || parts > extent)
+    return set_error(LIFE_ERR_TOO_MANY_PARTS, "cannot split %lld rows into %d non-empty parts",
+                     static_cast<long long>(extent), parts);
+  const int64_t base = extent / parts, extra = extent % parts;
+  int64_t at = 0;
+  bounds[0] = 0;
+  for (int32_t i = 0; i < parts; ++i) {
+    at += base + (i < extra ? 1 : 0);
+    bounds[i + 1] = at;
+  }
+  return LIFE_OK;
+}
+
+int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                         uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                         int64_t out_rows, int32_t generations, void* stream) {
+  if (generations < 1 || generations > LIFE_MAX_TEMPORAL_DEPTH)
+    return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [1, %d], got %d",
+                     LIFE_MAX_TEMPORAL_DEPTH, generations);
+  if (width < 1 || in_rows < 1 || out_rows < 0 || in_pitch < 2 * ceil_div(width, 64) ||
+      out_pitch < 2 * ceil_div(width, 64))
+    return set_error(LIFE_ERR_CONFIG, "bad packed step geometry");
+  if (out_rows == 0) return LIFE_OK;
+  PackedStepArgs a{};
+  a.in = in;
+  a.in_pitch = in_pitch;
+  a.in_row0 = in_row0;
+  a.in_rows = in_rows;
+  a.out = out;
+  a.out_pitch = out_pitch;
+  a.out_row0 = out_row0;
+  a.width = width;
+  a.out_rows = out_rows;
+  a.nw = static_cast<int32_t>(nw32(width));
+  a.n_strips = static_cast<int32_t>(ceil_div(a.nw, kStripWords));
+  a.tail_mask = tail_mask(width);
+  return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
+}
+
+int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                       uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                       int64_t out_rows, void* stream) {
+  if (width < 1 || in_rows < 1 || out_rows < 0 || in_pitch < ceil_div(width, 16) * 16 ||
+      out_pitch < ceil_div(width, 16) * 16 || (in_pitch & 15) || (out_pitch & 15))
+    return set_error(LIFE_ERR_CONFIG, "bad byte step geometry");
+  if (out_rows == 0) return LIFE_OK;
+  static int blocks_per_sm[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (blocks_per_sm[dev & 63] == 0) {
+    int nb = 0;
+    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, byte_step_kernel,
+                                                            kByteThreads, 0));
+    blocks_per_sm[dev & 63] = std::max(nb, 1);
+  }
+  ByteStepArgs a{};
+  a.in = in;
+  a.in_pitch = in_pitch;
+  a.in_row0 = in_row0;
+  a.in_rows = in_rows;
+  a.out = out;
+  a.out_pitch = out_pitch;
+  a.out_row0 = out_row0;
+  a.width = width;
+  a.out_rows = out_rows;
+  a.nv = static_cast<int32_t>(ceil_div(width, 16));
+  a.n_strips = static_cast<int32_t>(ceil_div(a.nv, 32));
+  const int64_t resident_warps =
+      static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kByteThreads / 32) * sm_count();
+  // Two waves of warps, segments >= 32 rows (halo re-read <= 2/32).
+  const int64_t segs_target = std::max<int64_t>(1, 2 * resident_warps / a.n_strips);
+  a.seg_rows = std::max<int64_t>(ceil_div(out_rows, segs_target), 32);
+  const int64_t warps = ceil_div(out_rows, a.seg_rows) * a.n_strips;
+  const int64_t blocks = ceil_div(warps, kByteThreads / 32);
+  byte_step_kernel<<<static_cast<unsigned>(blocks), kByteThreads, 0,
+                     static_cast<cudaStream_t>(stream)>>>(a);
+  LIFE_CHECK_LAUNCH("byte_step_kernel");
+  return LIFE_OK;
+}
+
+int life_dev_packed_random(uint32_t* out, int64_t pitch, int64_t width, int64_t y0, int64_t rows,
+                           double density, uint64_t seed, void* stream) {
+  if (!(density >= 0.0 && density <= 1.0))
+    return set_error(LIFE_ERR_CONFIG, "density must be in [0, 1], got %f", density);
+  const int64_t n = rows * pitch;
+  packed_random_kernel<<<grid_stride_blocks(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      out, pitch, width, y0, rows, static_cast<int32_t>(nw32(width)), seed,
+      density_threshold(density));
+  LIFE_CHECK_LAUNCH("packed_random_kernel");
+  return LIFE_OK;
+}
+
+int life_dev_packed_population(const uint32_t* grid, int64_t pitch, int64_t width, int64_t rows,
+                               uint64_t* dev_count, void* stream) {
+  const int64_t n = rows * pitch;
+  packed_popcount_kernel<<<grid_stride_blocks(n / 4, 256), 256, 0,
+                           static_cast<cudaStream_t>(stream)>>>(
+      grid, pitch, static_cast<int32_t>(nw32(width)), rows,
+      reinterpret_cast<unsigned long long*>(dev_count));
+  LIFE_CHECK_LAUNCH("packed_popcount_kernel");
+  return LIFE_OK;
+}
+
+int life_dev_pack(const uint8_t* cells, int64_t cell_pitch, uint32_t* words, int64_t pitch,
+                  int64_t width, int64_t rows, void* stream) {
+  const int64_t warps = rows * ceil_div(pitch, 32);
+  pack_kernel<<<grid_stride_blocks(warps * 32, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      cells, cell_pitch, words, pitch, width, rows);
+  LIFE_CHECK_LAUNCH("pack_kernel");
+  return LIFE_OK;
+}
+
+int life_dev_unpack(const uint32_t* words, int64_t pitch, uint8_t* cells, int64_t cell_pitch,
+                    int64_t width, int64_t rows, void* stream) {
+  if (cell_pitch & 15) return set_error(LIFE_ERR_CONFIG, "byte pitch must be a multiple of 16");
+  const int64_t n = rows * (cell_pitch / 16);
+  unpack_kernel<<<grid_stride_blocks(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      words, pitch, cells, cell_pitch, width, rows);
+  LIFE_CHECK_LAUNCH("unpack_kernel");
+  return LIFE_OK;
+}
+
+int life_measure_int_peak(int device, int64_t iters, double* ops_per_s, double* seconds) {
+  LIFE_CUDA(cudaSetDevice(device));
+  uint32_t* sink = nullptr;
+  LIFE_CUDA(cudaMalloc(&sink, 4));
+  cudaEvent_t e0, e1;
+  LIFE_CUDA(cudaEventCreate(&e0));
+  LIFE_CUDA(cudaEventCreate(&e1));
+  const int blocks = sm_count() * 8, threads = 256;
+  int_peak_kernel<<<blocks, threads>>>(sink, std::max<int64_t>(iters / 8, 1), 1u);  // warm-up
+  LIFE_CHECK_LAUNCH("int_peak_kernel");
+  LIFE_CUDA(cudaEventRecord(e0));
+  int_peak_kernel<<<blocks, threads>>>(sink, iters, 2u);
+  LIFE_CHECK_LAUNCH("int_peak_kernel");
+  LIFE_CUDA(cudaEventRecord(e1));
+  LIFE_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  LIFE_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  const double ops = double(blocks) * threads * double(iters) * 16.0 * 8.0;
+  *seconds = ms * 1e-3;
+  *ops_per_s = ops / (ms * 1e-3);
+  return LIFE_OK;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Contexts: one resident grid on one GPU, the reference's run() on top.
+// ===========================================================================
+enum Layout { kNone = -1, kPacked = LIFE_ENGINE_PACKED, kByte = LIFE_ENGINE_BYTE };
+
+struct life_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int64_t W = 0, H = 0;
+  int layout = kNone;
+  uint32_t* pk[2] = {nullptr, nullptr};
+  int64_t pk_pitch = 0;  // uint32 words
+  int pk_cur = 0;
+  uint8_t* by[2] = {nullptr, nullptr};
+  int64_t by_pitch = 0;  // bytes
+  int by_cur = 0;
+  unsigned long long* counts = nullptr;
+  int64_t counts_cap = 0;
+  uint8_t* window = nullptr;
+  int64_t window_cap = 0;
+};
+
+namespace {
+
+int activate(life_ctx* c) {
+  if (!c) return set_error(LIFE_ERR_STATE, "null context");
+  LIFE_CUDA(cudaSetDevice(c->device));
+  return LIFE_OK;
+}
+
+void free_buffers(life_ctx* c) {
+  for (int i = 0; i < 2; ++i) {
+    if (c->pk[i]) cudaFree(c->pk[i]);
+    if (c->by[i]) cudaFree(c->by[i]);
+    c->pk[i] = nullptr;
+    c->by[i] = nullptr;
+  }
+  c->layout = kNone;
+}
+
+int set_dims(life_ctx* c, int64_t w, int64_t h) {
+  LIFE_TRY(check_dims(w, h));
+  if (w != c->W || h != c->H) {
+    LIFE_CUDA(cudaStreamSynchronize(c->stream));
+    free_buffers(c);
+    c->W = w;
+    c->H = h;
+    c->pk_pitch = life_packed_pitch_words(w);
+    c->by_pitch = life_byte_pitch(w);
+  }
+  return LIFE_OK;
+}
+
+int ensure_packed(life_ctx* c) {
+  for (int i = 0; i < 2; ++i) {
+    if (!c->pk[i]) {
+      const size_t bytes = static_cast<size_t>(c->pk_pitch) * c->H * 4;
+      LIFE_CUDA(cudaMalloc(&c->pk[i], bytes));
+      LIFE_CUDA(cudaMemsetAsync(c->pk[i], 0, bytes, c->stream));
+    }
+  }
+  return LIFE_OK;
+}
+
+int ensure_byte(life_ctx* c) {
+  for (int i = 0; i < 2; ++i) {
+    if (!c->by[i]) {
+      const size_t bytes = static_cast<size_t>(c->by_pitch) * c->H;
+      LIFE_CUDA(cudaMalloc(&c->by[i], bytes));
+      LIFE_CUDA(cudaMemsetAsync(c->by[i], 0, bytes, c->stream));
+    }
+  }
+  return LIFE_OK;
+}
+
+int ensure_counts(life_ctx* c, int64_t n) {
+  if (n > c->counts_cap) {
+    if (c->counts) cudaFree(c->counts);
+    c->counts = nullptr;
+    LIFE_CUDA(cudaMalloc(&c->counts, sizeof(unsigned long long) * n));
+    c->counts_cap = n;
+  }
+  return LIFE_OK;
+}
+
+// Converts the resident grid to `layout` (device-side pack / unpack).
+int to_layout(life_ctx* c, int layout) {
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  if (c->layout == layout) return LIFE_OK;
+  if (layout == kPacked) {
+    LIFE_TRY(ensure_packed(c));
+    LIFE_TRY(life_dev_pack(c->by[c->by_cur], c->by_pitch, c->pk[0], c->pk_pitch, c->W, c->H,
+                           c->stream));
+    c->pk_cur = 0;
+  } else {
+    LIFE_TRY(ensure_byte(c));
+    LIFE_TRY(life_dev_unpack(c->pk[c->pk_cur], c->pk_pitch, c->by[0], c->by_pitch, c->W, c->H,
+                             c->stream));
+    c->by_cur = 0;
+  }
+  c->layout = layout;
+  return LIFE_OK;
+}
+
+int population_async(life_ctx* c, unsigned long long* slot) {
+  LIFE_CUDA(cudaMemsetAsync(slot, 0, sizeof(unsigned long long), c->stream));
+  if (c->layout == kPacked) {
+    return life_dev_packed_population(c->pk[c->pk_cur], c->pk_pitch, c->W, c->H,
+                                      reinterpret_cast<uint64_t*>(slot), c->stream);
+  }
+  const int64_t n = c->H * c->by_pitch / 16;
+  byte_popcount_kernel<<<grid_stride_blocks(n / 4, 256), 256, 0, c->stream>>>(
+      c->by[c->by_cur], c->by_pitch, c->H, slot);
+  LIFE_CHECK_LAUNCH("byte_popcount_kernel");
+  return LIFE_OK;
+}
+
+int check_engine(int engine) {
+  if (engine != LIFE_ENGINE_PACKED && engine != LIFE_ENGINE_BYTE)
+    return set_error(LIFE_ERR_CONFIG, "unknown engine %d", engine);
+  return LIFE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int life_ctx_create(int device, life_ctx** out) {
+  if (!out) return set_error(LIFE_ERR_CONFIG, "null output pointer");
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    return set_error(LIFE_ERR_NO_DEVICE, "no CUDA device available (%s)",
+                     e == cudaSuccess ? "count 0" : cudaGetErrorString(e));
+  if (device < 0 || device >= n)
+    return set_error(LIFE_ERR_NO_DEVICE, "device %d out of range [0, %d)", device, n);
+  LIFE_CUDA(cudaSetDevice(device));
+  life_ctx* c = new life_ctx();
+  c->device = device;
+  e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return cuda_fail(e, "cudaStreamCreate");
+  }
+  c->stream = c->own;
+  *out = c;
+  return LIFE_OK;
+}
+
+int life_ctx_destroy(life_ctx* c) {
+  if (!c) return LIFE_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  free_buffers(c);
+  if (c->counts) cudaFree(c->counts);
+  if (c->window) cudaFree(c->window);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return LIFE_OK;
+}
+
+int life_ctx_set_stream(life_ctx* c, void* stream) {
+  LIFE_TRY(activate(c));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+  return LIFE_OK;
+}
+
+int life_ctx_sync(life_ctx* c) {
+  LIFE_TRY(activate(c));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_grid_dims(life_ctx* c, int64_t* w, int64_t* h) {
+  if (!c) return set_error(LIFE_ERR_STATE, "null context");
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  *w = c->W;
+  *h = c->H;
+  return LIFE_OK;
+}
+
+int life_grid_upload_u8(life_ctx* c, const uint8_t* cells, int64_t width, int64_t height,
+                        int64_t row_stride) {
+  LIFE_TRY(activate(c));
+  if (!cells) return set_error(LIFE_ERR_CONFIG, "null cell buffer");
+  LIFE_TRY(set_dims(c, width, height));
+  if (row_stride < width) return set_error(LIFE_ERR_CONFIG, "row_stride < width");
+  LIFE_TRY(ensure_byte(c));
+  c->by_cur = 0;
+  LIFE_CUDA(cudaMemcpy2DAsync(c->by[0], c->by_pitch, cells, row_stride, width, height,
+                              cudaMemcpyHostToDevice, c->stream));
+  const int64_t n = c->H * c->by_pitch;
+  byte_normalise_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(c->by[0], c->by_pitch,
+                                                                           width, height);
+  LIFE_CHECK_LAUNCH("byte_normalise_kernel");
+  c->layout = kByte;
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_grid_upload_packed(life_ctx* c, const uint64_t* words, int64_t width, int64_t height,
+                            int64_t words_per_row) {
+  LIFE_TRY(activate(c));
+  if (!words) return set_error(LIFE_ERR_CONFIG, "null word buffer");
+  LIFE_TRY(set_dims(c, width, height));
+  const int64_t wpr = ceil_div(width, 64);
+  if (words_per_row < wpr) return set_error(LIFE_ERR_CONFIG, "words_per_row < ceil(W/64)");
+  LIFE_TRY(ensure_packed(c));
+  c->pk_cur = 0;
+  LIFE_CUDA(cudaMemcpy2DAsync(c->pk[0], c->pk_pitch * 4, words, words_per_row * 8, wpr * 8,
+                              height, cudaMemcpyHostToDevice, c->stream));
+  const int32_t nw = static_cast<int32_t>(nw32(width));
+  const int64_t n = height * (c->pk_pitch - nw + 1);
+  packed_mask_tail_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(
+      c->pk[0], c->pk_pitch, nw, tail_mask(width), height);
+  LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
+  c->layout = kPacked;
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_grid_init_random(life_ctx* c, int64_t width, int64_t height, double density,
+                          uint64_t seed, int engine) {
+  LIFE_TRY(activate(c));
+  LIFE_TRY(check_engine(engine));
+  if (!(density >= 0.0 && density <= 1.0))
+    return set_error(LIFE_ERR_CONFIG, "density must be in [0, 1], got %f", density);
+  LIFE_TRY(set_dims(c, width, height));
+  if (engine == LIFE_ENGINE_PACKED) {
+    LIFE_TRY(ensure_packed(c));
+    c->pk_cur = 0;
+    LIFE_TRY(life_dev_packed_random(c->pk[0], c->pk_pitch, width, 0, height, density, seed,
+                                    c->stream));
+    c->layout = kPacked;
+  } else {
+    LIFE_TRY(ensure_byte(c));
+    c->by_cur = 0;
+    const int64_t n = height * (c->by_pitch / 16);
+    byte_random_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(
+        c->by[0], c->by_pitch, width, 0, height, seed, density_threshold(density));
+    LIFE_CHECK_LAUNCH("byte_random_kernel");
+    c->layout = kByte;
+  }
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_grid_download_u8(life_ctx* c, uint8_t* cells, int64_t row_stride) {
+  LIFE_TRY(activate(c));
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  if (!cells || row_stride < c->W) return set_error(LIFE_ERR_CONFIG, "bad output buffer");
+  const uint8_t* src;
+  if (c->layout == kByte) {
+    src = c->by[c->by_cur];
+  } else {  // unpack into the (free) byte buffer
+    LIFE_TRY(ensure_byte(c));
+    LIFE_TRY(life_dev_unpack(c->pk[c->pk_cur], c->pk_pitch, c->by[0], c->by_pitch, c->W, c->H,
+                             c->stream));
+    src = c->by[0];
+  }
+  LIFE_CUDA(cudaMemcpy2DAsync(cells, row_stride, src, c->by_pitch, c->W, c->H,
+                              cudaMemcpyDeviceToHost, c->stream));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_grid_download_packed(life_ctx* c, uint64_t* words, int64_t words_per_row) {
+  LIFE_TRY(activate(c));
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  const int64_t wpr = ceil_div(c->W, 64);
+  if (!words || words_per_row < wpr) return set_error(LIFE_ERR_CONFIG, "bad output buffer");
+  const uint32_t* src;
+  if (c->layout == kPacked) {
+    src = c->pk[c->pk_cur];
+  } else {  // pack into the (free) packed buffer
+    LIFE_TRY(ensure_packed(c));
+    LIFE_TRY(life_dev_pack(c->by[c->by_cur], c->by_pitch, c->pk[0], c->pk_pitch, c->W, c->H,
+                           c->stream));
+    src = c->pk[0];
+  }
+  LIFE_CUDA(cudaMemcpy2DAsync(words, words_per_row * 8, src, c->pk_pitch * 4, wpr * 8, c->H,
+                              cudaMemcpyDeviceToHost, c->stream));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_grid_window_u8(life_ctx* c, int64_t x0, int64_t y0, int64_t w, int64_t h, uint8_t* out) {
+  LIFE_TRY(activate(c));
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  if (w < 0 || h < 0 || !out) return set_error(LIFE_ERR_CONFIG, "bad window");
+  const int64_t n = w * h;
+  if (n == 0) return LIFE_OK;
+  if (n > c->window_cap) {
+    if (c->window) cudaFree(c->window);
+    c->window = nullptr;
+    LIFE_CUDA(cudaMalloc(&c->window, n));
+    c->window_cap = n;
+  }
+  if (c->layout == kPacked) {
+    packed_window_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(
+        c->pk[c->pk_cur], c->pk_pitch, c->W, c->H, x0, y0, w, h, c->window);
+  } else {
+    byte_window_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(
+        c->by[c->by_cur], c->by_pitch, c->W, c->H, x0, y0, w, h, c->window);
+  }
+  LIFE_CHECK_LAUNCH("window_kernel");
+  LIFE_CUDA(cudaMemcpyAsync(out, c->window, n, cudaMemcpyDeviceToHost, c->stream));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_population(life_ctx* c, uint64_t* out) {
+  LIFE_TRY(activate(c));
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  LIFE_TRY(ensure_counts(c, 1));
+  LIFE_TRY(population_async(c, c->counts));
+  LIFE_CUDA(cudaMemcpyAsync(out, c->counts, 8, cudaMemcpyDeviceToHost, c->stream));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
+             const int64_t* checkpoints, int32_t n_checkpoints, uint64_t* populations) {
+  LIFE_TRY(activate(c));
+  LIFE_TRY(check_engine(engine));
+  // check_run_config (engine.cpp:127-148)
+  if (generations < 0)
+    return set_error(LIFE_ERR_CONFIG, "iteration count must be non-negative, got %lld",
+                     static_cast<long long>(generations));
+  if (n_checkpoints < 0 || (n_checkpoints > 0 && (!checkpoints || !populations)))
+    return set_error(LIFE_ERR_CONFIG, "bad checkpoint buffers");
+  int64_t prev = -1;
+  for (int32_t i = 0; i < n_checkpoints; ++i) {
+    const int64_t cp = checkpoints[i];
+    if (cp < 0 || cp > generations)
+      return set_error(LIFE_ERR_CONFIG, "checkpoint %lld is outside [0, iterations=%lld]",
+                       static_cast<long long>(cp), static_cast<long long>(generations));
+    if (cp <= prev) return set_error(LIFE_ERR_CONFIG, "checkpoints must be strictly ascending");
+    prev = cp;
+  }
+  int depth = temporal_depth;
+  if (engine == LIFE_ENGINE_PACKED) {
+    if (depth == 0) depth = LIFE_MAX_TEMPORAL_DEPTH;
+    if (depth < 1 || depth > LIFE_MAX_TEMPORAL_DEPTH)
+      return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [0, %d], got %d",
+                       LIFE_MAX_TEMPORAL_DEPTH, temporal_depth);
+  } else {
+    if (depth != 0 && depth != 1)
+      return set_error(LIFE_ERR_CONFIG, "the byte engine runs one generation per pass (depth 0/1)");
+    depth = 1;
+  }
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  LIFE_TRY(to_layout(c, engine));
+  if (n_checkpoints > 0) LIFE_TRY(ensure_counts(c, n_checkpoints));
+
+  int32_t ci = 0;
+  auto record = [&](int64_t gen) -> int {
+    while (ci < n_checkpoints && checkpoints[ci] == gen) {
+      LIFE_TRY(population_async(c, c->counts + ci));
+      ++ci;
+    }
+    return LIFE_OK;
+  };
+  LIFE_TRY(record(0));
+  int64_t done = 0;
+  while (done < generations) {
+    const int64_t stop = ci < n_checkpoints ? checkpoints[ci] : generations;
+    const int step = static_cast<int>(std::min<int64_t>(depth, stop - done));
+    if (engine == LIFE_ENGINE_PACKED) {
+      const int nxt = c->pk_cur ^ 1;
+      LIFE_TRY(life_dev_packed_step(c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt],
+                                    c->pk_pitch, 0, c->W, c->H, step, c->stream));
+      c->pk_cur = nxt;
+    } else {
+      const int nxt = c->by_cur ^ 1;
+      LIFE_TRY(life_dev_byte_step(c->by[c->by_cur], c->by_pitch, 0, c->H, c->by[nxt],
+                                  c->by_pitch, 0, c->W, c->H, c->stream));
+      c->by_cur = nxt;
+    }
+    done += step;
+    LIFE_TRY(record(done));
+  }
+  if (n_checkpoints > 0) {
+    LIFE_CUDA(cudaMemcpyAsync(populations, c->counts, sizeof(uint64_t) * n_checkpoints,
+                              cudaMemcpyDeviceToHost, c->stream));
+  }
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_step(life_ctx* c, int engine) { return life_run(c, 1, engine, 1, nullptr, 0, nullptr); }
+
+}  // extern "C"

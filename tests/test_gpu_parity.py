@@ -1,0 +1,247 @@
+"""GPU parity: the CUDA engine through the C-ABI vs the oracle and the
+reference-generated golden fixtures.  Bit-exact (integer work).
+
+Run on a B200:  python -m pytest tests -m gpu -x -q
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+PACKED, BYTE = 0, 1
+
+
+def fnv(oracle, a) -> str:
+    return f"{oracle.fnv1a64(np.ascontiguousarray(a)):016x}"
+
+
+def test_random_fill_on_device_matches_oracle(engine, oracle):
+    for (w, h, p, s) in [(3, 3, 0.5, 1), (31, 7, 0.3, 2), (64, 5, 0.5, 3), (65, 9, 0.7, 4),
+                         (1000, 37, 0.3, 5), (40961, 3, 0.02, 6), (97, 61, 0.0, 7),
+                         (97, 61, 1.0, 8)]:
+        want = oracle.random_fill(w, h, p, s)
+        for eng in (PACKED, BYTE):
+            engine.init_random(w, h, p, s, eng)
+            assert np.array_equal(engine.download(), want), (w, h, p, s, eng)
+            assert engine.population() == int(want.sum())
+
+
+def test_upload_download_roundtrip_and_nonbinary_contract(engine, oracle):
+    rng = np.random.default_rng(3)
+    for (w, h) in [(3, 3), (17, 5), (33, 40), (129, 7), (1000, 13)]:
+        g = rng.integers(0, 4, (h, w), dtype=np.uint8)  # nonzero bytes count as alive
+        engine.upload(g)
+        assert np.array_equal(engine.download(), (g != 0).astype(np.uint8))
+        packed = engine.download_packed()
+        assert np.array_equal(packed, oracle.pack(g != 0))
+        engine.upload_packed(packed, w)
+        assert np.array_equal(engine.download(), (g != 0).astype(np.uint8))
+        # one step from a non-0/1 upload = step_serial semantics
+        engine.upload(g)
+        engine.step(BYTE)
+        assert np.array_equal(engine.download(), oracle.step_serial(g))
+
+
+def test_packed_upload_ignores_tail_bits(engine, oracle):
+    g = oracle.random_fill(70, 9, 0.5, 1)
+    p = oracle.pack(g)
+    p[:, -1] |= np.uint64(0xFFFFFFFF) << np.uint64(32)  # garbage past column 70
+    engine.upload_packed(p, 70)
+    assert np.array_equal(engine.download(), g)
+    engine.run(5, PACKED, 3)
+    want, _ = oracle.run(g, 5)
+    assert np.array_equal(engine.download(), want)
+
+
+@pytest.mark.parametrize("eng,depth", [(PACKED, 1), (PACKED, 4), (PACKED, 7), (PACKED, 16),
+                                       (BYTE, 1)])
+def test_small_golden_cases(engine, oracle, golden_small, eng, depth):
+    for case in golden_small["small_cases"]:
+        engine.init_random(case["w"], case["h"], case["density"], case["seed"], eng)
+        pops = engine.run(case["gens"], eng, depth, [0, case["gens"]] if case["gens"] else [0])
+        got = engine.download()
+        assert fnv(oracle, got) == case["final"]["fnv_bytes"], (case, eng, depth)
+        assert pops[-1] == case["final"]["population"]
+        assert pops[0] == case["initial"]["population"]
+
+
+def test_cfg1_full_grid_at_1_10_100(engine, oracle, golden_small):
+    cfg1 = golden_small["cfg1"]
+    for eng, depth in [(PACKED, 16), (PACKED, 5), (BYTE, 1)]:
+        engine.init_random(1024, 1024, 0.5, 42, eng)
+        pops = engine.run(100, eng, depth, [0, 1, 10, 100])
+        assert pops == [524027, 286720, 211733, 98161]
+        assert fnv(oracle, engine.download()) == "37b6d88ff40a4f22"
+        for g in (1, 10, 100):
+            engine.init_random(1024, 1024, 0.5, 42, eng)
+            engine.run(g, eng, depth)
+            out = engine.download()
+            assert fnv(oracle, out) == cfg1[str(g)]["fnv_bytes"]
+            assert fnv(oracle, engine.download_packed()) == cfg1[str(g)]["fnv_packed"]
+
+
+def test_known_patterns(engine):
+    from paper_1209_4408_b200 import life
+    blinker = np.zeros((5, 5), np.uint8)
+    blinker[2, 1:4] = 1
+    block = np.zeros((6, 6), np.uint8)
+    block[2:4, 2:4] = 1
+    glider = np.zeros((16, 16), np.uint8)
+    for (x, y) in [(1, 0), (2, 1), (0, 2), (1, 2), (2, 2)]:
+        glider[6 + y, 6 + x] = 1
+    for strat in (life.Strategy.gpu_packed(), life.Strategy.gpu_packed(3), life.Strategy.gpu_byte()):
+        g = life.Grid.from_array(blinker)
+        one = life.step_parallel(g, strat)
+        assert one != g and life.step_parallel(one, strat) == g
+        r = life.run(g, life.RunConfig(strat, 1, 100), [1, 2, 100])
+        assert r.stats.population_checkpoints == [(1, 3), (2, 3), (100, 3)]
+        assert r.grid == g
+        b = life.Grid.from_array(block)
+        assert life.run(b, life.RunConfig(strat, 1, 100)).grid == b
+        gl = life.Grid.from_array(glider)
+        for cycle in (1, 5, 16):
+            got = life.run(gl, life.RunConfig(strat, 1, 4 * cycle)).grid
+            assert np.array_equal(got.cells, np.roll(np.roll(glider, cycle, 0), cycle, 1))
+
+
+def test_translation_commutes(engine, oracle):
+    for seed in range(3):
+        g = oracle.random_fill(133, 71, 0.3, seed)
+        for (dx, dy) in [(1, 0), (0, 1), (3, 5), (-2, 4), (11, -7), (64, 33)]:
+            t = np.roll(np.roll(g, dy, 0), dx, 1)
+            engine.upload(t)
+            engine.run(7, PACKED, 7)
+            a = engine.download()
+            engine.upload(g)
+            engine.run(7, PACKED, 7)
+            b = np.roll(np.roll(engine.download(), dy, 0), dx, 1)
+            assert np.array_equal(a, b)
+
+
+def test_depth_transparency_sweep(engine, oracle):
+    # "strategy transparency" (test_engine.cpp:49-83) -> every temporal depth
+    # and both engines give the same grid.
+    for seed in range(4):
+        w = 3 + (seed * 17 + 5) % 46 + seed * 37
+        h = 3 + (seed * 29 + 11) % 46
+        g = oracle.random_fill(w, h, 0.3, seed)
+        want, _ = oracle.run(g, 41)
+        for depth in range(1, 17):
+            engine.upload(g)
+            engine.run(41, PACKED, depth)
+            assert np.array_equal(engine.download(), want), (seed, depth)
+        engine.upload(g)
+        engine.run(41, BYTE, 1)
+        assert np.array_equal(engine.download(), want)
+
+
+def test_checkpoints_split_passes(engine, oracle):
+    g = oracle.random_fill(200, 150, 0.4, 9)
+    cps = [0, 1, 3, 17, 18, 40, 64]
+    _, want = oracle.run(g, 64, cps)
+    for depth in (1, 4, 16):
+        engine.upload(g)
+        assert engine.run(64, PACKED, depth, cps) == want
+
+
+def test_run_config_errors(engine):
+    from paper_1209_4408_b200 import life
+    g = life.Grid(8, 5)
+    with pytest.raises(life.TooManyParts):
+        life.run(g, life.RunConfig(life.Strategy.gpu_packed(), 10, 1))
+    with pytest.raises(life.ConfigError):
+        life.run(g, life.RunConfig(life.Strategy.gpu_packed(), 0, 1))
+    with pytest.raises(life.ConfigError):
+        life.run(g, life.RunConfig(life.Strategy.gpu_packed(), 1, -1))
+    with pytest.raises(life.ConfigError):
+        life.run(g, life.RunConfig(life.Strategy.gpu_packed(), 1, 2), [2, 1])
+    with pytest.raises(life.ConfigError):
+        life.run(g, life.RunConfig(life.Strategy.gpu_packed(), 1, 2), [3])
+    with pytest.raises(life.DimensionTooSmall):
+        engine.init_random(2, 5, 0.5, 1)
+    with pytest.raises(life.ConfigError):
+        engine.init_random(5, 5, 1.5, 1)
+    engine.init_random(5, 5, 0.5, 1)
+    with pytest.raises(life.ConfigError):
+        engine.run(3, BYTE, 4)
+    with pytest.raises(life.ConfigError):
+        engine.run(3, PACKED, 17)
+    r = life.run(g, life.RunConfig(life.Strategy.gpu_packed(), 1, 0), [0])
+    assert r.grid == g and r.stats.generations_computed == 0
+
+
+def test_windows_wrap(engine, oracle):
+    g = oracle.random_fill(300, 200, 0.5, 4)
+    for eng in (PACKED, BYTE):
+        engine.upload(g)
+        if eng == PACKED:
+            engine.run(0, PACKED)
+        for (x0, y0, w, h) in [(0, 0, 300, 200), (-7, -9, 40, 30), (290, 195, 33, 17),
+                               (-1000, 1000, 5, 5)]:
+            ys = (np.arange(h) + y0) % 200
+            xs = (np.arange(w) + x0) % 300
+            assert np.array_equal(engine.window(x0, y0, w, h), g[np.ix_(ys, xs)])
+
+
+# ---- BASELINE.json configs ----------------------------------------------
+
+def _check_schedule(engine, oracle, gold, eng, depth, init):
+    init()
+    done = 0
+    for gen in sorted(int(k) for k in gold["gens"]):
+        engine.run(gen - done, eng, depth)
+        done = gen
+        want = gold["gens"][str(gen)]
+        assert fnv(oracle, engine.download_packed()) == want["fnv_packed"], (eng, depth, gen)
+        assert engine.population() == want["population"]
+
+
+@pytest.mark.slow
+def test_cfg2_16384_1000_generations(engine, oracle):
+    gold = load_golden("golden_cfg2.json")
+    for eng, depth in [(BYTE, 1), (PACKED, 16), (PACKED, 8)]:
+        _check_schedule(engine, oracle, gold, eng, depth,
+                        lambda: engine.init_random(16384, 16384, 0.3, 42, eng))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("depth", [1, 4, 8, 16])
+def test_cfg3_65536_packed_depths(engine, oracle, depth):
+    gold = load_golden("golden_cfg3.json")
+    _check_schedule(engine, oracle, gold, PACKED, depth,
+                    lambda: engine.init_random(65536, 65536, 0.5, 42, PACKED))
+
+
+@pytest.mark.slow
+def test_cfg3_windows(engine, oracle):
+    gold = load_golden("golden_cfg3_windows.json")
+    engine.init_random(65536, 65536, 0.5, 42, PACKED)
+    engine.run(100, PACKED, 16)
+    for w in gold["windows_100"]:
+        got = engine.window(w["x0"], w["y0"], w["S"], w["S"])
+        assert fnv(oracle, got) == w["fnv_bytes"], w
+
+
+@pytest.mark.slow
+def test_cfg4_nonpow2_sparse_soup(engine, oracle):
+    gold = load_golden("golden_cfg4.json")
+    soup = oracle.sparse_soup(40961, 12289, seed=42)
+    for eng, depth in [(BYTE, 1), (PACKED, 16)]:
+        _check_schedule(engine, oracle, gold, eng, depth, lambda: engine.upload(soup))
+
+
+@pytest.mark.slow
+def test_cfg5_lightcone_windows(engine, oracle):
+    gold = load_golden("golden_cfg5_windows.json")
+    W = H = 262144
+    engine.init_random(W, H, 0.4, 42, PACKED)
+    engine.run(16, PACKED, 16)
+    for w in gold["windows_16"]:
+        assert fnv(oracle, engine.window(w["x0"], w["y0"], w["S"], w["S"])) == w["fnv_bytes"]
+    engine.run(500 - 16, PACKED, 16)
+    for w in gold["windows_500"]:
+        assert fnv(oracle, engine.window(w["x0"], w["y0"], w["S"], w["S"])) == w["fnv_bytes"], w

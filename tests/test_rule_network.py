@@ -1,0 +1,134 @@
+"""CPU checks of the packed engine's ALGORITHM (not the CUDA code): the
+12-op bit-sliced B3/S23 network of csrc/kernels.cuh verified exhaustively
+against next_state (grid.cpp:22-28), and a lane-exact numpy model of
+packed_tb_kernel (strips of 32 lanes with ghost lanes 0/31, shuffle edge
+semantics, wrapped word loads, segmented K-stage row pipeline) checked
+against the oracle.  The GPU parity tests then pin the CUDA code itself."""
+from __future__ import annotations
+
+import itertools
+
+import numpy as np
+import pytest
+
+M32 = np.uint32(0xFFFFFFFF)
+
+
+def maj(a, b, c):
+    return (a & b) | (a & c) | (b & c)
+
+
+def hsum(xl, x, xr):
+    L = ((x << np.uint32(1)) | (xl >> np.uint32(31))) & M32
+    R = ((x >> np.uint32(1)) | (xr << np.uint32(31))) & M32
+    return L ^ x ^ R, maj(L, x, R)
+
+
+def rule(a, b, c, self_):
+    t0 = a[0] ^ b[0] ^ c[0]
+    k0 = maj(a[0], b[0], c[0])
+    p = a[1] ^ b[1] ^ c[1]
+    q = maj(a[1], b[1], c[1])
+    u1 = p ^ k0
+    u2 = q ^ (p & k0)
+    v = (u2 & self_ & ~t0) | (~u2 & t0)
+    return v & (u1 ^ u2) & M32
+
+
+def next_state(alive, n):  # grid.cpp:22-28
+    return int(n in (2, 3)) if alive else int(n == 3)
+
+
+def test_network_exhaustive_512_neighbourhoods():
+    # Put each 3x3 neighbourhood at bit 1 of three words (bits 0..2 = columns).
+    for bits in range(512):
+        cells = [(bits >> i) & 1 for i in range(9)]
+        rows = [np.uint32(cells[0] | cells[1] << 1 | cells[2] << 2),
+                np.uint32(cells[3] | cells[4] << 1 | cells[5] << 2),
+                np.uint32(cells[6] | cells[7] << 1 | cells[8] << 2)]
+        z = np.uint32(0)
+        hs = [hsum(z, r, z) for r in rows]
+        out = rule(hs[0], hs[1], hs[2], rows[1])
+        n = sum(cells) - cells[4]
+        assert int((out >> np.uint32(1)) & np.uint32(1)) == next_state(cells[4], n), bits
+
+
+def pack32(g):
+    h, w = g.shape
+    nw = (w + 31) // 32
+    out = np.zeros((h, nw), np.uint32)
+    for x in range(w):
+        out[:, x // 32] |= (g[:, x].astype(np.uint32) << np.uint32(x % 32))
+    return out
+
+
+def unpack32(p, w):
+    cols = [((p[:, x // 32] >> np.uint32(x % 32)) & np.uint32(1)).astype(np.uint8) for x in range(w)]
+    return np.stack(cols, axis=1)
+
+
+def load_word(row, wi, W):
+    """load_word_wrapped: 32 cells from column 32*wi of the periodic row."""
+    nw = len(row)
+    c = (32 * int(wi)) % W
+    v, filled = 0, 0
+    while filled < 32:
+        n = min(W - c, 32 - filled)
+        w0 = c >> 5
+        lo = int(row[w0])
+        hi = int(row[w0 + 1]) if w0 + 1 < nw else 0
+        bits = ((hi << 32 | lo) >> (c & 31)) & 0xFFFFFFFF
+        if n < 32:
+            bits &= (1 << n) - 1
+        v |= bits << filled
+        filled += n
+        c += n
+        if c >= W:
+            c = 0
+    return np.uint32(v & 0xFFFFFFFF)
+
+
+def model_packed_pass(p, W, K, seg_rows):
+    """Lane-exact model of packed_tb_kernel<K> over a torus (in_row0 = 0)."""
+    H, nw = p.shape
+    out = np.zeros_like(p)
+    n_strips = -(-nw // 30)
+    tail = W % 32
+    tail_mask = np.uint32(0xFFFFFFFF if tail == 0 else (1 << tail) - 1)
+    for strip in range(n_strips):
+        wi = np.arange(32) + strip * 30 - 1
+        for y0 in range(0, H, seg_rows):
+            rows = min(seg_rows, H - y0)
+            total = rows + 2 * K
+            sa = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
+            sb = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
+            ss = [np.zeros(32, np.uint32) for _ in range(K)]
+            for i in range(total):
+                r = (y0 - K + i) % H
+                x = np.array([p[r, w] if (w >= 0 and (w + 1) * 32 <= W) else load_word(p[r], w, W)
+                              for w in wi], np.uint32)
+                for g in range(K):
+                    xl = np.concatenate([x[:1], x[:-1]])   # shfl_up: lane 0 keeps own
+                    xr = np.concatenate([x[1:], x[-1:]])   # shfl_down: lane 31 keeps own
+                    c = hsum(xl, x, xr)
+                    y = rule(sa[g], sb[g], c, ss[g])
+                    sa[g], sb[g], ss[g] = sb[g], c, x
+                    x = y
+                if i >= 2 * K:
+                    orow = y0 + i - 2 * K
+                    for lane in range(1, 31):
+                        w = wi[lane]
+                        if w < nw:
+                            out[orow, w] = x[lane] & (tail_mask if w == nw - 1 else M32)
+    return out
+
+
+@pytest.mark.parametrize("W,H,K,seg", [(3, 3, 1, 1), (5, 7, 3, 4), (31, 9, 4, 5), (33, 17, 16, 6),
+                                       (64, 12, 2, 12), (97, 23, 5, 7), (1000, 11, 16, 64),
+                                       (1921, 6, 8, 4)])
+def test_kernel_model_matches_oracle(oracle, W, H, K, seg):
+    g = oracle.random_fill(W, H, 0.45, W * 31 + H)
+    p = pack32(g)
+    got = unpack32(model_packed_pass(p, W, K, seg), W)
+    want, _ = oracle.run(g, K)
+    assert np.array_equal(got, want)
