@@ -38,18 +38,22 @@ def _sources() -> list[str]:
     return files + [os.path.join(ROOT, "include", "life_gpu.h")]
 
 
-def build_lib(force: bool = False, verbose: bool = False) -> str:
+def build_lib(force: bool = False, verbose: bool = False, out: str = LIB,
+              defines: tuple = ()) -> str:
+    """Builds the engine library; `defines` (e.g. ("LIFE_FMA_SHIFT",)) build
+    experimental kernel variants into another file, selected at run time with
+    the LIFE_GPU_LIB environment variable."""
     srcs = _sources()
-    if not force and _newer(LIB, srcs + [os.path.abspath(__file__)]):
-        return LIB
-    cmd = [NVCC, *NVCC_FLAGS, "-shared", "-cudart", "static", "-o", LIB + ".tmp",
-           os.path.join(CSRC, "life_gpu.cu")]
+    if not force and _newer(out, srcs + [os.path.abspath(__file__)]):
+        return out
+    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-cudart", "static",
+           "-o", out + ".tmp", os.path.join(CSRC, "life_gpu.cu")]
     if verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 def build_host_test(force: bool = False) -> str:

@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liblife_gpu.so")
+LIB_PATH = os.environ.get("LIFE_GPU_LIB") or os.path.join(PKG, "liblife_gpu.so")
 
 # Status codes (include/life_gpu.h).
 OK = 0

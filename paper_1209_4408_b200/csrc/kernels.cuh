@@ -53,6 +53,29 @@ __device__ __forceinline__ HSum hsum(uint32_t xl, uint32_t x, uint32_t xr) {
   return HSum{L ^ x ^ R, maj3(L, x, R)};
 }
 
+// The same neighbour words built on the FMA pipe instead of the ALU pipe
+// (the ALU pipe carries all the LOP3s):  with two = 2 and half = 2^31 held in
+// registers (kernel arguments, so ptxas cannot strength-reduce them),
+//   L = x*2 + hi(xl*2)          = (x << 1) | (xl >> 31)
+//   R = hi(x*2^31) + lo(xr*2^31) = (x >> 1) | (xr << 31)
+// (the two addends never overlap, so + is |).
+__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+__device__ __forceinline__ HSum hsum_fma(uint32_t xl, uint32_t x, uint32_t xr, uint32_t two,
+                                         uint32_t half) {
+  const uint32_t L = mad_lo(x, two, mad_hi(xl, two, 0u));
+  const uint32_t R = mad_hi(x, half, mad_lo(xr, half, 0u));
+  return HSum{L ^ x ^ R, maj3(L, x, R)};
+}
+
 __device__ __forceinline__ uint32_t rule(HSum a, HSum b, HSum c, uint32_t self) {
   const uint32_t t0 = a.h0 ^ b.h0 ^ c.h0;
   const uint32_t k0 = maj3(a.h0, b.h0, c.h0);
@@ -109,17 +132,83 @@ struct PackedStepArgs {
   int32_t nw;         // ceil(width / 32): words holding cells
   int32_t n_strips;   // ceil(nw / 30)
   uint32_t tail_mask; // valid bits of word nw-1
+  uint32_t two;       // 2     (hsum_fma operands)
+  uint32_t half;      // 2^31
+  void* trace;        // LIFE_TRACE builds: per-warp (smid, start, end)
 };
 
 constexpr int kStripWords = 30;  // output words per warp (lanes 1..30; 0 and 31 are ghosts)
 constexpr int kPackedThreads = 128;
 
-// Rows prefetched ahead per lane; a multiple of 3 so the 3-row stage ring
-// renames without moves after unrolling.
+
+// Steps unrolled per loop trip; a multiple of 3 so the 3-row stage window
+// renames without moves.
+// kMaxThreads: the warps of one SM that fit the pipeline's registers
+// (16K registers per SM sub-partition / (warps per sub-partition x 32 x
+// regs)); one such block per SM.
 template <int K>
 struct PackedTraits {
-  static constexpr int kPrefetch = K <= 1 ? 12 : (K <= 3 ? 6 : 3);
+  static constexpr int kPrefetch = K <= 3 ? 6 : 3;
+  static constexpr int kWarps[17] = {0, 32, 32, 28, 24, 20, 20, 16, 16, 12, 12, 12, 12, 12, 12, 8, 8};
+  static constexpr int kMaxThreads = 32 * kWarps[K];
+  static constexpr int kRingBytes = 2 * kPrefetch * 96 * 4;  // per warp
 };
+
+#ifndef LIFE_GROUP
+#define LIFE_GROUP 4
+#endif
+constexpr int kGroup = LIFE_GROUP;  // stages issued level by level together
+
+// How a lane fetches its 32-cell word of a row.  The column is the same for
+// every row, so the plan is computed once per warp segment:
+//   mode 0: the word lies inside [0, W): one aligned load;
+//   mode 1: the word straddles the torus seam or lies outside [0, W) and
+//           W >= 32: n1 cells from column c (two words, funnel-shifted) then
+//           32-n1 cells from column 0 (Grid::wrap, grid.hpp:48-54);
+//   mode 2: W < 32 (the row wraps several times inside one word): loop.
+struct WordPlan {
+  int mode;
+  int32_t p0, p1;   // words holding columns c.. (mode 1)
+  uint32_t sh;      // c & 31
+  uint32_t m1, m2;  // masks of the two segments
+  uint32_t s2;      // shift of the second segment (n1 & 31)
+};
+
+__device__ __forceinline__ WordPlan make_plan(int64_t wi, int64_t width, int32_t nw) {
+  WordPlan p{};
+  if (wi >= 0 && (wi + 1) * 32 <= width) {
+    p.mode = 0;
+    return p;
+  }
+  if (width < 32) {
+    p.mode = 2;
+    return p;
+  }
+  int64_t c = (32 * wi) % width;
+  if (c < 0) c += width;
+  const int64_t n1 = width - c < 32 ? width - c : 32;
+  p.mode = 1;
+  p.p0 = static_cast<int32_t>(c >> 5);
+  p.p1 = p.p0 + 1 < nw ? p.p0 + 1 : p.p0;
+  p.sh = static_cast<uint32_t>(c & 31);
+  p.m1 = n1 == 32 ? 0xffffffffu : ((1u << n1) - 1u);
+  p.m2 = n1 == 32 ? 0u : ~p.m1;  // the low 32-n1 bits of word 0, shifted up by n1
+  p.s2 = static_cast<uint32_t>(n1 & 31);
+  return p;
+}
+
+// cp.async (LDGSTS) of one 32-bit word into this lane's ring slot.
+__device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // Temporal-blocked packed step: K generations per pass, no shared memory,
@@ -127,81 +216,213 @@ struct PackedTraits {
 // words + one ghost word per side; a ghost word covers K <= 32 cells of
 // light cone) and a segment of seg_rows output rows, and streams input rows
 // y0-K .. y1+K-1 through a K-stage register pipeline: stage g turns the row
-// stream of generation g-1 into generation g, one row per step, keeping the
-// 3-row (h0,h1,self) window of its input in registers.  Horizontal
-// neighbour words come from __shfl_up/down_sync.  Every input row is read
-// once per pass and every output row written once, so the HBM traffic per
-// cell-update is (1 bit read + 1 bit write)/K plus the ghost overlap
-// (32/30 on reads, (seg+2K)/seg vertically).
+// stream of generation g into generation g+1, keeping the 3-row (h0,h1,self)
+// window of its input in registers.  Horizontal neighbour words come from
+// __shfl_up/down_sync.
+//
+// The pipeline is SKEWED: stage g consumes what stage g-1 emitted on the
+// previous step, so the K stages of one step are independent and their
+// instruction chains (shuffle -> funnel -> 6 LOP3 levels) interleave.
+// Stage g (0-based) emits at step i generation g+1 of input row i-1-2g;
+// the last stage emits generation K of output row i-3K+1.
+//
+// Every input row is read once per pass and every output row written once,
+// so the HBM traffic per cell-update is (1 bit read + 1 bit write)/K plus the
+// ghost overlap (32/30 on reads, (seg+3K)/seg vertically).
+//
+// Replaces compute_region (engine.cpp:17-48) x K generations with the
+// per-generation barrier of WorkerTeam (engine.cpp:79-96) removed inside a
+// pass: the dependency is carried by the pipeline order instead.
+// ---------------------------------------------------------------------------
+// The per-warp pass.  EDGE warps (a lane touches the torus seam, or W < 32)
+// fetch 3 words per lane per row and combine them; interior warps (all but
+// at most two strips) run the branch-free path.
+template <int K, bool EDGE>
+__device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int lane, const int64_t wi,
+                                            const WordPlan& plan, const int64_t y0, const int rows,
+                                            uint32_t* ring) {
+  constexpr int PF = PackedTraits<K>::kPrefetch;
+  constexpr int kLag = 3 * K - 1;  // output row j leaves the pipeline at step j + 3K - 1
+  const bool tiny = a.width < 32;  // warp-uniform (EDGE only)
+  const bool store_lane = lane >= 1 && lane <= kStripWords && wi < a.nw;
+  const uint32_t store_mask = (wi == a.nw - 1) ? a.tail_mask : kFull;
+
+  // Row cursor: physical input row of the next row to fetch (32-bit).
+  int lrow = static_cast<int>(wrap_row(a.in_row0, y0 - K, a.in_rows));
+  const int in_rows = static_cast<int>(a.in_rows);
+  auto issue = [&](int slot) {
+    const uint32_t* row = a.in + static_cast<int64_t>(lrow) * a.in_pitch;
+    uint32_t* s = ring + slot * 96;
+    if (!EDGE) {
+      cp_async4(s, row + wi);
+    } else if (tiny) {
+      s[0] = load_word_wrapped(row, wi, a.width, a.nw);
+    } else if (plan.mode == 0) {
+      cp_async4(s, row + wi);
+    } else {
+      cp_async4(s, row + plan.p0);
+      cp_async4(s + 32, row + plan.p1);
+      cp_async4(s + 64, row);
+    }
+    cp_async_commit();
+    lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
+  };
+  auto consume = [&](int slot) -> uint32_t {
+    const uint32_t* s = ring + slot * 96;
+    if (!EDGE || tiny || plan.mode == 0) return s[0];
+    return (__funnelshift_r(s[0], s[32], plan.sh) & plan.m1) | ((s[64] << plan.s2) & plan.m2);
+  };
+
+  // Ring of 2*PF row slots; step i lives in slot i mod 2PF and is fetched
+  // PF steps ahead.  `half` = (trip base) mod 2PF is 0 or PF.
+#pragma unroll
+  for (int u = 0; u < PF; ++u) issue(u);
+
+  HSum sa[K], sb[K];
+  uint32_t sself[K], xin[K];
+#pragma unroll
+  for (int g = 0; g < K; ++g) {
+    sa[g] = HSum{0u, 0u};
+    sb[g] = HSum{0u, 0u};
+    sself[g] = 0u;
+    xin[g] = 0u;
+  }
+
+#ifdef LIFE_NO_LOCKSTEP
+  const int total = rows + kLag;
+#else
+  // Every warp of the block runs the same number of steps: the block is all
+  // the warps resident on one SM, kept in lockstep by a barrier per loop
+  // trip, because the warp arbiter otherwise starves some warps and the SM
+  // ends the pass with too few warps to fill the ALU pipe.
+  const int total = static_cast<int>(a.seg_rows) + kLag;
+#endif
+  uint32_t* const out_base = a.out + (a.out_row0 + y0) * a.out_pitch + wi;
+  int half = 0;
+  for (int base = 0; base < total; base += PF) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      issue((half ^ PF) + u);
+      cp_async_wait<PF>();
+      xin[0] = consume(half + u);
+      // The K stages of a step are independent (skewed pipeline); they are
+      // issued in groups of kGroup, level by level (all shuffles, then all
+      // funnels, ...), so consecutive instructions do not depend on each
+      // other and the ALU pipe sees several independent chains per warp.
+      uint32_t y[K];
+#pragma unroll
+      for (int g0 = 0; g0 < K; g0 += kGroup) {
+        uint32_t xl[kGroup], xr[kGroup];
+        HSum c[kGroup];
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+          if (g0 + j < K) {
+            xl[j] = __shfl_up_sync(kFull, xin[g0 + j], 1);
+            xr[j] = __shfl_down_sync(kFull, xin[g0 + j], 1);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+          if (g0 + j < K) {
+#ifdef LIFE_FMA_SHIFT
+            c[j] = hsum_fma(xl[j], xin[g0 + j], xr[j], a.two, a.half);
+#else
+            c[j] = hsum(xl[j], xin[g0 + j], xr[j]);
+#endif
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+          if (g0 + j < K) {
+            const int g = g0 + j;
+            y[g] = rule(sa[g], sb[g], c[j], sself[g]);
+            sa[g] = sb[g];
+            sb[g] = c[j];
+            sself[g] = xin[g];
+          }
+        }
+      }
+#pragma unroll
+      for (int g = 1; g < K; ++g) xin[g] = y[g - 1];
+      const int j = base + u - kLag;  // output row of this step
+      if (store_lane && static_cast<unsigned>(j) < static_cast<unsigned>(rows)) {
+        out_base[static_cast<int64_t>(j) * a.out_pitch] = y[K - 1] & store_mask;
+      }
+    }
+    half ^= PF;
+#ifndef LIFE_NO_LOCKSTEP
+    __syncthreads();
+#endif
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// Temporal-blocked packed step: K generations per pass, no block-level
+// data sharing.  Each warp owns a vertical strip of 32 words (30 output
+// words + one ghost word per side; a ghost word covers K <= 32 cells of
+// light cone) and a segment of seg_rows output rows, and streams input rows
+// y0-K .. y1+K-1 through a K-stage register pipeline: stage g turns the row
+// stream of generation g into generation g+1, keeping the 3-row (h0,h1,self)
+// window of its input in registers.  Horizontal neighbour words come from
+// __shfl_up/down_sync.  Input rows arrive through a per-warp shared-memory
+// ring filled by cp.async PF rows ahead, so no load latency sits on the
+// compute chain.
+//
+// The pipeline is SKEWED: stage g consumes what stage g-1 emitted on the
+// previous step, so the K stages of one step are independent and their
+// instruction chains (shuffle -> funnel -> 6 LOP3 levels) interleave.
+// Stage g (0-based) emits at step i generation g+1 of input row i-1-2g;
+// the last stage emits generation K of output row i-3K+1.
+//
+// Every input row is read once per pass and every output row written once,
+// so the HBM traffic per cell-update is (1 bit read + 1 bit write)/K plus the
+// ghost overlap (32/30 on reads, (seg+3K)/seg vertically).
 //
 // Replaces compute_region (engine.cpp:17-48) x K generations with the
 // per-generation barrier of WorkerTeam (engine.cpp:79-96) removed inside a
 // pass: the dependency is carried by the pipeline order instead.
 // ---------------------------------------------------------------------------
 template <int K>
-__global__ void __launch_bounds__(kPackedThreads)
+__global__ void __launch_bounds__(PackedTraits<K>::kMaxThreads)
 packed_tb_kernel(const PackedStepArgs a) {
-  constexpr int PF = PackedTraits<K>::kPrefetch;
   const int lane = threadIdx.x & 31;
-  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kPackedThreads + threadIdx.x) >> 5;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int strip = static_cast<int>(gwarp % a.n_strips);
   const int64_t seg = gwarp / a.n_strips;
   const int64_t y0 = seg * a.seg_rows;
+#ifdef LIFE_NO_LOCKSTEP
   if (y0 >= a.out_rows) return;  // warp-uniform
-  const int64_t rows = min(a.seg_rows, a.out_rows - y0);
-
+#endif
+  // Output rows of this warp (0 for spare warps of the last block, which
+  // still step in lockstep with their block but store nothing).
+  const int64_t rows_left = a.out_rows - y0;
+  const int rows = static_cast<int>(rows_left < 0 ? 0 : (rows_left < a.seg_rows ? rows_left : a.seg_rows));
+#ifdef LIFE_TRACE
+  uint64_t t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   const int64_t wi = static_cast<int64_t>(strip) * kStripWords + lane - 1;
-  const bool interior = wi >= 0 && (wi + 1) * 32 <= a.width;
-  const bool store_lane = lane >= 1 && lane <= kStripWords && wi < a.nw;
-  const uint32_t store_mask = (wi == a.nw - 1) ? a.tail_mask : kFull;
-
-  // Input row cursor (physical), advanced with wrap.
-  int64_t lrow = wrap_row(a.in_row0, y0 - K, a.in_rows);
-  auto load_next = [&]() -> uint32_t {
-    const uint32_t* row = a.in + lrow * a.in_pitch;
-    uint32_t v = interior ? __ldg(row + wi) : load_word_wrapped(row, wi, a.width, a.nw);
-    if (++lrow == a.in_rows) lrow = 0;
-    return v;
-  };
-
-  uint32_t pf[PF];
-#pragma unroll
-  for (int u = 0; u < PF; ++u) pf[u] = load_next();
-
-  HSum sa[K], sb[K];
-  uint32_t sself[K];
-#pragma unroll
-  for (int g = 0; g < K; ++g) {
-    sa[g] = HSum{0u, 0u};
-    sb[g] = HSum{0u, 0u};
-    sself[g] = 0u;
+  const WordPlan plan = make_plan(wi, a.width, a.nw);
+  extern __shared__ uint32_t ring_smem[];
+  uint32_t* ring = ring_smem + (threadIdx.x >> 5) * (2 * PackedTraits<K>::kPrefetch * 96) + lane;
+  if (__any_sync(kFull, plan.mode != 0)) {
+    packed_pass<K, true>(a, lane, wi, plan, y0, rows, ring);
+  } else {
+    packed_pass<K, false>(a, lane, wi, plan, y0, rows, ring);
   }
-
-  const int64_t total = rows + 2 * K;  // stage K emits output row i-2K at step i
-  uint32_t* out_base = a.out + (a.out_row0 + y0 - 2 * K) * a.out_pitch + wi;
-
-  for (int64_t base = 0; base < total; base += PF) {
-#pragma unroll
-    for (int u = 0; u < PF; ++u) {
-      uint32_t x = pf[u];
-      pf[u] = load_next();
-#pragma unroll
-      for (int g = 0; g < K; ++g) {
-        const uint32_t xl = __shfl_up_sync(kFull, x, 1);
-        const uint32_t xr = __shfl_down_sync(kFull, x, 1);
-        const HSum c = hsum(xl, x, xr);
-        const uint32_t y = rule(sa[g], sb[g], c, sself[g]);
-        sa[g] = sb[g];
-        sb[g] = c;
-        sself[g] = x;
-        x = y;
-      }
-      const int64_t i = base + u;
-      if (store_lane && i >= 2 * K && i < total) {
-        out_base[i * a.out_pitch] = x & store_mask;
-      }
-    }
+#ifdef LIFE_TRACE
+  if (lane == 0) {
+    uint64_t t_end;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    unsigned long long* tr = reinterpret_cast<unsigned long long*>(a.trace) + 3 * gwarp;
+    tr[0] = smid;
+    tr[1] = t_start;
+    tr[2] = t_end;
   }
+#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -23,6 +23,7 @@ namespace {
 
 thread_local std::string g_error;
 std::atomic<uint64_t> g_launches{0};
+void* g_trace = nullptr;  // device buffer for LIFE_TRACE builds (life_debug_set_trace)
 
 int set_error(int code, const char* fmt, ...) {
   char buf[512];
@@ -87,26 +88,49 @@ uint64_t density_threshold(double density) {
 // ---- packed temporal-blocked step: template dispatch on K ----------------
 template <int K>
 int launch_packed(PackedStepArgs a, cudaStream_t s) {
-  static int blocks_per_sm[64] = {0};  // per device
+  // Per device: warps per block = every warp one SM holds (register-limited),
+  // one block per SM, so the block barrier keeps all of an SM's warps in
+  // lockstep (LIFE_NO_LOCKSTEP builds use 4-warp blocks instead).
+  static int warps_per_block[64] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (blocks_per_sm[dev & 63] == 0) {
+  int& wpb = warps_per_block[dev & 63];
+  if (wpb == 0) {
+    LIFE_CUDA(cudaFuncSetAttribute(packed_tb_kernel<K>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (PackedTraits<K>::kMaxThreads / 32) * PackedTraits<K>::kRingBytes));
     int nb = 0;
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, packed_tb_kernel<K>,
-                                                            kPackedThreads, 0));
-    blocks_per_sm[dev & 63] = std::max(nb, 1);
+                                                            kPackedThreads,
+                                                            4 * PackedTraits<K>::kRingBytes));
+    int w = std::min(std::max(nb, 1) * (kPackedThreads / 32), PackedTraits<K>::kMaxThreads / 32);
+#ifdef LIFE_NO_LOCKSTEP
+    w = kPackedThreads / 32;
+#else
+    for (; w > 1; --w) {
+      int nb2 = 0;
+      LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, packed_tb_kernel<K>, 32 * w,
+                                                              w * PackedTraits<K>::kRingBytes));
+      if (nb2 >= 1) break;
+    }
+#endif
+    wpb = w;
   }
-  const int64_t resident_warps =
-      static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kPackedThreads / 32) * sm_count();
+  int blocks_per_sm = 1;
+#ifdef LIFE_NO_LOCKSTEP
+  LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, packed_tb_kernel<K>,
+                                                          32 * wpb, wpb * PackedTraits<K>::kRingBytes));
+#endif
+  const int64_t resident_warps = static_cast<int64_t>(wpb) * blocks_per_sm * sm_count();
   // One wave: split rows so that n_strips * n_segs ~ resident warps, with
-  // segments at least 4K rows tall (vertical ghost overhead <= 2K/seg).
+  // segments at least 4K rows tall (vertical pipeline fill <= 3K/seg).
   const int64_t segs_target = std::max<int64_t>(1, resident_warps / a.n_strips);
   a.seg_rows = std::max<int64_t>(ceil_div(a.out_rows, segs_target), 4 * K);
   const int64_t n_segs = ceil_div(a.out_rows, a.seg_rows);
   const int64_t warps = n_segs * a.n_strips;
-  const int64_t blocks = ceil_div(warps, kPackedThreads / 32);
+  const int64_t blocks = ceil_div(warps, wpb);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
-  packed_tb_kernel<K><<<static_cast<unsigned>(blocks), kPackedThreads, 0, s>>>(a);
+  packed_tb_kernel<K><<<static_cast<unsigned>(blocks), 32 * wpb, wpb * PackedTraits<K>::kRingBytes, s>>>(a);
   LIFE_CHECK_LAUNCH("packed_tb_kernel");
   return LIFE_OK;
 }
@@ -139,6 +163,9 @@ extern "C" {
 const char* life_last_error(void) { return g_error.c_str(); }
 const char* life_version(void) { return "life-b200 0.1 (sm_100a)"; }
 uint64_t life_kernel_launches(void) { return g_launches.load(); }
+// Debug hook (not in the public header): LIFE_TRACE builds record per-warp
+// (smid, start ns, end ns) of packed passes into this device buffer.
+void life_debug_set_trace(void* dev_buf) { g_trace = dev_buf; }
 
 int64_t life_packed_pitch_words(int64_t width) {
   return ceil_div(2 * ceil_div(width, 64), 32) * 32;
@@ -183,6 +210,9 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
   a.nw = static_cast<int32_t>(nw32(width));
   a.n_strips = static_cast<int32_t>(ceil_div(a.nw, kStripWords));
   a.tail_mask = tail_mask(width);
+  a.two = 2u;
+  a.half = 0x80000000u;
+  a.trace = g_trace;
   return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
 }
 

@@ -99,27 +99,31 @@ def model_packed_pass(p, W, K, seg_rows):
         wi = np.arange(32) + strip * 30 - 1
         for y0 in range(0, H, seg_rows):
             rows = min(seg_rows, H - y0)
-            total = rows + 2 * K
+            total = rows + 3 * K - 1
             sa = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
             sb = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
             ss = [np.zeros(32, np.uint32) for _ in range(K)]
+            xin = [np.zeros(32, np.uint32) for _ in range(K)]
             for i in range(total):
                 r = (y0 - K + i) % H
-                x = np.array([p[r, w] if (w >= 0 and (w + 1) * 32 <= W) else load_word(p[r], w, W)
-                              for w in wi], np.uint32)
-                for g in range(K):
+                xin[0] = np.array([p[r, w] if (w >= 0 and (w + 1) * 32 <= W) else
+                                   load_word(p[r], w, W) for w in wi], np.uint32)
+                ys = []
+                for g in range(K):  # skewed: stage g eats stage g-1's previous output
+                    x = xin[g]
                     xl = np.concatenate([x[:1], x[:-1]])   # shfl_up: lane 0 keeps own
                     xr = np.concatenate([x[1:], x[-1:]])   # shfl_down: lane 31 keeps own
                     c = hsum(xl, x, xr)
-                    y = rule(sa[g], sb[g], c, ss[g])
+                    ys.append(rule(sa[g], sb[g], c, ss[g]))
                     sa[g], sb[g], ss[g] = sb[g], c, x
-                    x = y
-                if i >= 2 * K:
-                    orow = y0 + i - 2 * K
+                for g in range(1, K):
+                    xin[g] = ys[g - 1]
+                if i >= 3 * K - 1:
+                    orow = y0 + i - (3 * K - 1)
                     for lane in range(1, 31):
                         w = wi[lane]
                         if w < nw:
-                            out[orow, w] = x[lane] & (tail_mask if w == nw - 1 else M32)
+                            out[orow, w] = ys[K - 1][lane] & (tail_mask if w == nw - 1 else M32)
     return out
 
 
