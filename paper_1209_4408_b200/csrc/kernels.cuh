@@ -128,30 +128,35 @@ struct PackedStepArgs {
   int64_t out_row0;
   int64_t width;      // cells
   int64_t out_rows;
-  int64_t seg_rows;   // output rows per warp segment
+  int64_t seg_rows;   // output rows per tile (strip x segment)
+  int32_t steps;      // loop trips (block barriers) every warp runs (lockstep)
   int32_t nw;         // ceil(width / 32): words holding cells
-  int32_t n_strips;   // ceil(nw / 30)
+  int32_t n_strips;   // ceil((nw + 1) / 31)
   uint32_t tail_mask; // valid bits of word nw-1
   uint32_t two;       // 2     (hsum_fma operands)
   uint32_t half;      // 2^31
   void* trace;        // LIFE_TRACE builds: per-warp (smid, start, end)
 };
 
-constexpr int kStripWords = 30;  // output words per warp (lanes 1..30; 0 and 31 are ghosts)
+// A warp covers 32 consecutive words; strips advance by 31 words, so
+// neighbouring strips share one word: lane 31 of strip s and lane 0 of strip
+// s+1.  After K <= 16 generations the shuffle edges have corrupted at most K
+// bits at each end of the warp, so lane 31 still holds valid bits 0..15 and
+// lane 0 valid bits 16..31: they store those halves (16-bit stores), and
+// lanes 1..30 store whole words.  Ghost overhead is 1 word in 32.
+constexpr int kStripStride = 31;
 constexpr int kPackedThreads = 128;
 
-
-// Steps unrolled per loop trip; a multiple of 3 so the 3-row stage window
-// renames without moves.
 // kMaxThreads: the warps of one SM that fit the pipeline's registers
 // (16K registers per SM sub-partition / (warps per sub-partition x 32 x
 // regs)); one such block per SM.
 template <int K>
 struct PackedTraits {
   static constexpr int kPrefetch = K <= 3 ? 6 : 3;
-  static constexpr int kWarps[17] = {0, 32, 32, 28, 24, 20, 20, 16, 16, 12, 12, 12, 12, 12, 12, 8, 8};
+  static constexpr int kWarps[17] = {0, 28, 24, 24, 20, 16, 16, 16, 16, 12, 12, 12, 12, 12, 8, 8, 8};
   static constexpr int kMaxThreads = 32 * kWarps[K];
   static constexpr int kRingBytes = 2 * kPrefetch * 96 * 4;  // per warp
+  static constexpr int kLag = 3 * K - 1;  // output row j leaves the pipeline at step j + 3K - 1
 };
 
 #ifndef LIFE_GROUP
@@ -160,14 +165,17 @@ struct PackedTraits {
 constexpr int kGroup = LIFE_GROUP;  // stages issued level by level together
 
 // How a lane fetches its 32-cell word of a row.  The column is the same for
-// every row, so the plan is computed once per warp segment:
-//   mode 0: the word lies inside [0, W): one aligned load;
-//   mode 1: the word straddles the torus seam or lies outside [0, W) and
-//           W >= 32: n1 cells from column c (two words, funnel-shifted) then
-//           32-n1 cells from column 0 (Grid::wrap, grid.hpp:48-54);
+// every row, so the plan is computed once per strip:
+//   mode 0: one aligned load of word `src` -- the word lies inside [0, W),
+//           or W is a multiple of 32 and the torus wrap (Grid::wrap,
+//           grid.hpp:48-54) is just an index wrap;
+//   mode 1: W % 32 != 0 and the word straddles the seam or lies outside
+//           [0, W): n1 cells from column c (two words, funnel-shifted) then
+//           32-n1 cells from column 0;
 //   mode 2: W < 32 (the row wraps several times inside one word): loop.
 struct WordPlan {
   int mode;
+  int32_t src;      // mode 0
   int32_t p0, p1;   // words holding columns c.. (mode 1)
   uint32_t sh;      // c & 31
   uint32_t m1, m2;  // masks of the two segments
@@ -178,10 +186,17 @@ __device__ __forceinline__ WordPlan make_plan(int64_t wi, int64_t width, int32_t
   WordPlan p{};
   if (wi >= 0 && (wi + 1) * 32 <= width) {
     p.mode = 0;
+    p.src = static_cast<int32_t>(wi);
     return p;
   }
   if (width < 32) {
     p.mode = 2;
+    return p;
+  }
+  if ((width & 31) == 0) {
+    p.mode = 0;
+    int64_t w = wi % nw;
+    p.src = static_cast<int32_t>(w < 0 ? w + nw : w);
     return p;
   }
   int64_t c = (32 * wi) % width;
@@ -210,55 +225,42 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// ---------------------------------------------------------------------------
-// Temporal-blocked packed step: K generations per pass, no shared memory,
-// no block barriers.  Each warp owns a vertical strip of 32 words (30 output
-// words + one ghost word per side; a ghost word covers K <= 32 cells of
-// light cone) and a segment of seg_rows output rows, and streams input rows
-// y0-K .. y1+K-1 through a K-stage register pipeline: stage g turns the row
-// stream of generation g into generation g+1, keeping the 3-row (h0,h1,self)
-// window of its input in registers.  Horizontal neighbour words come from
-// __shfl_up/down_sync.
-//
-// The pipeline is SKEWED: stage g consumes what stage g-1 emitted on the
-// previous step, so the K stages of one step are independent and their
-// instruction chains (shuffle -> funnel -> 6 LOP3 levels) interleave.
-// Stage g (0-based) emits at step i generation g+1 of input row i-1-2g;
-// the last stage emits generation K of output row i-3K+1.
-//
-// Every input row is read once per pass and every output row written once,
-// so the HBM traffic per cell-update is (1 bit read + 1 bit write)/K plus the
-// ghost overlap (32/30 on reads, (seg+3K)/seg vertically).
-//
-// Replaces compute_region (engine.cpp:17-48) x K generations with the
-// per-generation barrier of WorkerTeam (engine.cpp:79-96) removed inside a
-// pass: the dependency is carried by the pipeline order instead.
-// ---------------------------------------------------------------------------
-// The per-warp pass.  EDGE warps (a lane touches the torus seam, or W < 32)
-// fetch 3 words per lane per row and combine them; interior warps (all but
-// at most two strips) run the branch-free path.
-template <int K, bool EDGE>
-__device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int lane, const int64_t wi,
-                                            const WordPlan& plan, const int64_t y0, const int rows,
-                                            uint32_t* ring) {
-  constexpr int PF = PackedTraits<K>::kPrefetch;
-  constexpr int kLag = 3 * K - 1;  // output row j leaves the pipeline at step j + 3K - 1
-  const bool tiny = a.width < 32;  // warp-uniform (EDGE only)
-  const bool store_lane = lane >= 1 && lane <= kStripWords && wi < a.nw;
-  const uint32_t store_mask = (wi == a.nw - 1) ? a.tail_mask : kFull;
+// A warp's work is a range of the virtual row space strip*out_rows + y
+// (int32: the host checks n_strips*out_rows < 2^31): one or more segments
+// (strip, y, n), each a fresh pipeline of n + kLag steps.
 
-  // Row cursor: physical input row of the next row to fetch (32-bit).
-  int lrow = static_cast<int>(wrap_row(a.in_row0, y0 - K, a.in_rows));
+// One pipeline segment of a warp: strip `strip`, output rows [y, y+n).
+// Runs ceil((n + kLag) / PF) loop trips (one block barrier each) and returns
+// that count.  EDGE warps (W % 32 != 0 and a lane touches the seam, or
+// W < 32) fetch 3 words per lane per row and combine them; all other warps
+// run the branch-free single-load path.
+template <int K, bool EDGE>
+__device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int lane,
+                                              const int strip, const int y, const int n,
+                                              uint32_t* ring) {
+  constexpr int PF = PackedTraits<K>::kPrefetch;
+  constexpr int kLag = PackedTraits<K>::kLag;
+  const bool tiny = a.width < 32;  // warp-uniform (EDGE only)
   const int in_rows = static_cast<int>(a.in_rows);
+  const int64_t wi = static_cast<int64_t>(strip) * kStripStride + lane - 1;
+  const WordPlan plan = make_plan(wi, a.width, a.nw);
+
+  // Input rows y-K, y-K+1, ... stream through a ring of 2*PF slots; step i
+  // lives in slot i mod 2PF and is fetched PF steps ahead.  Row addresses
+  // are one IMAD.WIDE (FMA pipe) from a 32-bit row index and byte pitch.
+  int lrow = static_cast<int>(wrap_row(a.in_row0, static_cast<int64_t>(y) - K, a.in_rows));
+  const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch * 4);
+  const char* const in_lane = reinterpret_cast<const char*>(a.in + plan.src);
   auto issue = [&](int slot) {
     const uint32_t* row = a.in + static_cast<int64_t>(lrow) * a.in_pitch;
     uint32_t* s = ring + slot * 96;
     if (!EDGE) {
-      cp_async4(s, row + wi);
+      cp_async4(s, reinterpret_cast<const uint32_t*>(
+                       in_lane + static_cast<uint64_t>(static_cast<uint32_t>(lrow)) * in_pitch_b));
     } else if (tiny) {
       s[0] = load_word_wrapped(row, wi, a.width, a.nw);
     } else if (plan.mode == 0) {
-      cp_async4(s, row + wi);
+      cp_async4(s, row + plan.src);
     } else {
       cp_async4(s, row + plan.p0);
       cp_async4(s + 32, row + plan.p1);
@@ -273,8 +275,16 @@ __device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int l
     return (__funnelshift_r(s[0], s[32], plan.sh) & plan.m1) | ((s[64] << plan.s2) & plan.m2);
   };
 
-  // Ring of 2*PF row slots; step i lives in slot i mod 2PF and is fetched
-  // PF steps ahead.  `half` = (trip base) mod 2PF is 0 or PF.
+  // Stores, as two predicated 16-bit halves (no divergent branches): lanes
+  // 1..30 write both, lane 0 only bits 16..31 and lane 31 only bits 0..15 of
+  // the words they share with the neighbouring strips.
+  const bool in_grid = wi >= 0 && wi < a.nw;
+  const bool st_lo = in_grid && lane >= 1;
+  const bool st_hi = in_grid && lane <= 30;
+  const uint32_t st_mask = wi == a.nw - 1 ? a.tail_mask : kFull;
+  char* const out_seg = reinterpret_cast<char*>(a.out + (a.out_row0 + y) * a.out_pitch + wi);
+  const uint32_t out_pitch_b = static_cast<uint32_t>(a.out_pitch * 4);
+
 #pragma unroll
   for (int u = 0; u < PF; ++u) issue(u);
 
@@ -288,18 +298,9 @@ __device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int l
     xin[g] = 0u;
   }
 
-#ifdef LIFE_NO_LOCKSTEP
-  const int total = rows + kLag;
-#else
-  // Every warp of the block runs the same number of steps: the block is all
-  // the warps resident on one SM, kept in lockstep by a barrier per loop
-  // trip, because the warp arbiter otherwise starves some warps and the SM
-  // ends the pass with too few warps to fill the ALU pipe.
-  const int total = static_cast<int>(a.seg_rows) + kLag;
-#endif
-  uint32_t* const out_base = a.out + (a.out_row0 + y0) * a.out_pitch + wi;
+  const int trips = (n + kLag + PF - 1) / PF;
   int half = 0;
-  for (int base = 0; base < total; base += PF) {
+  for (int t = 0; t < trips; ++t) {
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
       issue((half ^ PF) + u);
@@ -309,7 +310,7 @@ __device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int l
       // issued in groups of kGroup, level by level (all shuffles, then all
       // funnels, ...), so consecutive instructions do not depend on each
       // other and the ALU pipe sees several independent chains per warp.
-      uint32_t y[K];
+      uint32_t yv[K];
 #pragma unroll
       for (int g0 = 0; g0 < K; g0 += kGroup) {
         uint32_t xl[kGroup], xr[kGroup];
@@ -335,7 +336,7 @@ __device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int l
         for (int j = 0; j < kGroup; ++j) {
           if (g0 + j < K) {
             const int g = g0 + j;
-            y[g] = rule(sa[g], sb[g], c[j], sself[g]);
+            yv[g] = rule(sa[g], sb[g], c[j], sself[g]);
             sa[g] = sb[g];
             sb[g] = c[j];
             sself[g] = xin[g];
@@ -343,10 +344,14 @@ __device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int l
         }
       }
 #pragma unroll
-      for (int g = 1; g < K; ++g) xin[g] = y[g - 1];
-      const int j = base + u - kLag;  // output row of this step
-      if (store_lane && static_cast<unsigned>(j) < static_cast<unsigned>(rows)) {
-        out_base[static_cast<int64_t>(j) * a.out_pitch] = y[K - 1] & store_mask;
+      for (int g = 1; g < K; ++g) xin[g] = yv[g - 1];
+      // Output row j of the segment leaves the pipeline at step j + kLag.
+      const int j = t * PF + u - kLag;
+      if (static_cast<unsigned>(j) < static_cast<unsigned>(n)) {
+        char* p = out_seg + static_cast<uint64_t>(static_cast<uint32_t>(j)) * out_pitch_b;
+        const uint32_t v = yv[K - 1] & st_mask;
+        if (st_lo) *reinterpret_cast<uint16_t*>(p) = static_cast<uint16_t>(v);
+        if (st_hi) *reinterpret_cast<uint16_t*>(p + 2) = static_cast<uint16_t>(v >> 16);
       }
     }
     half ^= PF;
@@ -355,19 +360,17 @@ __device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int l
 #endif
   }
   cp_async_wait<0>();
+  return trips;
 }
 
 // ---------------------------------------------------------------------------
 // Temporal-blocked packed step: K generations per pass, no block-level
-// data sharing.  Each warp owns a vertical strip of 32 words (30 output
-// words + one ghost word per side; a ghost word covers K <= 32 cells of
-// light cone) and a segment of seg_rows output rows, and streams input rows
-// y0-K .. y1+K-1 through a K-stage register pipeline: stage g turns the row
-// stream of generation g into generation g+1, keeping the 3-row (h0,h1,self)
-// window of its input in registers.  Horizontal neighbour words come from
-// __shfl_up/down_sync.  Input rows arrive through a per-warp shared-memory
-// ring filled by cp.async PF rows ahead, so no load latency sits on the
-// compute chain.
+// data sharing.  Each warp streams input rows of a 32-word strip through a
+// K-stage register pipeline: stage g turns the row stream of generation g
+// into generation g+1, keeping the 3-row (h0,h1,self) window of its input in
+// registers.  Horizontal neighbour words come from __shfl_up/down_sync.
+// Input rows arrive through a per-warp shared-memory ring filled by
+// cp.async PF rows ahead, so no load latency sits on the compute chain.
 //
 // The pipeline is SKEWED: stage g consumes what stage g-1 emitted on the
 // previous step, so the K stages of one step are independent and their
@@ -375,9 +378,15 @@ __device__ __forceinline__ void packed_pass(const PackedStepArgs& a, const int l
 // Stage g (0-based) emits at step i generation g+1 of input row i-1-2g;
 // the last stage emits generation K of output row i-3K+1.
 //
+// Work: tiles of one strip x seg_rows rows, one per warp, strip fastest; a
+// block is all the warps one SM holds, stepped in lockstep (one barrier per
+// loop trip) because the warp arbiter otherwise starves some warps and the
+// SM ends the pass with too few warps to fill the ALU pipe.  The host picks
+// seg_rows so the number of block waves is nearly an integer.
+//
 // Every input row is read once per pass and every output row written once,
 // so the HBM traffic per cell-update is (1 bit read + 1 bit write)/K plus the
-// ghost overlap (32/30 on reads, (seg+3K)/seg vertically).
+// ghost overlap (32/31 on reads, (seg_rows+2K)/seg_rows vertically).
 //
 // Replaces compute_region (engine.cpp:17-48) x K generations with the
 // per-generation barrier of WorkerTeam (engine.cpp:79-96) removed inside a
@@ -387,30 +396,39 @@ template <int K>
 __global__ void __launch_bounds__(PackedTraits<K>::kMaxThreads)
 packed_tb_kernel(const PackedStepArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int strip = static_cast<int>(gwarp % a.n_strips);
-  const int64_t seg = gwarp / a.n_strips;
+  // Tile = (strip, segment), strip fastest: the warps of a block are
+  // neighbouring strips of the same rows, so the words they share (ghost
+  // lanes, half-word stores) meet in L1/L2 at the same time.
+  const int64_t tile = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int strip = static_cast<int>(tile % a.n_strips);
+  const int64_t seg = tile / a.n_strips;
   const int64_t y0 = seg * a.seg_rows;
+  const int64_t left = a.out_rows - y0;
+  const int n = static_cast<int>(left <= 0 ? 0 : (left < a.seg_rows ? left : a.seg_rows));
 #ifdef LIFE_NO_LOCKSTEP
-  if (y0 >= a.out_rows) return;  // warp-uniform
+  if (n == 0) return;  // warp-uniform
 #endif
-  // Output rows of this warp (0 for spare warps of the last block, which
-  // still step in lockstep with their block but store nothing).
-  const int64_t rows_left = a.out_rows - y0;
-  const int rows = static_cast<int>(rows_left < 0 ? 0 : (rows_left < a.seg_rows ? rows_left : a.seg_rows));
 #ifdef LIFE_TRACE
   uint64_t t_start;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 #endif
-  const int64_t wi = static_cast<int64_t>(strip) * kStripWords + lane - 1;
-  const WordPlan plan = make_plan(wi, a.width, a.nw);
   extern __shared__ uint32_t ring_smem[];
   uint32_t* ring = ring_smem + (threadIdx.x >> 5) * (2 * PackedTraits<K>::kPrefetch * 96) + lane;
-  if (__any_sync(kFull, plan.mode != 0)) {
-    packed_pass<K, true>(a, lane, wi, plan, y0, rows, ring);
-  } else {
-    packed_pass<K, false>(a, lane, wi, plan, y0, rows, ring);
+  int trips = 0;
+  if (n > 0) {
+    // EDGE if this strip needs the 3-word seam fetch.
+    const int64_t wi = static_cast<int64_t>(strip) * kStripStride + lane - 1;
+    const bool edge = a.width < 32 || __any_sync(kFull, make_plan(wi, a.width, a.nw).mode != 0);
+    if (edge) {
+      trips = packed_segment<K, true>(a, lane, strip, static_cast<int>(y0), n, ring);
+    } else {
+      trips = packed_segment<K, false>(a, lane, strip, static_cast<int>(y0), n, ring);
+    }
   }
+#ifndef LIFE_NO_LOCKSTEP
+  // Shorter (last) segments and spare warps pad to the block's trip count.
+  for (; trips < a.steps; ++trips) __syncthreads();
+#endif
 #ifdef LIFE_TRACE
   if (lane == 0) {
     uint64_t t_end;

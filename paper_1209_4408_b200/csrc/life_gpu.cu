@@ -121,14 +121,32 @@ int launch_packed(PackedStepArgs a, cudaStream_t s) {
   LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, packed_tb_kernel<K>,
                                                           32 * wpb, wpb * PackedTraits<K>::kRingBytes));
 #endif
-  const int64_t resident_warps = static_cast<int64_t>(wpb) * blocks_per_sm * sm_count();
-  // One wave: split rows so that n_strips * n_segs ~ resident warps, with
-  // segments at least 4K rows tall (vertical pipeline fill <= 3K/seg).
-  const int64_t segs_target = std::max<int64_t>(1, resident_warps / a.n_strips);
-  a.seg_rows = std::max<int64_t>(ceil_div(a.out_rows, segs_target), 4 * K);
-  const int64_t n_segs = ceil_div(a.out_rows, a.seg_rows);
-  const int64_t warps = n_segs * a.n_strips;
-  const int64_t blocks = ceil_div(warps, wpb);
+  // Tiles of seg_rows rows x one strip; pick the segment count that
+  // minimises (block waves) x (rows per tile + pipeline fill): blocks run
+  // in lockstep internally, and the last wave's idle SMs are the loss.
+  constexpr int kLag = PackedTraits<K>::kLag;
+  constexpr int PF = PackedTraits<K>::kPrefetch;
+  if (a.out_rows >= (int64_t(1) << 31) || a.in_rows >= (int64_t(1) << 31) ||
+      a.in_pitch * 4 >= (int64_t(1) << 32) || a.out_pitch * 4 >= (int64_t(1) << 32))
+    return set_error(LIFE_ERR_CONFIG, "grid too large for one packed pass");
+  const int64_t slots = static_cast<int64_t>(blocks_per_sm) * sm_count();  // blocks per wave
+  int64_t best_segs = 1;
+  double best_cost = 1e300;
+  const int64_t max_segs = std::max<int64_t>(1, std::min<int64_t>(a.out_rows / (4 * K) + 1, 4096));
+  for (int64_t segs = 1; segs <= max_segs; ++segs) {
+    const int64_t rows = ceil_div(a.out_rows, segs);
+    const int64_t blocks = ceil_div(static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, rows), wpb);
+    // + 64 rows per wave: block start-up and pipeline refill.
+    const double cost = double(ceil_div(blocks, slots)) * double(rows + kLag + PF + 64);
+    if (cost < best_cost * 0.999) {
+      best_cost = cost;
+      best_segs = segs;
+    }
+  }
+  a.seg_rows = ceil_div(a.out_rows, best_segs);
+  const int64_t tiles = static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, a.seg_rows);
+  a.steps = static_cast<int32_t>(ceil_div(a.seg_rows + kLag, PF));
+  const int64_t blocks = ceil_div(tiles, wpb);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
   packed_tb_kernel<K><<<static_cast<unsigned>(blocks), 32 * wpb, wpb * PackedTraits<K>::kRingBytes, s>>>(a);
   LIFE_CHECK_LAUNCH("packed_tb_kernel");
@@ -208,7 +226,7 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
   a.width = width;
   a.out_rows = out_rows;
   a.nw = static_cast<int32_t>(nw32(width));
-  a.n_strips = static_cast<int32_t>(ceil_div(a.nw, kStripWords));
+  a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
   a.tail_mask = tail_mask(width);
   a.two = 2u;
   a.half = 0x80000000u;

@@ -88,48 +88,64 @@ def load_word(row, wi, W):
     return np.uint32(v & 0xFFFFFFFF)
 
 
-def model_packed_pass(p, W, K, seg_rows):
-    """Lane-exact model of packed_tb_kernel<K> over a torus (in_row0 = 0)."""
+def run_segment(p, W, K, strip, y, n, out):
+    """One pipeline segment of packed_pass: strip `strip`, output rows y..y+n-1."""
     H, nw = p.shape
-    out = np.zeros_like(p)
-    n_strips = -(-nw // 30)
+    wi = np.arange(32) + strip * 31 - 1
     tail = W % 32
     tail_mask = np.uint32(0xFFFFFFFF if tail == 0 else (1 << tail) - 1)
-    for strip in range(n_strips):
-        wi = np.arange(32) + strip * 30 - 1
-        for y0 in range(0, H, seg_rows):
-            rows = min(seg_rows, H - y0)
-            total = rows + 3 * K - 1
-            sa = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
-            sb = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
-            ss = [np.zeros(32, np.uint32) for _ in range(K)]
-            xin = [np.zeros(32, np.uint32) for _ in range(K)]
-            for i in range(total):
-                r = (y0 - K + i) % H
-                xin[0] = np.array([p[r, w] if (w >= 0 and (w + 1) * 32 <= W) else
-                                   load_word(p[r], w, W) for w in wi], np.uint32)
-                ys = []
-                for g in range(K):  # skewed: stage g eats stage g-1's previous output
-                    x = xin[g]
-                    xl = np.concatenate([x[:1], x[:-1]])   # shfl_up: lane 0 keeps own
-                    xr = np.concatenate([x[1:], x[-1:]])   # shfl_down: lane 31 keeps own
-                    c = hsum(xl, x, xr)
-                    ys.append(rule(sa[g], sb[g], c, ss[g]))
-                    sa[g], sb[g], ss[g] = sb[g], c, x
-                for g in range(1, K):
-                    xin[g] = ys[g - 1]
-                if i >= 3 * K - 1:
-                    orow = y0 + i - (3 * K - 1)
-                    for lane in range(1, 31):
-                        w = wi[lane]
-                        if w < nw:
-                            out[orow, w] = ys[K - 1][lane] & (tail_mask if w == nw - 1 else M32)
+    lag = 3 * K - 1
+    sa = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
+    sb = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
+    ss = [np.zeros(32, np.uint32) for _ in range(K)]
+    xin = [np.zeros(32, np.uint32) for _ in range(K)]
+    for i in range(n + lag):
+        r = (y - K + i) % H
+        xin[0] = np.array([p[r, w] if (w >= 0 and (w + 1) * 32 <= W) else load_word(p[r], w, W)
+                           for w in wi], np.uint32)
+        ys = []
+        for g in range(K):  # skewed: stage g eats stage g-1's previous output
+            x = xin[g]
+            xl = np.concatenate([x[:1], x[:-1]])   # shfl_up: lane 0 keeps own
+            xr = np.concatenate([x[1:], x[-1:]])   # shfl_down: lane 31 keeps own
+            c = hsum(xl, x, xr)
+            ys.append(rule(sa[g], sb[g], c, ss[g]))
+            sa[g], sb[g], ss[g] = sb[g], c, x
+        for g in range(1, K):
+            xin[g] = ys[g - 1]
+        j = i - lag
+        if 0 <= j < n:
+            for lane in range(32):
+                w = wi[lane]
+                if not (0 <= w < nw):
+                    continue
+                v = int(ys[K - 1][lane] & (tail_mask if w == nw - 1 else M32))
+                cur = int(out[y + j, w])
+                if 1 <= lane <= 30:
+                    cur = v
+                elif lane == 0:   # high half of the word shared with the previous strip
+                    cur = (cur & 0xFFFF) | (v & 0xFFFF0000)
+                else:             # lane 31: low half
+                    cur = (cur & 0xFFFF0000) | (v & 0xFFFF)
+                out[y + j, w] = cur
+
+
+def model_packed_pass(p, W, K, seg_rows):
+    """Lane-exact model of packed_tb_kernel<K> over a torus: tiles of one
+    strip (32 lanes, strips advancing by 31 words) x seg_rows rows, each a
+    fresh pipeline."""
+    H, nw = p.shape
+    n_strips = -(-(nw + 1) // 31)
+    out = np.zeros_like(p)
+    for y0 in range(0, H, seg_rows):
+        for strip in range(n_strips):
+            run_segment(p, W, K, strip, y0, min(seg_rows, H - y0), out)
     return out
 
 
 @pytest.mark.parametrize("W,H,K,seg", [(3, 3, 1, 1), (5, 7, 3, 4), (31, 9, 4, 5), (33, 17, 16, 6),
                                        (64, 12, 2, 12), (97, 23, 5, 7), (1000, 11, 16, 64),
-                                       (1921, 6, 8, 4)])
+                                       (1921, 6, 8, 4), (992, 5, 16, 3), (961, 4, 2, 9)])
 def test_kernel_model_matches_oracle(oracle, W, H, K, seg):
     g = oracle.random_fill(W, H, 0.45, W * 31 + H)
     p = pack32(g)
