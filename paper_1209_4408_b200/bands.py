@@ -114,17 +114,24 @@ class BandDriver:
         r, p = self.geo.rank, self.geo.world
         return (r - 1) % p, (r + 1) % p  # above, below (torus ring)
 
+    def halo_views(self, k: int):
+        """(top rows, bottom rows, top ghost rows, bottom ghost rows) of the
+        current buffer for a depth-k pass."""
+        g = self.geo
+        a = self.buf[self.cur]
+        top = a[g.ghost:g.ghost + k]
+        bottom = a[g.ghost + g.band_rows - k:g.ghost + g.band_rows]
+        ghost_top = a[g.ghost - k:g.ghost]
+        ghost_bottom = a[g.ghost + g.band_rows:g.ghost + g.band_rows + k]
+        return top, bottom, ghost_top, ghost_bottom
+
     def post_exchange(self, k: int):
         """Sends my top/bottom k rows, receives k ghost rows on each side."""
         g = self.geo
         if g.world == 1:
             return None
-        a = self.buf[self.cur]
         up, down = self._peers()
-        top = a[g.ghost:g.ghost + k]
-        bottom = a[g.ghost + g.band_rows - k:g.ghost + g.band_rows]
-        ghost_top = a[g.ghost - k:g.ghost]
-        ghost_bottom = a[g.ghost + g.band_rows:g.ghost + g.band_rows + k]
+        top, bottom, ghost_top, ghost_bottom = self.halo_views(k)
         # Same issue order on every rank: per peer pair, the i-th send
         # matches the i-th receive (needed when up == down, world == 2).
         ops = [dist.P2POp(dist.isend, top, up, self.group),
@@ -141,26 +148,45 @@ class BandDriver:
                 w.wait()
 
     # -- one pass ------------------------------------------------------
+    def compute_interior(self, k: int) -> bool:
+        """Output rows [k, band-k): local rows only.  Returns False when the
+        band is too thin to split (compute_all must then run after the halos)."""
+        g = self.geo
+        n = g.band_rows
+        if not (self.overlap and n > 2 * k):
+            return False
+        a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
+        self.stepper(a, g.ghost + k, g.buf_rows, b, g.ghost + k, n - 2 * k, k)
+        return True
+
+    def compute_edges(self, k: int, interior_done: bool) -> None:
+        """The two k-row edge strips (or the whole band), after the halos."""
+        g = self.geo
+        n = g.band_rows
+        a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
+        if interior_done:
+            self.stepper(a, g.ghost, g.buf_rows, b, g.ghost, k, k)
+            self.stepper(a, g.ghost + n - k, g.buf_rows, b, g.ghost + n - k, k, k)
+        else:
+            self.stepper(a, g.ghost, g.buf_rows, b, g.ghost, n, k)
+
+    def finish_pass(self, k: int) -> None:
+        self.cur ^= 1
+        self.generations += k
+
     def pass_(self, k: int) -> None:
         g = self.geo
         if not 1 <= k <= g.depth:
             raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
-        a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
         if g.world == 1:
+            a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
             self.stepper(a, 0, g.height, b, 0, g.height, k)
         else:
             works = self.post_exchange(k)
-            n = g.band_rows
-            if self.overlap and n > 2 * k:
-                self.stepper(a, g.ghost + k, g.buf_rows, b, g.ghost + k, n - 2 * k, k)
-                self.wait(works)
-                self.stepper(a, g.ghost, g.buf_rows, b, g.ghost, k, k)
-                self.stepper(a, g.ghost + n - k, g.buf_rows, b, g.ghost + n - k, k, k)
-            else:
-                self.wait(works)
-                self.stepper(a, g.ghost, g.buf_rows, b, g.ghost, n, k)
-        self.cur ^= 1
-        self.generations += k
+            interior = self.compute_interior(k)
+            self.wait(works)
+            self.compute_edges(k, interior)
+        self.finish_pass(k)
 
     def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None) -> None:
         if generations < 0:
@@ -192,3 +218,48 @@ class BandDriver:
         if g.world > 1:
             dist.all_reduce(acc, group=self.group)
         return int(acc.item())
+
+
+class LocalBands:
+    """P row bands of one torus on ONE device, halos exchanged by device
+    copies instead of NCCL: exercises the band seams, ghost addressing and
+    interior/edge split of BandDriver with the real kernels on a single GPU
+    (no rank ever waits on another)."""
+
+    def __init__(self, width: int, height: int, parts: int, depth: int, device: torch.device,
+                 overlap: bool = True):
+        self.drivers = [BandDriver(make_geometry(width, height, r, parts, depth), device,
+                                   overlap=overlap) for r in range(parts)]
+
+    def init_random(self, density: float, seed: int) -> None:
+        for d in self.drivers:
+            d.init_random(density, seed)
+
+    def pass_(self, k: int) -> None:
+        ds = self.drivers
+        p = len(ds)
+        if p == 1:
+            ds[0].pass_(k)
+            return
+        views = [d.halo_views(k) for d in ds]
+        done = [d.compute_interior(k) for d in ds]
+        for r in range(p):
+            up, down = (r - 1) % p, (r + 1) % p
+            views[r][2].copy_(views[up][1])    # my top ghosts <- bottom rows of the band above
+            views[r][3].copy_(views[down][0])  # my bottom ghosts <- top rows of the band below
+        for d, i in zip(ds, done):
+            d.compute_edges(k, i)
+        for d in ds:
+            d.finish_pass(k)
+
+    def run(self, generations: int) -> None:
+        depth = self.drivers[0].geo.depth
+        done = 0
+        while done < generations:
+            k = min(depth, generations - done)
+            self.pass_(k)
+            done += k
+
+    def gather(self) -> torch.Tensor:
+        """The whole torus as packed uint32 rows (device)."""
+        return torch.cat([d.band() for d in self.drivers], dim=0)

@@ -1,0 +1,186 @@
+// life_gpu.hpp -- C++ host mirror of the reference's step-loop API over the
+// C-ABI of include/life_gpu.h (header only, C++20).
+//
+// Mirrors /root/reference/proj/core/include/life/engine.hpp:11-43:
+//     RunResult run(Grid&& initial, const RunConfig&, const std::vector<int>& checkpoints);
+//     Grid step_parallel(const Grid&, const Strategy&, int workers);
+// and the exception hierarchy of errors.hpp:9-60.  The functions are
+// templates over the grid type: any type with `width()`, `height()`,
+// `data()` (uint8_t*, row-major, W*H bytes) and a `(width, height)`
+// constructor works -- including the reference's own `life::Grid`
+// (grid.hpp:24-70), which is what makes this a drop-in for its `run()`
+// (see INTEGRATION.md).  Populations are uint64 (grid.cpp:40-46's int
+// overflows above 2^31-1).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "life_gpu.h"
+
+namespace lifegpu {
+
+// errors.hpp:9-60
+class Error : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+class ConfigError : public Error {
+ public:
+  using Error::Error;
+};
+class DimensionTooSmall : public ConfigError {
+ public:
+  using ConfigError::ConfigError;
+};
+class TooManyParts : public ConfigError {
+ public:
+  using ConfigError::ConfigError;
+};
+class OutOfBounds : public ConfigError {
+ public:
+  using ConfigError::ConfigError;
+};
+class CudaError : public Error {
+ public:
+  using Error::Error;
+};
+
+inline void check(int rc) {
+  if (rc == LIFE_OK) return;
+  const std::string msg = life_last_error();
+  switch (rc) {
+    case LIFE_ERR_CONFIG: throw ConfigError(msg);
+    case LIFE_ERR_DIMENSION_TOO_SMALL: throw DimensionTooSmall(msg);
+    case LIFE_ERR_TOO_MANY_PARTS: throw TooManyParts(msg);
+    case LIFE_ERR_OUT_OF_BOUNDS: throw OutOfBounds(msg);
+    case LIFE_ERR_CUDA:
+    case LIFE_ERR_NO_DEVICE:
+    case LIFE_ERR_OUT_OF_MEMORY: throw CudaError(msg);
+    default: throw Error(msg);
+  }
+}
+
+enum class Engine { Packed = LIFE_ENGINE_PACKED, Byte = LIFE_ENGINE_BYTE };
+
+// RunConfig (engine.hpp:11-15) with the GPU strategy fields.
+struct RunConfig {
+  Engine engine = Engine::Packed;
+  int temporal_depth = 0;  // generations per packed kernel pass, 0 = 16
+  int workers = 1;         // validated like the reference (>= 1, <= rows)
+  int64_t iterations = 0;
+  int device = 0;
+};
+
+// RunStats (engine.hpp:17-22) with uint64 populations.
+struct RunStats {
+  int64_t generations_computed = 0;
+  std::vector<std::pair<int64_t, uint64_t>> population_checkpoints;
+};
+
+template <class GridT>
+struct RunResult {
+  GridT grid;
+  RunStats stats;
+};
+
+// One C-ABI context: a grid resident on one GPU.
+class Context {
+ public:
+  explicit Context(int device = 0) { check(life_ctx_create(device, &ctx_)); }
+  ~Context() { life_ctx_destroy(ctx_); }
+  Context(const Context&) = delete;
+  Context& operator=(const Context&) = delete;
+
+  template <class GridT>
+  void upload(const GridT& g) {
+    check(life_grid_upload_u8(ctx_, g.data(), g.width(), g.height(), g.width()));
+  }
+  void init_random(int64_t w, int64_t h, double density, uint64_t seed,
+                   Engine e = Engine::Packed) {
+    check(life_grid_init_random(ctx_, w, h, density, seed, static_cast<int>(e)));
+  }
+  template <class GridT>
+  void download(GridT& g) {
+    check(life_grid_download_u8(ctx_, g.data(), g.width()));
+  }
+  std::vector<uint64_t> run(int64_t generations, Engine e, int depth,
+                            const std::vector<int64_t>& checkpoints) {
+    std::vector<uint64_t> pops(checkpoints.size());
+    check(life_run(ctx_, generations, static_cast<int>(e), depth,
+                   checkpoints.empty() ? nullptr : checkpoints.data(),
+                   static_cast<int32_t>(checkpoints.size()), pops.empty() ? nullptr : pops.data()));
+    return pops;
+  }
+  uint64_t population() {
+    uint64_t p = 0;
+    check(life_population(ctx_, &p));
+    return p;
+  }
+  std::vector<uint8_t> window(int64_t x0, int64_t y0, int64_t w, int64_t h) {
+    std::vector<uint8_t> out(static_cast<size_t>(w * h));
+    check(life_grid_window_u8(ctx_, x0, y0, w, h, out.data()));
+    return out;
+  }
+  life_ctx* handle() const { return ctx_; }
+
+ private:
+  life_ctx* ctx_ = nullptr;
+};
+
+// run (engine.cpp:157-214): check_run_config's rules (:127-148) and
+// partition_rows' TooManyParts (decomposition.cpp:26-30) on `workers`, then
+// `iterations` generations on the GPU; checkpoint 0 is the initial grid.
+// Takes the grid by value: an rvalue moves in (the reference's Grid&&
+// overload), an lvalue is copied (its const Grid& overload, engine.cpp:157-160).
+template <class GridT>
+RunResult<GridT> run(GridT initial, const RunConfig& cfg,
+                     const std::vector<int64_t>& checkpoints = {}) {
+  if (cfg.workers < 1)
+    throw ConfigError("worker count must be at least 1, got " + std::to_string(cfg.workers));
+  if (cfg.workers > initial.height())
+    throw TooManyParts("cannot split " + std::to_string(initial.height()) + " rows into " +
+                       std::to_string(cfg.workers) + " non-empty parts");
+  if (cfg.iterations < 0)
+    throw ConfigError("iteration count must be non-negative, got " +
+                      std::to_string(cfg.iterations));
+  int64_t prev = -1;
+  for (int64_t cp : checkpoints) {
+    if (cp < 0 || cp > cfg.iterations)
+      throw ConfigError("checkpoint " + std::to_string(cp) + " is outside [0, iterations=" +
+                        std::to_string(cfg.iterations) + "]");
+    if (cp <= prev) throw ConfigError("checkpoints must be strictly ascending");
+    prev = cp;
+  }
+  Context ctx(cfg.device);
+  ctx.upload(initial);
+  const std::vector<uint64_t> pops = ctx.run(cfg.iterations, cfg.engine, cfg.temporal_depth, checkpoints);
+  ctx.download(initial);
+  RunStats stats;
+  stats.generations_computed = cfg.iterations;
+  for (size_t i = 0; i < checkpoints.size(); ++i)
+    stats.population_checkpoints.emplace_back(checkpoints[i], pops[i]);
+  return RunResult<GridT>{std::move(initial), std::move(stats)};
+}
+
+// step_parallel (engine.cpp:152-155).
+template <class GridT>
+GridT step_parallel(const GridT& grid, RunConfig cfg) {
+  cfg.iterations = 1;
+  return run(grid, cfg).grid;
+}
+
+// random_fill (pattern.cpp:330-342), generated on the device.
+template <class GridT>
+GridT random_fill(int width, int height, double density, uint64_t seed, int device = 0) {
+  GridT g(width, height);
+  Context ctx(device);
+  ctx.init_random(width, height, density, seed, Engine::Byte);
+  ctx.download(g);
+  return g;
+}
+
+}  // namespace lifegpu
