@@ -132,41 +132,52 @@ def cpu_engine():
     return "port", Oracle()
 
 
-def cpu_measure(cfg: dict, budget_s: float, variants=("blocks",)) -> dict:
+def cpu_measure(cfg: dict, budget_s: float,
+                variants=("serial", "rows", "cols", "blocks")) -> dict:
     """Times the reference's run() (bench.cpp:77-111 time_run semantics: the
     timer includes run()'s buffer allocation and thread spawn) on a bounded
     sample of the workload: a 8192x8192 torus with the config's density and
-    seed, generations sized to ~budget_s per variant."""
+    seed, generations sized so all variants together take ~budget_s.  The
+    reference's parallel variants are its Strategy::rows / cols / blocks(m,n)
+    over std::thread workers = all host threads (it has no OpenMP code,
+    SURVEY.md section 0); serial is the single-threaded baseline."""
     kind, eng = cpu_engine()
     threads = os.cpu_count() or 1
     side = min(8192, cfg["w"], cfg["h"])
+    if kind != "reference":
+        variants = ("serial",)
+    share = {v: (0.1 if v == "serial" and len(variants) > 1 else 1.0) for v in variants}
+    norm = sum(share.values())
     res = {}
     for var in variants:
+        per = budget_s * share[var] / norm
         workers = 1 if var == "serial" else threads
         bx, by = blocks_shape(threads) if var == "blocks" else (1, 1)
         if kind == "reference":
-            t1, _, _ = eng.time_run(side, side, 2, var, workers, (bx, by), 42, cfg["p"], 1, 0)
-            gens = max(2, int(budget_s / max(t1 / 2, 1e-6)))
+            cal = 4 if var == "serial" else 12
+            t1, _, _ = eng.time_run(side, side, cal, var, workers, (bx, by), 42, cfg["p"], 1, 0)
+            gens = max(2, int(per / max(t1 / cal, 1e-6)))
             t, _, hw = eng.time_run(side, side, gens, var, workers, (bx, by), 42, cfg["p"], 1, 0)
-            cores = workers
         else:  # single-threaded C port of compute_region
             g = eng.random_fill(side, side, cfg["p"], 42)
             t0 = time.perf_counter()
             eng.run(g, 1)
             t1 = time.perf_counter() - t0
-            gens = max(1, int(budget_s / max(t1, 1e-6)))
+            gens = max(1, int(per / max(t1, 1e-6)))
             t0 = time.perf_counter()
             eng.run(g, gens)
             t = time.perf_counter() - t0
-            cores = 1
-        res[var] = {"value": side * side * gens / t / 1e9, "seconds": t, "gens": gens,
-                    "cores": cores}
+            workers = 1
+        name = f"blocks:{bx}x{by}" if var == "blocks" else var
+        res[name] = {"value": side * side * gens / t / 1e9, "seconds": round(t, 3), "gens": gens,
+                     "threads": workers}
     best = max(res, key=lambda v: res[v]["value"])
-    return {"value": res[best]["value"], "unit": UNIT, "cores": res[best]["cores"], "kind": kind,
+    return {"value": res[best]["value"], "unit": UNIT, "cores": res[best]["threads"], "kind": kind,
             "sample": f"{side}x{side} torus, p={cfg['p']}, seed 42, {res[best]['gens']} generations, "
-                      f"strategy {best} x{res[best]['cores']} threads (reference time_run; "
-                      f"timer includes allocation + thread spawn)",
-            "variants": {k: round(v["value"], 4) for k, v in res.items()},
+                      f"best reference variant = {best} x{res[best]['threads']} threads "
+                      f"(reference time_run; timer includes allocation + thread spawn)",
+            "variants": {k: {"gcups": round(v["value"], 4), "threads": v["threads"],
+                             "gens": v["gens"], "seconds": v["seconds"]} for k, v in res.items()},
             "host_threads": threads}
 
 
@@ -347,30 +358,22 @@ def run_gpu_arm(args) -> None:
     # ---- e2e through the public API, host buffers ------------------------
     e2e = None
     if not args.no_e2e:
-        steps_e2e = max(1, min(args.steps, 3))
+        steps_e2e = max(2, args.steps)
         if world == 1:
+            # life_run_batch: every step uploads its 8 GiB packed grid from
+            # pinned memory, runs the generations and downloads the result;
+            # step i's copies overlap step i+-1's compute (copy engines).
             eng = Engine(local)
-            stream = torch.cuda.Stream(dev)
-            eng.set_stream(stream.cuda_stream)
             wpr = math.ceil(W / 64)
-            host = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
+            host_in = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
+            host_out = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
             eng.init_random(W, H, cfg["p"], 42, capi.ENGINE_PACKED)
-            eng.download_packed(host.numpy().view("uint64"))
-            hv = host.numpy().view("uint64")
-            ms = []
-            for i in range(1 + steps_e2e):
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                eng.upload_packed(hv, W)
-                eng.run(gens, capi.ENGINE_PACKED, depth)
-                eng.download_packed(hv)
-                e1.record(stream)
-                e1.synchronize()
-                if i > 0:
-                    ms.append(e0.elapsed_time(e1))
+            hin = host_in.numpy().view("uint64")
+            hout = host_out.numpy().view("uint64")
+            eng.download_packed(hin)
+            eng.run_batch([hin], [hout], W, gens, depth)  # warm-up (allocates buffers)
+            e2e_ms = eng.run_batch([hin] * steps_e2e, [hout] * steps_e2e, W, gens, depth)
             eng.close()
-            e2e_ms = sum(ms)
             bi = bo = H * wpr * 8
         else:
             drv = BandDriver(geo, dev)
@@ -397,7 +400,8 @@ def run_gpu_arm(args) -> None:
             del drv
         e2e = {"value": W * H * gens * steps_e2e / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
-               "api": "C-ABI life_grid_upload_packed + life_run + life_grid_download_packed"
+               "api": "C-ABI life_run_batch (per step: H2D packed grid, run, D2H; copies "
+                      "overlapped with the neighbouring steps' compute)"
                       if world == 1 else "BandDriver band upload/run/download (pinned host)",
                "steps": steps_e2e}
 
@@ -431,6 +435,81 @@ def run_gpu_arm(args) -> None:
         dist.destroy_process_group()
 
 
+def run_byte_arm(args) -> None:
+    """The byte engine (one generation per pass, 2 B of HBM per cell-update)
+    on one GPU: config's grid, per-launch CUDA events, HBM roofline."""
+    import torch
+
+    from paper_1209_4408_b200 import capi
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": "byte engine is single-GPU"}))
+        return
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    L = capi.lib()
+    cfg = CONFIGS[args.config]
+    W, H, gens = cfg["w"], cfg["h"], args.gens or cfg["gens"]
+    pitch = int(L.life_byte_pitch(W))
+    if 2 * pitch * H > 120e9:
+        print(json.dumps({"metric": METRIC, "unavailable": "grid too large for the byte layout"}))
+        return
+    bufs = [torch.zeros((H, pitch), dtype=torch.uint8, device=dev) for _ in range(2)]
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    from paper_1209_4408_b200.life import check
+    check(L.life_dev_byte_random(bufs[0].data_ptr(), pitch, W, 0, H, cfg["p"], 42, stream))
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if 2 * pitch * H < 4 * L2_BYTES else None
+    launches = []
+    cur = [0]
+
+    def step(record: bool):
+        for _ in range(gens):
+            a, b = bufs[cur[0]], bufs[cur[0] ^ 1]
+            if record:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            check(L.life_dev_byte_step(a.data_ptr(), pitch, 0, H, b.data_ptr(), pitch, 0, W, H, stream))
+            if record:
+                e1.record()
+                launches.append((e0, e1))
+            cur[0] ^= 1
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    l0 = L.life_kernel_launches()
+    ms = []
+    with ClockSampler(0) as clocks:
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.fill_(1)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step(True)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+    n_launch = int(L.life_kernel_launches() - l0)
+    kern_ms = sum(a.elapsed_time(b) for a, b in launches) / max(len(launches), 1)
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = 2.0 * W * H / (kern_ms * 1e-3) / 1e9
+    value = W * H * gens * args.steps / (sum(ms) * 1e-3) / 1e9
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sum(ms) / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8 (byte per cell)", "data": "synthetic",
+        "config": {"workload": cfg["desc"].replace("bit-packed engine", "byte engine"),
+                   "engine": "byte", "generations": gens,
+                   "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
+        "roofline": {"bound": "hbm", "kernel": "byte_step_kernel", "achieved": achieved,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
+                     "bytes_per_cell_update": 2.0, "mean_launch_ms": kern_ms,
+                     "traffic": ncu_traffic(args.config, 0)},
+        "gpu_launches": n_launch, "clocks": clocks.summary()}), flush=True)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -442,10 +521,13 @@ def main() -> None:
     ap.add_argument("--gens", type=int, default=0, help="override the config's generations")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--engine", choices=["packed", "byte"], default="packed")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.engine == "byte":
+        run_byte_arm(args)
     else:
         run_gpu_arm(args)
 

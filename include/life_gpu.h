@@ -106,6 +106,17 @@ int life_run(life_ctx* ctx, int64_t generations, int engine, int temporal_depth,
              const int64_t* checkpoints, int32_t n_checkpoints, uint64_t* populations);
 /* Replaces step_parallel (engine.cpp:152-155): run(..., iterations = 1). */
 int life_step(life_ctx* ctx, int engine);
+/* Throughput form of run() for a stream of independent packed grids (same
+ * W x H; the reference's time_run repetitions, bench.cpp:101-107): each of the
+ * `n` host grids inputs[i] is uploaded, run for `generations` on the packed
+ * engine and downloaded to outputs[i] (may alias inputs[i]).  The H2D copy of
+ * grid i+1 and the D2H copy of grid i-1 overlap the compute of grid i (copy
+ * engines, three streams); use pinned host memory for the overlap.
+ * *elapsed_ms (optional) = CUDA-event time from the first upload to the last
+ * download.  The context's resident grid is not touched. */
+int life_run_batch(life_ctx* ctx, const uint64_t* const* inputs, uint64_t* const* outputs,
+                   int32_t n, int64_t width, int64_t height, int64_t words_per_row,
+                   int64_t generations, int temporal_depth, float* elapsed_ms);
 
 /* ---- row-band decomposition (multi-GPU) --------------------------------- */
 /* Mirrors band_bounds / partition_rows (decomposition.cpp:12-24, :93-104):
@@ -135,6 +146,9 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
 /* Rows [y0, y0+rows) of random_fill(W, H, density, seed) into a packed buffer. */
 int life_dev_packed_random(uint32_t* out, int64_t pitch, int64_t width, int64_t y0,
                            int64_t rows, double density, uint64_t seed, void* stream);
+/* The same rows of the soup in the byte layout (pitch a multiple of 16). */
+int life_dev_byte_random(uint8_t* out, int64_t pitch, int64_t width, int64_t y0, int64_t rows,
+                         double density, uint64_t seed, void* stream);
 /* Adds the population of `rows` packed rows to *dev_count (device uint64). */
 int life_dev_packed_population(const uint32_t* grid, int64_t pitch, int64_t width,
                                int64_t rows, uint64_t* dev_count, void* stream);

@@ -48,6 +48,8 @@ SIGNATURES = [
     ("life_population", C.c_int, [_vp, C.POINTER(_u64)]),
     ("life_run", C.c_int, [_vp, _i64, C.c_int, C.c_int, _vp, _i32, _vp]),
     ("life_step", C.c_int, [_vp, C.c_int]),
+    ("life_run_batch", C.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _i64, C.c_int,
+                                 C.POINTER(C.c_float)]),
     ("life_band_bounds", C.c_int, [_i64, _i32, _vp]),
     ("life_packed_pitch_words", _i64, [_i64]),
     ("life_byte_pitch", _i64, [_i64]),
@@ -55,6 +57,7 @@ SIGNATURES = [
                                        _vp]),
     ("life_dev_byte_step", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
     ("life_dev_packed_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),
+    ("life_dev_byte_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),
     ("life_dev_packed_population", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
     ("life_dev_pack", C.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
     ("life_dev_unpack", C.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),

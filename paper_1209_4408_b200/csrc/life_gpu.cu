@@ -287,6 +287,18 @@ int life_dev_packed_random(uint32_t* out, int64_t pitch, int64_t width, int64_t 
   return LIFE_OK;
 }
 
+int life_dev_byte_random(uint8_t* out, int64_t pitch, int64_t width, int64_t y0, int64_t rows,
+                         double density, uint64_t seed, void* stream) {
+  if (!(density >= 0.0 && density <= 1.0))
+    return set_error(LIFE_ERR_CONFIG, "density must be in [0, 1], got %f", density);
+  if ((pitch & 15) || pitch < width) return set_error(LIFE_ERR_CONFIG, "bad byte pitch");
+  const int64_t n = rows * (pitch / 16);
+  byte_random_kernel<<<grid_stride_blocks(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      out, pitch, width, y0, rows, seed, density_threshold(density));
+  LIFE_CHECK_LAUNCH("byte_random_kernel");
+  return LIFE_OK;
+}
+
 int life_dev_packed_population(const uint32_t* grid, int64_t pitch, int64_t width, int64_t rows,
                                uint64_t* dev_count, void* stream) {
   const int64_t n = rows * pitch;
@@ -366,6 +378,10 @@ struct life_ctx {
   int64_t counts_cap = 0;
   uint8_t* window = nullptr;
   int64_t window_cap = 0;
+  // life_run_batch: 2 slots x (upload/ping, pong) buffers and copy streams
+  uint32_t* batch[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t batch_bytes = 0;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
 };
 
 namespace {
@@ -503,6 +519,10 @@ int life_ctx_destroy(life_ctx* c) {
   free_buffers(c);
   if (c->counts) cudaFree(c->counts);
   if (c->window) cudaFree(c->window);
+  for (auto& b : c->batch)
+    if (b) cudaFree(b);
+  if (c->h2d) cudaStreamDestroy(c->h2d);
+  if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return LIFE_OK;
@@ -585,10 +605,8 @@ int life_grid_init_random(life_ctx* c, int64_t width, int64_t height, double den
   } else {
     LIFE_TRY(ensure_byte(c));
     c->by_cur = 0;
-    const int64_t n = height * (c->by_pitch / 16);
-    byte_random_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(
-        c->by[0], c->by_pitch, width, 0, height, seed, density_threshold(density));
-    LIFE_CHECK_LAUNCH("byte_random_kernel");
+    LIFE_TRY(life_dev_byte_random(c->by[0], c->by_pitch, width, 0, height, density, seed,
+                                  c->stream));
     c->layout = kByte;
   }
   LIFE_CUDA(cudaStreamSynchronize(c->stream));
@@ -739,5 +757,97 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
 }
 
 int life_step(life_ctx* c, int engine) { return life_run(c, 1, engine, 1, nullptr, 0, nullptr); }
+
+int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* outputs, int32_t n,
+                   int64_t width, int64_t height, int64_t words_per_row, int64_t generations,
+                   int temporal_depth, float* elapsed_ms) {
+  LIFE_TRY(activate(c));
+  LIFE_TRY(check_dims(width, height));
+  if (n < 0 || (n > 0 && (!inputs || !outputs)))
+    return set_error(LIFE_ERR_CONFIG, "bad batch buffers");
+  if (generations < 0)
+    return set_error(LIFE_ERR_CONFIG, "iteration count must be non-negative, got %lld",
+                     static_cast<long long>(generations));
+  int depth = temporal_depth == 0 ? LIFE_MAX_TEMPORAL_DEPTH : temporal_depth;
+  if (depth < 1 || depth > LIFE_MAX_TEMPORAL_DEPTH)
+    return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [0, %d], got %d",
+                     LIFE_MAX_TEMPORAL_DEPTH, temporal_depth);
+  const int64_t wpr = ceil_div(width, 64);
+  if (words_per_row < wpr) return set_error(LIFE_ERR_CONFIG, "words_per_row < ceil(W/64)");
+  if (n == 0) return LIFE_OK;
+  const int64_t pitch = life_packed_pitch_words(width);
+  const size_t bytes = static_cast<size_t>(pitch) * height * 4;
+  if (c->batch_bytes != bytes) {
+    for (auto& b : c->batch) {
+      if (b) cudaFree(b);
+      b = nullptr;
+    }
+    c->batch_bytes = 0;
+    for (auto& b : c->batch) {
+      LIFE_CUDA(cudaMalloc(&b, bytes));
+      LIFE_CUDA(cudaMemsetAsync(b, 0, bytes, c->stream));
+    }
+    c->batch_bytes = bytes;
+    LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  if (!c->h2d) LIFE_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  if (!c->d2h) LIFE_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  std::vector<cudaEvent_t> up(n), comp(n), down(n);
+  cudaEvent_t t0, t1;
+  LIFE_CUDA(cudaEventCreate(&t0));
+  LIFE_CUDA(cudaEventCreate(&t1));
+  for (int32_t i = 0; i < n; ++i) {
+    LIFE_CUDA(cudaEventCreateWithFlags(&up[i], cudaEventDisableTiming));
+    LIFE_CUDA(cudaEventCreateWithFlags(&comp[i], cudaEventDisableTiming));
+    LIFE_CUDA(cudaEventCreateWithFlags(&down[i], cudaEventDisableTiming));
+  }
+  const int32_t nw = static_cast<int32_t>(nw32(width));
+  LIFE_CUDA(cudaEventRecord(t0, c->h2d));
+  int rc = LIFE_OK;
+  for (int32_t i = 0; i < n && rc == LIFE_OK; ++i) {
+    uint32_t* a = c->batch[2 * (i & 1)];
+    uint32_t* b = c->batch[2 * (i & 1) + 1];
+    // Upload grid i into its slot once grid i-2 has left it.
+    if (i >= 2) LIFE_CUDA(cudaStreamWaitEvent(c->h2d, down[i - 2], 0));
+    LIFE_CUDA(cudaMemcpy2DAsync(a, pitch * 4, inputs[i], words_per_row * 8, wpr * 8, height,
+                                cudaMemcpyHostToDevice, c->h2d));
+    LIFE_CUDA(cudaEventRecord(up[i], c->h2d));
+    // Compute on the context stream.
+    LIFE_CUDA(cudaStreamWaitEvent(c->stream, up[i], 0));
+    const int64_t mask_n = height * (pitch - nw + 1);
+    packed_mask_tail_kernel<<<grid_stride_blocks(mask_n, 256), 256, 0, c->stream>>>(
+        a, pitch, nw, tail_mask(width), height);
+    LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
+    uint32_t* cur = a;
+    uint32_t* nxt = b;
+    for (int64_t done = 0; done < generations && rc == LIFE_OK;) {
+      const int step = static_cast<int>(std::min<int64_t>(depth, generations - done));
+      rc = life_dev_packed_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, step,
+                                c->stream);
+      std::swap(cur, nxt);
+      done += step;
+    }
+    LIFE_CUDA(cudaEventRecord(comp[i], c->stream));
+    // Download on the D2H stream.
+    LIFE_CUDA(cudaStreamWaitEvent(c->d2h, comp[i], 0));
+    LIFE_CUDA(cudaMemcpy2DAsync(outputs[i], words_per_row * 8, cur, pitch * 4, wpr * 8, height,
+                                cudaMemcpyDeviceToHost, c->d2h));
+    LIFE_CUDA(cudaEventRecord(down[i], c->d2h));
+  }
+  LIFE_CUDA(cudaEventRecord(t1, c->d2h));
+  LIFE_CUDA(cudaEventSynchronize(t1));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  float ms = 0;
+  LIFE_CUDA(cudaEventElapsedTime(&ms, t0, t1));
+  if (elapsed_ms) *elapsed_ms = ms;
+  for (int32_t i = 0; i < n; ++i) {
+    cudaEventDestroy(up[i]);
+    cudaEventDestroy(comp[i]);
+    cudaEventDestroy(down[i]);
+  }
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  return rc;
+}
 
 }  // extern "C"

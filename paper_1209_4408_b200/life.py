@@ -307,6 +307,26 @@ class Engine:
     def step(self, engine: int = capi.ENGINE_PACKED) -> None:
         check(self._lib.life_step(self._ctx, engine))
 
+    def run_batch(self, inputs: Sequence[np.ndarray], outputs: Sequence[np.ndarray], width: int,
+                  generations: int, depth: int = 0) -> float:
+        """life_run_batch: packed host grids (uint64 rows) in, results out,
+        copies overlapped with compute.  Returns the CUDA-event time in ms."""
+        n = len(inputs)
+        if len(outputs) != n:
+            raise ConfigError("inputs and outputs differ in length")
+        if n == 0:
+            return 0.0
+        h, wpr = inputs[0].shape
+        for a in list(inputs) + list(outputs):
+            if a.shape != (h, wpr) or a.dtype != np.uint64 or not a.flags.c_contiguous:
+                raise ConfigError("batch buffers must be C-contiguous uint64 (H, words_per_row)")
+        ins = (C.c_void_p * n)(*[a.ctypes.data for a in inputs])
+        outs = (C.c_void_p * n)(*[a.ctypes.data for a in outputs])
+        ms = C.c_float()
+        check(self._lib.life_run_batch(self._ctx, ins, outs, n, width, h, wpr, generations, depth,
+                                       C.byref(ms)))
+        return float(ms.value)
+
 
 def _check_workers(config: RunConfig, height: int) -> None:
     if config.workers < 1:

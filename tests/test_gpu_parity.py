@@ -245,3 +245,20 @@ def test_cfg5_lightcone_windows(engine, oracle):
     engine.run(500 - 16, PACKED, 16)
     for w in gold["windows_500"]:
         assert fnv(oracle, engine.window(w["x0"], w["y0"], w["S"], w["S"])) == w["fnv_bytes"], w
+
+
+def test_run_batch_pipelined(engine, oracle):
+    """life_run_batch: every grid of the stream equals the oracle run; outputs may alias inputs."""
+    W, H, G = 1000, 77, 37
+    grids = [oracle.random_fill(W, H, 0.3 + 0.1 * i, i) for i in range(5)]
+    ins = [oracle.pack(g) for g in grids]
+    outs = [np.zeros_like(p) for p in ins]
+    ms = engine.run_batch(ins, outs, W, G, 8)
+    assert ms > 0
+    for g, out in zip(grids, outs):
+        want, _ = oracle.run(g, G)
+        assert np.array_equal(oracle.unpack(out, W), want)
+    engine.run_batch(ins, ins, W, G, 16)  # in-place
+    for g, out in zip(grids, ins):
+        want, _ = oracle.run(g, G)
+        assert np.array_equal(oracle.unpack(out, W), want)
