@@ -192,14 +192,15 @@ def run_reference_arm(args) -> None:
     bx, by = blocks_shape(threads)
     # calibrate so the whole K+W run stays within ~3 minutes
     if kind == "reference":
-        t1, _, _ = eng.time_run(side, side, 2, "blocks", threads, (bx, by), 42, cfg["p"], 1, 0)
+        t1, _, _ = eng.time_run(side, side, 12, "blocks", threads, (bx, by), 42, cfg["p"], 1, 0)
+        per_gen = t1 / 12
     else:
         g = eng.random_fill(side, side, cfg["p"], 42)
         t0 = time.perf_counter()
         eng.run(g, 1)
-        t1 = 2 * (time.perf_counter() - t0)
+        per_gen = time.perf_counter() - t0
     per_step = min(20.0, 170.0 / max(1, args.steps + args.warmup))
-    gens = max(1, int(per_step / max(t1 / 2, 1e-6)))
+    gens = max(1, int(per_step / max(per_gen, 1e-6)))
     times = []
     for i in range(args.warmup + args.steps):
         if kind == "reference":
