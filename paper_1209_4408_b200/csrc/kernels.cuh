@@ -509,10 +509,19 @@ __device__ __forceinline__ ByteRow byte_row(const uint4 v, uint32_t left_byte,
   return row;
 }
 
-struct ByteRaw {
-  uint4 v;
-  uint32_t lb, rb, col0;
-};
+// Byte-engine row staging: a per-warp shared-memory ring of kByteRing rows
+// filled by cp.async kByteRing-1 rows ahead.  A slot holds each lane's
+// 16-byte vector plus three 4-byte words for the lanes that need a neighbour
+// byte from outside the warp (left of lane 0, right of lane 31) or column 0
+// at the torus seam.
+constexpr int kByteRing = 8;
+constexpr int kByteSlotWords = 32 * 4 + 32 * 3;
+constexpr int kByteSmem = (kByteThreads / 32) * kByteRing * kByteSlotWords * 4;  // per block
+
+__device__ __forceinline__ void cp_async16(uint32_t* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
 
 __global__ void __launch_bounds__(kByteThreads) byte_step_kernel(const ByteStepArgs a) {
   const int lane = threadIdx.x & 31;
@@ -529,55 +538,63 @@ __global__ void __launch_bounds__(kByteThreads) byte_step_kernel(const ByteStepA
   // Position of column W-1 inside this lane's vector, or -1.
   const int seam_pos =
       (active && a.width - 1 - c0 < 16) ? static_cast<int>(a.width - 1 - c0) : -1;
-  // Columns read by single-byte loads: lane 0 needs the column left of c0,
+  // Columns outside the warp's vectors: lane 0 needs the column left of c0,
   // lane 31 (or the seam lane) the column right of its vector.
   const int64_t left_col = c0 == 0 ? a.width - 1 : c0 - 1;
   const int64_t right_col = c0 + 16 < a.width ? c0 + 16 : 0;
   const bool need_left = active && lane == 0;
   const bool need_right = active && (lane == 31 || seam_pos == 15);
 
+  extern __shared__ uint32_t byte_ring[];
+  uint32_t* ring = byte_ring + (threadIdx.x >> 5) * (kByteRing * kByteSlotWords);
   int64_t lrow = wrap_row(a.in_row0, y0 - 1, a.in_rows);
-  // Issues the loads of the next input row (prefetched kBytePrefetch ahead).
-  auto fetch = [&]() -> ByteRaw {
+  auto issue = [&](int64_t step) {
     const uint8_t* row = a.in + lrow * a.in_pitch;
-    ByteRaw q;
-    q.v = active ? __ldg(reinterpret_cast<const uint4*>(row + c0)) : make_uint4(0, 0, 0, 0);
-    q.lb = need_left ? __ldg(row + left_col) : 0u;
-    q.rb = need_right ? __ldg(row + right_col) : 0u;
-    q.col0 = seam_pos >= 0 ? static_cast<uint32_t>(__ldg(row)) : 0u;
+    uint32_t* s = ring + (static_cast<int>(step) & (kByteRing - 1)) * kByteSlotWords;
+    if (active) cp_async16(s + lane * 4, row + c0);
+    if (need_left) cp_async4(s + 128 + lane, reinterpret_cast<const uint32_t*>(row + (left_col & ~3LL)));
+    if (need_right) cp_async4(s + 160 + lane, reinterpret_cast<const uint32_t*>(row + (right_col & ~3LL)));
+    if (seam_pos >= 0) cp_async4(s + 192 + lane, reinterpret_cast<const uint32_t*>(row));
+    cp_async_commit();
     if (++lrow == a.in_rows) lrow = 0;
-    return q;
   };
-  auto build = [&](const ByteRaw& q) -> ByteRow {
-    uint32_t lb = __shfl_up_sync(kFull, q.v.w >> 24, 1);
-    uint32_t rb = __shfl_down_sync(kFull, q.v.x & 0xffu, 1);
-    if (need_left) lb = q.lb;
-    if (need_right) rb = q.rb;
-    return byte_row(q.v, lb, rb, seam_pos, q.col0);
+  auto consume = [&](int64_t step) -> ByteRow {
+    const uint32_t* s = ring + (static_cast<int>(step) & (kByteRing - 1)) * kByteSlotWords;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (active) v = *reinterpret_cast<const uint4*>(s + lane * 4);
+    uint32_t lb = __shfl_up_sync(kFull, v.w >> 24, 1);
+    uint32_t rb = __shfl_down_sync(kFull, v.x & 0xffu, 1);
+    if (need_left) lb = (s[128 + lane] >> ((left_col & 3) * 8)) & 0xffu;
+    if (need_right) rb = (s[160 + lane] >> ((right_col & 3) * 8)) & 0xffu;
+    const uint32_t col0 = seam_pos >= 0 ? (s[192 + lane] & 0xffu) : 0u;
+    return byte_row(v, lb, rb, seam_pos, col0);
   };
 
-  ByteRaw pf[kBytePrefetch];
 #pragma unroll
-  for (int u = 0; u < kBytePrefetch; ++u) pf[u] = fetch();
-  ByteRow up = build(pf[0]);
-  pf[0] = fetch();
-  ByteRow mid = build(pf[1]);
-  pf[1] = fetch();
+  for (int u = 0; u < kByteRing - 1; ++u) issue(u);
+  issue(kByteRing - 1);
+  cp_async_wait<kByteRing - 1>();
+  ByteRow up = consume(0);
+  issue(kByteRing);
+  cp_async_wait<kByteRing - 1>();
+  ByteRow mid = consume(1);
 
   uint8_t* out_row = a.out + (a.out_row0 + y0) * a.out_pitch + c0;
   for (int64_t r0 = 0; r0 < rows; r0 += kBytePrefetch) {
 #pragma unroll
     for (int u = 0; u < kBytePrefetch; ++u) {
-      const ByteRow dn = build(pf[(u + 2) % kBytePrefetch]);
-      pf[(u + 2) % kBytePrefetch] = fetch();
+      const int64_t t = r0 + u + 2;  // consumption step of the row below
+      issue(t + kByteRing - 1);
+      cp_async_wait<kByteRing - 1>();
+      const ByteRow dn = consume(t);
       uint32_t o[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const uint32_t n = up.h[i] + dn.h[i] + mid.hn[i];  // 8-neighbour count per byte
         // (n | self) == 3  <=>  next alive (engine.cpp:32 on 0/1 bytes);
         // t = (n|self)^3 is 0..15 per byte; zero-test via the byte's bit 7.
-        const uint32_t t = (n | mid.x[i]) ^ 0x03030303u;
-        o[i] = (~(t + 0x7f7f7f7fu) & 0x80808080u) >> 7;
+        const uint32_t tt = (n | mid.x[i]) ^ 0x03030303u;
+        o[i] = (~(tt + 0x7f7f7f7fu) & 0x80808080u) >> 7;
       }
       if (seam_pos >= 0) {  // zero the padding bytes past column W-1
         const int keep = seam_pos + 1;
@@ -596,6 +613,7 @@ __global__ void __launch_bounds__(kByteThreads) byte_step_kernel(const ByteStepA
       mid = dn;
     }
   }
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------

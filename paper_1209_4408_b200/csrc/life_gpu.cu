@@ -246,8 +246,10 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
   cudaGetDevice(&dev);
   if (blocks_per_sm[dev & 63] == 0) {
     int nb = 0;
+    LIFE_CUDA(cudaFuncSetAttribute(byte_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   8 * kByteSmem));
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, byte_step_kernel,
-                                                            kByteThreads, 0));
+                                                            kByteThreads, kByteSmem));
     blocks_per_sm[dev & 63] = std::max(nb, 1);
   }
   ByteStepArgs a{};
@@ -269,7 +271,7 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
   a.seg_rows = std::max<int64_t>(ceil_div(out_rows, segs_target), 32);
   const int64_t warps = ceil_div(out_rows, a.seg_rows) * a.n_strips;
   const int64_t blocks = ceil_div(warps, kByteThreads / 32);
-  byte_step_kernel<<<static_cast<unsigned>(blocks), kByteThreads, 0,
+  byte_step_kernel<<<static_cast<unsigned>(blocks), kByteThreads, kByteSmem,
                      static_cast<cudaStream_t>(stream)>>>(a);
   LIFE_CHECK_LAUNCH("byte_step_kernel");
   return LIFE_OK;
