@@ -82,6 +82,18 @@ int life_grid_upload_packed(life_ctx* ctx, const uint64_t* words, int64_t width,
  * `engine` selects the resident layout. */
 int life_grid_init_random(life_ctx* ctx, int64_t width, int64_t height, double density,
                           uint64_t seed, int engine);
+/* Config-4 sparse soup (the reference has no generator, it is
+ * pinned from SplitMix64 + place_pattern, pattern.cpp:309-328) generated on the
+ * device: an empty W x H field, B = llround(coverage*W*H/bs^2) bs x bs blocks
+ * of Bernoulli(density) cells at seeded positions, later blocks overwriting
+ * earlier ones.  Needs 4*W*H bytes of device scratch during the call. */
+int life_grid_init_soup(life_ctx* ctx, int64_t width, int64_t height, double coverage,
+                        int32_t block_size, double density, uint64_t seed, int engine);
+/* place_pattern (pattern.cpp:309-328) on the resident grid: the pw x ph
+ * footprint at (x0, y0) is overwritten by `pattern` (row-major bytes,
+ * nonzero = alive); LIFE_ERR_OUT_OF_BOUNDS if it does not fit (no wrap). */
+int life_grid_place_u8(life_ctx* ctx, const uint8_t* pattern, int64_t pw, int64_t ph,
+                       int64_t x0, int64_t y0);
 /* Replaces reading `Grid::data()` of RunResult::grid (engine.hpp:24-27). */
 int life_grid_download_u8(life_ctx* ctx, uint8_t* cells, int64_t row_stride);
 int life_grid_download_packed(life_ctx* ctx, uint64_t* words, int64_t words_per_row);

@@ -319,3 +319,14 @@ int orc_band_bounds(int64_t extent, int32_t parts, int64_t* bounds) {
   }
   return 0;
 }
+
+/* place_pattern (pattern.cpp:309-328): the pw x ph footprint at (x0, y0) is
+ * cleared and the pattern's live (nonzero) cells set; no wrap.  Returns -1
+ * when the footprint does not fit (OutOfBounds, pattern.cpp:310-316). */
+int orc_place_pattern(uint8_t* grid, int64_t width, int64_t height, const uint8_t* pat,
+                      int64_t pw, int64_t ph, int64_t x0, int64_t y0) {
+  if (x0 < 0 || y0 < 0 || x0 + pw > width || y0 + ph > height) return -1;
+  for (int64_t j = 0; j < ph; ++j)
+    for (int64_t i = 0; i < pw; ++i) grid[(y0 + j) * width + x0 + i] = pat[j * pw + i] != 0;
+  return 0;
+}

@@ -60,6 +60,8 @@ class Oracle:
         L.orc_pack.argtypes = [_u8p, C.c_int64, C.c_int64, _u64p]
         L.orc_unpack.argtypes = [_u64p, C.c_int64, C.c_int64, _u8p]
         L.orc_band_bounds.argtypes = [C.c_int64, C.c_int32, _i64p]
+        L.orc_place_pattern.argtypes = [_u8p, C.c_int64, C.c_int64, _u8p, C.c_int64, C.c_int64,
+                                        C.c_int64, C.c_int64]
 
     def splitmix(self, seed: int, n: int) -> np.ndarray:
         out = np.empty(n, np.uint64)
@@ -142,6 +144,14 @@ class Oracle:
         self.lib.orc_unpack(words, w, h, out)
         return out
 
+    def place_pattern(self, grid: np.ndarray, pattern: np.ndarray, x0: int, y0: int) -> np.ndarray:
+        g = np.array(grid, dtype=np.uint8, order="C", copy=True)
+        p = np.ascontiguousarray(pattern, dtype=np.uint8)
+        if self.lib.orc_place_pattern(g, g.shape[1], g.shape[0], p, p.shape[1], p.shape[0],
+                                      x0, y0) != 0:
+            raise IndexError("pattern footprint exceeds the grid")
+        return g
+
     def band_bounds(self, extent: int, parts: int) -> list[int]:
         b = np.zeros(max(parts, 0) + 1, np.int64)
         if self.lib.orc_band_bounds(extent, parts, b) != 0:
@@ -178,6 +188,8 @@ class Reference:
         L.ref_sparse_soup_small.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
                                             C.c_uint64, _u8p]
         L.ref_population.argtypes = [_u8p, C.c_int, C.c_int]
+        L.ref_place_pattern.argtypes = [_u8p, C.c_int, C.c_int, _u8p, C.c_int, C.c_int, C.c_int,
+                                        C.c_int]
 
     def _check(self, rc: int) -> None:
         if rc != 0:
@@ -254,3 +266,10 @@ class Reference:
     def population(self, g: np.ndarray) -> int:
         g = np.ascontiguousarray(g, dtype=np.uint8)
         return int(self.lib.ref_population(g, g.shape[1], g.shape[0]))
+
+    def place_pattern(self, grid: np.ndarray, pattern: np.ndarray, x0: int, y0: int) -> np.ndarray:
+        g = np.array(grid, dtype=np.uint8, order="C", copy=True)
+        p = np.ascontiguousarray(pattern, dtype=np.uint8)
+        self._check(self.lib.ref_place_pattern(g, g.shape[1], g.shape[0], p, p.shape[1],
+                                               p.shape[0], x0, y0))
+        return g

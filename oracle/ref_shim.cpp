@@ -200,6 +200,23 @@ int ref_sparse_soup_small(int w, int h, double coverage, int bs, double p, std::
   }
 }
 
+// life::place_pattern (pattern.cpp:309-328) with a Pattern built from bytes.
+int ref_place_pattern(std::uint8_t* cells, int w, int h, const std::uint8_t* pat, int pw, int ph,
+                      int x0, int y0) {
+  try {
+    life::Pattern p{pw, ph, {}};
+    for (int j = 0; j < ph; ++j)
+      for (int i = 0; i < pw; ++i)
+        if (pat[j * pw + i]) p.live_cells.push_back({i, j});
+    p.normalize();
+    const life::Grid g = life::place_pattern(grid_of(cells, w, h), p, {x0, y0});
+    std::memcpy(cells, g.data(), static_cast<std::size_t>(w) * h);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e);
+  }
+}
+
 // life::population (grid.cpp:40-46) -- returns the reference's int.
 int ref_population(const std::uint8_t* cells, int w, int h) {
   return life::population(grid_of(cells, w, h));

@@ -100,6 +100,9 @@ class BandDriver:
         self.stepper = stepper or cuda_stepper(geo.width)
         shape = (geo.buf_rows, geo.pitch)
         self.buf = [torch.zeros(shape, dtype=torch.int32, device=device) for _ in range(2)]
+        # CUDA: the k-row edge strips run on a side stream as soon as the
+        # halos land, filling SMs between the interior kernel's block waves.
+        self.edge_stream = torch.cuda.Stream(device) if device.type == "cuda" else None
         self.cur = 0
         self.generations = 0
         self.exchange_bytes = 0  # per pass, both directions, this rank
@@ -181,11 +184,24 @@ class BandDriver:
         if g.world == 1:
             a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
             self.stepper(a, 0, g.height, b, 0, g.height, k)
-        else:
+        elif self.edge_stream is None:
             works = self.post_exchange(k)
             interior = self.compute_interior(k)
             self.wait(works)
             self.compute_edges(k, interior)
+        else:
+            main = torch.cuda.current_stream(self.device)
+            start = torch.cuda.Event()
+            start.record(main)
+            works = self.post_exchange(k)  # NCCL waits for `main` (last pass done)
+            interior = self.compute_interior(k)
+            with torch.cuda.stream(self.edge_stream):
+                self.edge_stream.wait_event(start)
+                self.wait(works)  # edge stream waits for the halos
+                self.compute_edges(k, interior)
+                done = torch.cuda.Event()
+                done.record(self.edge_stream)
+            main.wait_event(done)
         self.finish_pass(k)
 
     def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None) -> None:

@@ -41,6 +41,9 @@ SIGNATURES = [
     ("life_grid_upload_u8", C.c_int, [_vp, _vp, _i64, _i64, _i64]),
     ("life_grid_upload_packed", C.c_int, [_vp, _vp, _i64, _i64, _i64]),
     ("life_grid_init_random", C.c_int, [_vp, _i64, _i64, C.c_double, _u64, C.c_int]),
+    ("life_grid_init_soup", C.c_int, [_vp, _i64, _i64, C.c_double, _i32, C.c_double, _u64,
+                                      C.c_int]),
+    ("life_grid_place_u8", C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64]),
     ("life_grid_download_u8", C.c_int, [_vp, _vp, _i64]),
     ("life_grid_download_packed", C.c_int, [_vp, _vp, _i64]),
     ("life_grid_window_u8", C.c_int, [_vp, _i64, _i64, _i64, _i64, _vp]),

@@ -153,7 +153,11 @@ constexpr int kPackedThreads = 128;
 template <int K>
 struct PackedTraits {
   static constexpr int kPrefetch = K <= 3 ? 6 : 3;
+#ifdef LIFE_WARPS16
+  static constexpr int kWarps[17] = {0, 28, 24, 24, 20, 16, 16, 16, 16, 12, 12, 12, 12, 12, LIFE_WARPS16, LIFE_WARPS16, LIFE_WARPS16};
+#else
   static constexpr int kWarps[17] = {0, 28, 24, 24, 20, 16, 16, 16, 16, 12, 12, 12, 12, 12, 8, 8, 8};
+#endif
   static constexpr int kMaxThreads = 32 * kWarps[K];
   static constexpr int kRingBytes = 2 * kPrefetch * 96 * 4;  // per warp
   static constexpr int kLag = 3 * K - 1;  // output row j leaves the pipeline at step j + 3K - 1
@@ -310,9 +314,12 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
       // issued in groups of kGroup, level by level (all shuffles, then all
       // funnels, ...), so consecutive instructions do not depend on each
       // other and the ALU pipe sees several independent chains per warp.
-      uint32_t yv[K];
+      // Groups run top stage first: stage g reads xin[g] and then writes its
+      // output into xin[g+1], which stage g+1 has already consumed this step,
+      // so no second array of K outputs is live (saves ~K registers).
+      uint32_t y_last = 0;
 #pragma unroll
-      for (int g0 = 0; g0 < K; g0 += kGroup) {
+      for (int g0 = ((K - 1) / kGroup) * kGroup; g0 >= 0; g0 -= kGroup) {
         uint32_t xl[kGroup], xr[kGroup];
         HSum c[kGroup];
 #pragma unroll
@@ -333,23 +340,26 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
           }
         }
 #pragma unroll
-        for (int j = 0; j < kGroup; ++j) {
+        for (int j = kGroup - 1; j >= 0; --j) {
           if (g0 + j < K) {
             const int g = g0 + j;
-            yv[g] = rule(sa[g], sb[g], c[j], sself[g]);
+            const uint32_t yg = rule(sa[g], sb[g], c[j], sself[g]);
             sa[g] = sb[g];
             sb[g] = c[j];
             sself[g] = xin[g];
+            if (g + 1 < K) {
+              xin[g + 1] = yg;
+            } else {
+              y_last = yg;
+            }
           }
         }
       }
-#pragma unroll
-      for (int g = 1; g < K; ++g) xin[g] = yv[g - 1];
       // Output row j of the segment leaves the pipeline at step j + kLag.
       const int j = t * PF + u - kLag;
       if (static_cast<unsigned>(j) < static_cast<unsigned>(n)) {
         char* p = out_seg + static_cast<uint64_t>(static_cast<uint32_t>(j)) * out_pitch_b;
-        const uint32_t v = yv[K - 1] & st_mask;
+        const uint32_t v = y_last & st_mask;
         if (st_lo) *reinterpret_cast<uint16_t*>(p) = static_cast<uint16_t>(v);
         if (st_hi) *reinterpret_cast<uint16_t*>(p + 2) = static_cast<uint16_t>(v >> 16);
       }
@@ -669,6 +679,88 @@ __global__ void byte_random_kernel(uint8_t* __restrict__ out, int64_t pitch, int
       s += kGamma;
     }
     *reinterpret_cast<uint4*>(out + r * pitch + c0) = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
+// Config-4 sparse soup in counter form: block b of
+// the SplitMix64(seed) stream uses draws [b*(2+bs^2), (b+1)*(2+bs^2)):
+// x0 = draw % (W-bs+1), y0 = draw % (H-bs+1), then bs^2 cell draws,
+// alive iff (draw >> 11) < thr.  place_pattern's overwrite order
+// (pattern.cpp:309-328, later blocks win) is resolved with a per-cell
+// atomicMax of (block+1): pass 1 claims, pass 2 writes the winners' cells.
+__device__ __forceinline__ uint64_t draw_at(uint64_t seed, uint64_t k) {
+  return mix64(seed + (k + 1) * kGamma);
+}
+
+__global__ void soup_claim_kernel(unsigned int* __restrict__ owner, int64_t width, int64_t height,
+                                  int64_t blocks, int32_t bs, uint64_t seed) {
+  const int64_t per = static_cast<int64_t>(bs) * bs;
+  const int64_t n = blocks * per;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = t / per;
+    const int j = static_cast<int>(t - b * per);
+    const uint64_t k0 = static_cast<uint64_t>(b) * static_cast<uint64_t>(2 + per);
+    const int64_t x0 = static_cast<int64_t>(draw_at(seed, k0) % static_cast<uint64_t>(width - bs + 1));
+    const int64_t y0 = static_cast<int64_t>(draw_at(seed, k0 + 1) % static_cast<uint64_t>(height - bs + 1));
+    const int64_t cell = (y0 + j / bs) * width + x0 + j % bs;
+    atomicMax(owner + cell, static_cast<unsigned int>(b + 1));
+  }
+}
+
+__global__ void soup_write_kernel(const unsigned int* __restrict__ owner, uint8_t* __restrict__ cells,
+                                  int64_t pitch, int64_t width, int64_t height, int64_t blocks,
+                                  int32_t bs, uint64_t seed, uint64_t thr) {
+  const int64_t per = static_cast<int64_t>(bs) * bs;
+  const int64_t n = blocks * per;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t b = t / per;
+    const int j = static_cast<int>(t - b * per);
+    const uint64_t k0 = static_cast<uint64_t>(b) * static_cast<uint64_t>(2 + per);
+    const int64_t x0 = static_cast<int64_t>(draw_at(seed, k0) % static_cast<uint64_t>(width - bs + 1));
+    const int64_t y0 = static_cast<int64_t>(draw_at(seed, k0 + 1) % static_cast<uint64_t>(height - bs + 1));
+    const int64_t x = x0 + j % bs, y = y0 + j / bs;
+    if (owner[y * width + x] == static_cast<unsigned int>(b + 1)) {
+      cells[y * pitch + x] = static_cast<uint8_t>((draw_at(seed, k0 + 2 + j) >> 11) < thr);
+    }
+  }
+}
+
+// place_pattern (pattern.cpp:309-328) on a resident grid: the pw x ph
+// footprint at (x0, y0) becomes the pattern (0/1; dead pattern cells clear).
+__global__ void place_byte_kernel(uint8_t* __restrict__ cells, int64_t pitch,
+                                  const uint8_t* __restrict__ pat, int64_t pw, int64_t ph,
+                                  int64_t x0, int64_t y0) {
+  const int64_t n = pw * ph;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = t / pw, i = t - j * pw;
+    cells[(y0 + j) * pitch + x0 + i] = pat[t] != 0;
+  }
+}
+
+// Packed layout: one thread per (pattern row, grid word) read-modify-write.
+__global__ void place_packed_kernel(uint32_t* __restrict__ words, int64_t pitch,
+                                    const uint8_t* __restrict__ pat, int64_t pw, int64_t ph,
+                                    int64_t x0, int64_t y0) {
+  const int64_t w_first = x0 >> 5, w_last = (x0 + pw - 1) >> 5;
+  const int64_t nwords = w_last - w_first + 1;
+  const int64_t n = nwords * ph;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t j = t / nwords;
+    const int64_t w = w_first + (t - j * nwords);
+    uint32_t mask = 0, bits = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t i = w * 32 + b - x0;  // pattern column
+      if (i >= 0 && i < pw) {
+        mask |= 1u << b;
+        if (pat[j * pw + i]) bits |= 1u << b;
+      }
+    }
+    uint32_t* p = words + (y0 + j) * pitch + w;
+    *p = (*p & ~mask) | bits;
   }
 }
 

@@ -615,6 +615,76 @@ int life_grid_init_random(life_ctx* c, int64_t width, int64_t height, double den
   return LIFE_OK;
 }
 
+int life_grid_init_soup(life_ctx* c, int64_t width, int64_t height, double coverage,
+                        int32_t block_size, double density, uint64_t seed, int engine) {
+  LIFE_TRY(activate(c));
+  LIFE_TRY(check_engine(engine));
+  if (!(density >= 0.0 && density <= 1.0))
+    return set_error(LIFE_ERR_CONFIG, "density must be in [0, 1], got %f", density);
+  if (!(coverage >= 0.0)) return set_error(LIFE_ERR_CONFIG, "coverage must be >= 0");
+  LIFE_TRY(check_dims(width, height));
+  if (block_size < 1 || block_size > width || block_size > height)
+    return set_error(LIFE_ERR_OUT_OF_BOUNDS, "soup block %d does not fit a %lldx%lld field",
+                     block_size, static_cast<long long>(width), static_cast<long long>(height));
+  if (width * height >= (int64_t(1) << 40))
+    return set_error(LIFE_ERR_CONFIG, "soup field too large for the owner scratch");
+  LIFE_TRY(set_dims(c, width, height));
+  LIFE_TRY(ensure_byte(c));
+  const double bsq = double(block_size) * double(block_size);
+  const int64_t blocks = std::llround(coverage * double(width) * double(height) / bsq);
+  if (blocks >= (int64_t(1) << 32) - 1) return set_error(LIFE_ERR_CONFIG, "too many soup blocks");
+  unsigned int* owner = nullptr;
+  LIFE_CUDA(cudaMallocAsync(&owner, sizeof(unsigned int) * width * height, c->stream));
+  LIFE_CUDA(cudaMemsetAsync(owner, 0, sizeof(unsigned int) * width * height, c->stream));
+  LIFE_CUDA(cudaMemsetAsync(c->by[0], 0, static_cast<size_t>(c->by_pitch) * height, c->stream));
+  c->by_cur = 0;
+  const int64_t n = blocks * block_size * block_size;
+  if (n > 0) {
+    soup_claim_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(owner, width, height,
+                                                                        blocks, block_size, seed);
+    LIFE_CHECK_LAUNCH("soup_claim_kernel");
+    soup_write_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(
+        owner, c->by[0], c->by_pitch, width, height, blocks, block_size, seed,
+        density_threshold(density));
+    LIFE_CHECK_LAUNCH("soup_write_kernel");
+  }
+  LIFE_CUDA(cudaFreeAsync(owner, c->stream));
+  c->layout = kByte;
+  if (engine == LIFE_ENGINE_PACKED) LIFE_TRY(to_layout(c, kPacked));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_grid_place_u8(life_ctx* c, const uint8_t* pattern, int64_t pw, int64_t ph, int64_t x0,
+                       int64_t y0) {
+  LIFE_TRY(activate(c));
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  if (pw < 0 || ph < 0 || (pw * ph > 0 && !pattern))
+    return set_error(LIFE_ERR_CONFIG, "bad pattern buffer");
+  if (x0 < 0 || y0 < 0 || x0 + pw > c->W || y0 + ph > c->H)
+    return set_error(LIFE_ERR_OUT_OF_BOUNDS,
+                     "pattern footprint %lldx%lld at (%lld, %lld) exceeds grid %lldx%lld",
+                     static_cast<long long>(pw), static_cast<long long>(ph),
+                     static_cast<long long>(x0), static_cast<long long>(y0),
+                     static_cast<long long>(c->W), static_cast<long long>(c->H));
+  if (pw * ph == 0) return LIFE_OK;
+  uint8_t* dpat = nullptr;
+  LIFE_CUDA(cudaMallocAsync(&dpat, pw * ph, c->stream));
+  LIFE_CUDA(cudaMemcpyAsync(dpat, pattern, pw * ph, cudaMemcpyHostToDevice, c->stream));
+  if (c->layout == kByte) {
+    place_byte_kernel<<<grid_stride_blocks(pw * ph, 256), 256, 0, c->stream>>>(
+        c->by[c->by_cur], c->by_pitch, dpat, pw, ph, x0, y0);
+  } else {
+    const int64_t n = (((x0 + pw - 1) >> 5) - (x0 >> 5) + 1) * ph;
+    place_packed_kernel<<<grid_stride_blocks(n, 256), 256, 0, c->stream>>>(
+        c->pk[c->pk_cur], c->pk_pitch, dpat, pw, ph, x0, y0);
+  }
+  LIFE_CHECK_LAUNCH("place_kernel");
+  LIFE_CUDA(cudaFreeAsync(dpat, c->stream));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
 int life_grid_download_u8(life_ctx* c, uint8_t* cells, int64_t row_stride) {
   LIFE_TRY(activate(c));
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");

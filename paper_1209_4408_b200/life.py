@@ -265,6 +265,18 @@ class Engine:
                     engine: int = capi.ENGINE_PACKED) -> None:
         check(self._lib.life_grid_init_random(self._ctx, width, height, density, seed, engine))
 
+    def init_soup(self, width: int, height: int, coverage: float = 0.02, block: int = 5,
+                  density: float = 0.5, seed: int = 42, engine: int = capi.ENGINE_PACKED) -> None:
+        """Config-4 sparse soup generated on the device (life_grid_init_soup)."""
+        check(self._lib.life_grid_init_soup(self._ctx, width, height, coverage, block, density,
+                                            seed, engine))
+
+    def place(self, pattern: np.ndarray, x0: int, y0: int) -> None:
+        """place_pattern (pattern.cpp:309-328) on the resident grid."""
+        pat = np.ascontiguousarray(pattern, dtype=np.uint8)
+        ph, pw = pat.shape
+        check(self._lib.life_grid_place_u8(self._ctx, pat.ctypes.data, pw, ph, x0, y0))
+
     def dims(self) -> tuple[int, int]:
         w, h = C.c_int64(), C.c_int64()
         check(self._lib.life_grid_dims(self._ctx, C.byref(w), C.byref(h)))

@@ -262,3 +262,43 @@ def test_run_batch_pipelined(engine, oracle):
     for g, out in zip(grids, ins):
         want, _ = oracle.run(g, G)
         assert np.array_equal(oracle.unpack(out, W), want)
+
+
+def test_device_soup_matches_oracle(engine, oracle):
+    for (w, h, cov, bs, p, seed) in [(200, 150, 0.02, 5, 0.5, 3), (409, 121, 0.02, 5, 0.5, 42),
+                                     (97, 61, 0.3, 5, 0.5, 7), (64, 64, 0.5, 3, 0.7, 1),
+                                     (33, 40, 1.0, 7, 0.5, 9), (10, 10, 0.0, 5, 0.5, 1)]:
+        want = oracle.sparse_soup(w, h, seed=seed, coverage=cov, block=bs, p=p)
+        for eng in (PACKED, BYTE):
+            engine.init_soup(w, h, cov, bs, p, seed, eng)
+            assert np.array_equal(engine.download(), want), (w, h, cov, bs, p, seed, eng)
+
+
+@pytest.mark.slow
+def test_device_soup_cfg4_golden(engine, oracle):
+    gold = load_golden("golden_cfg4.json")
+    engine.init_soup(40961, 12289, 0.02, 5, 0.5, 42, PACKED)
+    assert fnv(oracle, engine.download_packed()) == gold["gens"]["0"]["fnv_packed"]
+    engine.run(100, PACKED, 16)
+    assert fnv(oracle, engine.download_packed()) == gold["gens"]["100"]["fnv_packed"]
+
+
+def test_device_place_pattern(engine, oracle):
+    from paper_1209_4408_b200 import life
+    rng = np.random.default_rng(11)
+    for trial in range(12):
+        w, h = int(rng.integers(3, 300)), int(rng.integers(3, 60))
+        g = (rng.random((h, w)) < 0.5).astype(np.uint8)
+        pw, ph = int(rng.integers(0, min(w, 70) + 1)), int(rng.integers(0, h + 1))
+        pat = rng.integers(0, 3, (ph, pw)).astype(np.uint8)
+        x0, y0 = int(rng.integers(0, w - pw + 1)), int(rng.integers(0, h - ph + 1))
+        want = oracle.place_pattern(g, pat, x0, y0)
+        for eng in (PACKED, BYTE):
+            engine.upload(g)
+            if eng == PACKED:
+                engine.run(0, PACKED)  # resident layout -> packed
+            engine.place(pat, x0, y0)
+            assert np.array_equal(engine.download(), want), (trial, eng)
+    engine.upload(np.zeros((5, 5), np.uint8))
+    with pytest.raises(life.OutOfBounds):
+        engine.place(np.ones((3, 3), np.uint8), 3, 0)

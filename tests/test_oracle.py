@@ -167,3 +167,19 @@ def test_reference_nonbinary_bytes_divergence_is_pinned(oracle, reference):
     g2[3, 3] = 2
     g2[10, 11] = 255
     assert np.array_equal(reference.step_serial(g2), oracle.step_serial((g2 != 0).astype(np.uint8)))
+
+
+def test_place_pattern_vs_reference(oracle, reference):
+    rng = np.random.default_rng(5)
+    for _ in range(30):
+        w, h = int(rng.integers(3, 40)), int(rng.integers(3, 40))
+        g = (rng.random((h, w)) < 0.5).astype(np.uint8)
+        pw, ph = int(rng.integers(0, w + 1)), int(rng.integers(0, h + 1))
+        pat = (rng.random((ph, pw)) < 0.4).astype(np.uint8)
+        x0, y0 = int(rng.integers(0, w - pw + 1)), int(rng.integers(0, h - ph + 1))
+        assert np.array_equal(oracle.place_pattern(g, pat, x0, y0),
+                              reference.place_pattern(g, pat, x0, y0))
+    with pytest.raises(IndexError):
+        oracle.place_pattern(np.zeros((5, 5), np.uint8), np.ones((3, 3), np.uint8), 3, 0)
+    with pytest.raises(RuntimeError):
+        reference.place_pattern(np.zeros((5, 5), np.uint8), np.ones((3, 3), np.uint8), 3, 0)
