@@ -38,6 +38,9 @@ CONFIGS = {
             desc="cfg2: 16384x16384 torus, p=0.3, seed 42, 1000 generations, bit-packed engine"),
     3: dict(w=65536, h=65536, p=0.5, gens=1000,
             desc="cfg3: 65536x65536 torus (512 MiB packed), p=0.5, seed 42, 1000 generations"),
+    4: dict(w=40961, h=12289, p=0.5, gens=5000, soup=True,
+            desc="cfg4: 12289 rows x 40961 cols torus, 5x5 Bernoulli(0.5) soups at 2% coverage "
+                 "(device-generated, seed 42), 5000 generations, bit-packed engine"),
     5: dict(w=262144, h=262144, p=0.4, gens=500,
             desc="cfg5: 262144x262144 torus (8 GiB packed), p=0.4, seed 42, 500 generations, "
                  "row bands over the GPUs"),
@@ -290,7 +293,14 @@ def run_gpu_arm(args) -> None:
             base_step(inp, in_row0, in_rows, out, out_row0, out_rows, k)
 
     drv = BandDriver(geo, dev, stepper=timed_step)
-    drv.init_random(cfg["p"], 42)
+    soup_host = None
+    if cfg.get("soup"):
+        with Engine(local) as e:  # device soup, shared by every rank's band
+            e.init_soup(W, H, 0.02, 5, cfg["p"], 42, capi.ENGINE_PACKED)
+            soup_host = e.download_packed()
+        drv.load_rows(soup_host)
+    else:
+        drv.init_random(cfg["p"], 42)
     grid_bytes = H * math.ceil(W / 64) * 8
     flush = None
     if grid_bytes * 2 < 4 * L2_BYTES:
@@ -368,7 +378,10 @@ def run_gpu_arm(args) -> None:
             wpr = math.ceil(W / 64)
             host_in = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
             host_out = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
-            eng.init_random(W, H, cfg["p"], 42, capi.ENGINE_PACKED)
+            if soup_host is not None:
+                eng.upload_packed(soup_host, W)
+            else:
+                eng.init_random(W, H, cfg["p"], 42, capi.ENGINE_PACKED)
             hin = host_in.numpy().view("uint64")
             hout = host_out.numpy().view("uint64")
             eng.download_packed(hin)
@@ -379,7 +392,10 @@ def run_gpu_arm(args) -> None:
         else:
             drv = BandDriver(geo, dev)
             host = torch.empty(tuple(drv.band().shape), dtype=torch.int32, pin_memory=True)
-            drv.init_random(cfg["p"], 42)
+            if soup_host is not None:
+                drv.load_rows(soup_host)
+            else:
+                drv.init_random(cfg["p"], 42)
             host.copy_(drv.band())
             ms = []
             for i in range(1 + steps_e2e):

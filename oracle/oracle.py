@@ -273,3 +273,58 @@ class Reference:
         self._check(self.lib.ref_place_pattern(g, g.shape[1], g.shape[0], p, p.shape[1],
                                                p.shape[0], x0, y0))
         return g
+
+
+class PatternIO:
+    """Pattern I/O + renderers through an extern-C library with the lio_/ref_
+    signatures: the reference (oracle/_ref/liblife_ref.so, prefix "ref_") or
+    the engine's host layer (paper_1209_4408_b200/host/liblife_io.so,
+    prefix "lio_")."""
+
+    def __init__(self, path: str, prefix: str):
+        L = C.CDLL(path)
+        self.p = prefix
+        self.L = L
+        ip = C.POINTER(C.c_int)
+        for name in ("parse_rle", "parse_plaintext"):
+            f = getattr(L, prefix + name)
+            f.argtypes = [C.c_char_p, ip, ip, ip, ip, C.c_int, ip, ip, ip, C.c_char_p, C.c_int]
+        f = getattr(L, prefix + "serialize_rle")
+        f.argtypes = [C.c_int, C.c_int, ip, ip, C.c_int, C.c_char_p, C.c_int]
+        for name in ("render_ascii", "render_pbm"):
+            getattr(L, prefix + name).argtypes = [_u8p, C.c_int, C.c_int, C.c_char_p, C.c_int]
+
+    def _parse(self, name: str, text: str):
+        cap = max(16, len(text) * 64 + 1024)
+        w, h, n, line, col = (C.c_int(0) for _ in range(5))
+        xs = (C.c_int * cap)()
+        ys = (C.c_int * cap)()
+        msg = C.create_string_buffer(512)
+        rc = getattr(self.L, self.p + name)(text.encode(), C.byref(w), C.byref(h), xs, ys, cap,
+                                            C.byref(n), C.byref(line), C.byref(col), msg, 512)
+        if rc == 3:
+            return {"error": "parse", "line": line.value, "column": col.value}
+        if rc != 0:
+            return {"error": f"rc{rc}"}
+        return {"w": w.value, "h": h.value, "cells": [[xs[i], ys[i]] for i in range(n.value)]}
+
+    def parse_rle(self, text: str):
+        return self._parse("parse_rle", text)
+
+    def parse_plaintext(self, text: str):
+        return self._parse("parse_plaintext", text)
+
+    def serialize_rle(self, w: int, h: int, cells):
+        n = len(cells)
+        xs = (C.c_int * max(n, 1))(*[c[0] for c in cells])
+        ys = (C.c_int * max(n, 1))(*[c[1] for c in cells])
+        out = C.create_string_buffer(64 + 16 * (n + w * h))
+        rc = getattr(self.L, self.p + "serialize_rle")(w, h, xs, ys, n, out, len(out))
+        return out.value.decode() if rc == 0 else {"error": f"rc{rc}"}
+
+    def render(self, kind: str, grid: np.ndarray) -> str:
+        g = np.ascontiguousarray(grid, dtype=np.uint8)
+        out = C.create_string_buffer(4 * g.size + 64)
+        rc = getattr(self.L, self.p + "render_" + kind)(g, g.shape[1], g.shape[0], out, len(out))
+        assert rc == 0
+        return out.value.decode()

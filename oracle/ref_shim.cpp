@@ -20,6 +20,7 @@
 #include "life/engine.hpp"
 #include "life/grid.hpp"
 #include "life/pattern.hpp"
+#include "life/render.hpp"
 #include "life/rng.hpp"
 
 namespace {
@@ -215,6 +216,69 @@ int ref_place_pattern(std::uint8_t* cells, int w, int h, const std::uint8_t* pat
   } catch (const std::exception& e) {
     return fail(e);
   }
+}
+
+// Pattern I/O and renderers (pattern.cpp:147-292, render.cpp:5-38), for the
+// parity tests of the GPU engine's host I/O layer.
+static int copy_str(const std::string& s, char* out, int cap) {
+  if (static_cast<int>(s.size()) + 1 > cap) return -1;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+static int export_pattern(const life::Pattern& p, int* w, int* h, int* xs, int* ys, int cap,
+                          int* n) {
+  *w = p.width;
+  *h = p.height;
+  *n = static_cast<int>(p.live_cells.size());
+  if (*n > cap) return -1;
+  for (int i = 0; i < *n; ++i) {
+    xs[i] = p.live_cells[i].x;
+    ys[i] = p.live_cells[i].y;
+  }
+  return 0;
+}
+
+int ref_parse_rle(const char* text, int* w, int* h, int* xs, int* ys, int cap, int* n, int* line,
+                  int* col, char* msg, int msgcap) {
+  try {
+    return export_pattern(life::parse_rle(text), w, h, xs, ys, cap, n);
+  } catch (const life::ParseError& e) {
+    *line = e.line();
+    *col = e.column();
+    copy_str(e.what(), msg, msgcap);
+    return 3;
+  }
+}
+
+int ref_parse_plaintext(const char* text, int* w, int* h, int* xs, int* ys, int cap, int* n,
+                        int* line, int* col, char* msg, int msgcap) {
+  try {
+    return export_pattern(life::parse_plaintext(text), w, h, xs, ys, cap, n);
+  } catch (const life::ParseError& e) {
+    *line = e.line();
+    *col = e.column();
+    copy_str(e.what(), msg, msgcap);
+    return 3;
+  }
+}
+
+int ref_serialize_rle(int w, int h, const int* xs, const int* ys, int n, char* out, int cap) {
+  life::Pattern p{w, h, {}};
+  for (int i = 0; i < n; ++i) p.live_cells.push_back({xs[i], ys[i]});
+  try {
+    return copy_str(life::serialize_rle(p), out, cap);
+  } catch (const life::ConfigError&) {
+    return 1;
+  }
+}
+
+int ref_render_ascii(const std::uint8_t* cells, int w, int h, char* out, int cap) {
+  return copy_str(life::render_ascii(grid_of(cells, w, h)), out, cap);
+}
+
+int ref_render_pbm(const std::uint8_t* cells, int w, int h, char* out, int cap) {
+  return copy_str(life::render_pbm(grid_of(cells, w, h)), out, cap);
 }
 
 // life::population (grid.cpp:40-46) -- returns the reference's int.

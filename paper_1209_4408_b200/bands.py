@@ -224,6 +224,15 @@ class BandDriver:
                                                 g.band_rows, density, seed, stream))
         self.generations = 0
 
+    def load_rows(self, words) -> None:
+        """Loads this band's rows [y0, y1) from a host packed grid (numpy
+        uint64 rows of ceil(W/64) words, the include/life_gpu.h exchange format)."""
+        g = self.geo
+        rows = words[g.y0:g.y1]
+        src = torch.from_numpy(rows.view("int32").copy())
+        self.band()[:, :src.shape[1]].copy_(src)
+        self.generations = 0
+
     def population(self) -> int:
         """Band population (CUDA popcount), summed over ranks when distributed."""
         g = self.geo

@@ -71,9 +71,38 @@ def build_host_test(force: bool = False) -> str:
     return out
 
 
+def _gxx(out: str, srcs: list[str], deps: list[str], extra: list[str], force: bool) -> str:
+    if not force and _newer(out, srcs + deps):
+        return out
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"), "-I",
+           os.path.join(PKG, "host"), "-o", out + ".tmp", *srcs, *extra]
+    subprocess.run(cmd, check=True)
+    os.replace(out + ".tmp", out)
+    return out
+
+
+HOST = os.path.join(PKG, "host")
+HOST_HDRS = [os.path.join(HOST, f) for f in ("life_gpu.hpp", "life_io.hpp", "life_harness.hpp")]
+
+
+def build_io_lib(force: bool = False) -> str:
+    """host/liblife_io.so: extern "C" view of life_io.hpp (host only, no CUDA)."""
+    return _gxx(os.path.join(HOST, "liblife_io.so"), [os.path.join(HOST, "life_io_capi.cpp")],
+                HOST_HDRS, ["-shared", "-fPIC"], force)
+
+
+def build_cli(force: bool = False) -> str:
+    """host/life-bench-gpu: the reference's life-bench CLI on the GPU engine."""
+    return _gxx(os.path.join(HOST, "life-bench-gpu"), [os.path.join(HOST, "life_bench_gpu.cpp")],
+                HOST_HDRS + [LIB], ["-L", PKG, "-llife_gpu", "-Wl,-rpath,$ORIGIN/..", "-lpthread"],
+                force)
+
+
 def build(force: bool = False, verbose: bool = False) -> None:
     build_lib(force=force, verbose=verbose)
     build_host_test(force=force)
+    build_io_lib(force=force)
+    build_cli(force=force)
 
 
 if __name__ == "__main__":

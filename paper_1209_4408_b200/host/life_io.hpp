@@ -1,0 +1,343 @@
+// life_io.hpp -- grid I/O at the boundary of the GPU engine (SURVEY.md 8f
+// rank 3): pattern formats, placement and renderers, with the reference's
+// behaviour (header only, C++20).
+//
+// Restates /root/reference/proj/core/include/life/pattern.hpp and render.hpp:
+//   parse_rle          pattern.cpp:147-212   (RLE: header "x = W, y = H[, rule = B3/S23]",
+//                                              runs of b/o, '$' row ends, '!' terminator,
+//                                              '#' comment lines; ParseError with 1-based
+//                                              line/column)
+//   serialize_rle      pattern.cpp:214-253   (canonical: maximal runs, no count on 1,
+//                                              trailing dead cells/rows omitted)
+//   parse_plaintext    pattern.cpp:255-292   ('.' dead, 'O' alive, '!' comment lines,
+//                                              ragged rows padded)
+//   load_pattern_file  pattern.cpp:294-307   (.rle / .cells by extension)
+//   place_pattern      pattern.cpp:309-328   (footprint overwrite, OutOfBounds, no wrap)
+//   render_ascii       render.cpp:5-15       ('#' / '.', rows joined by '\n')
+//   render_pbm         render.cpp:17-38      (plain P1, at most 35 digits per line)
+// Parity with the reference is pinned by tests/test_host_io.py (reference
+// library outputs and committed fixtures).
+#pragma once
+
+#include <algorithm>
+#include <cctype>
+#include <cstdint>
+#include <fstream>
+#include <sstream>
+#include <string>
+#include <string_view>
+#include <utility>
+#include <vector>
+
+#include "life_gpu.hpp"
+
+namespace lifegpu {
+
+// errors.hpp:46-60 -- malformed pattern input (the CLI maps it to exit 3).
+class ParseError : public Error {
+ public:
+  ParseError(const std::string& message, int line, int column)
+      : Error("parse error at line " + std::to_string(line) + ", column " +
+              std::to_string(column) + ": " + message),
+        line_(line),
+        column_(column) {}
+  int line() const noexcept { return line_; }
+  int column() const noexcept { return column_; }
+
+ private:
+  int line_, column_;
+};
+
+struct Coord {
+  int x = 0;
+  int y = 0;
+  friend bool operator==(const Coord&, const Coord&) = default;
+};
+
+// pattern.hpp:12-25: live cells kept sorted by (y, x) and unique.
+struct Pattern {
+  int width = 0;
+  int height = 0;
+  std::vector<Coord> live_cells;
+
+  void normalize() {
+    std::sort(live_cells.begin(), live_cells.end(),
+              [](const Coord& a, const Coord& b) { return a.y != b.y ? a.y < b.y : a.x < b.x; });
+    live_cells.erase(std::unique(live_cells.begin(), live_cells.end()), live_cells.end());
+  }
+  friend bool operator==(const Pattern&, const Pattern&) = default;
+};
+
+namespace detail {
+
+inline bool blank(char c) {
+  return c == ' ' || c == '\t' || c == '\r' || c == '\n' || c == '\v' || c == '\f';
+}
+inline std::string lowered(std::string s) {
+  for (char& ch : s) ch = static_cast<char>(std::tolower(static_cast<unsigned char>(ch)));
+  return s;
+}
+
+// Text reader that knows the 1-based line/column of the next character.
+class Reader {
+ public:
+  explicit Reader(std::string_view t) : text_(t) {}
+  bool done() const { return pos_ >= text_.size(); }
+  char cur() const { return text_[pos_]; }
+  int line() const { return line_; }
+  int col() const { return col_; }
+  char next() {
+    const char ch = text_[pos_++];
+    if (ch == '\n') {
+      ++line_;
+      col_ = 1;
+    } else {
+      ++col_;
+    }
+    return ch;
+  }
+  void skip_while(bool (*pred)(char)) {
+    while (!done() && pred(cur())) next();
+  }
+  [[noreturn]] void error(const std::string& what) const { throw ParseError(what, line_, col_); }
+  void expect(char ch, const char* what) {
+    if (done() || cur() != ch) error(std::string("expected ") + what);
+    next();
+  }
+  // Decimal run count; counts above 1e9 are rejected (pattern.cpp:14, :62-70).
+  long number() {
+    long v = 0;
+    while (!done() && std::isdigit(static_cast<unsigned char>(cur()))) {
+      v = v * 10 + (cur() - '0');
+      if (v > 1000000000L) error("run count too large");
+      next();
+    }
+    return v;
+  }
+
+ private:
+  std::string_view text_;
+  size_t pos_ = 0;
+  int line_ = 1, col_ = 1;
+};
+
+inline bool space_or_tab(char c) { return c == ' ' || c == '\t'; }
+inline bool is_blank(char c) { return blank(c); }
+
+}  // namespace detail
+
+inline Pattern parse_rle(std::string_view text) {
+  using detail::Reader;
+  Reader r(text);
+  // '#' comment lines and blank lines before the header.
+  for (;;) {
+    r.skip_while(detail::is_blank);
+    if (r.done() || r.cur() != '#') break;
+    while (!r.done() && r.next() != '\n') {
+    }
+  }
+  if (r.done()) r.error("missing RLE header");
+
+  Pattern p;
+  auto header_int = [&](const char* what) {
+    r.skip_while(detail::space_or_tab);
+    if (r.done() || !std::isdigit(static_cast<unsigned char>(r.cur())))
+      r.error(std::string("expected ") + what);
+    return static_cast<int>(r.number());
+  };
+  r.skip_while(detail::space_or_tab);
+  r.expect('x', "'x' at start of RLE header");
+  r.skip_while(detail::space_or_tab);
+  r.expect('=', "'=' after 'x'");
+  p.width = header_int("width after 'x ='");
+  r.skip_while(detail::space_or_tab);
+  r.expect(',', "',' after width");
+  r.skip_while(detail::space_or_tab);
+  r.expect('y', "'y' in RLE header");
+  r.skip_while(detail::space_or_tab);
+  r.expect('=', "'=' after 'y'");
+  p.height = header_int("height after 'y ='");
+  r.skip_while(detail::space_or_tab);
+  if (!r.done() && r.cur() == ',') {
+    r.next();
+    r.skip_while(detail::space_or_tab);
+    std::string key;
+    while (!r.done() && std::isalpha(static_cast<unsigned char>(r.cur()))) key += r.next();
+    if (detail::lowered(key) != "rule") r.error("unknown RLE header field '" + key + "'");
+    r.skip_while(detail::space_or_tab);
+    r.expect('=', "'=' after 'rule'");
+    r.skip_while(detail::space_or_tab);
+    std::string rule;
+    while (!r.done() && !detail::blank(r.cur()) && r.cur() != ',') rule += r.next();
+    const std::string lr = detail::lowered(rule);
+    if (lr != "b3/s23" && lr != "23/3") r.error("unsupported rule '" + rule + "' (only B3/S23)");
+    r.skip_while(detail::space_or_tab);
+  }
+  if (!r.done() && r.cur() != '\n') r.error("trailing characters after RLE header");
+  if (!r.done()) r.next();
+
+  int x = 0, y = 0;
+  for (;;) {
+    r.skip_while(detail::is_blank);
+    if (r.done()) r.error("missing '!' terminator");
+    long count = 1;
+    if (std::isdigit(static_cast<unsigned char>(r.cur()))) {
+      count = r.number();
+      if (count == 0) r.error("run count must be positive");
+      r.skip_while(detail::is_blank);
+      if (r.done()) r.error("run count without a tag");
+    }
+    const int tl = r.line(), tc = r.col();
+    const char tag = r.next();
+    if (tag == 'b' || tag == 'B' || tag == 'o' || tag == 'O') {
+      if (y >= p.height)
+        throw ParseError("cell row " + std::to_string(y) + " exceeds declared height " +
+                             std::to_string(p.height), tl, tc);
+      if (x + count > p.width)
+        throw ParseError("run exceeds declared width " + std::to_string(p.width), tl, tc);
+      if (tag == 'o' || tag == 'O')
+        for (long k = 0; k < count; ++k) p.live_cells.push_back({x + static_cast<int>(k), y});
+      x += static_cast<int>(count);
+    } else if (tag == '$') {
+      y += static_cast<int>(count);
+      x = 0;
+    } else if (tag == '!') {
+      if (count != 1) throw ParseError("run count before '!'", tl, tc);
+      break;  // anything after '!' is ignored
+    } else {
+      throw ParseError(std::string("unexpected character '") + tag + "'", tl, tc);
+    }
+  }
+  return p;
+}
+
+inline std::string serialize_rle(const Pattern& pattern) {
+  Pattern p = pattern;
+  p.normalize();
+  for (const Coord& c : p.live_cells)
+    if (c.x < 0 || c.x >= p.width || c.y < 0 || c.y >= p.height)
+      throw ConfigError("pattern has live cells outside its declared bounds");
+  std::string out = "x = " + std::to_string(p.width) + ", y = " + std::to_string(p.height) + "\n";
+  auto put = [&out](long n, char tag) {
+    if (n > 1) out += std::to_string(n);
+    out += tag;
+  };
+  int row = 0, col = 0;
+  for (size_t i = 0; i < p.live_cells.size();) {
+    const Coord start = p.live_cells[i];
+    if (start.y > row) {
+      put(start.y - row, '$');
+      row = start.y;
+      col = 0;
+    }
+    size_t j = i + 1;
+    while (j < p.live_cells.size() && p.live_cells[j].y == start.y &&
+           p.live_cells[j].x == start.x + static_cast<int>(j - i))
+      ++j;
+    if (start.x > col) put(start.x - col, 'b');
+    put(static_cast<long>(j - i), 'o');
+    col = start.x + static_cast<int>(j - i);
+    i = j;
+  }
+  out += '!';
+  return out;
+}
+
+inline Pattern parse_plaintext(std::string_view text) {
+  Pattern p;
+  int row = 0, line_no = 0;
+  size_t start = 0;
+  while (start < text.size()) {
+    const size_t nl = text.find('\n', start);
+    const std::string_view ln =
+        text.substr(start, (nl == std::string_view::npos ? text.size() : nl) - start);
+    ++line_no;
+    if (ln.empty() || ln[0] != '!') {
+      int x = 0;
+      for (size_t i = 0; i < ln.size(); ++i) {
+        if (ln[i] == '.') {
+          ++x;
+        } else if (ln[i] == 'O') {
+          p.live_cells.push_back({x++, row});
+        } else if (!detail::blank(ln[i])) {
+          throw ParseError(std::string("unexpected character '") + ln[i] + "'", line_no,
+                           static_cast<int>(i) + 1);
+        }
+      }
+      p.width = std::max(p.width, x);
+      ++row;
+    }
+    if (nl == std::string_view::npos) break;
+    start = nl + 1;
+  }
+  p.height = row;
+  return p;
+}
+
+inline Pattern load_pattern_file(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw ConfigError("cannot read pattern file '" + path + "'");
+  std::ostringstream body;
+  body << in.rdbuf();
+  const size_t dot = path.rfind('.');
+  const std::string ext = dot == std::string::npos ? "" : detail::lowered(path.substr(dot));
+  if (ext == ".rle") return parse_rle(body.str());
+  if (ext == ".cells") return parse_plaintext(body.str());
+  throw ConfigError("unsupported pattern extension '" + ext + "' (expected .rle or .cells)");
+}
+
+// place_pattern on a host grid (any GridT with width()/height()/data()).
+template <class GridT>
+GridT place_pattern(const GridT& grid, const Pattern& pattern, Coord origin) {
+  if (origin.x < 0 || origin.y < 0 || origin.x + pattern.width > grid.width() ||
+      origin.y + pattern.height > grid.height())
+    throw OutOfBounds("pattern footprint " + std::to_string(pattern.width) + "x" +
+                      std::to_string(pattern.height) + " at (" + std::to_string(origin.x) + ", " +
+                      std::to_string(origin.y) + ") exceeds grid " +
+                      std::to_string(grid.width()) + "x" + std::to_string(grid.height()));
+  GridT out = grid;
+  uint8_t* cells = out.data();
+  const int64_t w = out.width();
+  for (int j = 0; j < pattern.height; ++j)
+    std::fill_n(cells + (origin.y + j) * w + origin.x, pattern.width, uint8_t{0});
+  for (const Coord& c : pattern.live_cells) cells[(origin.y + c.y) * w + origin.x + c.x] = 1;
+  return out;
+}
+
+// The pattern as a dense pw x ph 0/1 byte block (for life_grid_place_u8).
+inline std::vector<uint8_t> pattern_bytes(const Pattern& p) {
+  std::vector<uint8_t> b(static_cast<size_t>(p.width) * p.height, 0);
+  for (const Coord& c : p.live_cells)
+    if (c.x >= 0 && c.x < p.width && c.y >= 0 && c.y < p.height)
+      b[static_cast<size_t>(c.y) * p.width + c.x] = 1;
+  return b;
+}
+
+template <class GridT>
+std::string render_ascii(const GridT& g) {
+  std::string out;
+  out.reserve(static_cast<size_t>(g.height()) * (g.width() + 1));
+  const uint8_t* c = g.data();
+  for (int64_t y = 0; y < g.height(); ++y) {
+    if (y) out += '\n';
+    for (int64_t x = 0; x < g.width(); ++x) out += c[y * g.width() + x] ? '#' : '.';
+  }
+  return out;
+}
+
+template <class GridT>
+std::string render_pbm(const GridT& g) {
+  constexpr int kDigitsPerLine = 35;  // 35 digits + 34 spaces = 69 <= 70 columns
+  std::string out = "P1\n" + std::to_string(g.width()) + " " + std::to_string(g.height()) + "\n";
+  const uint8_t* c = g.data();
+  for (int64_t y = 0; y < g.height(); ++y) {
+    for (int64_t x = 0; x < g.width(); ++x) {
+      if (x > 0) out += (x % kDigitsPerLine == 0) ? '\n' : ' ';
+      out += c[y * g.width() + x] ? '1' : '0';
+    }
+    out += '\n';
+  }
+  return out;
+}
+
+}  // namespace lifegpu

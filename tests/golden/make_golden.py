@@ -194,6 +194,63 @@ def cfg3w() -> None:
     dump("golden_cfg3_windows.json", res)
 
 
+def io_cases():
+    """Inputs for the pattern I/O parity cases (reference tests + fuzz)."""
+    rng = np.random.default_rng(1234)
+    rle = ["x = 3, y = 1\n3o!", "x = 3, y = 3\nbo$2bo$3o!",
+           "#N Glider\n#C the classic\nx = 3, y = 3, rule = B3/S23\nbo$2bo$3o!\n",
+           "x = 2, y = 1\nBO!", "x = 3, y = 1, rule = 23/3\n3o!", "x = 3, y = 1, rule = B36/S23\n3o!",
+           "x = 3, y = 5\no3$o$o!", "x = 3, y = 3\no!", "x = 2, y = 1\n5o!", "x = 3, y = 1\no$o!",
+           "x = 3, y = 1\n2b2b!", "", "y = 1, x = 3\n3o!", "x = 3, y = 1\n3o", "x = 3, y = 1\n3!",
+           "x = 3, y = 1\n0o!", "x = 3, y = 1\noqo!", "x = 3, y = 1\n3o! trailing notes\nmore",
+           "x = 3, y = 1\n2o1o!", "x = 3, y = 2\nooo$!", "x = 3, y = 1\n1o1b1o!",
+           "x=3,y=1\n3o!", "x = 3 , y = 1 , rule = b3/s23 \n3o!", "x = 3, y = 1, foo = 1\n3o!",
+           "x = 3, y = 1 junk\n3o!", "   \n\n#c\nx = 4, y = 2\n 2o\n b $ o !", "x = , y = 1\n!",
+           "x = 99999999999, y = 1\n!", "x = 3, y = 1\n1!", "x = 3, y = 1\n12", "#only comment",
+           "x = 10, y = 3\n10o$10b$10o!", "x = 3, y = 1\nb\n\no\n\nb!", "x = 1, y = 1\n!"]
+    for _ in range(80):  # mutate canonical forms
+        w, h = int(rng.integers(1, 20)), int(rng.integers(1, 12))
+        cells = [[x, y] for y in range(h) for x in range(w) if rng.random() < 0.35]
+        text = R_IO.serialize_rle(w, h, cells)
+        if rng.random() < 0.5:
+            i = int(rng.integers(0, len(text)))
+            text = text[:i] + str(rng.choice(list("ob$!2 \n#xq0"))) + text[i:]
+        rle.append(text)
+    plain = [".O.\n..O\nOOO", "OOO", "!block\nOO\nOO", ".O\nO\n\n..O", "OXO", "", "\n", "O\n",
+             "!c\n!d", " O . O \t\n..", "..\r\nO.\r\n", "O.O\n!x\nO"]
+    for _ in range(40):
+        rows = ["".join(rng.choice(list("..O O\t"), int(rng.integers(0, 9)))) for _ in range(int(rng.integers(0, 6)))]
+        t = "\n".join(rows)
+        if rng.random() < 0.2:
+            t += str(rng.choice(list("X*o#")))
+        plain.append(t)
+    ser = [(3, 1, [[0, 0], [1, 0], [2, 0]]), (1, 1, []), (3, 4, [[0, 0], [1, 0], [2, 0]]),
+           (1, 4, [[0, 0], [0, 3]]), (2, 2, [[5, 0]]), (4, 4, [[3, 3], [0, 0], [0, 0], [1, 0]])]
+    for _ in range(40):
+        w, h = int(rng.integers(1, 32)), int(rng.integers(1, 32))
+        ser.append((w, h, [[x, y] for y in range(h) for x in range(w) if rng.random() < 0.35]))
+    grids = [(int(rng.integers(3, 80)), int(rng.integers(3, 12)), int(s)) for s in range(12)] + \
+            [(35, 3, 99), (36, 4, 98), (70, 3, 97), (71, 3, 96)]
+    return rle, plain, ser, grids
+
+
+def io() -> None:
+    global R_IO
+    from oracle.oracle import REF_SO, PatternIO
+    R_IO = PatternIO(REF_SO, "ref_")
+    rle, plain, ser, grids = io_cases()
+    res = {"rle": [{"text": t, "ref": R_IO.parse_rle(t)} for t in rle],
+           "plaintext": [{"text": t, "ref": R_IO.parse_plaintext(t)} for t in plain],
+           "serialize": [{"w": w, "h": h, "cells": c, "ref": R_IO.serialize_rle(w, h, c)}
+                         for (w, h, c) in ser],
+           "render": []}
+    for (w, h, seed) in grids:
+        g = O.random_fill(w, h, 0.4, seed)
+        res["render"].append({"w": w, "h": h, "seed": seed, "ascii": R_IO.render("ascii", g),
+                              "pbm": R_IO.render("pbm", g)})
+    dump("golden_io.json", res)
+
+
 if __name__ == "__main__":
     for stage in sys.argv[1:] or ["small"]:
         print("stage", stage, flush=True)
