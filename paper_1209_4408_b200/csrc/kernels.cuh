@@ -476,11 +476,14 @@ struct ByteStepArgs {
   int64_t out_rows;
   int64_t seg_rows;
   int32_t nv;        // ceil(width / 16) vectors per row
-  int32_t n_strips;  // ceil(nv / 32)
+  int32_t n_strips;  // ceil(nv / 30)
 };
 
 constexpr int kByteThreads = 128;
-constexpr int kBytePrefetch = 3;
+constexpr int kBytePF = 6;                         // rows fetched ahead (multiple of 3)
+constexpr int kByteSlotWords = 32 * 4 + 2 * 32;    // 16-B vector + 2 seam words per lane
+constexpr int kByteSmem = (kByteThreads / 32) * 2 * kBytePF * kByteSlotWords * 4;  // per block
+constexpr int kByteStride = 30;                    // vectors stored per warp (lanes 1..30)
 
 struct ByteRow {
   uint32_t h[4];   // L + x + R per byte
@@ -519,111 +522,132 @@ __device__ __forceinline__ ByteRow byte_row(const uint4 v, uint32_t left_byte,
   return row;
 }
 
-// Byte-engine row staging: a per-warp shared-memory ring of kByteRing rows
-// filled by cp.async kByteRing-1 rows ahead.  A slot holds each lane's
-// 16-byte vector plus three 4-byte words for the lanes that need a neighbour
-// byte from outside the warp (left of lane 0, right of lane 31) or column 0
-// at the torus seam.
-constexpr int kByteRing = 8;
-constexpr int kByteSlotWords = 32 * 4 + 32 * 3;
-constexpr int kByteSmem = (kByteThreads / 32) * kByteRing * kByteSlotWords * 4;  // per block
-
 __device__ __forceinline__ void cp_async16(uint32_t* smem_dst, const void* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
 }
 
+// One warp, one strip x segment of the byte engine.  Lanes 0 and 31 hold
+// the neighbouring strips' edge vectors (ghosts; their neighbour bytes come
+// from the shuffles of the lanes inside), lanes 1..30 store.  When W % 16 ==
+// 0 the torus seam is an index wrap and every warp takes the plain path;
+// otherwise EDGE warps fetch, per row, the byte left of column 0 and column 0
+// itself for the seam lanes (compute_region's peeled columns,
+// engine.cpp:35-39, :44-46).
+template <bool EDGE>
+__device__ __forceinline__ void byte_pass(const ByteStepArgs& a, const int lane, const int64_t vi,
+                                          const int64_t y0, const int rows, uint32_t* ring) {
+  constexpr int PF = kBytePF;
+  const int64_t nv = a.nv;
+  int64_t src = vi % nv;
+  if (src < 0) src += nv;
+  const bool store = lane >= 1 && lane <= kByteStride && vi >= 0 && vi < nv;
+  const bool need_left = EDGE && store && vi == 0;  // byte left of column 0 = column W-1
+  const int seam_pos =
+      (EDGE && store && vi == nv - 1) ? static_cast<int>(a.width - 1 - vi * 16) : -1;
+  const int64_t left_word = ((a.width - 1) & ~3LL);
+  const uint32_t left_shift = static_cast<uint32_t>(((a.width - 1) & 3) * 8);
+
+  const int in_rows = static_cast<int>(a.in_rows);
+  int lrow = static_cast<int>(wrap_row(a.in_row0, y0 - 1, a.in_rows));
+  const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch);
+  const uint8_t* const in_lane = a.in + src * 16;
+  auto issue = [&](int slot) {
+    uint32_t* s = ring + slot * kByteSlotWords;
+    const uint64_t off = static_cast<uint64_t>(static_cast<uint32_t>(lrow)) * in_pitch_b;
+    cp_async16(s + lane * 4, in_lane + off);
+    if (EDGE) {
+      if (need_left) cp_async4(s + 128 + lane, reinterpret_cast<const uint32_t*>(a.in + off + left_word));
+      if (seam_pos >= 0) cp_async4(s + 160 + lane, reinterpret_cast<const uint32_t*>(a.in + off));
+    }
+    cp_async_commit();
+    lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
+  };
+  auto consume = [&](int slot) -> ByteRow {
+    const uint32_t* s = ring + slot * kByteSlotWords;
+    const uint4 v = *reinterpret_cast<const uint4*>(s + lane * 4);
+    uint32_t lb = __shfl_up_sync(kFull, v.w >> 24, 1);
+    const uint32_t rb = __shfl_down_sync(kFull, v.x & 0xffu, 1);
+    uint32_t col0 = 0;
+    if (EDGE) {
+      if (need_left) lb = (s[128 + lane] >> left_shift) & 0xffu;
+      if (seam_pos >= 0) col0 = s[160 + lane] & 0xffu;
+    }
+    return byte_row(v, lb, rb, seam_pos, col0);
+  };
+
+  const uint32_t out_pitch_b = static_cast<uint32_t>(a.out_pitch);
+  uint8_t* const out_lane = a.out + (a.out_row0 + y0) * a.out_pitch + vi * 16;
+#pragma unroll
+  for (int u = 0; u < PF; ++u) issue(u);
+  ByteRow up{}, mid{};
+  // Step t consumes input row y0-1+t; output row t-2 leaves at step t >= 2.
+  const int trips = (rows + 2 + PF - 1) / PF;
+  int half = 0;
+  for (int tr = 0; tr < trips; ++tr) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      issue((half ^ PF) + u);
+      cp_async_wait<PF>();
+      const ByteRow dn = consume(half + u);
+      const int j = tr * PF + u - 2;
+      if (store && static_cast<unsigned>(j) < static_cast<unsigned>(rows)) {
+        uint32_t o[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t n = up.h[i] + dn.h[i] + mid.hn[i];  // 8-neighbour count per byte
+          // (n | self) == 3  <=>  next alive (engine.cpp:32 on 0/1 bytes);
+          // t = (n|self)^3 is 0..15 per byte; zero-test via the byte's bit 7.
+          const uint32_t t = (n | mid.x[i]) ^ 0x03030303u;
+          o[i] = (~(t + 0x7f7f7f7fu) & 0x80808080u) >> 7;
+        }
+        if (EDGE && seam_pos >= 0) {  // zero the padding bytes past column W-1
+          const int keep = seam_pos + 1;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int lo = i * 4;
+            if (keep <= lo) o[i] = 0;
+            else if (keep < lo + 4) o[i] &= (1u << ((keep - lo) * 8)) - 1u;
+          }
+        }
+        *reinterpret_cast<uint4*>(out_lane + static_cast<uint64_t>(static_cast<uint32_t>(j)) *
+                                                 out_pitch_b) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+      up = mid;
+      mid = dn;
+    }
+    half ^= PF;
+  }
+  cp_async_wait<0>();
+}
+
+// Byte engine: one generation per pass over the byte layout.  Each lane owns
+// 16 cells (one uint4) of a row and walks down a segment of rows, keeping
+// the 3-row window of horizontal byte sums in registers; rows arrive through
+// a per-warp cp.async ring kBytePF rows ahead, so each input row is read once
+// (plus 2 halo rows per segment) and each output row written once: 2 B of HBM
+// traffic per cell-update.  SWAR: bytes hold 0..9, so uint32 adds never carry
+// between cells.  Restates compute_region (engine.cpp:17-48).
 __global__ void __launch_bounds__(kByteThreads) byte_step_kernel(const ByteStepArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kByteThreads + threadIdx.x) >> 5;
   const int strip = static_cast<int>(gwarp % a.n_strips);
   const int64_t seg = gwarp / a.n_strips;
   const int64_t y0 = seg * a.seg_rows;
-  if (y0 >= a.out_rows) return;
-  const int64_t rows = min(a.seg_rows, a.out_rows - y0);
-
-  const int64_t vi = static_cast<int64_t>(strip) * 32 + lane;
-  const int64_t c0 = vi * 16;
-  const bool active = vi < a.nv;
-  // Position of column W-1 inside this lane's vector, or -1.
-  const int seam_pos =
-      (active && a.width - 1 - c0 < 16) ? static_cast<int>(a.width - 1 - c0) : -1;
-  // Columns outside the warp's vectors: lane 0 needs the column left of c0,
-  // lane 31 (or the seam lane) the column right of its vector.
-  const int64_t left_col = c0 == 0 ? a.width - 1 : c0 - 1;
-  const int64_t right_col = c0 + 16 < a.width ? c0 + 16 : 0;
-  const bool need_left = active && lane == 0;
-  const bool need_right = active && (lane == 31 || seam_pos == 15);
-
+  if (y0 >= a.out_rows) return;  // warp-uniform
+  const int rows = static_cast<int>(min(a.seg_rows, a.out_rows - y0));
+  const int64_t vi = static_cast<int64_t>(strip) * kByteStride + lane - 1;
   extern __shared__ uint32_t byte_ring[];
-  uint32_t* ring = byte_ring + (threadIdx.x >> 5) * (kByteRing * kByteSlotWords);
-  int64_t lrow = wrap_row(a.in_row0, y0 - 1, a.in_rows);
-  auto issue = [&](int64_t step) {
-    const uint8_t* row = a.in + lrow * a.in_pitch;
-    uint32_t* s = ring + (static_cast<int>(step) & (kByteRing - 1)) * kByteSlotWords;
-    if (active) cp_async16(s + lane * 4, row + c0);
-    if (need_left) cp_async4(s + 128 + lane, reinterpret_cast<const uint32_t*>(row + (left_col & ~3LL)));
-    if (need_right) cp_async4(s + 160 + lane, reinterpret_cast<const uint32_t*>(row + (right_col & ~3LL)));
-    if (seam_pos >= 0) cp_async4(s + 192 + lane, reinterpret_cast<const uint32_t*>(row));
-    cp_async_commit();
-    if (++lrow == a.in_rows) lrow = 0;
-  };
-  auto consume = [&](int64_t step) -> ByteRow {
-    const uint32_t* s = ring + (static_cast<int>(step) & (kByteRing - 1)) * kByteSlotWords;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (active) v = *reinterpret_cast<const uint4*>(s + lane * 4);
-    uint32_t lb = __shfl_up_sync(kFull, v.w >> 24, 1);
-    uint32_t rb = __shfl_down_sync(kFull, v.x & 0xffu, 1);
-    if (need_left) lb = (s[128 + lane] >> ((left_col & 3) * 8)) & 0xffu;
-    if (need_right) rb = (s[160 + lane] >> ((right_col & 3) * 8)) & 0xffu;
-    const uint32_t col0 = seam_pos >= 0 ? (s[192 + lane] & 0xffu) : 0u;
-    return byte_row(v, lb, rb, seam_pos, col0);
-  };
-
-#pragma unroll
-  for (int u = 0; u < kByteRing - 1; ++u) issue(u);
-  issue(kByteRing - 1);
-  cp_async_wait<kByteRing - 1>();
-  ByteRow up = consume(0);
-  issue(kByteRing);
-  cp_async_wait<kByteRing - 1>();
-  ByteRow mid = consume(1);
-
-  uint8_t* out_row = a.out + (a.out_row0 + y0) * a.out_pitch + c0;
-  for (int64_t r0 = 0; r0 < rows; r0 += kBytePrefetch) {
-#pragma unroll
-    for (int u = 0; u < kBytePrefetch; ++u) {
-      const int64_t t = r0 + u + 2;  // consumption step of the row below
-      issue(t + kByteRing - 1);
-      cp_async_wait<kByteRing - 1>();
-      const ByteRow dn = consume(t);
-      uint32_t o[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const uint32_t n = up.h[i] + dn.h[i] + mid.hn[i];  // 8-neighbour count per byte
-        // (n | self) == 3  <=>  next alive (engine.cpp:32 on 0/1 bytes);
-        // t = (n|self)^3 is 0..15 per byte; zero-test via the byte's bit 7.
-        const uint32_t tt = (n | mid.x[i]) ^ 0x03030303u;
-        o[i] = (~(tt + 0x7f7f7f7fu) & 0x80808080u) >> 7;
-      }
-      if (seam_pos >= 0) {  // zero the padding bytes past column W-1
-        const int keep = seam_pos + 1;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int lo = i * 4;
-          if (keep <= lo) o[i] = 0;
-          else if (keep < lo + 4) o[i] &= (1u << ((keep - lo) * 8)) - 1u;
-        }
-      }
-      if (active && r0 + u < rows) {
-        *reinterpret_cast<uint4*>(out_row) = make_uint4(o[0], o[1], o[2], o[3]);
-      }
-      out_row += a.out_pitch;
-      up = mid;
-      mid = dn;
-    }
+  uint32_t* ring = byte_ring + (threadIdx.x >> 5) * (2 * kBytePF * kByteSlotWords);
+  // EDGE: W % 16 != 0 and this warp stores column 0 or column W-1.
+  const bool edge = (a.width & 15) != 0 &&
+                    __any_sync(kFull, lane >= 1 && lane <= kByteStride &&
+                                          (vi == 0 || vi == a.nv - 1));
+  if (edge) {
+    byte_pass<true>(a, lane, vi, y0, rows, ring);
+  } else {
+    byte_pass<false>(a, lane, vi, y0, rows, ring);
   }
-  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------

@@ -247,7 +247,7 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
   if (blocks_per_sm[dev & 63] == 0) {
     int nb = 0;
     LIFE_CUDA(cudaFuncSetAttribute(byte_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   8 * kByteSmem));
+                                   kByteSmem));
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, byte_step_kernel,
                                                             kByteThreads, kByteSmem));
     blocks_per_sm[dev & 63] = std::max(nb, 1);
@@ -263,7 +263,10 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
   a.width = width;
   a.out_rows = out_rows;
   a.nv = static_cast<int32_t>(ceil_div(width, 16));
-  a.n_strips = static_cast<int32_t>(ceil_div(a.nv, 32));
+  a.n_strips = static_cast<int32_t>(ceil_div(a.nv, kByteStride));
+  if (in_rows >= (int64_t(1) << 31) || in_pitch >= (int64_t(1) << 32) ||
+      out_pitch >= (int64_t(1) << 32) || out_rows >= (int64_t(1) << 31))
+    return set_error(LIFE_ERR_CONFIG, "grid too large for the byte engine");
   const int64_t resident_warps =
       static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kByteThreads / 32) * sm_count();
   // Two waves of warps, segments >= 32 rows (halo re-read <= 2/32).
