@@ -445,7 +445,7 @@ packed_tb_kernel(const PackedStepArgs a) {
     uint32_t smid;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    unsigned long long* tr = reinterpret_cast<unsigned long long*>(a.trace) + 3 * gwarp;
+    unsigned long long* tr = reinterpret_cast<unsigned long long*>(a.trace) + 3 * tile;
     tr[0] = smid;
     tr[1] = t_start;
     tr[2] = t_end;
