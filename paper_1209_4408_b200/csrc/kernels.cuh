@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 namespace lifegpu {
@@ -302,14 +303,20 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
     xin[g] = 0u;
   }
 
-  const int trips = (n + kLag + PF - 1) / PF;
+  // One loop trip (PF steps).  FILL trips cover the pipeline fill: stage g
+  // only sees valid input from step 3g on (stage g-1's first valid output),
+  // so a group of stages whose lowest stage is g0 is skipped (warp-uniform
+  // branch) while step < 3*g0 -- its window is overwritten by valid rows
+  // before its first valid output at step 3g0+2.
   int half = 0;
-  for (int t = 0; t < trips; ++t) {
+  auto trip = [&](const int t, auto fill_tag) {
+    constexpr bool FILL = decltype(fill_tag)::value;
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
       issue((half ^ PF) + u);
       cp_async_wait<PF>();
       xin[0] = consume(half + u);
+      const int step = t * PF + u;
       // The K stages of a step are independent (skewed pipeline); they are
       // issued in groups of kGroup, level by level (all shuffles, then all
       // funnels, ...), so consecutive instructions do not depend on each
@@ -320,6 +327,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
       uint32_t y_last = 0;
 #pragma unroll
       for (int g0 = ((K - 1) / kGroup) * kGroup; g0 >= 0; g0 -= kGroup) {
+        if (FILL && step < 3 * g0) continue;
         uint32_t xl[kGroup], xr[kGroup];
         HSum c[kGroup];
 #pragma unroll
@@ -356,19 +364,31 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
         }
       }
       // Output row j of the segment leaves the pipeline at step j + kLag.
-      const int j = t * PF + u - kLag;
-      if (static_cast<unsigned>(j) < static_cast<unsigned>(n)) {
-        char* p = out_seg + static_cast<uint64_t>(static_cast<uint32_t>(j)) * out_pitch_b;
-        const uint32_t v = y_last & st_mask;
-        if (st_lo) *reinterpret_cast<uint16_t*>(p) = static_cast<uint16_t>(v);
-        if (st_hi) *reinterpret_cast<uint16_t*>(p + 2) = static_cast<uint16_t>(v >> 16);
+      const int j = step - kLag;
+      if (!FILL) {  // no output leaves the pipeline during the fill trips
+        if (static_cast<unsigned>(j) < static_cast<unsigned>(n)) {
+          char* p = out_seg + static_cast<uint64_t>(static_cast<uint32_t>(j)) * out_pitch_b;
+          const uint32_t v = y_last & st_mask;
+          if (st_lo) *reinterpret_cast<uint16_t*>(p) = static_cast<uint16_t>(v);
+          if (st_hi) *reinterpret_cast<uint16_t*>(p + 2) = static_cast<uint16_t>(v >> 16);
+        }
       }
     }
     half ^= PF;
 #ifndef LIFE_NO_LOCKSTEP
     __syncthreads();
 #endif
-  }
+  };
+
+  const int trips = (n + kLag + PF - 1) / PF;
+  // Trips with a skippable group: while step < 3*(top group's lowest stage).
+  constexpr int kTopG0 = ((K - 1) / kGroup) * kGroup;
+  constexpr int kFillTrips = (3 * kTopG0 + PF - 1) / PF;
+  static_assert(PF * kFillTrips <= kLag, "fill trips must end before the first output");
+  const int fill_trips = trips < kFillTrips ? trips : kFillTrips;
+  int t = 0;
+  for (; t < fill_trips; ++t) trip(t, std::true_type{});
+  for (; t < trips; ++t) trip(t, std::false_type{});
   cp_async_wait<0>();
   return trips;
 }
