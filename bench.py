@@ -202,7 +202,7 @@ def run_reference_arm(args) -> None:
         t0 = time.perf_counter()
         eng.run(g, 1)
         per_gen = time.perf_counter() - t0
-    per_step = min(20.0, 170.0 / max(1, args.steps + args.warmup))
+    per_step = min(args.cpu_budget, 170.0 / max(1, args.steps + args.warmup))
     gens = max(1, int(per_step / max(per_gen, 1e-6)))
     times = []
     for i in range(args.warmup + args.steps):

@@ -1,0 +1,44 @@
+"""bench.py keeps the driver's JSON contract (one line, required keys)."""
+from __future__ import annotations
+
+import json
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+
+def run_bench(*args, timeout=600):
+    r = subprocess.run([sys.executable, "bench.py", *args], cwd=ROOT, capture_output=True,
+                       text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    j = run_bench("--impl", "reference", "--steps", "1", "--warmup", "0", "--config", "1",
+                  "--cpu-budget", "0.5")
+    assert j["impl"] == "reference" and j["unit"] == "GCUPS" and j["value"] > 0
+    for k in ("metric", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+              "cpu_baseline", "e2e", "config"):
+        assert k in j
+    assert j["e2e"]["h2d_bytes_per_step"] == 0 and j["cpu_baseline"]["cores"] >= 1
+
+
+@pytest.mark.gpu
+def test_gpu_arm_line():
+    j = run_bench("--config", "1", "--steps", "3", "--warmup", "3", "--cpu-budget", "1")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert k in j, k
+    assert j["value"] > 0 and j["gpu_launches"] > 0
+    assert j["roofline"]["bound"] == "int" and 0 < j["roofline"]["frac"] < 1.2
+    assert j["e2e"]["h2d_bytes_per_step"] == 1024 * 16 * 8 and j["e2e"]["value"] > 0
+    assert j["cpu_baseline"]["value"] > 0
+    b = run_bench("--engine", "byte", "--config", "1", "--steps", "3", "--warmup", "3")
+    assert b["roofline"]["bound"] == "hbm" and b["value"] > 0
