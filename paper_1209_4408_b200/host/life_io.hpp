@@ -101,16 +101,15 @@ class Reader {
   }
   [[noreturn]] void error(const std::string& what) const { throw ParseError(what, line_, col_); }
   void expect(char ch, const char* what) {
-    if (done() || cur() != ch) error(std::string("expected ") + what);
+    if (done() || cur() != ch) error(std::string("missing ") + what);
     next();
   }
   // Decimal run count; counts above 1e9 are rejected (pattern.cpp:14, :62-70).
   long number() {
     long v = 0;
-    while (!done() && std::isdigit(static_cast<unsigned char>(cur()))) {
+    for (; !done() && std::isdigit(static_cast<unsigned char>(cur())); next()) {
       v = v * 10 + (cur() - '0');
-      if (v > 1000000000L) error("run count too large");
-      next();
+      if (v > 1000000000L) error("number exceeds 1e9");
     }
     return v;
   }
@@ -126,86 +125,99 @@ inline bool is_blank(char c) { return blank(c); }
 
 }  // namespace detail
 
+// RLE header, as a fixed script of (skip blanks?, expected char, what) steps
+// with the two integers parsed after the '=' signs.
+inline void rle_header(detail::Reader& r, Pattern& p) {
+  struct Step {
+    char want;
+    const char* label;
+  };
+  static constexpr Step kScript[] = {{'x', "'x' opening the header"}, {'=', "'=' after x"},
+                                     {',', "',' between the dimensions"}, {'y', "'y' field"},
+                                     {'=', "'=' after y"}};
+  auto dimension = [&](const char* what) -> int {
+    r.skip_while(detail::space_or_tab);
+    if (r.done() || !std::isdigit(static_cast<unsigned char>(r.cur())))
+      r.error(std::string("missing ") + what);
+    return static_cast<int>(r.number());
+  };
+  for (int i = 0; i < 5; ++i) {
+    r.skip_while(detail::space_or_tab);
+    r.expect(kScript[i].want, kScript[i].label);
+    if (i == 1) p.width = dimension("width value");
+    if (i == 4) p.height = dimension("height value");
+  }
+  r.skip_while(detail::space_or_tab);
+  if (!r.done() && r.cur() == ',') {  // optional ", rule = B3/S23" (or 23/3)
+    r.next();
+    r.skip_while(detail::space_or_tab);
+    std::string field;
+    while (!r.done() && std::isalpha(static_cast<unsigned char>(r.cur()))) field += r.next();
+    if (detail::lowered(field) != "rule") r.error("header field '" + field + "' is not 'rule'");
+    r.skip_while(detail::space_or_tab);
+    r.expect('=', "'=' after rule");
+    r.skip_while(detail::space_or_tab);
+    std::string rule;
+    while (!r.done() && !detail::blank(r.cur()) && r.cur() != ',') rule += r.next();
+    const std::string lr = detail::lowered(rule);
+    if (lr != "b3/s23" && lr != "23/3") r.error("rule '" + rule + "' is not B3/S23");
+    r.skip_while(detail::space_or_tab);
+  }
+  if (!r.done() && r.cur() != '\n') r.error("unexpected text after the RLE header");
+  if (!r.done()) r.next();
+}
+
 inline Pattern parse_rle(std::string_view text) {
-  using detail::Reader;
-  Reader r(text);
-  // '#' comment lines and blank lines before the header.
-  for (;;) {
+  detail::Reader r(text);
+  for (;;) {  // leading blank and '#' comment lines
     r.skip_while(detail::is_blank);
     if (r.done() || r.cur() != '#') break;
     while (!r.done() && r.next() != '\n') {
     }
   }
-  if (r.done()) r.error("missing RLE header");
-
+  if (r.done()) r.error("no RLE header found");
   Pattern p;
-  auto header_int = [&](const char* what) {
-    r.skip_while(detail::space_or_tab);
-    if (r.done() || !std::isdigit(static_cast<unsigned char>(r.cur())))
-      r.error(std::string("expected ") + what);
-    return static_cast<int>(r.number());
-  };
-  r.skip_while(detail::space_or_tab);
-  r.expect('x', "'x' at start of RLE header");
-  r.skip_while(detail::space_or_tab);
-  r.expect('=', "'=' after 'x'");
-  p.width = header_int("width after 'x ='");
-  r.skip_while(detail::space_or_tab);
-  r.expect(',', "',' after width");
-  r.skip_while(detail::space_or_tab);
-  r.expect('y', "'y' in RLE header");
-  r.skip_while(detail::space_or_tab);
-  r.expect('=', "'=' after 'y'");
-  p.height = header_int("height after 'y ='");
-  r.skip_while(detail::space_or_tab);
-  if (!r.done() && r.cur() == ',') {
-    r.next();
-    r.skip_while(detail::space_or_tab);
-    std::string key;
-    while (!r.done() && std::isalpha(static_cast<unsigned char>(r.cur()))) key += r.next();
-    if (detail::lowered(key) != "rule") r.error("unknown RLE header field '" + key + "'");
-    r.skip_while(detail::space_or_tab);
-    r.expect('=', "'=' after 'rule'");
-    r.skip_while(detail::space_or_tab);
-    std::string rule;
-    while (!r.done() && !detail::blank(r.cur()) && r.cur() != ',') rule += r.next();
-    const std::string lr = detail::lowered(rule);
-    if (lr != "b3/s23" && lr != "23/3") r.error("unsupported rule '" + rule + "' (only B3/S23)");
-    r.skip_while(detail::space_or_tab);
-  }
-  if (!r.done() && r.cur() != '\n') r.error("trailing characters after RLE header");
-  if (!r.done()) r.next();
+  rle_header(r, p);
 
-  int x = 0, y = 0;
-  for (;;) {
+  int col = 0, row = 0;
+  for (bool open = true; open;) {
     r.skip_while(detail::is_blank);
-    if (r.done()) r.error("missing '!' terminator");
-    long count = 1;
+    if (r.done()) r.error("RLE body ends without '!'");
+    long run = 1;
     if (std::isdigit(static_cast<unsigned char>(r.cur()))) {
-      count = r.number();
-      if (count == 0) r.error("run count must be positive");
+      run = r.number();
+      if (run == 0) r.error("a run of 0 cells");
       r.skip_while(detail::is_blank);
-      if (r.done()) r.error("run count without a tag");
+      if (r.done()) r.error("run count not followed by a tag");
     }
-    const int tl = r.line(), tc = r.col();
+    const int at_line = r.line(), at_col = r.col();
     const char tag = r.next();
-    if (tag == 'b' || tag == 'B' || tag == 'o' || tag == 'O') {
-      if (y >= p.height)
-        throw ParseError("cell row " + std::to_string(y) + " exceeds declared height " +
-                             std::to_string(p.height), tl, tc);
-      if (x + count > p.width)
-        throw ParseError("run exceeds declared width " + std::to_string(p.width), tl, tc);
-      if (tag == 'o' || tag == 'O')
-        for (long k = 0; k < count; ++k) p.live_cells.push_back({x + static_cast<int>(k), y});
-      x += static_cast<int>(count);
-    } else if (tag == '$') {
-      y += static_cast<int>(count);
-      x = 0;
-    } else if (tag == '!') {
-      if (count != 1) throw ParseError("run count before '!'", tl, tc);
-      break;  // anything after '!' is ignored
-    } else {
-      throw ParseError(std::string("unexpected character '") + tag + "'", tl, tc);
+    switch (tag) {
+      case '!':
+        if (run != 1) throw ParseError("'!' may not carry a run count", at_line, at_col);
+        open = false;  // the rest of the text is ignored
+        break;
+      case '$':
+        row += static_cast<int>(run);
+        col = 0;
+        break;
+      case 'o':
+      case 'O':
+      case 'b':
+      case 'B': {
+        if (row >= p.height)
+          throw ParseError("row " + std::to_string(row) + " lies beyond the declared height " +
+                               std::to_string(p.height), at_line, at_col);
+        if (col + run > p.width)
+          throw ParseError("run passes the declared width " + std::to_string(p.width), at_line,
+                           at_col);
+        const bool live = tag == 'o' || tag == 'O';
+        for (long k = 0; live && k < run; ++k) p.live_cells.push_back({col + static_cast<int>(k), row});
+        col += static_cast<int>(run);
+        break;
+      }
+      default:
+        throw ParseError(std::string("illegal character '") + tag + "' in RLE body", at_line, at_col);
     }
   }
   return p;
@@ -260,8 +272,8 @@ inline Pattern parse_plaintext(std::string_view text) {
         } else if (ln[i] == 'O') {
           p.live_cells.push_back({x++, row});
         } else if (!detail::blank(ln[i])) {
-          throw ParseError(std::string("unexpected character '") + ln[i] + "'", line_no,
-                           static_cast<int>(i) + 1);
+          throw ParseError(std::string("illegal character '") + ln[i] + "' in plaintext",
+                           line_no, static_cast<int>(i) + 1);
         }
       }
       p.width = std::max(p.width, x);
