@@ -288,3 +288,206 @@ class LocalBands:
     def gather(self) -> torch.Tensor:
         """The whole torus as packed uint32 rows (device)."""
         return torch.cat([d.band() for d in self.drivers], dim=0)
+
+
+# ---------------------------------------------------------------------------
+# Fused halo over NVLink: the pass kernel reads the neighbour bands' rows
+# straight from their HBM (CUDA IPC peer mappings), so a pass is ONE launch
+# per GPU and there is no separate exchange step; a stream-ordered barrier
+# (a 1-element NCCL all-reduce) between passes keeps neighbours from
+# overwriting rows that are still being read.
+# ---------------------------------------------------------------------------
+class DeviceBuffer:
+    """cudaMalloc'd packed rows (IPC-shareable), exposed to torch zero-copy."""
+
+    def __init__(self, rows: int, pitch: int, device: torch.device):
+        import ctypes as C
+        self.rows, self.pitch, self.device = rows, pitch, device
+        self.ptr = C.c_void_p()
+        with torch.cuda.device(device):
+            check(capi.lib().life_dev_alloc(rows * pitch * 4, C.byref(self.ptr)))
+        self.tensor = torch.as_tensor(_CudaArray(self.ptr.value, (rows, pitch), device),
+                                      device=device)
+
+    def handle(self) -> bytes:
+        import ctypes as C
+        h = (C.c_ubyte * 64)()
+        check(capi.lib().life_ipc_get_handle(self.ptr, h))
+        return bytes(h)
+
+    def free(self) -> None:
+        if self.ptr:
+            capi.lib().life_dev_free(self.ptr)
+            self.ptr = None
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ view so torch can wrap a raw pointer."""
+
+    def __init__(self, ptr: int, shape, device: torch.device):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i4",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def open_peer(handle: bytes) -> int:
+    import ctypes as C
+    buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+    out = C.c_void_p()
+    check(capi.lib().life_ipc_open(buf, C.byref(out)))
+    return out.value
+
+
+def peer_step(width: int, src: int, up: int, up_rows: int, down: int, down_rows: int,
+              pitch: int, band_rows: int, dst: int, k: int, device: torch.device) -> None:
+    stream = torch.cuda.current_stream(device).cuda_stream
+    check(capi.lib().life_dev_packed_step_peer(src, up, up_rows, down, down_rows, pitch,
+                                               band_rows, dst, width, k, stream))
+
+
+class PeerBandDriver:
+    """One rank's band for the fused NVLink halo (see above).  `barrier`
+    defaults to a stream-ordered NCCL all-reduce; a host barrier
+    (synchronize + dist.barrier) is used with non-NCCL process groups."""
+
+    def __init__(self, geo: BandGeometry, device: torch.device, group=None):
+        if geo.world < 2:
+            raise ConfigError("PeerBandDriver needs at least two ranks")
+        self.geo = geo
+        self.device = device
+        self.group = group
+        self.buf = [DeviceBuffer(geo.band_rows, geo.pitch, device) for _ in range(2)]
+        self.cur = 0
+        self.generations = 0
+        # Exchange IPC handles and band heights with every rank.
+        mine = (geo.band_rows, [b.handle() for b in self.buf])
+        allinfo = [None] * geo.world
+        dist.all_gather_object(allinfo, mine, group=group)
+        up, down = (geo.rank - 1) % geo.world, (geo.rank + 1) % geo.world
+        self._opened = []
+
+        def peer_ptrs(r):
+            rows, handles = allinfo[r]
+            ptrs = []
+            for i, h in enumerate(handles):
+                if r == geo.rank:
+                    ptrs.append(self.buf[i].ptr.value)
+                else:
+                    p = open_peer(h)
+                    self._opened.append(p)
+                    ptrs.append(p)
+            return rows, ptrs
+
+        with torch.cuda.device(device):
+            self.up_rows, self.up_ptrs = peer_ptrs(up)
+            self.down_rows, self.down_ptrs = (self.up_rows, self.up_ptrs) if down == up \
+                else peer_ptrs(down)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=device)
+        self._nccl = dist.get_backend(group) == "nccl"
+
+    def band(self) -> torch.Tensor:
+        return self.buf[self.cur].tensor
+
+    def barrier(self) -> None:
+        if self._nccl:
+            dist.all_reduce(self._flag, group=self.group)  # ordered on the current stream
+        else:
+            torch.cuda.synchronize(self.device)
+            dist.barrier(group=self.group)
+
+    def pass_(self, k: int) -> None:
+        g = self.geo
+        if not 1 <= k <= g.depth:
+            raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
+        c = self.cur
+        peer_step(g.width, self.buf[c].ptr.value, self.up_ptrs[c], self.up_rows,
+                  self.down_ptrs[c], self.down_rows, g.pitch, g.band_rows,
+                  self.buf[c ^ 1].ptr.value, k, self.device)
+        self.barrier()
+        self.cur ^= 1
+        self.generations += k
+
+    def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None) -> None:
+        if generations < 0:
+            raise ConfigError(f"iteration count must be non-negative, got {generations}")
+        self.barrier()  # every rank's initial band is in place
+        done = 0
+        while done < generations:
+            k = min(self.geo.depth, generations - done)
+            self.pass_(k)
+            done += k
+            if on_pass:
+                on_pass(k)
+
+    def init_random(self, density: float, seed: int) -> None:
+        g = self.geo
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_random(self.band().data_ptr(), g.pitch, g.width, g.y0,
+                                                g.band_rows, density, seed, stream))
+        self.generations = 0
+
+    def load_rows(self, words) -> None:
+        g = self.geo
+        src = torch.from_numpy(words[g.y0:g.y1].view("int32").copy())
+        self.band()[:, :src.shape[1]].copy_(src)
+        self.generations = 0
+
+    def population(self) -> int:
+        g = self.geo
+        acc = torch.zeros(1, dtype=torch.int64, device=self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_population(self.band().data_ptr(), g.pitch, g.width,
+                                                    g.band_rows, acc.data_ptr(), stream))
+        dist.all_reduce(acc, group=self.group)
+        return int(acc.item())
+
+    def close(self) -> None:
+        torch.cuda.synchronize(self.device)
+        for p in self._opened:
+            capi.lib().life_ipc_close(p)
+        self._opened = []
+        for b in self.buf:
+            b.free()
+
+
+class LocalPeerBands:
+    """P bands of one torus on ONE device through the fused-halo kernel
+    (life_dev_packed_step_peer with the neighbours' local buffers as the
+    peers): exercises the in-kernel cross-band row addressing with no
+    cross-GPU waits."""
+
+    def __init__(self, width: int, height: int, parts: int, depth: int, device: torch.device):
+        if parts < 2:
+            raise ConfigError("LocalPeerBands needs at least two bands")
+        self.geos = [make_geometry(width, height, r, parts, depth) for r in range(parts)]
+        self.device = device
+        self.bufs = [[torch.zeros((g.band_rows, g.pitch), dtype=torch.int32, device=device)
+                      for _ in range(2)] for g in self.geos]
+        self.cur = 0
+
+    def init_random(self, density: float, seed: int) -> None:
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        for g, b in zip(self.geos, self.bufs):
+            check(capi.lib().life_dev_packed_random(b[self.cur].data_ptr(), g.pitch, g.width, g.y0,
+                                                    g.band_rows, density, seed, stream))
+
+    def pass_(self, k: int) -> None:
+        p = len(self.geos)
+        c = self.cur
+        for r, g in enumerate(self.geos):
+            up, down = (r - 1) % p, (r + 1) % p
+            peer_step(g.width, self.bufs[r][c].data_ptr(), self.bufs[up][c].data_ptr(),
+                      self.geos[up].band_rows, self.bufs[down][c].data_ptr(),
+                      self.geos[down].band_rows, g.pitch, g.band_rows,
+                      self.bufs[r][c ^ 1].data_ptr(), k, self.device)
+        self.cur ^= 1
+
+    def run(self, generations: int) -> None:
+        depth = self.geos[0].depth
+        done = 0
+        while done < generations:
+            k = min(depth, generations - done)
+            self.pass_(k)
+            done += k
+
+    def gather(self) -> torch.Tensor:
+        return torch.cat([b[self.cur] for b in self.bufs], dim=0)

@@ -58,6 +58,13 @@ SIGNATURES = [
     ("life_byte_pitch", _i64, [_i64]),
     ("life_dev_packed_step", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i32,
                                        _vp]),
+    ("life_dev_packed_step_peer", C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64,
+                                            _i32, _vp]),
+    ("life_dev_alloc", C.c_int, [_i64, C.POINTER(_vp)]),
+    ("life_dev_free", C.c_int, [_vp]),
+    ("life_ipc_get_handle", C.c_int, [_vp, _vp]),
+    ("life_ipc_open", C.c_int, [_vp, C.POINTER(_vp)]),
+    ("life_ipc_close", C.c_int, [_vp]),
     ("life_dev_byte_step", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
     ("life_dev_packed_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),
     ("life_dev_byte_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),

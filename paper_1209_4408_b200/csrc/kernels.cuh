@@ -137,6 +137,16 @@ struct PackedStepArgs {
   uint32_t two;       // 2     (hsum_fma operands)
   uint32_t half;      // 2^31
   void* trace;        // LIFE_TRACE builds: per-warp (smid, start, end)
+  // Peer mode (multi-GPU row bands over NVLink): input relative row r < 0 is
+  // row up_rows + r of `up` (the band above, a peer GPU's buffer), r >=
+  // in_rows is row r - in_rows of `down` (the band below); in_row0 = 0 and
+  // no modular wrap.  The halo never leaves the kernel: edge tiles cp.async
+  // their ghost rows straight from the neighbours' HBM.
+  const uint32_t* up;
+  const uint32_t* down;
+  int64_t up_rows;
+  int64_t down_rows;
+  int32_t peer;
 };
 
 // A warp covers 32 consecutive words; strips advance by 31 words, so
@@ -256,8 +266,22 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   int lrow = static_cast<int>(wrap_row(a.in_row0, static_cast<int64_t>(y) - K, a.in_rows));
   const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch * 4);
   const char* const in_lane = reinterpret_cast<const char*>(a.in + plan.src);
+  if (EDGE && a.peer) lrow = y - K;  // relative row, resolved across the three bands
   auto issue = [&](int slot) {
-    const uint32_t* row = a.in + static_cast<int64_t>(lrow) * a.in_pitch;
+    const uint32_t* row;
+    if (EDGE && a.peer) {
+      const int64_t r = lrow;
+      if (r < 0) {
+        row = a.up + (a.up_rows + r) * a.in_pitch;
+      } else if (r < in_rows) {
+        row = a.in + r * a.in_pitch;
+      } else {
+        const int64_t d = r - in_rows;  // rows past the light cone are over-reads: clamp
+        row = a.down + (d < a.down_rows ? d : a.down_rows - 1) * a.in_pitch;
+      }
+    } else {
+      row = a.in + static_cast<int64_t>(lrow) * a.in_pitch;
+    }
     uint32_t* s = ring + slot * 96;
     if (!EDGE) {
       cp_async4(s, reinterpret_cast<const uint32_t*>(
@@ -272,7 +296,11 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
       cp_async4(s + 64, row);
     }
     cp_async_commit();
-    lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
+    if (EDGE && a.peer) {
+      ++lrow;
+    } else {
+      lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
+    }
   };
   auto consume = [&](int slot) -> uint32_t {
     const uint32_t* s = ring + slot * 96;
@@ -446,9 +474,14 @@ packed_tb_kernel(const PackedStepArgs a) {
   uint32_t* ring = ring_smem + (threadIdx.x >> 5) * (2 * PackedTraits<K>::kPrefetch * 96) + lane;
   int trips = 0;
   if (n > 0) {
-    // EDGE if this strip needs the 3-word seam fetch.
+    // EDGE if this strip needs the 3-word seam fetch, or (peer mode) the
+    // tile's rows reach past the band into a neighbour GPU's band.
     const int64_t wi = static_cast<int64_t>(strip) * kStripStride + lane - 1;
-    const bool edge = a.width < 32 || __any_sync(kFull, make_plan(wi, a.width, a.nw).mode != 0);
+    constexpr int PF = PackedTraits<K>::kPrefetch;
+    const int64_t last_row = y0 - K + (static_cast<int64_t>(a.steps) + 1) * PF;  // last row issued
+    const bool near_band_edge = a.peer && (y0 < K || last_row >= a.in_rows);
+    const bool edge = a.width < 32 || near_band_edge ||
+                      __any_sync(kFull, make_plan(wi, a.width, a.nw).mode != 0);
     if (edge) {
       trips = packed_segment<K, true>(a, lane, strip, static_cast<int>(y0), n, ring);
     } else {

@@ -234,6 +234,75 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
   return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
 }
 
+int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
+                              const uint32_t* down, int64_t down_rows, int64_t pitch,
+                              int64_t band_rows, uint32_t* out, int64_t width,
+                              int32_t generations, void* stream) {
+  if (generations < 1 || generations > LIFE_MAX_TEMPORAL_DEPTH)
+    return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [1, %d], got %d",
+                     LIFE_MAX_TEMPORAL_DEPTH, generations);
+  if (!in || !up || !down || !out || width < 1 || pitch < 2 * ceil_div(width, 64))
+    return set_error(LIFE_ERR_CONFIG, "bad peer step geometry");
+  if (band_rows < generations || up_rows < generations || down_rows < generations)
+    return set_error(LIFE_ERR_TOO_MANY_PARTS, "bands must be at least %d rows", generations);
+  PackedStepArgs a{};
+  a.in = in;
+  a.in_pitch = pitch;
+  a.in_row0 = 0;
+  a.in_rows = band_rows;
+  a.out = out;
+  a.out_pitch = pitch;
+  a.out_row0 = 0;
+  a.width = width;
+  a.out_rows = band_rows;
+  a.nw = static_cast<int32_t>(nw32(width));
+  a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
+  a.tail_mask = tail_mask(width);
+  a.two = 2u;
+  a.half = 0x80000000u;
+  a.trace = g_trace;
+  a.up = up;
+  a.down = down;
+  a.up_rows = up_rows;
+  a.down_rows = down_rows;
+  a.peer = 1;
+  return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
+}
+
+int life_dev_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return set_error(LIFE_ERR_CONFIG, "bad allocation request");
+  *out = nullptr;
+  LIFE_CUDA(cudaMalloc(out, bytes > 0 ? bytes : 1));
+  LIFE_CUDA(cudaMemset(*out, 0, bytes > 0 ? bytes : 1));
+  return LIFE_OK;
+}
+
+int life_dev_free(void* p) {
+  if (p) LIFE_CUDA(cudaFree(p));
+  return LIFE_OK;
+}
+
+int life_ipc_get_handle(void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return set_error(LIFE_ERR_CONFIG, "null pointer");
+  cudaIpcMemHandle_t h;
+  LIFE_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return LIFE_OK;
+}
+
+int life_ipc_open(const void* handle, void** out) {
+  if (!handle || !out) return set_error(LIFE_ERR_CONFIG, "null pointer");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  LIFE_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return LIFE_OK;
+}
+
+int life_ipc_close(void* dev_ptr) {
+  if (dev_ptr) LIFE_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return LIFE_OK;
+}
+
 int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
                        uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
                        int64_t out_rows, void* stream) {
