@@ -247,10 +247,19 @@ def run_gpu_arm(args) -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # LIFE_BENCH_DEVICE / LIFE_BENCH_BACKEND exist for the single-GPU test of
+    # the multi-rank path (ranks sharing cuda:0 over gloo, host barriers only,
+    # so no kernel ever waits on another rank): tests/test_bench_contract.py.
+    if os.environ.get("LIFE_BENCH_DEVICE"):
+        local = int(os.environ["LIFE_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("LIFE_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     L = capi.lib()
     cfg = CONFIGS[args.config]
     W, H, gens, depth = cfg["w"], cfg["h"], args.gens or cfg["gens"], args.depth
@@ -292,7 +301,33 @@ def run_gpu_arm(args) -> None:
         else:
             base_step(inp, in_row0, in_rows, out, out_row0, out_rows, k)
 
-    drv = BandDriver(geo, dev, stepper=timed_step)
+    halo = "none" if world == 1 else args.halo
+    drv = None
+    if halo == "peer":
+        # Fused halo: the pass kernels read the neighbour bands' rows over
+        # NVLink (CUDA IPC); NCCL is only the per-pass barrier.
+        try:
+            from paper_1209_4408_b200.bands import PeerBandDriver
+            drv = PeerBandDriver(geo, dev)
+            inner = drv.compute
+
+            def timed_compute(k):
+                if record["on"]:
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    inner(k)
+                    e1.record()
+                    launches.append((e0, e1, geo.band_rows * W * k, k, geo.band_rows))
+                else:
+                    inner(k)
+            drv.compute = timed_compute
+        except Exception as exc:  # no IPC / peer access: NCCL send/recv halos
+            print(f"peer halo unavailable ({exc!r}); using NCCL send/recv", file=sys.stderr)
+            halo = "nccl"
+            drv = None
+    if drv is None:
+        drv = BandDriver(geo, dev, stepper=timed_step)
     soup_host = None
     if cfg.get("soup"):
         with Engine(local) as e:  # device soup, shared by every rank's band
@@ -365,6 +400,8 @@ def run_gpu_arm(args) -> None:
         "roofline_updates_per_s": min(int_ops / OPS_PER_UPDATE if int_ops else float("inf"),
                                       hbm_peak * 1e9 / alg_bytes_per_update),
     }
+    if hasattr(drv, "close"):
+        drv.close()
     del drv
     torch.cuda.empty_cache()
 
@@ -392,7 +429,11 @@ def run_gpu_arm(args) -> None:
             eng.close()
             bi = bo = H * wpr * 8
         else:
-            drv = BandDriver(geo, dev)
+            if halo == "peer":
+                from paper_1209_4408_b200.bands import PeerBandDriver
+                drv = PeerBandDriver(geo, dev)
+            else:
+                drv = BandDriver(geo, dev)
             host = torch.empty(tuple(drv.band().shape), dtype=torch.int32, pin_memory=True)
             if soup_host is not None:
                 drv.load_rows(soup_host)
@@ -416,6 +457,8 @@ def run_gpu_arm(args) -> None:
             t = torch.tensor([host.numel() * 4], dtype=torch.int64, device=dev)
             dist.all_reduce(t)
             bi = bo = int(t.item())
+            if hasattr(drv, "close"):
+                drv.close()
             del drv
         e2e = {"value": W * H * gens * steps_e2e / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
@@ -441,6 +484,9 @@ def run_gpu_arm(args) -> None:
             "config": {"workload": cfg["desc"], "width": W, "height": H, "generations": gens,
                        "temporal_depth": depth, "global_cells": W * H,
                        "parallelism": f"rowbands{world}" if world > 1 else "single-gpu",
+                       "halo": {"peer": "in-kernel NVLink peer reads (CUDA IPC) + NCCL barrier",
+                                "nccl": "NCCL send/recv of k ghost rows, interior overlapped",
+                                "none": "torus wraps inside the kernel"}[halo],
                        "l2": ("inputs larger than L2" if flush is None else
                               "L2 flushed (256 MiB write) between steps")},
             "roofline": roofline,
@@ -542,6 +588,8 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--engine", choices=["packed", "byte"], default="packed")
+    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
+                    help="multi-GPU halo: in-kernel NVLink peer reads or NCCL send/recv")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

@@ -155,14 +155,16 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0,
  * halo read IN the kernel over NVLink: input rows above the band come from
  * `up` (the last rows of the band above, up_rows tall -- a peer GPU's buffer
  * opened with life_ipc_open), rows below from `down` (the first rows of the
- * band below).  Output rows [0, band_rows) go to `out`.  All four buffers use
- * `pitch`.  The caller orders passes across GPUs (a barrier per pass: the
- * neighbours must have finished writing `up`/`down` and reading the buffer
- * this pass overwrites).  Bands must be >= `generations` rows. */
+ * band below).  Band rows [out_row0, out_row0+out_rows) are written to the
+ * same rows of `out`.  All buffers use `pitch`.  The caller orders passes
+ * across GPUs (a barrier per pass: the neighbours must have finished writing
+ * `up`/`down` and reading the buffer this pass overwrites).  Bands must be
+ * >= `generations` rows. */
 int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
                               const uint32_t* down, int64_t down_rows, int64_t pitch,
-                              int64_t band_rows, uint32_t* out, int64_t width,
-                              int32_t generations, void* stream);
+                              int64_t band_rows, uint32_t* out, int64_t out_row0,
+                              int64_t out_rows, int64_t width, int32_t generations,
+                              void* stream);
 /* Device buffers shareable across processes (cudaMalloc, zeroed) and CUDA
  * IPC: a 64-byte handle per buffer, opened in the peer process. */
 int life_dev_alloc(int64_t bytes, void** out);

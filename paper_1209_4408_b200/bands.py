@@ -337,11 +337,29 @@ def open_peer(handle: bytes) -> int:
     return out.value
 
 
-def peer_step(width: int, src: int, up: int, up_rows: int, down: int, down_rows: int,
-              pitch: int, band_rows: int, dst: int, k: int, device: torch.device) -> None:
-    stream = torch.cuda.current_stream(device).cuda_stream
-    check(capi.lib().life_dev_packed_step_peer(src, up, up_rows, down, down_rows, pitch,
-                                               band_rows, dst, width, k, stream))
+def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows: int,
+              pitch: int, band_rows: int, dst: int, k: int, device: torch.device,
+              edge_stream: Optional["torch.cuda.Stream"] = None) -> None:
+    """One depth-k pass of a band with in-kernel NVLink halos: the interior
+    rows [k, band-k) read only the band's own rows (the branch-free kernel
+    path); the two k-row edge strips read the neighbours' rows through peer
+    pointers and run on `edge_stream` (if given) beside the interior."""
+    L = capi.lib()
+    main = torch.cuda.current_stream(device)
+    if band_rows <= 2 * k:
+        check(L.life_dev_packed_step_peer(src, up, up_rows, down, down_rows, pitch, band_rows,
+                                          dst, 0, band_rows, width, k, main.cuda_stream))
+        return
+    if edge_stream is not None:
+        edge_stream.wait_stream(main)
+    check(L.life_dev_packed_step(src, pitch, k, band_rows, dst, pitch, k, width,
+                                 band_rows - 2 * k, k, main.cuda_stream))
+    es = edge_stream.cuda_stream if edge_stream is not None else main.cuda_stream
+    for r0 in (0, band_rows - k):
+        check(L.life_dev_packed_step_peer(src, up, up_rows, down, down_rows, pitch, band_rows,
+                                          dst, r0, k, width, k, es))
+    if edge_stream is not None:
+        main.wait_stream(edge_stream)
 
 
 class PeerBandDriver:
@@ -383,6 +401,7 @@ class PeerBandDriver:
                 else peer_ptrs(down)
         self._flag = torch.zeros(1, dtype=torch.int32, device=device)
         self._nccl = dist.get_backend(group) == "nccl"
+        self.edge_stream = torch.cuda.Stream(device)
 
     def band(self) -> torch.Tensor:
         return self.buf[self.cur].tensor
@@ -394,14 +413,19 @@ class PeerBandDriver:
             torch.cuda.synchronize(self.device)
             dist.barrier(group=self.group)
 
+    def compute(self, k: int) -> None:
+        """The pass's kernels (interior + peer edge strips), no barrier."""
+        g = self.geo
+        c = self.cur
+        peer_pass(g.width, self.buf[c].ptr.value, self.up_ptrs[c], self.up_rows,
+                  self.down_ptrs[c], self.down_rows, g.pitch, g.band_rows,
+                  self.buf[c ^ 1].ptr.value, k, self.device, self.edge_stream)
+
     def pass_(self, k: int) -> None:
         g = self.geo
         if not 1 <= k <= g.depth:
             raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
-        c = self.cur
-        peer_step(g.width, self.buf[c].ptr.value, self.up_ptrs[c], self.up_rows,
-                  self.down_ptrs[c], self.down_rows, g.pitch, g.band_rows,
-                  self.buf[c ^ 1].ptr.value, k, self.device)
+        self.compute(k)
         self.barrier()
         self.cur ^= 1
         self.generations += k
@@ -463,6 +487,7 @@ class LocalPeerBands:
         self.bufs = [[torch.zeros((g.band_rows, g.pitch), dtype=torch.int32, device=device)
                       for _ in range(2)] for g in self.geos]
         self.cur = 0
+        self.edge_stream = torch.cuda.Stream(device)
 
     def init_random(self, density: float, seed: int) -> None:
         stream = torch.cuda.current_stream(self.device).cuda_stream
@@ -475,10 +500,10 @@ class LocalPeerBands:
         c = self.cur
         for r, g in enumerate(self.geos):
             up, down = (r - 1) % p, (r + 1) % p
-            peer_step(g.width, self.bufs[r][c].data_ptr(), self.bufs[up][c].data_ptr(),
+            peer_pass(g.width, self.bufs[r][c].data_ptr(), self.bufs[up][c].data_ptr(),
                       self.geos[up].band_rows, self.bufs[down][c].data_ptr(),
                       self.geos[down].band_rows, g.pitch, g.band_rows,
-                      self.bufs[r][c ^ 1].data_ptr(), k, self.device)
+                      self.bufs[r][c ^ 1].data_ptr(), k, self.device, self.edge_stream)
         self.cur ^= 1
 
     def run(self, generations: int) -> None:

@@ -59,7 +59,7 @@ SIGNATURES = [
     ("life_dev_packed_step", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i32,
                                        _vp]),
     ("life_dev_packed_step_peer", C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64,
-                                            _i32, _vp]),
+                                            _i64, _i64, _i32, _vp]),
     ("life_dev_alloc", C.c_int, [_i64, C.POINTER(_vp)]),
     ("life_dev_free", C.c_int, [_vp]),
     ("life_ipc_get_handle", C.c_int, [_vp, _vp]),

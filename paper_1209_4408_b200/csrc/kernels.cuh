@@ -266,7 +266,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   int lrow = static_cast<int>(wrap_row(a.in_row0, static_cast<int64_t>(y) - K, a.in_rows));
   const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch * 4);
   const char* const in_lane = reinterpret_cast<const char*>(a.in + plan.src);
-  if (EDGE && a.peer) lrow = y - K;  // relative row, resolved across the three bands
+  if (EDGE && a.peer) lrow = static_cast<int>(a.in_row0) + y - K;  // band row, resolved across bands
   auto issue = [&](int slot) {
     const uint32_t* row;
     if (EDGE && a.peer) {
@@ -478,8 +478,9 @@ packed_tb_kernel(const PackedStepArgs a) {
     // tile's rows reach past the band into a neighbour GPU's band.
     const int64_t wi = static_cast<int64_t>(strip) * kStripStride + lane - 1;
     constexpr int PF = PackedTraits<K>::kPrefetch;
-    const int64_t last_row = y0 - K + (static_cast<int64_t>(a.steps) + 1) * PF;  // last row issued
-    const bool near_band_edge = a.peer && (y0 < K || last_row >= a.in_rows);
+    const int64_t yb = a.in_row0 + y0;  // band row of the tile's first output row
+    const int64_t last_row = yb - K + (static_cast<int64_t>(a.steps) + 1) * PF;  // last row issued
+    const bool near_band_edge = a.peer && (yb < K || last_row >= a.in_rows);
     const bool edge = a.width < 32 || near_band_edge ||
                       __any_sync(kFull, make_plan(wi, a.width, a.nw).mode != 0);
     if (edge) {

@@ -236,8 +236,9 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
 
 int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
                               const uint32_t* down, int64_t down_rows, int64_t pitch,
-                              int64_t band_rows, uint32_t* out, int64_t width,
-                              int32_t generations, void* stream) {
+                              int64_t band_rows, uint32_t* out, int64_t out_row0,
+                              int64_t out_rows, int64_t width, int32_t generations,
+                              void* stream) {
   if (generations < 1 || generations > LIFE_MAX_TEMPORAL_DEPTH)
     return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [1, %d], got %d",
                      LIFE_MAX_TEMPORAL_DEPTH, generations);
@@ -245,16 +246,19 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
     return set_error(LIFE_ERR_CONFIG, "bad peer step geometry");
   if (band_rows < generations || up_rows < generations || down_rows < generations)
     return set_error(LIFE_ERR_TOO_MANY_PARTS, "bands must be at least %d rows", generations);
+  if (out_row0 < 0 || out_rows < 0 || out_row0 + out_rows > band_rows)
+    return set_error(LIFE_ERR_CONFIG, "output rows outside the band");
+  if (out_rows == 0) return LIFE_OK;
   PackedStepArgs a{};
   a.in = in;
   a.in_pitch = pitch;
-  a.in_row0 = 0;
+  a.in_row0 = out_row0;  // band coordinates: relative row 0 = band row out_row0
   a.in_rows = band_rows;
   a.out = out;
   a.out_pitch = pitch;
-  a.out_row0 = 0;
+  a.out_row0 = out_row0;
   a.width = width;
-  a.out_rows = band_rows;
+  a.out_rows = out_rows;
   a.nw = static_cast<int32_t>(nw32(width));
   a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
   a.tail_mask = tail_mask(width);

@@ -42,3 +42,33 @@ def test_gpu_arm_line():
     assert j["cpu_baseline"]["value"] > 0
     b = run_bench("--engine", "byte", "--config", "1", "--steps", "3", "--warmup", "3")
     assert b["roofline"]["bound"] == "hbm" and b["value"] > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("halo", ["peer", "nccl"])
+def test_multirank_path_on_one_gpu(halo):
+    """bench.py's N>1 path (row bands, peer or NCCL halos, max-over-ranks
+    timing, e2e band copies) with 2 ranks sharing cuda:0 over gloo -- host
+    barriers only, so no kernel waits on another rank."""
+    import os
+    import socket
+    if halo == "nccl":
+        pytest.skip("NCCL refuses two ranks on one GPU; the send/recv driver is covered "
+                    "by tests/test_bands_gloo.py and test_gpu_bands.py")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, LIFE_BENCH_DEVICE="0", LIFE_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), "bench.py", "--gpus", "2", "--config", "1", "--steps", "3",
+                        "--warmup", "3", "--halo", halo], cwd=ROOT, capture_output=True,
+                       text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == 2 and j["value"] > 0 and j["config"]["parallelism"] == "rowbands2"
+    assert "peer" in j["config"]["halo"] or "NCCL" in j["config"]["halo"]
+    assert j["e2e"]["value"] > 0 and j["cpu_baseline"] is None
