@@ -269,21 +269,36 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   if (EDGE && a.peer) lrow = static_cast<int>(a.in_row0) + y - K;  // band row, resolved across bands
   auto issue = [&](int slot) {
     const uint32_t* row;
+    bool peer_row = false;
     if (EDGE && a.peer) {
       const int64_t r = lrow;
       if (r < 0) {
         row = a.up + (a.up_rows + r) * a.in_pitch;
+        peer_row = true;
       } else if (r < in_rows) {
         row = a.in + r * a.in_pitch;
       } else {
         const int64_t d = r - in_rows;  // rows past the light cone are over-reads: clamp
         row = a.down + (d < a.down_rows ? d : a.down_rows - 1) * a.in_pitch;
+        peer_row = true;
       }
     } else {
       row = a.in + static_cast<int64_t>(lrow) * a.in_pitch;
     }
     uint32_t* s = ring + slot * 96;
-    if (!EDGE) {
+    if (EDGE && peer_row) {
+      // A neighbour GPU's row over NVLink: plain loads (peer UVA addresses)
+      // staged into the ring; only the 2K ghost rows of edge tiles take this.
+      if (tiny) {
+        s[0] = load_word_wrapped(row, wi, a.width, a.nw);
+      } else if (plan.mode == 0) {
+        s[0] = row[plan.src];
+      } else {
+        s[0] = row[plan.p0];
+        s[32] = row[plan.p1];
+        s[64] = row[0];
+      }
+    } else if (!EDGE) {
       cp_async4(s, reinterpret_cast<const uint32_t*>(
                        in_lane + static_cast<uint64_t>(static_cast<uint32_t>(lrow)) * in_pitch_b));
     } else if (tiny) {
