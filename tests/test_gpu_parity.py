@@ -264,6 +264,20 @@ def test_run_batch_pipelined(engine, oracle):
         assert np.array_equal(oracle.unpack(out, W), want)
 
 
+@pytest.mark.parametrize("W,H,G,depth", [(1000, 2100, 37, 8), (333, 2051, 41, 16),
+                                         (2048, 600, 16, 16), (96, 4099, 0, 16), (640, 1030, 5, 3)])
+def test_run_batch_banded(engine, oracle, W, H, G, depth):
+    """life_run_batch on taller grids: several waves of row tiles per pass, W % 32 != 0,
+    G not a multiple of the depth, G = 0, more grids than buffer slots."""
+    grids = [oracle.random_fill(W, H, 0.35, 100 + i) for i in range(3)]
+    ins = [oracle.pack(g) for g in grids]
+    outs = [np.zeros_like(p) for p in ins]
+    engine.run_batch(ins, outs, W, G, depth)
+    for g, out in zip(grids, outs):
+        want, _ = oracle.run(g, G)
+        assert np.array_equal(oracle.unpack(out, W), want)
+
+
 def test_device_soup_matches_oracle(engine, oracle):
     for (w, h, cov, bs, p, seed) in [(200, 150, 0.02, 5, 0.5, 3), (409, 121, 0.02, 5, 0.5, 42),
                                      (97, 61, 0.3, 5, 0.5, 7), (64, 64, 0.5, 3, 0.7, 1),
