@@ -163,7 +163,11 @@ constexpr int kPackedThreads = 128;
 // regs)); one such block per SM.
 template <int K>
 struct PackedTraits {
+#ifdef LIFE_PF_HI
+  static constexpr int kPrefetch = K <= 3 ? 6 : LIFE_PF_HI;
+#else
   static constexpr int kPrefetch = K <= 3 ? 6 : 3;
+#endif
 #ifdef LIFE_WARPS16
   static constexpr int kWarps[17] = {0, 28, 24, 24, 20, 16, 16, 16, 16, 12, 12, 12, 12, 12, LIFE_WARPS16, LIFE_WARPS16, LIFE_WARPS16};
 #else
@@ -178,6 +182,10 @@ struct PackedTraits {
 #define LIFE_GROUP 4
 #endif
 constexpr int kGroup = LIFE_GROUP;  // stages issued level by level together
+#ifndef LIFE_SYNC_EVERY
+#define LIFE_SYNC_EVERY 1
+#endif
+constexpr int kSyncEvery = LIFE_SYNC_EVERY;  // loop trips per block barrier
 
 // How a lane fetches its 32-cell word of a row.  The column is the same for
 // every row, so the plan is computed once per strip:
@@ -246,31 +254,62 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // One pipeline segment of a warp: strip `strip`, output rows [y, y+n).
 // Runs ceil((n + kLag) / PF) loop trips (one block barrier each) and returns
-// that count.  EDGE warps (W % 32 != 0 and a lane touches the seam, or
-// W < 32) fetch 3 words per lane per row and combine them; all other warps
-// run the branch-free single-load path.
-template <int K, bool EDGE>
+// that count.  Three fetch paths, chosen per warp (warp-uniform):
+//   kPathFast:  every lane's word is one aligned word of the row (W % 32 == 0
+//               or the strip does not touch the seam): one cp.async per row;
+//   kPathSeam:  W % 32 != 0 and some lane's word straddles the seam: every
+//               lane fetches three words and funnel-combines them (lanes whose
+//               word is aligned use a plan that reduces to their own word), so
+//               the loop stays branch-free;
+//   kPathGeneral: W < 32 (the row wraps several times inside one word) or a
+//               peer-mode tile whose rows reach into a neighbour band.
+constexpr int kPathFast = 0, kPathSeam = 1, kPathGeneral = 2;
+
+template <int K, int PATH>
 __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int lane,
                                               const int strip, const int y, const int n,
                                               uint32_t* ring) {
   constexpr int PF = PackedTraits<K>::kPrefetch;
   constexpr int kLag = PackedTraits<K>::kLag;
-  const bool tiny = a.width < 32;  // warp-uniform (EDGE only)
+  constexpr bool EDGE = PATH == kPathGeneral;
+  const bool tiny = a.width < 32;  // warp-uniform (general path only)
   const int in_rows = static_cast<int>(a.in_rows);
   const int64_t wi = static_cast<int64_t>(strip) * kStripStride + lane - 1;
-  const WordPlan plan = make_plan(wi, a.width, a.nw);
+  WordPlan plan = make_plan(wi, a.width, a.nw);
+  if (PATH == kPathSeam && plan.mode == 0) {  // aligned word through the 3-word formula
+    plan.p0 = plan.p1 = plan.src;
+    plan.sh = 0u;
+    plan.m1 = kFull;
+    plan.m2 = 0u;
+    plan.s2 = 0u;
+  }
 
   // Input rows y-K, y-K+1, ... stream through a ring of 2*PF slots; step i
   // lives in slot i mod 2PF and is fetched PF steps ahead.  Row addresses
   // are one IMAD.WIDE (FMA pipe) from a 32-bit row index and byte pitch.
   int lrow = static_cast<int>(wrap_row(a.in_row0, static_cast<int64_t>(y) - K, a.in_rows));
   const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch * 4);
-  const char* const in_lane = reinterpret_cast<const char*>(a.in + plan.src);
+  const char* const in_lane = reinterpret_cast<const char*>(
+      a.in + (PATH == kPathSeam ? plan.p0 : plan.src));
+  const char* const in_lane1 = reinterpret_cast<const char*>(a.in + plan.p1);
+  const char* const in_row0w = reinterpret_cast<const char*>(a.in);
   if (EDGE && a.peer) lrow = static_cast<int>(a.in_row0) + y - K;  // band row, resolved across bands
   auto issue = [&](int slot) {
+    uint32_t* s = ring + slot * 96;
+    if (!EDGE) {
+      const uint64_t off = static_cast<uint64_t>(static_cast<uint32_t>(lrow)) * in_pitch_b;
+      cp_async4(s, reinterpret_cast<const uint32_t*>(in_lane + off));
+      if (PATH == kPathSeam) {
+        cp_async4(s + 32, reinterpret_cast<const uint32_t*>(in_lane1 + off));
+        cp_async4(s + 64, reinterpret_cast<const uint32_t*>(in_row0w + off));
+      }
+      cp_async_commit();
+      lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
+      return;
+    }
     const uint32_t* row;
     bool peer_row = false;
-    if (EDGE && a.peer) {
+    if (a.peer) {
       const int64_t r = lrow;
       if (r < 0) {
         row = a.up + (a.up_rows + r) * a.in_pitch;
@@ -285,8 +324,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
     } else {
       row = a.in + static_cast<int64_t>(lrow) * a.in_pitch;
     }
-    uint32_t* s = ring + slot * 96;
-    if (EDGE && peer_row) {
+    if (peer_row) {
       // A neighbour GPU's row over NVLink: plain loads (peer UVA addresses)
       // staged into the ring; only the 2K ghost rows of edge tiles take this.
       if (tiny) {
@@ -298,9 +336,6 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
         s[32] = row[plan.p1];
         s[64] = row[0];
       }
-    } else if (!EDGE) {
-      cp_async4(s, reinterpret_cast<const uint32_t*>(
-                       in_lane + static_cast<uint64_t>(static_cast<uint32_t>(lrow)) * in_pitch_b));
     } else if (tiny) {
       s[0] = load_word_wrapped(row, wi, a.width, a.nw);
     } else if (plan.mode == 0) {
@@ -311,7 +346,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
       cp_async4(s + 64, row);
     }
     cp_async_commit();
-    if (EDGE && a.peer) {
+    if (a.peer) {
       ++lrow;
     } else {
       lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
@@ -319,7 +354,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   };
   auto consume = [&](int slot) -> uint32_t {
     const uint32_t* s = ring + slot * 96;
-    if (!EDGE || tiny || plan.mode == 0) return s[0];
+    if (PATH == kPathFast || (EDGE && (tiny || plan.mode == 0))) return s[0];
     return (__funnelshift_r(s[0], s[32], plan.sh) & plan.m1) | ((s[64] << plan.s2) & plan.m2);
   };
 
@@ -376,6 +411,13 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) {
           if (g0 + j < K) {
+#if defined(LIFE_FMA_J) && defined(LIFE_FMA_PRE)
+            if (j < LIFE_FMA_J) {
+              xl[j] = __shfl_up_sync(kFull, mad_hi(xin[g0 + j], a.two, 0u), 1);
+              xr[j] = __shfl_down_sync(kFull, mad_lo(xin[g0 + j], a.half, 0u), 1);
+              continue;
+            }
+#endif
             xl[j] = __shfl_up_sync(kFull, xin[g0 + j], 1);
             xr[j] = __shfl_down_sync(kFull, xin[g0 + j], 1);
           }
@@ -383,7 +425,19 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) {
           if (g0 + j < K) {
-#ifdef LIFE_FMA_SHIFT
+#if defined(LIFE_FMA_J) && defined(LIFE_FMA_PRE)
+            if (j < LIFE_FMA_J) {  // xl = left lane's x>>31, xr = right lane's x<<31
+              const uint32_t x = xin[g0 + j];
+              const uint32_t L = mad_lo(x, a.two, xl[j]);
+              const uint32_t R = mad_hi(x, a.half, xr[j]);
+              c[j] = HSum{L ^ x ^ R, maj3(L, x, R)};
+            } else {
+              c[j] = hsum(xl[j], xin[g0 + j], xr[j]);
+            }
+#elif defined(LIFE_FMA_J)
+            if (j < LIFE_FMA_J) c[j] = hsum_fma(xl[j], xin[g0 + j], xr[j], a.two, a.half);
+            else c[j] = hsum(xl[j], xin[g0 + j], xr[j]);
+#elif defined(LIFE_FMA_SHIFT)
             c[j] = hsum_fma(xl[j], xin[g0 + j], xr[j], a.two, a.half);
 #else
             c[j] = hsum(xl[j], xin[g0 + j], xr[j]);
@@ -419,7 +473,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
     }
     half ^= PF;
 #ifndef LIFE_NO_LOCKSTEP
-    __syncthreads();
+    if (t % kSyncEvery == kSyncEvery - 1) __syncthreads();
 #endif
   };
 
@@ -489,24 +543,33 @@ packed_tb_kernel(const PackedStepArgs a) {
   uint32_t* ring = ring_smem + (threadIdx.x >> 5) * (2 * PackedTraits<K>::kPrefetch * 96) + lane;
   int trips = 0;
   if (n > 0) {
-    // EDGE if this strip needs the 3-word seam fetch, or (peer mode) the
-    // tile's rows reach past the band into a neighbour GPU's band.
+    // General path for W < 32 and (peer mode) tiles whose rows reach past
+    // the band into a neighbour GPU's band; seam path if a lane's word
+    // straddles the torus seam (W % 32 != 0); otherwise the fast path.
     const int64_t wi = static_cast<int64_t>(strip) * kStripStride + lane - 1;
     constexpr int PF = PackedTraits<K>::kPrefetch;
     const int64_t yb = a.in_row0 + y0;  // band row of the tile's first output row
     const int64_t last_row = yb - K + (static_cast<int64_t>(a.steps) + 1) * PF;  // last row issued
     const bool near_band_edge = a.peer && (yb < K || last_row >= a.in_rows);
-    const bool edge = a.width < 32 || near_band_edge ||
-                      __any_sync(kFull, make_plan(wi, a.width, a.nw).mode != 0);
-    if (edge) {
-      trips = packed_segment<K, true>(a, lane, strip, static_cast<int>(y0), n, ring);
+#ifdef LIFE_FORCE_EDGE
+    const int path = kPathGeneral;
+#else
+    const int path = (a.width < 32 || near_band_edge) ? kPathGeneral
+                     : __any_sync(kFull, make_plan(wi, a.width, a.nw).mode != 0) ? kPathSeam
+                                                                                  : kPathFast;
+#endif
+    if (path == kPathFast) {
+      trips = packed_segment<K, kPathFast>(a, lane, strip, static_cast<int>(y0), n, ring);
+    } else if (path == kPathSeam) {
+      trips = packed_segment<K, kPathSeam>(a, lane, strip, static_cast<int>(y0), n, ring);
     } else {
-      trips = packed_segment<K, false>(a, lane, strip, static_cast<int>(y0), n, ring);
+      trips = packed_segment<K, kPathGeneral>(a, lane, strip, static_cast<int>(y0), n, ring);
     }
   }
 #ifndef LIFE_NO_LOCKSTEP
   // Shorter (last) segments and spare warps pad to the block's trip count.
-  for (; trips < a.steps; ++trips) __syncthreads();
+  for (; trips < a.steps; ++trips)
+    if (trips % kSyncEvery == kSyncEvery - 1) __syncthreads();
 #endif
 #ifdef LIFE_TRACE
   if (lane == 0) {

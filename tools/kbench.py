@@ -1,0 +1,25 @@
+"""Quick packed-engine timing over arbitrary shapes (kernel-variant sweeps under gpurun).
+usage: LIFE_GPU_LIB=... python tools/kbench.py WxH[,WxH...] GENS DEPTH  -> one JSON line per shape"""
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_1209_4408_b200 import capi, life  # noqa: E402
+
+shapes = [tuple(int(v) for v in s.split("x")) for s in sys.argv[1].split(",")]
+gens, depth = int(sys.argv[2]), int(sys.argv[3])
+eng = life.Engine(0)
+for (w, h) in shapes:
+    eng.init_random(w, h, 0.4, 42)
+    eng.run(depth, capi.ENGINE_PACKED, depth)
+    eng.sync()
+    best = 1e30
+    for _ in range(3):
+        t = time.perf_counter()
+        eng.run(gens, capi.ENGINE_PACKED, depth)
+        eng.sync()
+        best = min(best, time.perf_counter() - t)
+    print(json.dumps({"lib": os.path.basename(os.environ.get("LIFE_GPU_LIB", "default")), "w": w, "h": h,
+                      "depth": depth, "gcups": round(w * h * gens / best / 1e9, 1)}))
