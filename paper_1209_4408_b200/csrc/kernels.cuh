@@ -130,7 +130,8 @@ struct PackedStepArgs {
   int64_t width;      // cells
   int64_t out_rows;
   int64_t seg_rows;   // output rows per tile (strip x segment)
-  int32_t steps;      // loop trips (block barriers) every warp runs (lockstep)
+  int32_t steps;      // loop trips every warp runs (lockstep)
+  int32_t sync_every; // loop trips per block barrier
   int32_t nw;         // ceil(width / 32): words holding cells
   int32_t n_strips;   // ceil((nw + 1) / 31)
   uint32_t tail_mask; // valid bits of word nw-1
@@ -166,7 +167,7 @@ struct PackedTraits {
 #ifdef LIFE_PF_HI
   static constexpr int kPrefetch = K <= 3 ? 6 : LIFE_PF_HI;
 #else
-  static constexpr int kPrefetch = K <= 3 ? 6 : 3;
+  static constexpr int kPrefetch = K <= 3 ? 6 : 4;
 #endif
 #ifdef LIFE_WARPS16
   static constexpr int kWarps[17] = {0, 28, 24, 24, 20, 16, 16, 16, 16, 12, 12, 12, 12, 12, LIFE_WARPS16, LIFE_WARPS16, LIFE_WARPS16};
@@ -182,10 +183,6 @@ struct PackedTraits {
 #define LIFE_GROUP 4
 #endif
 constexpr int kGroup = LIFE_GROUP;  // stages issued level by level together
-#ifndef LIFE_SYNC_EVERY
-#define LIFE_SYNC_EVERY 1
-#endif
-constexpr int kSyncEvery = LIFE_SYNC_EVERY;  // loop trips per block barrier
 
 // How a lane fetches its 32-cell word of a row.  The column is the same for
 // every row, so the plan is computed once per strip:
@@ -235,6 +232,45 @@ __device__ __forceinline__ WordPlan make_plan(int64_t wi, int64_t width, int32_t
   return p;
 }
 
+// Seam path (W % 32 != 0, W >= 64): every lane builds its word from two
+// aligned words A = row[p0], B = row[p1] of the same row as
+//   ((A >> sh) & m1) | ((B << s2) & ~m1).
+// Only three words straddle the torus seam (Grid::wrap, grid.hpp:48-54),
+// with r = W % 32 and d = 32 - r:
+//   wi = nw-1 (r cells, then columns 0..d-1):   A = nw-1, B = 0, sh = 0, s2 = r
+//   wi = nw   (columns d..d+31):                A = 0,    B = 1, sh = d, s2 = r
+//   wi = -1   (columns W-32..W-1):              A = nw-2, B = nw-1, sh = r, s2 = d
+// Aligned words use A = B = wi, sh = s2 = 0, m1 = ~0.  Words right of nw
+// and left of -1 are never needed: after K <= 16 generations their garbage
+// has reached at most 16 bits into the neighbouring ghost word.
+__device__ __forceinline__ WordPlan make_seam_plan(int64_t wi, int64_t width, int32_t nw) {
+  WordPlan p{};
+  p.mode = 1;
+  p.m1 = kFull;
+  const uint32_t r = static_cast<uint32_t>(width & 31), d = 32u - r;
+  if (wi >= 0 && wi < nw - 1) {
+    p.p0 = p.p1 = static_cast<int32_t>(wi);
+  } else if (wi == nw - 1) {
+    p.p0 = nw - 1;
+    p.p1 = 0;
+    p.s2 = r;
+    p.m1 = (1u << r) - 1u;
+  } else if (wi == nw) {
+    p.p0 = 0;
+    p.p1 = 1;
+    p.sh = d;
+    p.s2 = r;
+    p.m1 = (1u << r) - 1u;
+  } else if (wi == -1) {
+    p.p0 = nw - 2;
+    p.p1 = nw - 1;
+    p.sh = r;
+    p.s2 = d;
+    p.m1 = (1u << d) - 1u;
+  }  // else: p0 = p1 = 0, don't-care word
+  return p;
+}
+
 // cp.async (LDGSTS) of one 32-bit word into this lane's ring slot.
 __device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -276,13 +312,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   const int in_rows = static_cast<int>(a.in_rows);
   const int64_t wi = static_cast<int64_t>(strip) * kStripStride + lane - 1;
   WordPlan plan = make_plan(wi, a.width, a.nw);
-  if (PATH == kPathSeam && plan.mode == 0) {  // aligned word through the 3-word formula
-    plan.p0 = plan.p1 = plan.src;
-    plan.sh = 0u;
-    plan.m1 = kFull;
-    plan.m2 = 0u;
-    plan.s2 = 0u;
-  }
+  if (PATH == kPathSeam) plan = make_seam_plan(wi, a.width, a.nw);
 
   // Input rows y-K, y-K+1, ... stream through a ring of 2*PF slots; step i
   // lives in slot i mod 2PF and is fetched PF steps ahead.  Row addresses
@@ -292,17 +322,13 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   const char* const in_lane = reinterpret_cast<const char*>(
       a.in + (PATH == kPathSeam ? plan.p0 : plan.src));
   const char* const in_lane1 = reinterpret_cast<const char*>(a.in + plan.p1);
-  const char* const in_row0w = reinterpret_cast<const char*>(a.in);
   if (EDGE && a.peer) lrow = static_cast<int>(a.in_row0) + y - K;  // band row, resolved across bands
   auto issue = [&](int slot) {
     uint32_t* s = ring + slot * 96;
     if (!EDGE) {
       const uint64_t off = static_cast<uint64_t>(static_cast<uint32_t>(lrow)) * in_pitch_b;
       cp_async4(s, reinterpret_cast<const uint32_t*>(in_lane + off));
-      if (PATH == kPathSeam) {
-        cp_async4(s + 32, reinterpret_cast<const uint32_t*>(in_lane1 + off));
-        cp_async4(s + 64, reinterpret_cast<const uint32_t*>(in_row0w + off));
-      }
+      if (PATH == kPathSeam) cp_async4(s + 32, reinterpret_cast<const uint32_t*>(in_lane1 + off));
       cp_async_commit();
       lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
       return;
@@ -355,6 +381,10 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   auto consume = [&](int slot) -> uint32_t {
     const uint32_t* s = ring + slot * 96;
     if (PATH == kPathFast || (EDGE && (tiny || plan.mode == 0))) return s[0];
+    if (PATH == kPathSeam) {  // (A >> sh) on the m1 bits, (B << s2) on the others: 3 ALU ops
+      const uint32_t lo = s[0] >> plan.sh, hi = s[32] << plan.s2;
+      return (lo & plan.m1) | (hi & ~plan.m1);
+    }
     return (__funnelshift_r(s[0], s[32], plan.sh) & plan.m1) | ((s[64] << plan.s2) & plan.m2);
   };
 
@@ -387,6 +417,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   // branch) while step < 3*g0 -- its window is overwritten by valid rows
   // before its first valid output at step 3g0+2.
   int half = 0;
+  int sync_left = a.sync_every;  // barrier after trips t with (t + 1) % sync_every == 0
   auto trip = [&](const int t, auto fill_tag) {
     constexpr bool FILL = decltype(fill_tag)::value;
 #pragma unroll
@@ -473,7 +504,10 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
     }
     half ^= PF;
 #ifndef LIFE_NO_LOCKSTEP
-    if (t % kSyncEvery == kSyncEvery - 1) __syncthreads();
+    if (--sync_left == 0) {
+      sync_left = a.sync_every;
+      __syncthreads();
+    }
 #endif
   };
 
@@ -553,8 +587,10 @@ packed_tb_kernel(const PackedStepArgs a) {
     const bool near_band_edge = a.peer && (yb < K || last_row >= a.in_rows);
 #ifdef LIFE_FORCE_EDGE
     const int path = kPathGeneral;
+#elif defined(LIFE_FORCE_SEAM)
+    const int path = a.width < 32 ? kPathGeneral : kPathSeam;
 #else
-    const int path = (a.width < 32 || near_band_edge) ? kPathGeneral
+    const int path = (a.width < 64 || near_band_edge) ? kPathGeneral
                      : __any_sync(kFull, make_plan(wi, a.width, a.nw).mode != 0) ? kPathSeam
                                                                                   : kPathFast;
 #endif
@@ -569,7 +605,7 @@ packed_tb_kernel(const PackedStepArgs a) {
 #ifndef LIFE_NO_LOCKSTEP
   // Shorter (last) segments and spare warps pad to the block's trip count.
   for (; trips < a.steps; ++trips)
-    if (trips % kSyncEvery == kSyncEvery - 1) __syncthreads();
+    if ((trips + 1) % a.sync_every == 0) __syncthreads();
 #endif
 #ifdef LIFE_TRACE
   if (lane == 0) {

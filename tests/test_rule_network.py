@@ -88,6 +88,27 @@ def load_word(row, wi, W):
     return np.uint32(v & 0xFFFFFFFF)
 
 
+def seam_word(row, wi, W, junk):
+    """make_seam_plan (kernels.cuh): ((A >> sh) & m1) | ((B << s2) & ~m1) from two
+    aligned words; words right of nw and left of -1 are don't-care (`junk`)."""
+    nw = len(row)
+    r = W % 32
+    d = 32 - r
+    if 0 <= wi < nw - 1:
+        return np.uint32(row[wi])
+    if wi == nw - 1:
+        p0, p1, sh, s2, m1 = nw - 1, 0, 0, r, (1 << r) - 1
+    elif wi == nw:
+        p0, p1, sh, s2, m1 = 0, 1, d, r, (1 << r) - 1
+    elif wi == -1:
+        p0, p1, sh, s2, m1 = nw - 2, nw - 1, r, d, (1 << d) - 1
+    else:
+        return np.uint32(junk)
+    lo = int(row[p0]) >> sh
+    hi = (int(row[p1]) << s2) & 0xFFFFFFFF
+    return np.uint32((lo & m1) | (hi & ~m1 & 0xFFFFFFFF))
+
+
 def run_segment(p, W, K, strip, y, n, out):
     """One pipeline segment of packed_pass: strip `strip`, output rows y..y+n-1."""
     H, nw = p.shape
@@ -95,14 +116,22 @@ def run_segment(p, W, K, strip, y, n, out):
     tail = W % 32
     tail_mask = np.uint32(0xFFFFFFFF if tail == 0 else (1 << tail) - 1)
     lag = 3 * K - 1
+    aligned = [(w >= 0 and (w + 1) * 32 <= W) for w in wi]
+    seam = W >= 64 and W % 32 != 0 and not all(aligned)   # kPathSeam (else fast / general)
+    rng = np.random.default_rng(strip * 7919 + y)
     sa = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
     sb = [(np.zeros(32, np.uint32), np.zeros(32, np.uint32)) for _ in range(K)]
     ss = [np.zeros(32, np.uint32) for _ in range(K)]
     xin = [np.zeros(32, np.uint32) for _ in range(K)]
     for i in range(n + lag):
         r = (y - K + i) % H
-        xin[0] = np.array([p[r, w] if (w >= 0 and (w + 1) * 32 <= W) else load_word(p[r], w, W)
-                           for w in wi], np.uint32)
+        if seam:
+            junk = rng.integers(0, 1 << 32, 32)
+            xin[0] = np.array([seam_word(p[r], int(w), W, junk[lane]) for lane, w in enumerate(wi)],
+                              np.uint32)
+        else:
+            xin[0] = np.array([p[r, w] if ok else load_word(p[r], w, W)
+                               for w, ok in zip(wi, aligned)], np.uint32)
         ys = []
         for g in range(K):  # skewed: stage g eats stage g-1's previous output
             x = xin[g]
@@ -145,7 +174,9 @@ def model_packed_pass(p, W, K, seg_rows):
 
 @pytest.mark.parametrize("W,H,K,seg", [(3, 3, 1, 1), (5, 7, 3, 4), (31, 9, 4, 5), (33, 17, 16, 6),
                                        (64, 12, 2, 12), (97, 23, 5, 7), (1000, 11, 16, 64),
-                                       (1921, 6, 8, 4), (992, 5, 16, 3), (961, 4, 2, 9)])
+                                       (1921, 6, 8, 4), (992, 5, 16, 3), (961, 4, 2, 9),
+                                       (65, 9, 16, 9), (95, 8, 16, 4), (127, 7, 9, 7),
+                                       (2017, 5, 16, 5)])
 def test_kernel_model_matches_oracle(oracle, W, H, K, seg):
     g = oracle.random_fill(W, H, 0.45, W * 31 + H)
     p = pack32(g)
