@@ -54,28 +54,8 @@ __device__ __forceinline__ HSum hsum(uint32_t xl, uint32_t x, uint32_t xr) {
   return HSum{L ^ x ^ R, maj3(L, x, R)};
 }
 
-// The same neighbour words built on the FMA pipe instead of the ALU pipe
-// (the ALU pipe carries all the LOP3s):  with two = 2 and half = 2^31 held in
-// registers (kernel arguments, so ptxas cannot strength-reduce them),
-//   L = x*2 + hi(xl*2)          = (x << 1) | (xl >> 31)
-//   R = hi(x*2^31) + lo(xr*2^31) = (x >> 1) | (xr << 31)
-// (the two addends never overlap, so + is |).
-__device__ __forceinline__ uint32_t mad_lo(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-__device__ __forceinline__ uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-__device__ __forceinline__ HSum hsum_fma(uint32_t xl, uint32_t x, uint32_t xr, uint32_t two,
-                                         uint32_t half) {
-  const uint32_t L = mad_lo(x, two, mad_hi(xl, two, 0u));
-  const uint32_t R = mad_hi(x, half, mad_lo(xr, half, 0u));
-  return HSum{L ^ x ^ R, maj3(L, x, R)};
-}
+// (Building L and R on the FMA pipe -- IMAD / IMAD.HI by 2 and 2^31 -- to
+// offload the ALU pipe was measured 2-19 % slower for 1-4 of every 4 stages.)
 
 __device__ __forceinline__ uint32_t rule(HSum a, HSum b, HSum c, uint32_t self) {
   const uint32_t t0 = a.h0 ^ b.h0 ^ c.h0;
@@ -135,8 +115,6 @@ struct PackedStepArgs {
   int32_t nw;         // ceil(width / 32): words holding cells
   int32_t n_strips;   // ceil((nw + 1) / 31)
   uint32_t tail_mask; // valid bits of word nw-1
-  uint32_t two;       // 2     (hsum_fma operands)
-  uint32_t half;      // 2^31
   void* trace;        // LIFE_TRACE builds: per-warp (smid, start, end)
   // Peer mode (multi-GPU row bands over NVLink): input relative row r < 0 is
   // row up_rows + r of `up` (the band above, a peer GPU's buffer), r >=
@@ -248,8 +226,11 @@ __device__ __forceinline__ WordPlan make_seam_plan(int64_t wi, int64_t width, in
   p.mode = 1;
   p.m1 = kFull;
   const uint32_t r = static_cast<uint32_t>(width & 31), d = 32u - r;
-  if (wi >= 0 && wi < nw - 1) {
+  if (wi >= 0 && (wi + 1) * 32 <= width) {
     p.p0 = p.p1 = static_cast<int32_t>(wi);
+  } else if (r == 0) {  // (LIFE_FORCE_SEAM builds) W % 32 == 0: index wrap
+    const int64_t w = wi % nw;
+    p.p0 = p.p1 = static_cast<int32_t>(w < 0 ? w + nw : w);
   } else if (wi == nw - 1) {
     p.p0 = nw - 1;
     p.p1 = 0;
@@ -442,13 +423,6 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) {
           if (g0 + j < K) {
-#if defined(LIFE_FMA_J) && defined(LIFE_FMA_PRE)
-            if (j < LIFE_FMA_J) {
-              xl[j] = __shfl_up_sync(kFull, mad_hi(xin[g0 + j], a.two, 0u), 1);
-              xr[j] = __shfl_down_sync(kFull, mad_lo(xin[g0 + j], a.half, 0u), 1);
-              continue;
-            }
-#endif
             xl[j] = __shfl_up_sync(kFull, xin[g0 + j], 1);
             xr[j] = __shfl_down_sync(kFull, xin[g0 + j], 1);
           }
@@ -456,23 +430,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
 #pragma unroll
         for (int j = 0; j < kGroup; ++j) {
           if (g0 + j < K) {
-#if defined(LIFE_FMA_J) && defined(LIFE_FMA_PRE)
-            if (j < LIFE_FMA_J) {  // xl = left lane's x>>31, xr = right lane's x<<31
-              const uint32_t x = xin[g0 + j];
-              const uint32_t L = mad_lo(x, a.two, xl[j]);
-              const uint32_t R = mad_hi(x, a.half, xr[j]);
-              c[j] = HSum{L ^ x ^ R, maj3(L, x, R)};
-            } else {
-              c[j] = hsum(xl[j], xin[g0 + j], xr[j]);
-            }
-#elif defined(LIFE_FMA_J)
-            if (j < LIFE_FMA_J) c[j] = hsum_fma(xl[j], xin[g0 + j], xr[j], a.two, a.half);
-            else c[j] = hsum(xl[j], xin[g0 + j], xr[j]);
-#elif defined(LIFE_FMA_SHIFT)
-            c[j] = hsum_fma(xl[j], xin[g0 + j], xr[j], a.two, a.half);
-#else
             c[j] = hsum(xl[j], xin[g0 + j], xr[j]);
-#endif
           }
         }
 #pragma unroll
@@ -585,10 +543,8 @@ packed_tb_kernel(const PackedStepArgs a) {
     const int64_t yb = a.in_row0 + y0;  // band row of the tile's first output row
     const int64_t last_row = yb - K + (static_cast<int64_t>(a.steps) + 1) * PF;  // last row issued
     const bool near_band_edge = a.peer && (yb < K || last_row >= a.in_rows);
-#ifdef LIFE_FORCE_EDGE
-    const int path = kPathGeneral;
-#elif defined(LIFE_FORCE_SEAM)
-    const int path = a.width < 32 ? kPathGeneral : kPathSeam;
+#if defined(LIFE_FORCE_SEAM)  // test/measurement builds: every warp on the seam path
+    const int path = (a.width < 64 || near_band_edge) ? kPathGeneral : kPathSeam;
 #else
     const int path = (a.width < 64 || near_band_edge) ? kPathGeneral
                      : __any_sync(kFull, make_plan(wi, a.width, a.nw).mode != 0) ? kPathSeam

@@ -238,8 +238,6 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
   a.nw = static_cast<int32_t>(nw32(width));
   a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
   a.tail_mask = tail_mask(width);
-  a.two = 2u;
-  a.half = 0x80000000u;
   a.trace = g_trace;
   return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
 }
@@ -272,8 +270,6 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
   a.nw = static_cast<int32_t>(nw32(width));
   a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
   a.tail_mask = tail_mask(width);
-  a.two = 2u;
-  a.half = 0x80000000u;
   a.trace = g_trace;
   a.up = up;
   a.down = down;
