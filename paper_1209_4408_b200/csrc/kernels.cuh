@@ -252,6 +252,14 @@ __device__ __forceinline__ WordPlan make_seam_plan(int64_t wi, int64_t width, in
   return p;
 }
 
+// base + idx * stride as one IMAD.WIDE (FMA pipe) with the 64-bit base as
+// addend, so no IADD3 pair lands on the ALU pipe that the rule network fills.
+__device__ __forceinline__ const char* row_addr(const char* base, uint32_t idx, uint32_t stride) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(idx), "r"(stride), "l"(base));
+  return reinterpret_cast<const char*>(r);
+}
+
 // cp.async (LDGSTS) of one 32-bit word into this lane's ring slot.
 __device__ __forceinline__ void cp_async4(uint32_t* smem_dst, const uint32_t* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
@@ -307,9 +315,11 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   auto issue = [&](int slot) {
     uint32_t* s = ring + slot * 96;
     if (!EDGE) {
-      const uint64_t off = static_cast<uint64_t>(static_cast<uint32_t>(lrow)) * in_pitch_b;
-      cp_async4(s, reinterpret_cast<const uint32_t*>(in_lane + off));
-      if (PATH == kPathSeam) cp_async4(s + 32, reinterpret_cast<const uint32_t*>(in_lane1 + off));
+      cp_async4(s, reinterpret_cast<const uint32_t*>(
+                       row_addr(in_lane, static_cast<uint32_t>(lrow), in_pitch_b)));
+      if (PATH == kPathSeam)
+        cp_async4(s + 32, reinterpret_cast<const uint32_t*>(
+                              row_addr(in_lane1, static_cast<uint32_t>(lrow), in_pitch_b)));
       cp_async_commit();
       lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
       return;
@@ -399,8 +409,13 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   // before its first valid output at step 3g0+2.
   int half = 0;
   int sync_left = a.sync_every;  // barrier after trips t with (t + 1) % sync_every == 0
-  auto trip = [&](const int t, auto fill_tag) {
-    constexpr bool FILL = decltype(fill_tag)::value;
+  // Trip kinds: kFill (no output yet; lower stage groups skipped), kCheck
+  // (per-step test whether the output row is inside the segment), kSteady
+  // (every step stores: no per-step test, no branch).
+  constexpr int kFill = 0, kCheck = 1, kSteady = 2;
+  auto trip = [&](const int t, auto kind_tag) {
+    constexpr int KIND = decltype(kind_tag)::value;
+    constexpr bool FILL = KIND == kFill;
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
       issue((half ^ PF) + u);
@@ -452,9 +467,10 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
       // Output row j of the segment leaves the pipeline at step j + kLag.
       const int j = step - kLag;
       if (!FILL) {  // no output leaves the pipeline during the fill trips
-        if (static_cast<unsigned>(j) < static_cast<unsigned>(n)) {
-          char* p = out_seg + static_cast<uint64_t>(static_cast<uint32_t>(j)) * out_pitch_b;
-          const uint32_t v = y_last & st_mask;
+        if (KIND == kSteady || static_cast<unsigned>(j) < static_cast<unsigned>(n)) {
+          char* p = const_cast<char*>(row_addr(out_seg, static_cast<uint32_t>(j), out_pitch_b));
+          // Only the seam strip holds word nw-1 (the tail): fast-path strips skip the mask.
+          const uint32_t v = PATH == kPathFast ? y_last : y_last & st_mask;
           if (st_lo) *reinterpret_cast<uint16_t*>(p) = static_cast<uint16_t>(v);
           if (st_hi) *reinterpret_cast<uint16_t*>(p + 2) = static_cast<uint16_t>(v >> 16);
         }
@@ -475,9 +491,15 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   constexpr int kFillTrips = (3 * kTopG0 + PF - 1) / PF;
   static_assert(PF * kFillTrips <= kLag, "fill trips must end before the first output");
   const int fill_trips = trips < kFillTrips ? trips : kFillTrips;
+  // Steady trips: every step's output row j = t*PF + u - kLag is in [0, n).
+  const int steady_begin = (kLag + PF - 1) / PF;
+  const int steady_end = (n + kLag) / PF;
   int t = 0;
-  for (; t < fill_trips; ++t) trip(t, std::true_type{});
-  for (; t < trips; ++t) trip(t, std::false_type{});
+  for (; t < fill_trips; ++t) trip(t, std::integral_constant<int, kFill>{});
+  for (; t < trips && (t < steady_begin || t >= steady_end); ++t)
+    trip(t, std::integral_constant<int, kCheck>{});
+  for (; t < steady_end; ++t) trip(t, std::integral_constant<int, kSteady>{});
+  for (; t < trips; ++t) trip(t, std::integral_constant<int, kCheck>{});
   cp_async_wait<0>();
   return trips;
 }
