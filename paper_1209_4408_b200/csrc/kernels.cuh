@@ -728,34 +728,37 @@ __device__ __forceinline__ void byte_pass(const ByteStepArgs& a, const int lane,
   for (int u = 0; u < PF; ++u) issue(u);
   ByteRow up{}, mid{};
   // Step t consumes input row y0-1+t; output row t-2 leaves at step t >= 2.
+  // Steady trips (every step's output row inside the segment) store without
+  // a per-step bounds branch, so each trip is one basic block.
   const int trips = (rows + 2 + PF - 1) / PF;
   int half = 0;
-  for (int tr = 0; tr < trips; ++tr) {
+  auto trip = [&](const int tr, auto steady_tag) {
+    constexpr bool STEADY = decltype(steady_tag)::value;
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
       issue((half ^ PF) + u);
       cp_async_wait<PF>();
       const ByteRow dn = consume(half + u);
       const int j = tr * PF + u - 2;
-      if (store && static_cast<unsigned>(j) < static_cast<unsigned>(rows)) {
-        uint32_t o[4];
+      uint32_t o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t n = up.h[i] + dn.h[i] + mid.hn[i];  // 8-neighbour count per byte
+        // (n | self) == 3  <=>  next alive (engine.cpp:32 on 0/1 bytes);
+        // t = (n|self)^3 is 0..15 per byte; zero-test via the byte's bit 7.
+        const uint32_t t = (n | mid.x[i]) ^ 0x03030303u;
+        o[i] = (~(t + 0x7f7f7f7fu) & 0x80808080u) >> 7;
+      }
+      if (EDGE && seam_pos >= 0) {  // zero the padding bytes past column W-1
+        const int keep = seam_pos + 1;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const uint32_t n = up.h[i] + dn.h[i] + mid.hn[i];  // 8-neighbour count per byte
-          // (n | self) == 3  <=>  next alive (engine.cpp:32 on 0/1 bytes);
-          // t = (n|self)^3 is 0..15 per byte; zero-test via the byte's bit 7.
-          const uint32_t t = (n | mid.x[i]) ^ 0x03030303u;
-          o[i] = (~(t + 0x7f7f7f7fu) & 0x80808080u) >> 7;
+          const int lo = i * 4;
+          if (keep <= lo) o[i] = 0;
+          else if (keep < lo + 4) o[i] &= (1u << ((keep - lo) * 8)) - 1u;
         }
-        if (EDGE && seam_pos >= 0) {  // zero the padding bytes past column W-1
-          const int keep = seam_pos + 1;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int lo = i * 4;
-            if (keep <= lo) o[i] = 0;
-            else if (keep < lo + 4) o[i] &= (1u << ((keep - lo) * 8)) - 1u;
-          }
-        }
+      }
+      if (store && (STEADY || static_cast<unsigned>(j) < static_cast<unsigned>(rows))) {
         *reinterpret_cast<uint4*>(out_lane + static_cast<uint64_t>(static_cast<uint32_t>(j)) *
                                                  out_pitch_b) = make_uint4(o[0], o[1], o[2], o[3]);
       }
@@ -763,7 +766,13 @@ __device__ __forceinline__ void byte_pass(const ByteStepArgs& a, const int lane,
       mid = dn;
     }
     half ^= PF;
-  }
+  };
+  const int steady_begin = (2 + PF - 1) / PF;  // first trip with j >= 0 at u = 0
+  const int steady_end = (rows + 2) / PF;      // trips below this have j < rows throughout
+  int tr = 0;
+  for (; tr < trips && (tr < steady_begin || tr >= steady_end); ++tr) trip(tr, std::false_type{});
+  for (; tr < steady_end; ++tr) trip(tr, std::true_type{});
+  for (; tr < trips; ++tr) trip(tr, std::false_type{});
   cp_async_wait<0>();
 }
 
