@@ -561,6 +561,37 @@ def run_byte_arm(args) -> None:
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     achieved = 2.0 * W * H / (kern_ms * 1e-3) / 1e9
     value = W * H * gens * args.steps / (sum(ms) * 1e-3) / 1e9
+    e2e = None
+    if not args.no_e2e:
+        # The public API a user calls: Engine.upload (uint8 grid from pinned host
+        # memory) -> life_run(engine=BYTE) -> Engine.download, all synchronous C-ABI
+        # calls, host-timed per step (the context's own stream; no torch events).
+        from paper_1209_4408_b200 import life
+        host = torch.empty((H, W), dtype=torch.uint8, pin_memory=True).numpy()
+        host[:] = bufs[cur[0]][:, :W].cpu().numpy()
+        hout = torch.empty((H, W), dtype=torch.uint8, pin_memory=True).numpy()
+        steps_e2e = max(2, args.steps)
+        with life.Engine(0) as eng:
+            eng.upload(host)
+            eng.run(1, capi.ENGINE_BYTE)
+            eng.download(hout)
+            t0 = time.perf_counter()
+            for _ in range(steps_e2e):
+                eng.upload(host)
+                eng.run(gens, capi.ENGINE_BYTE)
+                eng.download(hout)
+            e2e_s = time.perf_counter() - t0
+        e2e = {"value": W * H * gens * steps_e2e / e2e_s / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": W * H, "d2h_bytes_per_step": W * H,
+               "api": "C-ABI life_grid_upload_u8 + life_run(LIFE_ENGINE_BYTE) + "
+                      "life_grid_download_u8 from/to pinned host memory (host-timed)",
+               "steps": steps_e2e}
+    cpu = None
+    if not args.no_cpu:
+        try:
+            cpu = cpu_measure(cfg, args.cpu_budget)
+        except Exception as exc:  # reported, not fatal
+            cpu = {"error": repr(exc)}
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sum(ms) / args.steps, "higher_is_better": True,
@@ -572,6 +603,7 @@ def run_byte_arm(args) -> None:
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
                      "bytes_per_cell_update": 2.0, "mean_launch_ms": kern_ms,
                      "traffic": ncu_traffic(args.config, 0)},
+        "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": n_launch, "clocks": clocks.summary()}), flush=True)
 
 

@@ -626,8 +626,11 @@ struct ByteStepArgs {
 };
 
 constexpr int kByteThreads = 128;
-constexpr int kBytePF = 6;                         // rows fetched ahead (multiple of 3)
-constexpr int kByteSlotWords = 32 * 4 + 2 * 32;    // 16-B vector + 2 seam words per lane
+#ifndef LIFE_BYTE_PF
+#define LIFE_BYTE_PF 6
+#endif
+constexpr int kBytePF = LIFE_BYTE_PF;              // rows fetched ahead
+constexpr int kByteSlotWords = 32 * 4 + 4;         // 16-B vector per lane + the 2 seam words
 constexpr int kByteSmem = (kByteThreads / 32) * 2 * kBytePF * kByteSlotWords * 4;  // per block
 constexpr int kByteStride = 30;                    // vectors stored per warp (lanes 1..30)
 
@@ -668,6 +671,14 @@ __device__ __forceinline__ ByteRow byte_row(const uint4 v, uint32_t left_byte,
   return row;
 }
 
+__device__ __forceinline__ void st_global_v4_if(void* p, const uint32_t (&o)[4], bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n"
+      " @q st.global.v4.u32 [%0], {%1, %2, %3, %4};\n}\n" ::"l"(p),
+      "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(uint32_t* smem_dst, const void* gmem_src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gmem_src) : "memory");
@@ -703,8 +714,9 @@ __device__ __forceinline__ void byte_pass(const ByteStepArgs& a, const int lane,
     const uint64_t off = static_cast<uint64_t>(static_cast<uint32_t>(lrow)) * in_pitch_b;
     cp_async16(s + lane * 4, in_lane + off);
     if (EDGE) {
-      if (need_left) cp_async4(s + 128 + lane, reinterpret_cast<const uint32_t*>(a.in + off + left_word));
-      if (seam_pos >= 0) cp_async4(s + 160 + lane, reinterpret_cast<const uint32_t*>(a.in + off));
+      // At most one lane of a warp needs each seam word.
+      if (need_left) cp_async4(s + 128, reinterpret_cast<const uint32_t*>(a.in + off + left_word));
+      if (seam_pos >= 0) cp_async4(s + 129, reinterpret_cast<const uint32_t*>(a.in + off));
     }
     cp_async_commit();
     lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
@@ -716,8 +728,8 @@ __device__ __forceinline__ void byte_pass(const ByteStepArgs& a, const int lane,
     const uint32_t rb = __shfl_down_sync(kFull, v.x & 0xffu, 1);
     uint32_t col0 = 0;
     if (EDGE) {
-      if (need_left) lb = (s[128 + lane] >> left_shift) & 0xffu;
-      if (seam_pos >= 0) col0 = s[160 + lane] & 0xffu;
+      if (need_left) lb = (s[128] >> left_shift) & 0xffu;
+      if (seam_pos >= 0) col0 = s[129] & 0xffu;
     }
     return byte_row(v, lb, rb, seam_pos, col0);
   };
@@ -758,10 +770,11 @@ __device__ __forceinline__ void byte_pass(const ByteStepArgs& a, const int lane,
           else if (keep < lo + 4) o[i] &= (1u << ((keep - lo) * 8)) - 1u;
         }
       }
-      if (store && (STEADY || static_cast<unsigned>(j) < static_cast<unsigned>(rows))) {
-        *reinterpret_cast<uint4*>(out_lane + static_cast<uint64_t>(static_cast<uint32_t>(j)) *
-                                                 out_pitch_b) = make_uint4(o[0], o[1], o[2], o[3]);
-      }
+      // Predicated store (no branch: a divergent branch here would make every
+      // following shuffle re-check convergence and split the trip into blocks).
+      const bool st = store && (STEADY || static_cast<unsigned>(j) < static_cast<unsigned>(rows));
+      st_global_v4_if(out_lane + static_cast<uint64_t>(static_cast<uint32_t>(j)) * out_pitch_b,
+                      o, st);
       up = mid;
       mid = dn;
     }
