@@ -819,6 +819,117 @@ __global__ void __launch_bounds__(kByteThreads) byte_step_kernel(const ByteStepA
 }
 
 // ---------------------------------------------------------------------------
+// Packed single-generation step (K = 1, W % 128 == 0): the HBM-bound end of
+// the temporal-depth range.  Each lane owns one 16-byte vector (4 words =
+// 128 cells) of a row and walks a segment of rows with the 3-row window of
+// (h0, h1, self) in registers; rows arrive through a cp.async ring kStep1PF
+// rows ahead.  Lanes 0 and 31 are ghosts (loaded, not stored): after one
+// generation only the strip's outermost bit is wrong.  Memory per
+// cell-update: 1 bit read + 1 bit written (plus 2 halo rows per segment and
+// the ghost vectors, both L2 hits).  Same rule network as packed_tb_kernel;
+// replaces compute_region (engine.cpp:17-48) for one generation.
+// ---------------------------------------------------------------------------
+struct Step1Args {
+  const uint32_t* in;
+  int64_t in_pitch;  // words (multiple of 4)
+  int64_t in_row0;
+  int64_t in_rows;
+  uint32_t* out;
+  int64_t out_pitch;
+  int64_t out_row0;
+  int64_t out_rows;
+  int64_t seg_rows;
+  int32_t nv;        // vectors per row = W / 128
+  int32_t n_strips;  // ceil(nv / 30)
+};
+
+constexpr int kStep1Threads = 128;
+constexpr int kStep1PF = 8;
+constexpr int kStep1Stride = 30;  // vectors stored per warp (lanes 1..30)
+constexpr int kStep1Smem = (kStep1Threads / 32) * 2 * kStep1PF * 32 * 16;  // per block
+
+struct Row4 {
+  HSum h[4];
+  uint32_t x[4];
+};
+
+__device__ __forceinline__ Row4 step1_row(const uint4 v) {
+  const uint32_t x[4] = {v.x, v.y, v.z, v.w};
+  const uint32_t left = __shfl_up_sync(kFull, x[3], 1);    // lane 0: own (ghost)
+  const uint32_t right = __shfl_down_sync(kFull, x[0], 1); // lane 31: own (ghost)
+  Row4 r;
+  r.h[0] = hsum(left, x[0], x[1]);
+  r.h[1] = hsum(x[0], x[1], x[2]);
+  r.h[2] = hsum(x[1], x[2], x[3]);
+  r.h[3] = hsum(x[2], x[3], right);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) r.x[i] = x[i];
+  return r;
+}
+
+__global__ void __launch_bounds__(kStep1Threads) packed_step1_kernel(const Step1Args a) {
+  constexpr int PF = kStep1PF;
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kStep1Threads + threadIdx.x) >> 5;
+  const int strip = static_cast<int>(gwarp % a.n_strips);
+  const int64_t seg = gwarp / a.n_strips;
+  const int64_t y0 = seg * a.seg_rows;
+  if (y0 >= a.out_rows) return;  // warp-uniform
+  const int rows = static_cast<int>(min(a.seg_rows, a.out_rows - y0));
+  const int64_t vi = static_cast<int64_t>(strip) * kStep1Stride + lane - 1;
+  int64_t src = vi % a.nv;  // W % 128 == 0: the torus wrap is an index remap
+  if (src < 0) src += a.nv;
+  const bool store = lane >= 1 && lane <= kStep1Stride && vi < a.nv;
+  extern __shared__ uint4 step1_ring[];
+  uint4* ring = step1_ring + (threadIdx.x >> 5) * (2 * PF * 32) + lane;
+
+  const int in_rows = static_cast<int>(a.in_rows);
+  int lrow = static_cast<int>(wrap_row(a.in_row0, y0 - 1, a.in_rows));
+  const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch * 4);
+  const char* const in_lane = reinterpret_cast<const char*>(a.in + src * 4);
+  auto issue = [&](int slot) {
+    cp_async16(reinterpret_cast<uint32_t*>(ring + slot * 32),
+               row_addr(in_lane, static_cast<uint32_t>(lrow), in_pitch_b));
+    cp_async_commit();
+    lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
+  };
+  const uint32_t out_pitch_b = static_cast<uint32_t>(a.out_pitch * 4);
+  char* const out_lane = reinterpret_cast<char*>(a.out + (a.out_row0 + y0) * a.out_pitch + vi * 4);
+
+#pragma unroll
+  for (int u = 0; u < PF; ++u) issue(u);
+  Row4 up{}, mid{};
+  const int trips = (rows + 2 + PF - 1) / PF;
+  int half = 0;
+  auto trip = [&](const int tr, auto steady_tag) {
+    constexpr bool STEADY = decltype(steady_tag)::value;
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      issue((half ^ PF) + u);
+      cp_async_wait<PF>();
+      const Row4 dn = step1_row(ring[(half + u) * 32]);
+      const int j = tr * PF + u - 2;  // output row j leaves at step j + 2
+      uint32_t o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = rule(up.h[i], mid.h[i], dn.h[i], mid.x[i]);
+      const bool st = store && (STEADY || static_cast<unsigned>(j) < static_cast<unsigned>(rows));
+      st_global_v4_if(const_cast<char*>(row_addr(out_lane, static_cast<uint32_t>(j), out_pitch_b)),
+                      o, st);
+      up = mid;
+      mid = dn;
+    }
+    half ^= PF;
+  };
+  const int steady_begin = (2 + PF - 1) / PF;
+  const int steady_end = (rows + 2) / PF;
+  int tr = 0;
+  for (; tr < trips && (tr < steady_begin || tr >= steady_end); ++tr) trip(tr, std::false_type{});
+  for (; tr < steady_end; ++tr) trip(tr, std::true_type{});
+  for (; tr < trips; ++tr) trip(tr, std::false_type{});
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
 // Layout conversion, seeded soup, population, windows.
 // ---------------------------------------------------------------------------
 

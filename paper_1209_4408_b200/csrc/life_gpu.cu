@@ -215,6 +215,48 @@ int life_band_bounds(int64_t extent, int32_t parts, int64_t* bounds) {
   return LIFE_OK;
 }
 
+namespace {
+// One generation over a W % 128 == 0 torus: packed_step1_kernel (16-byte
+// vectors, HBM-bound).  Segments of >= 32 rows in ~8 waves of independent
+// warps, as for the byte engine.
+int launch_step1(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                 uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                 int64_t out_rows, cudaStream_t stream) {
+  static int blocks_per_sm[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (blocks_per_sm[dev & 63] == 0) {
+    int nb = 0;
+    LIFE_CUDA(cudaFuncSetAttribute(packed_step1_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kStep1Smem));
+    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, packed_step1_kernel,
+                                                            kStep1Threads, kStep1Smem));
+    blocks_per_sm[dev & 63] = std::max(nb, 1);
+  }
+  Step1Args a{};
+  a.in = in;
+  a.in_pitch = in_pitch;
+  a.in_row0 = in_row0;
+  a.in_rows = in_rows;
+  a.out = out;
+  a.out_pitch = out_pitch;
+  a.out_row0 = out_row0;
+  a.out_rows = out_rows;
+  a.nv = static_cast<int32_t>(width / 128);
+  a.n_strips = static_cast<int32_t>(ceil_div(a.nv, kStep1Stride));
+  const int64_t resident_warps =
+      static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kStep1Threads / 32) * sm_count();
+  const int64_t segs_target = std::max<int64_t>(1, 8 * resident_warps / a.n_strips);
+  a.seg_rows = std::max<int64_t>(ceil_div(out_rows, segs_target), 32);
+  const int64_t warps = ceil_div(out_rows, a.seg_rows) * a.n_strips;
+  const int64_t blocks = ceil_div(warps, kStep1Threads / 32);
+  if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
+  packed_step1_kernel<<<static_cast<unsigned>(blocks), kStep1Threads, kStep1Smem, stream>>>(a);
+  LIFE_CHECK_LAUNCH("packed_step1_kernel");
+  return LIFE_OK;
+}
+}  // namespace
+
 int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
                          uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
                          int64_t out_rows, int32_t generations, void* stream) {
@@ -225,6 +267,12 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
       out_pitch < 2 * ceil_div(width, 64))
     return set_error(LIFE_ERR_CONFIG, "bad packed step geometry");
   if (out_rows == 0) return LIFE_OK;
+  if (generations == 1 && width % 128 == 0 && in_pitch % 4 == 0 && out_pitch % 4 == 0 &&
+      reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+      in_rows < (int64_t(1) << 31) && in_pitch * 4 < (int64_t(1) << 32) &&
+      out_pitch * 4 < (int64_t(1) << 32) && !g_trace)
+    return launch_step1(in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
+                        out_rows, static_cast<cudaStream_t>(stream));
   PackedStepArgs a{};
   a.in = in;
   a.in_pitch = in_pitch;

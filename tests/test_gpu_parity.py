@@ -139,6 +139,20 @@ def test_depth_transparency_sweep(engine, oracle):
         assert np.array_equal(engine.download(), want)
 
 
+@pytest.mark.parametrize("w,h", [(128, 3), (128, 5), (256, 31), (1024, 97), (3968, 40),
+                                 (4096, 300), (640, 1000)])
+def test_single_generation_vector_path(engine, oracle, w, h):
+    """Depth 1 with W % 128 == 0 takes packed_step1_kernel (16-byte vectors, ghost
+    lanes, index-remap torus wrap): every generation bit-exact, incl. 3-row tori
+    and more strips than one warp covers."""
+    g = oracle.random_fill(w, h, 0.35, w + h)
+    for gens in (1, 2, 7, 33):
+        want, _ = oracle.run(g, gens)
+        engine.upload(g)
+        engine.run(gens, PACKED, 1)
+        assert np.array_equal(engine.download(), want), (w, h, gens)
+
+
 def test_checkpoints_split_passes(engine, oracle):
     g = oracle.random_fill(200, 150, 0.4, 9)
     cps = [0, 1, 3, 17, 18, 40, 64]
