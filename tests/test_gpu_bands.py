@@ -23,6 +23,8 @@ def words_to_cells(words: np.ndarray, width: int) -> np.ndarray:
     (4096, 1025, 8, 16, 100, True),
     (40961, 12289 // 16, 8, 7, 30, True),
     (333, 64, 4, 16, 33, True),
+    (1024, 300, 3, 1, 9, True),       # depth 1, W % 128 == 0: the vector kernel per band
+    (1024, 300, 3, 1, 9, False),
 ])
 def test_local_bands_match_oracle(oracle, W, H, P, depth, gens, overlap):
     import torch
@@ -61,6 +63,7 @@ def test_cfg5_bands_equal_single_gpu_windows(oracle):
 @pytest.mark.parametrize("W,H,P,depth,gens", [
     (70, 37, 2, 4, 13), (1000, 97, 3, 16, 50), (4096, 1025, 8, 16, 100),
     (40961, 12289 // 16, 8, 7, 30), (333, 64, 4, 16, 33), (96, 40, 2, 16, 48),
+    (1024, 300, 3, 1, 9),
 ])
 def test_local_peer_bands_match_oracle(oracle, W, H, P, depth, gens):
     """The fused-halo kernel (ghost rows read from the neighbour bands'
