@@ -518,6 +518,7 @@ struct life_ctx {
   uint32_t* batch[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t batch_bytes = 0;
   cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaStream_t cs[4] = {};  // life_run_batch chunk streams (first / last grid)
 };
 
 namespace {
@@ -657,6 +658,8 @@ int life_ctx_destroy(life_ctx* c) {
   if (c->window) cudaFree(c->window);
   for (auto& b : c->batch)
     if (b) cudaFree(b);
+  for (auto& st : c->cs)
+    if (st) cudaStreamDestroy(st);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->own) cudaStreamDestroy(c->own);
@@ -964,6 +967,70 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
 
 int life_step(life_ctx* c, int engine) { return life_run(c, 1, engine, 1, nullptr, 0, nullptr); }
 
+namespace {
+// ---- life_run_batch: trapezoid / triangle schedule for the first and last grid
+//
+// With whole-grid passes, the first grid's upload and the last grid's
+// download (8 GiB each at config 5) are exposed.  The first and last grid of
+// a batch are instead cut into kTrapChunks row chunks.  Chunk c's TRAPEZOID
+// runs all P passes on its own rows only, pass p producing the rows
+// [start + kShrink*(p+1), end - kShrink*(p+1)) (each pass loses at most
+// kShrink = 16 >= K rows per side of valid data), so it starts as soon as
+// chunk c has arrived and its interior can leave as soon as it is done.  The
+// TRIANGLE at the boundary row B between chunks c-1 and c then runs the P
+// passes on [B - kShrink*(p+1), B + kShrink*(p+1)), reading the trapezoids'
+// outputs of the previous pass.  No launch overwrites rows another still
+// needs: trapezoid pass p+1 writes the buffer of pass p-1 only below
+// B - kShrink*(p+2), exactly where triangle pass p stops reading; triangles
+// run after both neighbouring trapezoids.  Middle grids keep whole-grid
+// passes (their copies overlap the neighbouring grids' compute anyway).
+constexpr int kTrapChunks = 16;
+constexpr int64_t kShrink = 16;
+
+struct BatchGeom {
+  int64_t width, height, wpr, words_per_row, pitch, generations;
+  int depth, passes;
+  int64_t bounds[kTrapChunks + 1];
+};
+
+// out rows [r0, r0 + rows) (mod H) of pass p: one launch per contiguous piece.
+int pass_rows(const BatchGeom& g, uint32_t* const* buf, int p, int64_t r0, int64_t rows,
+              cudaStream_t s) {
+  const int k = static_cast<int>(std::min<int64_t>(g.depth, g.generations - int64_t(p) * g.depth));
+  r0 %= g.height;
+  if (r0 < 0) r0 += g.height;
+  while (rows > 0) {
+    const int64_t piece = std::min(rows, g.height - r0);
+    LIFE_TRY(life_dev_packed_step(buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch, r0,
+                                  g.width, piece, k, s));
+    rows -= piece;
+    r0 = 0;
+  }
+  return LIFE_OK;
+}
+
+int copy_rows(const BatchGeom& g, void* host, const uint32_t* dev, int64_t r0, int64_t rows,
+              bool h2d, cudaStream_t s) {
+  r0 %= g.height;
+  if (r0 < 0) r0 += g.height;
+  while (rows > 0) {
+    const int64_t piece = std::min(rows, g.height - r0);
+    uint64_t* hrow = static_cast<uint64_t*>(host) + r0 * g.words_per_row;
+    uint32_t* drow = const_cast<uint32_t*>(dev) + r0 * g.pitch;
+    if (h2d) {
+      LIFE_CUDA(cudaMemcpy2DAsync(drow, g.pitch * 4, hrow, g.words_per_row * 8, g.wpr * 8, piece,
+                                  cudaMemcpyHostToDevice, s));
+    } else {
+      LIFE_CUDA(cudaMemcpy2DAsync(hrow, g.words_per_row * 8, drow, g.pitch * 4, g.wpr * 8, piece,
+                                  cudaMemcpyDeviceToHost, s));
+    }
+    rows -= piece;
+    r0 = 0;
+  }
+  return LIFE_OK;
+}
+}  // namespace
+
 int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* outputs, int32_t n,
                    int64_t width, int64_t height, int64_t words_per_row, int64_t generations,
                    int temporal_depth, float* elapsed_ms) {
@@ -998,59 +1065,135 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   }
   if (!c->h2d) LIFE_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   if (!c->d2h) LIFE_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  BatchGeom g{};
+  g.width = width;
+  g.height = height;
+  g.wpr = wpr;
+  g.words_per_row = words_per_row;
+  g.pitch = pitch;
+  g.generations = generations;
+  g.depth = depth;
+  g.passes = static_cast<int>(ceil_div(generations, depth));
+  // Chunked first/last grid when every chunk outlives its shrinking
+  // trapezoid with room to spare.
+  const bool trap = n >= 1 && generations > 0 &&
+                    height / kTrapChunks >= 2 * kShrink * g.passes + 1024;
+  if (trap) {
+    LIFE_TRY(life_band_bounds(height, kTrapChunks, g.bounds));
+    for (auto& st : c->cs)
+      if (!st) LIFE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  }
+  std::vector<cudaEvent_t> evs;
+  auto mk = [&](cudaEvent_t* e) -> int {
+    LIFE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    evs.push_back(*e);
+    return LIFE_OK;
+  };
   std::vector<cudaEvent_t> up(n), comp(n), down(n);
+  for (int32_t i = 0; i < n; ++i) {
+    LIFE_TRY(mk(&up[i]));
+    LIFE_TRY(mk(&comp[i]));
+    LIFE_TRY(mk(&down[i]));
+  }
+  cudaEvent_t chunk_up[kTrapChunks], trap_done[kTrapChunks], tri_done[kTrapChunks];
+  if (trap) {
+    for (int i = 0; i < kTrapChunks; ++i) {
+      LIFE_TRY(mk(&chunk_up[i]));
+      LIFE_TRY(mk(&trap_done[i]));
+      LIFE_TRY(mk(&tri_done[i]));
+    }
+  }
   cudaEvent_t t0, t1;
   LIFE_CUDA(cudaEventCreate(&t0));
   LIFE_CUDA(cudaEventCreate(&t1));
-  for (int32_t i = 0; i < n; ++i) {
-    LIFE_CUDA(cudaEventCreateWithFlags(&up[i], cudaEventDisableTiming));
-    LIFE_CUDA(cudaEventCreateWithFlags(&comp[i], cudaEventDisableTiming));
-    LIFE_CUDA(cudaEventCreateWithFlags(&down[i], cudaEventDisableTiming));
-  }
   const int32_t nw = static_cast<int32_t>(nw32(width));
+  const int P = g.passes;
   LIFE_CUDA(cudaEventRecord(t0, c->h2d));
   int rc = LIFE_OK;
   for (int32_t i = 0; i < n && rc == LIFE_OK; ++i) {
-    uint32_t* a = c->batch[2 * (i & 1)];
-    uint32_t* b = c->batch[2 * (i & 1) + 1];
+    uint32_t* buf[2] = {c->batch[2 * (i & 1)], c->batch[2 * (i & 1) + 1]};
     // Upload grid i into its slot once grid i-2 has left it.
     if (i >= 2) LIFE_CUDA(cudaStreamWaitEvent(c->h2d, down[i - 2], 0));
-    LIFE_CUDA(cudaMemcpy2DAsync(a, pitch * 4, inputs[i], words_per_row * 8, wpr * 8, height,
-                                cudaMemcpyHostToDevice, c->h2d));
-    LIFE_CUDA(cudaEventRecord(up[i], c->h2d));
-    // Compute on the context stream.
-    LIFE_CUDA(cudaStreamWaitEvent(c->stream, up[i], 0));
-    const int64_t mask_n = height * (pitch - nw + 1);
-    packed_mask_tail_kernel<<<grid_stride_blocks(mask_n, 256), 256, 0, c->stream>>>(
-        a, pitch, nw, tail_mask(width), height);
-    LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
-    uint32_t* cur = a;
-    uint32_t* nxt = b;
-    for (int64_t done = 0; done < generations && rc == LIFE_OK;) {
-      const int step = static_cast<int>(std::min<int64_t>(depth, generations - done));
-      rc = life_dev_packed_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, step,
-                                c->stream);
-      std::swap(cur, nxt);
-      done += step;
+    const bool chunked = trap && (i == 0 || i == n - 1);
+    if (!chunked) {
+      LIFE_CUDA(cudaMemcpy2DAsync(buf[0], pitch * 4, inputs[i], words_per_row * 8, wpr * 8, height,
+                                  cudaMemcpyHostToDevice, c->h2d));
+      LIFE_CUDA(cudaEventRecord(up[i], c->h2d));
+      // Compute on the context stream.
+      LIFE_CUDA(cudaStreamWaitEvent(c->stream, up[i], 0));
+      const int64_t mask_n = height * (pitch - nw + 1);
+      packed_mask_tail_kernel<<<grid_stride_blocks(mask_n, 256), 256, 0, c->stream>>>(
+          buf[0], pitch, nw, tail_mask(width), height);
+      LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
+      for (int p = 0; p < P && rc == LIFE_OK; ++p) rc = pass_rows(g, buf, p, 0, height, c->stream);
+      LIFE_CUDA(cudaEventRecord(comp[i], c->stream));
+      // Download on the D2H stream.
+      LIFE_CUDA(cudaStreamWaitEvent(c->d2h, comp[i], 0));
+      LIFE_CUDA(cudaMemcpy2DAsync(outputs[i], words_per_row * 8, buf[P & 1], pitch * 4, wpr * 8,
+                                  height, cudaMemcpyDeviceToHost, c->d2h));
+      LIFE_CUDA(cudaEventRecord(down[i], c->d2h));
+      continue;
     }
-    LIFE_CUDA(cudaEventRecord(comp[i], c->stream));
-    // Download on the D2H stream.
-    LIFE_CUDA(cudaStreamWaitEvent(c->d2h, comp[i], 0));
-    LIFE_CUDA(cudaMemcpy2DAsync(outputs[i], words_per_row * 8, cur, pitch * 4, wpr * 8, height,
-                                cudaMemcpyDeviceToHost, c->d2h));
+    const int nc = kTrapChunks;
+    const int64_t shrink = kShrink * P;  // rows per side the trapezoid gives up
+    for (int ch = 0; ch < nc; ++ch) {
+      const int64_t y0 = g.bounds[ch], rows = g.bounds[ch + 1] - y0;
+      LIFE_TRY(copy_rows(g, const_cast<uint64_t*>(inputs[i]), buf[0], y0, rows, true, c->h2d));
+      LIFE_CUDA(cudaEventRecord(chunk_up[ch], c->h2d));
+    }
+    // Trapezoids in chunk order on two streams (so they finish one after
+    // another and their interiors leave early), each as soon as its chunk has
+    // arrived; triangles on the other two streams, each as soon as its two
+    // trapezoids are done.
+    for (int ch = 0; ch < nc && rc == LIFE_OK; ++ch) {
+      cudaStream_t st = c->cs[ch % 2];
+      const int64_t y0 = g.bounds[ch], rows = g.bounds[ch + 1] - y0;
+      LIFE_CUDA(cudaStreamWaitEvent(st, chunk_up[ch], 0));
+      const int64_t mask_n = rows * (pitch - nw + 1);
+      packed_mask_tail_kernel<<<grid_stride_blocks(mask_n, 256), 256, 0, st>>>(
+          buf[0] + y0 * pitch, pitch, nw, tail_mask(width), rows);
+      LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
+      for (int p = 0; p < P && rc == LIFE_OK; ++p)
+        rc = pass_rows(g, buf, p, y0 + kShrink * (p + 1), rows - 2 * kShrink * (p + 1), st);
+      LIFE_CUDA(cudaEventRecord(trap_done[ch], st));
+    }
+    // Triangles at boundary b (row bounds[b]) between chunks b-1 and b.
+    for (int bi = 1; bi <= nc && rc == LIFE_OK; ++bi) {
+      const int b = bi % nc;  // boundary 0 (the torus seam) needs the last chunk: last
+      cudaStream_t st = c->cs[2 + bi % 2];
+      LIFE_CUDA(cudaStreamWaitEvent(st, trap_done[(b + nc - 1) % nc], 0));
+      LIFE_CUDA(cudaStreamWaitEvent(st, trap_done[b], 0));
+      for (int p = 0; p < P && rc == LIFE_OK; ++p)
+        rc = pass_rows(g, buf, p, g.bounds[b] - kShrink * (p + 1), 2 * kShrink * (p + 1), st);
+      LIFE_CUDA(cudaEventRecord(tri_done[b], st));
+    }
+    // Downloads: each chunk's interior when its trapezoid is done, then the
+    // boundary strips.
+    for (int ch = 0; ch <= nc; ++ch) {
+      if (ch < nc) {
+        const int64_t y0 = g.bounds[ch], rows = g.bounds[ch + 1] - y0;
+        LIFE_CUDA(cudaStreamWaitEvent(c->d2h, trap_done[ch], 0));
+        LIFE_TRY(
+            copy_rows(g, outputs[i], buf[P & 1], y0 + shrink, rows - 2 * shrink, false, c->d2h));
+      }
+      if (ch >= 1) {  // boundary ch (ch == nc: the seam, boundary 0)
+        const int b = ch % nc;
+        LIFE_CUDA(cudaStreamWaitEvent(c->d2h, tri_done[b], 0));
+        LIFE_TRY(copy_rows(g, outputs[i], buf[P & 1], g.bounds[b] - shrink, 2 * shrink, false,
+                           c->d2h));
+      }
+    }
     LIFE_CUDA(cudaEventRecord(down[i], c->d2h));
   }
   LIFE_CUDA(cudaEventRecord(t1, c->d2h));
   LIFE_CUDA(cudaEventSynchronize(t1));
   LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  if (trap)
+    for (auto& st : c->cs) LIFE_CUDA(cudaStreamSynchronize(st));
   float ms = 0;
   LIFE_CUDA(cudaEventElapsedTime(&ms, t0, t1));
   if (elapsed_ms) *elapsed_ms = ms;
-  for (int32_t i = 0; i < n; ++i) {
-    cudaEventDestroy(up[i]);
-    cudaEventDestroy(comp[i]);
-    cudaEventDestroy(down[i]);
-  }
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
   cudaEventDestroy(t0);
   cudaEventDestroy(t1);
   return rc;
