@@ -278,8 +278,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // (strip, y, n), each a fresh pipeline of n + kLag steps.
 
 // One pipeline segment of a warp: strip `strip`, output rows [y, y+n).
-// Runs ceil((n + kLag) / PF) loop trips (one block barrier each) and returns
-// that count.  Three fetch paths, chosen per warp (warp-uniform):
+// Runs ceil((n + kLag) / PF) loop trips (a block barrier after every
+// sync_every-th) and returns that count.  Three fetch paths, chosen per warp (warp-uniform):
 //   kPathFast:  every lane's word is one aligned word of the row (W % 32 == 0
 //               or the strip does not touch the seam): one cp.async per row;
 //   kPathSeam:  W % 32 != 0 and some lane's word straddles the seam: every
@@ -520,9 +520,9 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
 // the last stage emits generation K of output row i-3K+1.
 //
 // Work: tiles of one strip x seg_rows rows, one per warp, strip fastest; a
-// block is all the warps one SM holds, stepped in lockstep (one barrier per
-// loop trip) because the warp arbiter otherwise starves some warps and the
-// SM ends the pass with too few warps to fill the ALU pipe.  The host picks
+// block is all the warps one SM holds, stepped in lockstep (a barrier every
+// sync_every loop trips) because the warp arbiter otherwise starves some
+// warps and the SM ends the pass with too few warps to fill the ALU pipe.  The host picks
 // seg_rows so the number of block waves is nearly an integer.
 //
 // Every input row is read once per pass and every output row written once,
