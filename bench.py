@@ -306,9 +306,22 @@ def run_gpu_arm(args) -> None:
     if halo == "peer":
         # Fused halo: the pass kernels read the neighbour bands' rows over
         # NVLink (CUDA IPC); NCCL is only the per-pass barrier.
+        from paper_1209_4408_b200.bands import PeerBandDriver
+        err = None
         try:
-            from paper_1209_4408_b200.bands import PeerBandDriver
             drv = PeerBandDriver(geo, dev)
+        except Exception as exc:  # no IPC / peer access on this rank
+            err, drv = exc, None
+        # Collective decision: every rank falls back if any rank could not open
+        # its neighbours' buffers (mixed halo schemes would deadlock).
+        ok = torch.tensor([0 if drv is None else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0 and drv is not None:
+            drv.close()
+            drv = None
+        try:
+            if drv is None:
+                raise RuntimeError(f"peer halo unavailable on some rank ({err!r})")
             inner = drv.compute
 
             def timed_compute(k):
