@@ -1083,10 +1083,16 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
     for (auto& st : c->cs)
       if (!st) LIFE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   }
-  std::vector<cudaEvent_t> evs;
-  auto mk = [&](cudaEvent_t* e) -> int {
-    LIFE_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-    evs.push_back(*e);
+  // Every event is destroyed on every exit path (errors included).
+  struct Events {
+    std::vector<cudaEvent_t> v;
+    ~Events() {
+      for (cudaEvent_t e : v) cudaEventDestroy(e);
+    }
+  } evs;
+  auto mk = [&](cudaEvent_t* e, unsigned flags = cudaEventDisableTiming) -> int {
+    LIFE_CUDA(cudaEventCreateWithFlags(e, flags));
+    evs.v.push_back(*e);
     return LIFE_OK;
   };
   std::vector<cudaEvent_t> up(n), comp(n), down(n);
@@ -1104,8 +1110,8 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
     }
   }
   cudaEvent_t t0, t1;
-  LIFE_CUDA(cudaEventCreate(&t0));
-  LIFE_CUDA(cudaEventCreate(&t1));
+  LIFE_TRY(mk(&t0, cudaEventDefault));
+  LIFE_TRY(mk(&t1, cudaEventDefault));
   const int32_t nw = static_cast<int32_t>(nw32(width));
   const int P = g.passes;
   LIFE_CUDA(cudaEventRecord(t0, c->h2d));
@@ -1193,9 +1199,6 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   float ms = 0;
   LIFE_CUDA(cudaEventElapsedTime(&ms, t0, t1));
   if (elapsed_ms) *elapsed_ms = ms;
-  for (cudaEvent_t e : evs) cudaEventDestroy(e);
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
   return rc;
 }
 
