@@ -123,7 +123,9 @@ int life_step(life_ctx* ctx, int engine);
  * `n` host grids inputs[i] is uploaded, run for `generations` on the packed
  * engine and downloaded to outputs[i] (may alias inputs[i]).  The H2D copy of
  * grid i+1 and the D2H copy of grid i-1 overlap the compute of grid i (copy
- * engines, three streams); use pinned host memory for the overlap.
+ * engines); tall grids run their first and last grid as 16 row-chunk
+ * trapezoids plus boundary triangles so those copies overlap compute too.
+ * Use pinned host memory for the overlap.
  * *elapsed_ms (optional) = CUDA-event time from the first upload to the last
  * download.  The context's resident grid is not touched. */
 int life_run_batch(life_ctx* ctx, const uint64_t* const* inputs, uint64_t* const* outputs,
