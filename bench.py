@@ -5,6 +5,8 @@ cell-updates/s at 1/2/4/8 B200, as a fraction of the int/HBM roofline).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--depth 16]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference      # the reference's own CPU engine
+    python bench.py --config 2 --engine byte       # byte engine (HBM-bound)
+    python bench.py --config 1 --engine resident   # cluster-resident engine (small tori)
 
 One JSON line on rank 0.  A "step" is one full run of the configuration's
 generations (config 5: 500 generations of the 262144^2 torus) over the
@@ -655,6 +657,116 @@ def run_byte_arm(args) -> None:
         "gpu_launches": n_launch, "clocks": clocks.summary()}), flush=True)
 
 
+def run_resident_arm(args) -> None:
+    """The cluster-resident engine (whole torus in one thread-block cluster's
+    shared memory, every generation of a step in one launch) on one GPU;
+    small tori with W % 32 == 0 (config 1)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1209_4408_b200 import capi
+    from paper_1209_4408_b200.life import check
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": "resident engine is single-GPU"}))
+        return
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    L = capi.lib()
+    cfg = CONFIGS[args.config]
+    W, H, gens = cfg["w"], cfg["h"], args.gens or cfg["gens"]
+    n_cta = int(L.life_resident_cluster_size(W, H))
+    if n_cta == 0:
+        print(json.dumps({"metric": METRIC, "unavailable": f"{W}x{H} does not fit the resident engine"}))
+        return
+    pitch = int(L.life_packed_pitch_words(W))
+    bufs = [torch.zeros((H, pitch), dtype=torch.int32, device=dev) for _ in range(2)]
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    check(L.life_dev_packed_random(bufs[0].data_ptr(), pitch, W, 0, H, cfg["p"], 42, stream))
+    flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
+    int_ops = 0.0
+    o, sec = C.c_double(), C.c_double()
+    if L.life_measure_int_peak(0, 4000, C.byref(o), C.byref(sec)) == 0:
+        int_ops = o.value
+    cur = [0]
+
+    def step():
+        a, b = bufs[cur[0]], bufs[cur[0] ^ 1]
+        check(L.life_dev_packed_run_resident(a.data_ptr(), b.data_ptr(), pitch, W, H, gens, stream))
+        cur[0] ^= 1
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    l0 = L.life_kernel_launches()
+    ms = []
+    with ClockSampler(0) as clocks:
+        for _ in range(args.steps):
+            flush.fill_(1)  # the grid fits in L2: flush between steps
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+    n_launch = int(L.life_kernel_launches() - l0)
+    step_ms = sum(ms) / len(ms)
+    value = W * H * gens * args.steps / (sum(ms) * 1e-3) / 1e9
+    achieved = W * H * gens * OPS_PER_UPDATE / (step_ms * 1e-3) / 1e12
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak_cluster = int_ops / 1e12 * n_cta / sms
+    e2e = None
+    if not args.no_e2e:
+        # Public API: packed grid from pinned host memory -> life_run(RESIDENT)
+        # -> packed grid back, synchronous C-ABI calls, host-timed per step.
+        from paper_1209_4408_b200 import life
+        wpr = (W + 63) // 64
+        host = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True).numpy()
+        host[:] = bufs[cur[0]].cpu().numpy().view("int64")[:, :wpr]
+        hout = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True).numpy()
+        steps_e2e = max(5, args.steps)
+        with life.Engine(0) as eng:
+            eng.upload_packed(host.view("uint64"), W)
+            eng.run(gens, capi.ENGINE_RESIDENT)
+            eng.download_packed(hout.view("uint64"))
+            t0 = time.perf_counter()
+            for _ in range(steps_e2e):
+                eng.upload_packed(host.view("uint64"), W)
+                eng.run(gens, capi.ENGINE_RESIDENT)
+                eng.download_packed(hout.view("uint64"))
+            e2e_s = time.perf_counter() - t0
+        e2e = {"value": W * H * gens * steps_e2e / e2e_s / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": H * wpr * 8, "d2h_bytes_per_step": H * wpr * 8,
+               "api": "C-ABI life_grid_upload_packed + life_run(LIFE_ENGINE_RESIDENT) + "
+                      "life_grid_download_packed from/to pinned host memory (host-timed)",
+               "steps": steps_e2e}
+    cpu = None
+    if not args.no_cpu:
+        try:
+            cpu = cpu_measure(cfg, args.cpu_budget)
+        except Exception as exc:  # reported, not fatal
+            cpu = {"error": repr(exc)}
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32 bit-sliced (32 cells/word, exact integer)", "data": "synthetic",
+        "config": {"workload": cfg["desc"].replace("bit-packed engine", "cluster-resident engine"),
+                   "engine": "resident", "generations": gens, "cluster_ctas": n_cta,
+                   "l2": "L2 flushed between steps"},
+        "roofline": {"bound": "int", "kernel": "packed_resident_kernel",
+                     "achieved": achieved, "peak": peak_cluster, "unit": "Tops/s",
+                     "frac": achieved / peak_cluster if peak_cluster else None,
+                     "peak_source": f"measured LOP3 peak x {n_cta}/{sms} SMs (one cluster)",
+                     "frac_of_gpu": achieved / (int_ops / 1e12) if int_ops else None,
+                     "ops_per_cell_update": OPS_PER_UPDATE, "mean_launch_ms": step_ms,
+                     "traffic": None},
+        "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": n_launch, "clocks": clocks.summary()}), flush=True)
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -667,7 +779,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--engine", choices=["packed", "byte"], default="packed")
+    ap.add_argument("--engine", choices=["packed", "byte", "resident"], default="packed")
     ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
                     help="multi-GPU halo: in-kernel NVLink peer reads or NCCL send/recv")
     args = ap.parse_args()
@@ -675,6 +787,8 @@ def main() -> None:
         run_reference_arm(args)
     elif args.engine == "byte":
         run_byte_arm(args)
+    elif args.engine == "resident":
+        run_resident_arm(args)
     else:
         run_gpu_arm(args)
 

@@ -52,6 +52,11 @@ extern "C" {
  * gains GPU kinds). */
 #define LIFE_ENGINE_PACKED 0 /* 64 cells/uint64, LOP3 adder network, temporal blocking */
 #define LIFE_ENGINE_BYTE 1   /* one byte per cell, one generation per pass */
+/* Packed layout, whole torus resident in the shared memory of one thread-block
+ * cluster (<= 16 CTAs), every generation in one launch: small tori with
+ * W % 32 == 0 (LIFE_ERR_CONFIG otherwise).  LIFE_ENGINE_PACKED with
+ * temporal_depth 0 (auto) selects it when it is the faster engine. */
+#define LIFE_ENGINE_RESIDENT 2
 
 /* Largest temporal depth (generations per kernel pass) of the packed engine. */
 #define LIFE_MAX_TEMPORAL_DEPTH 16
@@ -167,6 +172,15 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
                               int64_t band_rows, uint32_t* out, int64_t out_row0,
                               int64_t out_rows, int64_t width, int32_t generations,
                               void* stream);
+/* `generations` packed generations of a whole W x H torus (rows of `pitch`
+ * words, in == out allowed) through the cluster-resident engine
+ * (LIFE_ENGINE_RESIDENT), one launch per 2^30 generations. */
+int life_dev_packed_run_resident(const uint32_t* in, uint32_t* out, int64_t pitch,
+                                 int64_t width, int64_t height, int64_t generations,
+                                 void* stream);
+/* CTAs per cluster the resident engine would use for a W x H torus on the
+ * current device; 0 if the torus does not fit it. */
+int life_resident_cluster_size(int64_t width, int64_t height);
 /* Device buffers shareable across processes (cudaMalloc, zeroed) and CUDA
  * IPC: a 64-byte handle per buffer, opened in the peer process. */
 int life_dev_alloc(int64_t bytes, void** out);

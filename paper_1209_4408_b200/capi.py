@@ -24,6 +24,7 @@ ERR_OUT_OF_MEMORY = 12
 
 ENGINE_PACKED = 0
 ENGINE_BYTE = 1
+ENGINE_RESIDENT = 2
 MAX_TEMPORAL_DEPTH = 16
 
 # Every function the header declares: (name, restype, argtypes).
@@ -60,6 +61,8 @@ SIGNATURES = [
                                        _vp]),
     ("life_dev_packed_step_peer", C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64,
                                             _i64, _i64, _i32, _vp]),
+    ("life_dev_packed_run_resident", C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _vp]),
+    ("life_resident_cluster_size", C.c_int, [_i64, _i64]),
     ("life_dev_alloc", C.c_int, [_i64, C.POINTER(_vp)]),
     ("life_dev_free", C.c_int, [_vp]),
     ("life_ipc_get_handle", C.c_int, [_vp, _vp]),

@@ -930,6 +930,219 @@ __global__ void __launch_bounds__(kStep1Threads) packed_step1_kernel(const Step1
 }
 
 // ---------------------------------------------------------------------------
+// Cluster-resident packed engine (small tori, W % 32 == 0): the whole torus
+// lives in the distributed shared memory of ONE thread-block cluster (up to
+// 16 CTAs, one per SM) and a single launch runs every generation.  CTA k of
+// the cluster owns the row band band_bounds(H, C)[k] (decomposition.cpp:12-24,
+// the paper's 1-D row decomposition) plus one halo row above and below,
+// double-buffered in its shared memory.  Per generation:
+//   __syncthreads          (this CTA's generation-g rows are complete)
+//   interior rows 1..B-2   (own rows only; overlaps the cluster barrier)
+//   barrier.cluster.wait   (the neighbours have pushed our generation-g
+//                           halo rows, and finished reading generation g-1)
+//   edge rows 0 and B-1    (local reads; each result is also stored into
+//                           the neighbour's halo row over DSMEM)
+//   barrier.cluster.arrive (release: our pushes of generation g+1)
+// No load crosses the cluster on the critical path: pushes are fire-and-
+// forget stores ordered by the barrier.  This replaces the per-generation
+// WorkerTeam barrier (engine.cpp:79-96) with the hardware cluster barrier,
+// and the HBM round trip of every pass with shared memory: small grids
+// (config 1) are latency-bound in the multi-pass engine (one launch and a
+// grid-wide dependency per K generations), here they are bound by the
+// cluster barrier and the ALU work of 16 SMs.  Same rule network as
+// packed_tb_kernel; the torus column wrap is an index wrap (W % 32 == 0).
+// ---------------------------------------------------------------------------
+struct ResidentArgs {
+  const uint32_t* in;
+  uint32_t* out;
+  int64_t pitch;        // words per HBM row
+  int32_t nw;           // W / 32
+  int32_t base_rows;    // H / C
+  int32_t extra_rows;   // H % C: the first extra_rows bands hold one more row
+  int32_t max_rows;     // rows of the largest band (smem slab = (max_rows + 2) * nw words)
+  int32_t groups;       // row groups per CTA: thread t works column t % nw, group t / nw
+  int32_t generations;
+};
+
+constexpr int kResidentMaxThreads = 1024;
+
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_ctas() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+// Shared-window address of the same variable in CTA `rank` of the cluster.
+__device__ __forceinline__ uint32_t map_rank(const void* smem_ptr, uint32_t rank) {
+  const uint32_t local = static_cast<uint32_t>(__cvta_generic_to_shared(smem_ptr));
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+  return remote;
+}
+// Remote store into CTA-rank memory of the cluster that also completes
+// 4 bytes of the transaction count of the receiver's mbarrier.
+__device__ __forceinline__ void st_async_u32(uint32_t remote_addr, uint32_t v, uint32_t remote_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.u32 [%0], %1, [%2];"
+               ::"r"(remote_addr), "r"(v), "r"(remote_mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+  asm volatile(
+      "{\n .reg .pred done;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 done, [%0], %1;\n"
+      " @!done bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity) : "memory");
+}
+
+__global__ void __launch_bounds__(kResidentMaxThreads)
+packed_resident_kernel(const ResidentArgs a) {
+  extern __shared__ __align__(16) uint32_t res_smem[];
+  __shared__ uint64_t halo_bar[2];  // halo rows of buffer b have landed
+  const int C = static_cast<int>(cluster_ctas());
+  const int k = static_cast<int>(cluster_rank());
+  const int nw = a.nw;
+  // Per buffer: slab row 0 = halo row above the band, rows 1..B = the band,
+  // row B+1 = halo row below.
+  const int slab = (a.max_rows + 2) * nw;
+  uint32_t* const buf0 = res_smem;
+  const int B = a.base_rows + (k < a.extra_rows ? 1 : 0);
+  const int64_t H = static_cast<int64_t>(a.base_rows) * C + a.extra_rows;
+  const int64_t y0 = static_cast<int64_t>(k) * a.base_rows + (k < a.extra_rows ? k : a.extra_rows);
+  const int up = k == 0 ? C - 1 : k - 1;
+  const int dn = k == C - 1 ? 0 : k + 1;
+  const int B_up = a.base_rows + (up < a.extra_rows ? 1 : 0);
+  // Where our edge rows go: our row 0 is the halo below the band above
+  // (its slab row B_up + 1), our row B-1 the halo above the band below.
+  const uint32_t push_up = map_rank(buf0 + (B_up + 1) * nw, static_cast<uint32_t>(up));
+  const uint32_t push_dn = map_rank(buf0, static_cast<uint32_t>(dn));
+  const uint32_t bar_up = map_rank(halo_bar, static_cast<uint32_t>(up));
+  const uint32_t bar_dn = map_rank(halo_bar, static_cast<uint32_t>(dn));
+  const uint32_t halo_bytes = static_cast<uint32_t>(2 * nw * 4);
+
+  // Band rows plus both halo rows of generation 0 straight from HBM.
+  for (int i = threadIdx.x; i < (B + 2) * nw; i += blockDim.x) {
+    const int r = i / nw;
+    int64_t y = y0 + r - 1;
+    y = y < 0 ? y + H : (y >= H ? y - H : y);
+    buf0[i] = __ldg(a.in + y * a.pitch + (i - r * nw));
+  }
+  // Halo generation g >= 1 lands in buffer g & 1; its mbarrier phase is
+  // armed two generations ahead (before we push the rows that let the
+  // neighbours compute it), so no complete_tx ever precedes its expect_tx.
+  if (threadIdx.x == 0) {
+    mbar_init(&halo_bar[0], 1);
+    mbar_init(&halo_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (a.generations >= 1) mbar_expect_tx(&halo_bar[1], halo_bytes);
+    if (a.generations >= 2) mbar_expect_tx(&halo_bar[0], halo_bytes);
+  }
+  // Every CTA of the cluster is running (and its mbarriers initialised)
+  // before anyone stores into its shared memory.
+  cluster_arrive_release();
+  cluster_wait_acquire();
+
+  // Warp roles: the first ceil(2 nw / 32) warps compute the two edge rows
+  // (and push them); the others the interior rows, column t % nw, a run of
+  // rows per group.
+  const int edge_threads = static_cast<int>((2 * nw + 31) / 32 * 32);
+  const bool is_edge = static_cast<int>(threadIdx.x) < edge_threads;
+  const int t = static_cast<int>(threadIdx.x) - (is_edge ? 0 : edge_threads);
+  const int interior = B - 2;
+  int w = t % nw, grp = t / nw;
+  const bool worker = !is_edge && grp < a.groups && interior > 0;
+  const int r_begin = 1 + (worker ? interior * grp / a.groups : 0);
+  const int r_end = 1 + (worker ? interior * (grp + 1) / a.groups : 0);
+  if (is_edge) w = t % nw;
+  const int wl = w == 0 ? nw - 1 : w - 1, wr = w == nw - 1 ? 0 : w + 1;
+  const bool edge_bottom = t >= nw;
+  const bool edge_active = is_edge && t < 2 * nw;
+  const int edge_r = edge_bottom ? B - 1 : 0;
+  const uint32_t edge_push = (edge_bottom ? push_dn : push_up) + static_cast<uint32_t>(w * 4);
+  const uint32_t edge_bar = edge_bottom ? bar_dn : bar_up;
+
+  for (int g = 0; g < a.generations; ++g) {
+    const int cur = g & 1;
+    const uint32_t* src = buf0 + cur * slab + nw;  // band row 0
+    uint32_t* dst = buf0 + (cur ^ 1) * slab + nw;
+    __syncthreads();  // this CTA's generation-g band rows are in place
+    if (!is_edge) {
+      if (r_begin < r_end) {
+        const uint32_t* p = src + (r_begin - 1) * nw;
+        HSum ha = hsum(p[wl], p[w], p[wr]);
+        p += nw;
+        uint32_t self = p[w];
+        HSum hb = hsum(p[wl], self, p[wr]);
+        uint32_t* q = dst + r_begin * nw + w;
+#pragma unroll 4
+        for (int r = r_begin; r < r_end; ++r) {
+          p += nw;
+          const uint32_t x = p[w];
+          const HSum hc = hsum(p[wl], x, p[wr]);
+          *q = rule(ha, hb, hc, self);
+          q += nw;
+          ha = hb;
+          hb = hc;
+          self = x;
+        }
+      }
+    } else {
+      if (g >= 1) {
+        const uint32_t use = static_cast<uint32_t>(cur ? (g - 1) / 2 : g / 2 - 1);
+        mbar_wait(&halo_bar[cur], use & 1);  // the neighbours' pushes of our generation-g halos
+        __syncwarp();
+        if (threadIdx.x == 0 && g + 2 <= a.generations) mbar_expect_tx(&halo_bar[cur], halo_bytes);
+      }
+      if (edge_active) {
+        // Edge rows 0 and B-1 (B >= 2) from local rows (the halos are
+        // local copies); each result also goes to a neighbour's halo row
+        // of the next buffer.
+        const uint32_t* p = src + (edge_r - 1) * nw;
+        const HSum ha = hsum(p[wl], p[w], p[wr]);
+        p += nw;
+        const uint32_t self = p[w];
+        const HSum hb = hsum(p[wl], self, p[wr]);
+        p += nw;
+        const uint32_t v = rule(ha, hb, hsum(p[wl], p[w], p[wr]), self);
+        dst[edge_r * nw + w] = v;
+        st_async_u32(edge_push + static_cast<uint32_t>((cur ^ 1) * slab * 4), v,
+                     edge_bar + static_cast<uint32_t>((cur ^ 1) * 8));
+      }
+    }
+  }
+  // The last pushes into our shared memory (generation G's halos) must land
+  // before the CTA exits.
+  const int G = a.generations;
+  if (G >= 1 && is_edge) {
+    const int b = G & 1;
+    mbar_wait(&halo_bar[b], static_cast<uint32_t>(b ? (G - 1) / 2 : G / 2 - 1) & 1);
+  }
+  __syncthreads();
+  const uint32_t* fin = buf0 + (G & 1) * slab + nw;
+  for (int i = threadIdx.x; i < B * nw; i += blockDim.x) {
+    const int r = i / nw;
+    a.out[(y0 + r) * a.pitch + (i - r * nw)] = fin[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Layout conversion, seeded soup, population, windows.
 // ---------------------------------------------------------------------------
 

@@ -333,6 +333,146 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
   return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
 }
 
+namespace {
+// Cluster-resident engine plan: the largest cluster (16, 8, 4, 2, 1 CTAs)
+// whose bands (>= 2 rows each, double-buffered) fit one CTA's shared memory
+// and that the device can co-schedule.
+struct ResidentPlan {
+  int C = 0, threads = 0, groups = 0;
+  size_t smem = 0;
+  ResidentArgs args{};
+};
+
+// Interior threads per CTA the resident engine aims for: enough warps to
+// hide shared-memory latency, few enough that each thread's run of rows
+// amortises the two rows of horizontal sums it recomputes per generation
+// (measured).
+// Sweep (T cell-updates/s, 800 generations): 1024^2 at 256/512/1024
+// threads 1.78/1.91/1.57; 2048^2 2.48/3.00/3.04; 2048x4096 2.71/3.33/3.53.
+int resident_target_threads(int nw) {
+  static int v = [] {
+    const char* e = std::getenv("LIFE_RESIDENT_THREADS");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v > 0 ? v : (nw <= 32 ? 512 : kResidentMaxThreads);
+}
+
+int plan_resident(int64_t width, int64_t height, ResidentPlan* plan) {
+  if (width < 32 || width % 32 != 0 || width / 32 > kResidentMaxThreads || height < 2)
+    return LIFE_ERR_CONFIG;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  LIFE_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  static int max_dyn[64] = {0};  // dynamic shared memory bytes per CTA (opt-in max - static)
+  if (max_dyn[dev & 63] == 0) {
+    cudaFuncAttributes fa{};
+    LIFE_CUDA(cudaFuncGetAttributes(&fa, packed_resident_kernel));
+    const int dyn = optin - static_cast<int>(fa.sharedSizeBytes);
+    LIFE_CUDA(cudaFuncSetAttribute(packed_resident_kernel,
+                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    LIFE_CUDA(cudaFuncSetAttribute(packed_resident_kernel,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    max_dyn[dev & 63] = dyn;
+  }
+  optin = max_dyn[dev & 63];
+  const int nw = static_cast<int>(width / 32);
+  for (int C : {16, 8, 4, 2, 1}) {
+    if (height < 2 * C) continue;
+    const int64_t max_rows = ceil_div(height, C);
+    const size_t smem = static_cast<size_t>(2 * (max_rows + 2) * nw) * 4;  // + 2 halo rows
+    if (smem > static_cast<size_t>(optin)) continue;
+    const int interior = static_cast<int>(height / C) - 2;
+    // Edge warps (the two rows next to the halos) + interior warps.
+    const int edge_threads = static_cast<int>(ceil_div(2 * nw, 32) * 32);
+    if (edge_threads + nw > kResidentMaxThreads) continue;
+    int groups = static_cast<int>(ceil_div(resident_target_threads(nw), nw));
+    groups = std::max(1, std::min({groups, std::max(interior, 1),
+                                   (kResidentMaxThreads - edge_threads) / nw}));
+    const int threads =
+        edge_threads + static_cast<int>(ceil_div(static_cast<int64_t>(groups) * nw, 32) * 32);
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, packed_resident_kernel, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (clusters < 1) continue;
+    plan->C = C;
+    plan->threads = threads;
+    plan->groups = groups;
+    plan->smem = smem;
+    plan->args.nw = nw;
+    plan->args.base_rows = static_cast<int32_t>(height / C);
+    plan->args.extra_rows = static_cast<int32_t>(height % C);
+    plan->args.max_rows = static_cast<int32_t>(max_rows);
+    plan->args.groups = groups;
+    return LIFE_OK;
+  }
+  return LIFE_ERR_CONFIG;
+}
+}  // namespace
+
+int life_resident_cluster_size(int64_t width, int64_t height) {
+  ResidentPlan p;
+  return plan_resident(width, height, &p) == LIFE_OK ? p.C : 0;
+}
+
+int life_dev_packed_run_resident(const uint32_t* in, uint32_t* out, int64_t pitch, int64_t width,
+                                 int64_t height, int64_t generations, void* stream) {
+  if (generations < 0) return set_error(LIFE_ERR_CONFIG, "generations must be non-negative");
+  if (!in || !out || pitch < width / 32)
+    return set_error(LIFE_ERR_CONFIG, "bad resident run geometry");
+  ResidentPlan p;
+  const int rc = plan_resident(width, height, &p);
+  if (rc != LIFE_OK) {
+    if (rc == LIFE_ERR_CONFIG)
+      return set_error(LIFE_ERR_CONFIG,
+                       "a %lldx%lld torus does not fit the cluster-resident engine "
+                       "(needs W %% 32 == 0, W <= 32768, H >= 2 and both buffers of "
+                       "every band in one CTA's shared memory)",
+                       static_cast<long long>(width), static_cast<long long>(height));
+    return rc;
+  }
+  p.args.in = in;
+  p.args.out = out;
+  p.args.pitch = pitch;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(p.C);
+  cfg.blockDim = dim3(p.threads);
+  cfg.dynamicSmemBytes = p.smem;
+  cfg.stream = static_cast<cudaStream_t>(stream);
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // One launch per 2^30 generations (the kernel counts in int32).
+  int64_t left = generations;
+  const uint32_t* src = in;
+  do {
+    const int64_t n = std::min<int64_t>(left, int64_t(1) << 30);
+    p.args.in = src;
+    p.args.generations = static_cast<int32_t>(n);
+    LIFE_CUDA(cudaLaunchKernelEx(&cfg, packed_resident_kernel, p.args));
+    LIFE_CHECK_LAUNCH("packed_resident_kernel");
+    left -= n;
+    src = out;
+  } while (left > 0);
+  return LIFE_OK;
+}
+
 int life_dev_alloc(int64_t bytes, void** out) {
   if (!out || bytes < 0) return set_error(LIFE_ERR_CONFIG, "bad allocation request");
   *out = nullptr;
@@ -623,9 +763,20 @@ int population_async(life_ctx* c, unsigned long long* slot) {
 }
 
 int check_engine(int engine) {
-  if (engine != LIFE_ENGINE_PACKED && engine != LIFE_ENGINE_BYTE)
+  if (engine != LIFE_ENGINE_PACKED && engine != LIFE_ENGINE_BYTE && engine != LIFE_ENGINE_RESIDENT)
     return set_error(LIFE_ERR_CONFIG, "unknown engine %d", engine);
   return LIFE_OK;
+}
+
+// The resident grid layout an engine computes on.
+int engine_layout(int engine) { return engine == LIFE_ENGINE_BYTE ? kByte : kPacked; }
+
+// temporal_depth 0 on the packed engine: the cluster-resident engine for
+// small tori (W % 32 == 0, at most kResidentAutoCells cells) where it beats
+// the multi-pass engine (measured), else K = 16 passes.
+constexpr int64_t kResidentAutoCells = int64_t(1) << 22;
+bool resident_auto(int64_t w, int64_t h) {
+  return w % 32 == 0 && w * h <= kResidentAutoCells && life_resident_cluster_size(w, h) > 0;
 }
 
 }  // namespace
@@ -741,7 +892,7 @@ int life_grid_init_random(life_ctx* c, int64_t width, int64_t height, double den
   if (!(density >= 0.0 && density <= 1.0))
     return set_error(LIFE_ERR_CONFIG, "density must be in [0, 1], got %f", density);
   LIFE_TRY(set_dims(c, width, height));
-  if (engine == LIFE_ENGINE_PACKED) {
+  if (engine != LIFE_ENGINE_BYTE) {
     LIFE_TRY(ensure_packed(c));
     c->pk_cur = 0;
     LIFE_TRY(life_dev_packed_random(c->pk[0], c->pk_pitch, width, 0, height, density, seed,
@@ -793,7 +944,7 @@ int life_grid_init_soup(life_ctx* c, int64_t width, int64_t height, double cover
   }
   LIFE_CUDA(cudaFreeAsync(owner, c->stream));
   c->layout = kByte;
-  if (engine == LIFE_ENGINE_PACKED) LIFE_TRY(to_layout(c, kPacked));
+  if (engine != LIFE_ENGINE_BYTE) LIFE_TRY(to_layout(c, kPacked));
   LIFE_CUDA(cudaStreamSynchronize(c->stream));
   return LIFE_OK;
 }
@@ -922,18 +1073,26 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
     prev = cp;
   }
   int depth = temporal_depth;
-  if (engine == LIFE_ENGINE_PACKED) {
-    if (depth == 0) depth = LIFE_MAX_TEMPORAL_DEPTH;
-    if (depth < 1 || depth > LIFE_MAX_TEMPORAL_DEPTH)
+  if (engine != LIFE_ENGINE_BYTE) {
+    if (depth < 0 || depth > LIFE_MAX_TEMPORAL_DEPTH)
       return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [0, %d], got %d",
                        LIFE_MAX_TEMPORAL_DEPTH, temporal_depth);
+    if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+    if (engine == LIFE_ENGINE_PACKED && depth == 0 && resident_auto(c->W, c->H))
+      engine = LIFE_ENGINE_RESIDENT;
+    if (engine == LIFE_ENGINE_RESIDENT && life_resident_cluster_size(c->W, c->H) == 0)
+      return set_error(LIFE_ERR_CONFIG,
+                       "a %lldx%lld torus does not fit the cluster-resident engine "
+                       "(needs W %% 32 == 0 and every band in one CTA's shared memory)",
+                       static_cast<long long>(c->W), static_cast<long long>(c->H));
+    if (depth == 0) depth = LIFE_MAX_TEMPORAL_DEPTH;
   } else {
     if (depth != 0 && depth != 1)
       return set_error(LIFE_ERR_CONFIG, "the byte engine runs one generation per pass (depth 0/1)");
     depth = 1;
   }
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
-  LIFE_TRY(to_layout(c, engine));
+  LIFE_TRY(to_layout(c, engine_layout(engine)));
   if (n_checkpoints > 0) LIFE_TRY(ensure_counts(c, n_checkpoints));
 
   int32_t ci = 0;
@@ -948,6 +1107,14 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
   int64_t done = 0;
   while (done < generations) {
     const int64_t stop = ci < n_checkpoints ? checkpoints[ci] : generations;
+    if (engine == LIFE_ENGINE_RESIDENT) {  // every generation up to the next stop in one launch
+      LIFE_TRY(life_dev_packed_run_resident(c->pk[c->pk_cur], c->pk[c->pk_cur ^ 1], c->pk_pitch,
+                                            c->W, c->H, stop - done, c->stream));
+      c->pk_cur ^= 1;
+      done = stop;
+      LIFE_TRY(record(done));
+      continue;
+    }
     const int step = static_cast<int>(std::min<int64_t>(depth, stop - done));
     if (engine == LIFE_ENGINE_PACKED) {
       const int nxt = c->pk_cur ^ 1;

@@ -64,7 +64,7 @@ inline void check(int rc) {
   }
 }
 
-enum class Engine { Packed = LIFE_ENGINE_PACKED, Byte = LIFE_ENGINE_BYTE };
+enum class Engine { Packed = LIFE_ENGINE_PACKED, Byte = LIFE_ENGINE_BYTE, Resident = LIFE_ENGINE_RESIDENT };
 
 // RunConfig (engine.hpp:11-15) with the GPU strategy fields.
 struct RunConfig {

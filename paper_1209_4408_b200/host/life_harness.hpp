@@ -11,7 +11,7 @@
 //                                          each cell's baseline, speedups against it)
 //   population_series  bench.cpp:167-176
 //   emit_csv           bench.cpp:178-191  (the pinned 12-column header)
-// with GPU strategy tokens ("gpu", "gpu:K", "gpu-byte" -- the reference's
+// with GPU strategy tokens ("gpu", "gpu:K", "gpu-byte", "gpu-resident" -- the reference's
 // parse_strategy, decomposition.cpp:68-91, gains these kinds) and an extended
 // CSV carrying GCUPS and the roofline fraction.  Populations are uint64.
 #pragma once
@@ -45,12 +45,14 @@ struct Strategy {
 
 inline std::string to_string(const Strategy& s) {
   if (s.engine == Engine::Byte) return "gpu-byte";
+  if (s.engine == Engine::Resident) return "gpu-resident";
   return s.depth == 0 ? "gpu" : "gpu:" + std::to_string(s.depth);
 }
 
 inline Strategy parse_strategy(const std::string& token) {
   if (token == "gpu") return {Engine::Packed, 0};
   if (token == "gpu-byte") return {Engine::Byte, 1};
+  if (token == "gpu-resident") return {Engine::Resident, 0};
   if (token.rfind("gpu:", 0) == 0) {
     const std::string k = token.substr(4);
     if (!k.empty() && k.size() <= 2 && std::all_of(k.begin(), k.end(), ::isdigit)) {
@@ -59,7 +61,7 @@ inline Strategy parse_strategy(const std::string& token) {
     }
   }
   throw ConfigError("unknown strategy '" + token +
-                    "' (expected gpu, gpu:K with K in 1..16, or gpu-byte)");
+                    "' (expected gpu, gpu:K with K in 1..16, gpu-byte or gpu-resident)");
 }
 
 inline double speedup(double baseline_s, double other_s) {

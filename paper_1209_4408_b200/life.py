@@ -139,8 +139,11 @@ class Strategy:
     """Strategy (decomposition.hpp:30-49) plus the GPU kinds this engine adds.
 
     `gpu_packed` runs the bit-packed temporal-blocked engine with `depth`
-    generations per kernel pass (0 = the engine's maximum, 16); `gpu_byte`
-    runs the byte-per-cell engine, one generation per pass."""
+    generations per kernel pass (0 = auto: the cluster-resident engine for
+    small tori with W % 32 == 0, else 16); `gpu_resident` keeps the whole
+    torus in one thread-block cluster's shared memory and runs every
+    generation in one launch; `gpu_byte` runs the byte-per-cell engine, one
+    generation per pass."""
 
     kind: str = "gpu_packed"
     blocks_x: int = 1
@@ -155,18 +158,27 @@ class Strategy:
     def gpu_byte() -> "Strategy":
         return Strategy("gpu_byte", 1, 1, 1)
 
+    @staticmethod
+    def gpu_resident() -> "Strategy":
+        return Strategy("gpu_resident", 1, 1, 0)
+
     def engine(self) -> int:
         if self.kind == "gpu_packed":
             return capi.ENGINE_PACKED
         if self.kind == "gpu_byte":
             return capi.ENGINE_BYTE
+        if self.kind == "gpu_resident":
+            return capi.ENGINE_RESIDENT
         raise ConfigError(f"strategy '{self.kind}' is not a GPU strategy")
 
 
 def to_string(strategy: Strategy) -> str:
-    """Strategy token (decomposition.cpp:51-66 style): gpu, gpu:K, gpu-byte."""
+    """Strategy token (decomposition.cpp:51-66 style): gpu, gpu:K, gpu-byte,
+    gpu-resident."""
     if strategy.kind == "gpu_byte":
         return "gpu-byte"
+    if strategy.kind == "gpu_resident":
+        return "gpu-resident"
     return "gpu" if strategy.depth == 0 else f"gpu:{strategy.depth}"
 
 
@@ -176,6 +188,8 @@ def parse_strategy(token: str) -> Strategy:
         return Strategy.gpu_packed()
     if token == "gpu-byte":
         return Strategy.gpu_byte()
+    if token == "gpu-resident":
+        return Strategy.gpu_resident()
     if token.startswith("gpu:"):
         try:
             k = int(token[4:])
@@ -183,7 +197,7 @@ def parse_strategy(token: str) -> Strategy:
             k = -1
         if 1 <= k <= capi.MAX_TEMPORAL_DEPTH:
             return Strategy.gpu_packed(k)
-    raise ConfigError(f"unknown strategy '{token}' (expected gpu, gpu:K (1..16) or gpu-byte)")
+    raise ConfigError(f"unknown strategy '{token}' (expected gpu, gpu:K (1..16), gpu-byte or gpu-resident)")
 
 
 @dataclass

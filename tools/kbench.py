@@ -1,5 +1,6 @@
 """Quick packed-engine timing over arbitrary shapes (kernel-variant sweeps under gpurun).
-usage: LIFE_GPU_LIB=... python tools/kbench.py WxH[,WxH...] GENS DEPTH  -> one JSON line per shape"""
+usage: LIFE_GPU_LIB=... python tools/kbench.py WxH[,WxH...] GENS DEPTH [ENGINE]  -> one JSON line per shape
+(ENGINE: 0 packed multi-pass (default), 2 cluster-resident)"""
 import json
 import os
 import sys
@@ -10,16 +11,17 @@ from paper_1209_4408_b200 import capi, life  # noqa: E402
 
 shapes = [tuple(int(v) for v in s.split("x")) for s in sys.argv[1].split(",")]
 gens, depth = int(sys.argv[2]), int(sys.argv[3])
+engine = int(sys.argv[4]) if len(sys.argv) > 4 else capi.ENGINE_PACKED
 eng = life.Engine(0)
 for (w, h) in shapes:
     eng.init_random(w, h, 0.4, 42)
-    eng.run(depth, capi.ENGINE_PACKED, depth)
+    eng.run(max(depth, 1), engine, depth)
     eng.sync()
     best = 1e30
     for _ in range(3):
         t = time.perf_counter()
-        eng.run(gens, capi.ENGINE_PACKED, depth)
+        eng.run(gens, engine, depth)
         eng.sync()
         best = min(best, time.perf_counter() - t)
     print(json.dumps({"lib": os.path.basename(os.environ.get("LIFE_GPU_LIB", "default")), "w": w, "h": h,
-                      "depth": depth, "gcups": round(w * h * gens / best / 1e9, 1)}))
+                      "depth": depth, "engine": engine, "gcups": round(w * h * gens / best / 1e9, 1)}))
