@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "cell-updates/sec (GCUPS) at 1/2/4/8 B200 and % of HBM/int roofline"
 UNIT = "GCUPS"
-OPS_PER_WORD = 12            # bit-sliced rule network, csrc/kernels.cuh
+OPS_PER_WORD = 11            # bit-sliced rule network (2 SHF + 9 LOP3), csrc/kernels.cuh
 OPS_PER_UPDATE = OPS_PER_WORD / 32.0
 
 CONFIGS = {

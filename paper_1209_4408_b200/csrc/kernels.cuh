@@ -30,15 +30,20 @@ constexpr uint64_t kGamma = 0x9E3779B97F4A7C15ULL;
 //   L = x<<1 | xl>>31,  R = x>>1 | xr<<31   (2 SHF.W funnel shifts)
 //   h0 = L^x^R,  h1 = maj(L,x,R)            (2 LOP3)
 // Three rows' planes a (above), b (the cell's row), c (below) give
-//   S = a + b + c = t0 + 2*u1 + 4*u2 + 8*(q&p&k0) with
-//   t0 = a0^b0^c0, k0 = maj(a0,b0,c0), p = a1^b1^c1, q = maj(a1,b1,c1),
-//   u1 = p^k0, u2 = q^(p&k0)                (6 LOP3)
-// and next = (S==3) | (S==4 & self) = V & (u1^u2) with
-//   V = u2 ? (self & ~t0) : t0              (2 LOP3).
-// S==3 <=> t0 & u1 & ~u2 (u1 = 1 excludes the carry term since S <= 9);
-// S==4 <=> ~t0 & ~u1 & u2.  12 integer ops per 32 cell-updates; verified
-// against next_state over all 512 3x3 neighbourhoods in
-// tests/test_rule_network.py.
+//   S = a + b + c = t0 + 2*(k0 + p + 2q) with
+//   t0 = a0^b0^c0, k0 = maj(a0,b0,c0), p = a1^b1^c1, q = maj(a1,b1,c1)
+//                                           (4 LOP3)
+// and next = (S==3) | (S==4 & self) in three more LOP3 (found by an
+// exhaustive search over 3-gate LUT3 circuits, tools/rule_search.c):
+//   g1 = (~t0 & ~self) | (t0 & ~q)
+//   g2 = (~p & ~k0) | (p & k0 & ~q)        [k0 + p + 2q in {0, 2}, q = 0 for 2]
+//   next = t0 ? (g1 & ~g2) : (~g1 & g2)    = t0 ? (~q & ~g2) : (self & g2)
+// t0 = 1: S == 3 <=> k0 + p + 2q == 1 <=> ~q & ~g2.  t0 = 0: S == 4 <=>
+// k0 + p + 2q == 2, i.e. g2 except k0 = p = q = 0 -- but then S = 0, and
+// S >= self because b = L + self + R, so self = 0 there: the don't-care
+// makes the 4-valued case split fit one gate.  11 integer ops per 32
+// cell-updates (2 SHF + 9 LOP3); verified against next_state over all 512
+// 3x3 neighbourhoods in tests/test_rule_network.py.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) {
   return (a & b) | (a & c) | (b & c);
@@ -57,15 +62,22 @@ __device__ __forceinline__ HSum hsum(uint32_t xl, uint32_t x, uint32_t xr) {
 // (Building L and R on the FMA pipe -- IMAD / IMAD.HI by 2 and 2^31 -- to
 // offload the ALU pipe was measured 2-19 % slower for 1-4 of every 4 stages.)
 
+template <uint32_t LUT>
+__device__ __forceinline__ uint32_t lop3(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t rule(HSum a, HSum b, HSum c, uint32_t self) {
   const uint32_t t0 = a.h0 ^ b.h0 ^ c.h0;
   const uint32_t k0 = maj3(a.h0, b.h0, c.h0);
   const uint32_t p = a.h1 ^ b.h1 ^ c.h1;
   const uint32_t q = maj3(a.h1, b.h1, c.h1);
-  const uint32_t u1 = p ^ k0;
-  const uint32_t u2 = q ^ (p & k0);
-  const uint32_t v = (u2 & self & ~t0) | (~u2 & t0);
-  return v & (u1 ^ u2);
+  // lop3 immediates: bit (x<<2 | y<<1 | z) of the LUT is f(x, y, z).
+  const uint32_t g1 = lop3<0x53>(t0, self, q);  // (~t0 & ~self) | (t0 & ~q)
+  const uint32_t g2 = lop3<0x43>(p, k0, q);     // (~p & ~k0) | (p & k0 & ~q)
+  return lop3<0x42>(t0, g1, g2);                // t0 ? (g1 & ~g2) : (~g1 & g2)
 }
 
 // Physical row index (base + r) mod m for possibly negative r.

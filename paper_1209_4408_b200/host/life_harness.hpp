@@ -271,7 +271,7 @@ inline std::string emit_csv(const std::vector<BenchRecord>& records) {
   return out;
 }
 
-// Roofline of a record: the packed engine is integer-bound (12 ops / 32
+// Roofline of a record: the packed engine is integer-bound (11 ops / 32
 // cell-updates against the measured LOP3 peak), the byte engine HBM-bound
 // (2 bytes per cell-update against the measured copy bandwidth).
 struct RooflinePeaks {
@@ -282,7 +282,7 @@ struct RooflinePeaks {
 inline double roofline_fraction(const BenchRecord& r, const RooflinePeaks& p) {
   const double ups = r.gcups() * 1e9;
   if (r.strategy.engine == Engine::Byte) return p.hbm_bytes_per_s > 0 ? ups * 2.0 / p.hbm_bytes_per_s : 0.0;
-  return p.int_ops_per_s > 0 ? ups * (12.0 / 32.0) / p.int_ops_per_s : 0.0;
+  return p.int_ops_per_s > 0 ? ups * (11.0 / 32.0) / p.int_ops_per_s : 0.0;
 }
 
 // The same rows plus gcups and roofline_frac columns.

@@ -1,5 +1,5 @@
 """CPU checks of the packed engine's ALGORITHM (not the CUDA code): the
-12-op bit-sliced B3/S23 network of csrc/kernels.cuh verified exhaustively
+11-op bit-sliced B3/S23 network of csrc/kernels.cuh verified exhaustively
 against next_state (grid.cpp:22-28), and a lane-exact numpy model of
 packed_tb_kernel (strips of 32 lanes with ghost lanes 0/31, shuffle edge
 semantics, wrapped word loads, segmented K-stage row pipeline) checked
@@ -24,19 +24,36 @@ def hsum(xl, x, xr):
     return L ^ x ^ R, maj(L, x, R)
 
 
+def lop3(x, y, z, lut):
+    """PTX lop3.b32: bit i of the result is bit (x_i << 2 | y_i << 1 | z_i) of lut."""
+    out = np.uint32(0)
+    for k in range(8):
+        if (lut >> k) & 1:
+            tx = x if k & 4 else ~x
+            ty = y if k & 2 else ~y
+            tz = z if k & 1 else ~z
+            out |= tx & ty & tz
+    return out & M32
+
+
 def rule(a, b, c, self_):
     t0 = a[0] ^ b[0] ^ c[0]
     k0 = maj(a[0], b[0], c[0])
     p = a[1] ^ b[1] ^ c[1]
     q = maj(a[1], b[1], c[1])
-    u1 = p ^ k0
-    u2 = q ^ (p & k0)
-    v = (u2 & self_ & ~t0) | (~u2 & t0)
-    return v & (u1 ^ u2) & M32
+    g1 = lop3(t0, self_, q, 0x53)
+    g2 = lop3(p, k0, q, 0x43)
+    return lop3(t0, g1, g2, 0x42)
 
 
 def next_state(alive, n):  # grid.cpp:22-28
     return int(n in (2, 3)) if alive else int(n == 3)
+
+
+def test_lop3_semantics():
+    x, y, z = np.uint32(0xF0F0F0F0), np.uint32(0xCCCCCCCC), np.uint32(0xAAAAAAAA)
+    for lut in (0x00, 0x42, 0x43, 0x53, 0x96, 0xE8, 0xFF):
+        assert int(lop3(x, y, z, lut)) == lut * 0x01010101
 
 
 def test_network_exhaustive_512_neighbourhoods():
