@@ -58,13 +58,14 @@ def measured_peaks() -> dict:
         return {}
 
 
-def ncu_traffic(config: int, depth: int):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def ncu_traffic(config: int, depth, engine: str = ""):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture
+    (key cfg{config}_k{depth}, byte engine cfg{config}_byte_k{depth})."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(f"cfg{config}_k{depth}")
+        return d.get(f"cfg{config}_{engine + '_' if engine else ''}k{depth}")
     except (OSError, ValueError):
         return None
 
@@ -550,6 +551,39 @@ def run_gpu_arm(args) -> None:
         dist.destroy_process_group()
 
 
+# byte_tb_kernel per 4-cell word (csrc/kernels.cuh byte_row_fma / byte_rule): ALU pipe --
+# 2 funnel shifts, (n|x)^3, ~y & m, >>7; FMA pipe (IMAD a*one+b) -- the adds h, hn, the
+# 3-way neighbour sum (2) and +0x7f7f7f7f.
+BYTE_ALU_OPS_PER_UPDATE = 5 / 4.0
+BYTE_FMA_OPS_PER_UPDATE = 5 / 4.0
+
+
+def byte_roofline(cell_updates: float, k: int, kern_ms: float, hbm_peak: float, int_ops: float,
+                  traffic) -> dict:
+    """Roofline of one byte-engine pass of depth k: HBM-bound at k = 1 (2 B per
+    cell-update); for k >= 2 instruction-bound: 1.25 ALU-pipe + 1.25 FMA-pipe
+    ops per cell-update, each pipe at the measured LOP3 lane rate P and one
+    instruction issued per cycle per sub-partition, so the peak of the mix is
+    2P lane-ops/s (bound P / 1.25 cell-updates/s)."""
+    t = kern_ms * 1e-3
+    hbm = {"achieved": 2.0 / k * cell_updates / t / 1e9, "peak": hbm_peak, "unit": "GB/s",
+           "bytes_per_cell_update": 2.0 / k}
+    hbm["frac"] = hbm["achieved"] / hbm_peak
+    if k == 1 or not int_ops:
+        return {"bound": "hbm", "kernel": "byte_step_kernel" if k == 1 else f"byte_tb_kernel<{k}>",
+                **hbm, "mean_launch_ms": kern_ms, "traffic": traffic}
+    ops = BYTE_ALU_OPS_PER_UPDATE + BYTE_FMA_OPS_PER_UPDATE
+    ach = cell_updates * ops / t / 1e12
+    peak = 2 * int_ops / 1e12
+    return {"bound": "int", "kernel": f"byte_tb_kernel<{k}>", "achieved": ach, "peak": peak,
+            "unit": "Tops/s", "frac": ach / peak, "ops_per_cell_update": ops,
+            "alu_ops_per_cell_update": BYTE_ALU_OPS_PER_UPDATE,
+            "fma_ops_per_cell_update": BYTE_FMA_OPS_PER_UPDATE,
+            "peak_source": "2 x measured LOP3 lane rate (ALU + FMA pipes, one issue per cycle)",
+            "roofline_updates_per_s": int_ops / BYTE_ALU_OPS_PER_UPDATE,
+            "hbm": hbm, "mean_launch_ms": kern_ms, "traffic": traffic}
+
+
 def run_byte_arm(args) -> None:
     """The byte engine (one generation per pass, 2 B of HBM per cell-update)
     on one GPU: config's grid, per-launch CUDA events, HBM roofline."""
@@ -577,17 +611,25 @@ def run_byte_arm(args) -> None:
     launches = []
     cur = [0]
 
+    depth = args.byte_depth or (6 if W * H >= 2 ** 26 else 4)
+    if W % 16:
+        depth = 1
+
     def step(record: bool):
-        for _ in range(gens):
+        done = 0
+        while done < gens:
+            k = min(depth, gens - done)
             a, b = bufs[cur[0]], bufs[cur[0] ^ 1]
             if record:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-            check(L.life_dev_byte_step(a.data_ptr(), pitch, 0, H, b.data_ptr(), pitch, 0, W, H, stream))
+            check(L.life_dev_byte_pass(a.data_ptr(), pitch, 0, H, b.data_ptr(), pitch, 0, W, H, k,
+                                       stream))
             if record:
                 e1.record()
-                launches.append((e0, e1))
+                launches.append((e0, e1, k))
             cur[0] ^= 1
+            done += k
 
     for _ in range(args.warmup):
         step(False)
@@ -606,11 +648,19 @@ def run_byte_arm(args) -> None:
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
     n_launch = int(L.life_kernel_launches() - l0)
-    kern_ms = sum(a.elapsed_time(b) for a, b in launches) / max(len(launches), 1)
+    full = [(a.elapsed_time(b), k) for a, b, k in launches if k == depth] or \
+        [(a.elapsed_time(b), k) for a, b, k in launches]
+    kern_ms = sum(t for t, _ in full) / len(full)
+    k_main = full[0][1]
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    achieved = 2.0 * W * H / (kern_ms * 1e-3) / 1e9
     value = W * H * gens * args.steps / (sum(ms) * 1e-3) / 1e9
+    int_ops = 0.0
+    if k_main > 1:
+        import ctypes as C
+        o, sec = C.c_double(), C.c_double()
+        if L.life_measure_int_peak(0, 4000, C.byref(o), C.byref(sec)) == 0:
+            int_ops = o.value
     e2e = None
     if not args.no_e2e:
         # The public API a user calls: Engine.upload (uint8 grid from pinned host
@@ -623,12 +673,12 @@ def run_byte_arm(args) -> None:
         steps_e2e = max(2, args.steps)
         with life.Engine(0) as eng:
             eng.upload(host)
-            eng.run(1, capi.ENGINE_BYTE)
+            eng.run(1, capi.ENGINE_BYTE, depth)
             eng.download(hout)
             t0 = time.perf_counter()
             for _ in range(steps_e2e):
                 eng.upload(host)
-                eng.run(gens, capi.ENGINE_BYTE)
+                eng.run(gens, capi.ENGINE_BYTE, depth)
                 eng.download(hout)
             e2e_s = time.perf_counter() - t0
         e2e = {"value": W * H * gens * steps_e2e / e2e_s / 1e9, "unit": UNIT,
@@ -647,12 +697,10 @@ def run_byte_arm(args) -> None:
         "warmup": args.warmup, "ms_per_step": sum(ms) / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u8 (byte per cell)", "data": "synthetic",
         "config": {"workload": cfg["desc"].replace("bit-packed engine", "byte engine"),
-                   "engine": "byte", "generations": gens,
+                   "engine": "byte", "generations": gens, "temporal_depth": depth,
                    "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
-        "roofline": {"bound": "hbm", "kernel": "byte_step_kernel", "achieved": achieved,
-                     "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak,
-                     "bytes_per_cell_update": 2.0, "mean_launch_ms": kern_ms,
-                     "traffic": ncu_traffic(args.config, 0)},
+        "roofline": byte_roofline(W * H * k_main, k_main, kern_ms, hbm_peak, int_ops,
+                                  ncu_traffic(args.config, k_main, "byte")),
         "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": n_launch, "clocks": clocks.summary()}), flush=True)
 
@@ -780,6 +828,8 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--engine", choices=["packed", "byte", "resident"], default="packed")
+    ap.add_argument("--byte-depth", type=int, default=0,
+                    help="byte engine generations per pass (0 = auto, 1 = HBM-bound single step)")
     ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
                     help="multi-GPU halo: in-kernel NVLink peer reads or NCCL send/recv")
     args = ap.parse_args()

@@ -51,7 +51,7 @@ extern "C" {
 /* Engines (the reference's Strategy::Kind dispatch, decomposition.hpp:31,
  * gains GPU kinds). */
 #define LIFE_ENGINE_PACKED 0 /* 64 cells/uint64, LOP3 adder network, temporal blocking */
-#define LIFE_ENGINE_BYTE 1   /* one byte per cell, one generation per pass */
+#define LIFE_ENGINE_BYTE 1   /* one byte per cell, SWAR sums, up to 8 generations per pass */
 /* Packed layout, whole torus resident in the shared memory of one thread-block
  * cluster (<= 16 CTAs), every generation in one launch: small tori with
  * W % 32 == 0 (LIFE_ERR_CONFIG otherwise).  LIFE_ENGINE_PACKED with
@@ -113,8 +113,8 @@ int life_population(life_ctx* ctx, uint64_t* out);
 /* ---- the step loop ------------------------------------------------------ */
 /* Replaces run(Grid&&, RunConfig, checkpoints) (engine.cpp:162-214):
  *   `generations` >= 0 (ConfigError otherwise, engine.cpp:133-136);
- *   `temporal_depth`: generations per packed kernel pass, 1..16, 0 = auto
- *     (the byte engine accepts 0 or 1);
+ *   `temporal_depth`: generations per kernel pass, 0 = auto; packed 1..16,
+ *     byte 1..8 (W % 16 == 0; other widths run one generation per pass);
  *   `checkpoints`: strictly ascending in [0, generations] (engine.cpp:137-147);
  *     `populations[i]` receives the population after checkpoints[i]
  *     generations (checkpoint 0 = the initial grid, engine.cpp:186).
@@ -192,6 +192,12 @@ int life_ipc_close(void* dev_ptr);
 int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
                        uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
                        int64_t out_rows, void* stream);
+/* `generations` (1..8) byte-engine generations in one pass (temporal blocking;
+ * more than one needs W % 16 == 0), same addressing as life_dev_byte_step;
+ * input relative rows -generations .. out_rows + generations are read. */
+int life_dev_byte_pass(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                       uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                       int64_t out_rows, int32_t generations, void* stream);
 /* Rows [y0, y0+rows) of random_fill(W, H, density, seed) into a packed buffer. */
 int life_dev_packed_random(uint32_t* out, int64_t pitch, int64_t width, int64_t y0,
                            int64_t rows, double density, uint64_t seed, void* stream);

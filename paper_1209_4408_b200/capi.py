@@ -26,6 +26,7 @@ ENGINE_PACKED = 0
 ENGINE_BYTE = 1
 ENGINE_RESIDENT = 2
 MAX_TEMPORAL_DEPTH = 16
+MAX_BYTE_DEPTH = 8
 
 # Every function the header declares: (name, restype, argtypes).
 _vp = C.c_void_p
@@ -69,6 +70,8 @@ SIGNATURES = [
     ("life_ipc_open", C.c_int, [_vp, C.POINTER(_vp)]),
     ("life_ipc_close", C.c_int, [_vp]),
     ("life_dev_byte_step", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
+    ("life_dev_byte_pass", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i32,
+                                     _vp]),
     ("life_dev_packed_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),
     ("life_dev_byte_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),
     ("life_dev_packed_population", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),

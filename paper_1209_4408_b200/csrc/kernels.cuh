@@ -635,6 +635,7 @@ struct ByteStepArgs {
   int64_t seg_rows;
   int32_t nv;        // ceil(width / 16) vectors per row
   int32_t n_strips;  // ceil(nv / 30)
+  uint32_t one;      // 1 (byte_tb_kernel's adds: a * one + b issues on the FMA pipe)
 };
 
 constexpr int kByteThreads = 128;
@@ -688,6 +689,14 @@ __device__ __forceinline__ void st_global_v4_if(void* p, const uint32_t (&o)[4],
       "{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n"
       " @q st.global.v4.u32 [%0], {%1, %2, %3, %4};\n}\n" ::"l"(p),
       "r"(o[0]), "r"(o[1]), "r"(o[2]), "r"(o[3]), "r"(static_cast<uint32_t>(pred))
+      : "memory");
+}
+
+__device__ __forceinline__ void st_global_v2_if(void* p, uint32_t a, uint32_t b, bool pred) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.u32 q, %3, 0;\n"
+      " @q st.global.v2.u32 [%0], {%1, %2};\n}\n" ::"l"(p),
+      "r"(a), "r"(b), "r"(static_cast<uint32_t>(pred))
       : "memory");
 }
 
@@ -828,6 +837,171 @@ __global__ void __launch_bounds__(kByteThreads) byte_step_kernel(const ByteStepA
   } else {
     byte_pass<false>(a, lane, vi, y0, rows, ring);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Temporal-blocked byte engine: K generations per pass over the byte layout
+// (W % 16 == 0, so the torus column wrap is an index wrap of 16-byte
+// vectors).  The register pipeline of packed_tb_kernel with SWAR bytes: each
+// lane owns 16 cells (one uint4) of a row; stage g keeps the (h, hn, x) byte
+// sums of its 3-row window and turns the generation-g row stream into
+// generation g+1; stage g eats what stage g-1 emitted on the previous step
+// (skewed), so the K stages of a step are independent instruction chains.
+// Lanes 0 and 31 are ghosts: K <= 8 generations corrupt at most K bytes at
+// the outer end of their vectors, so lane 0 still holds 8 valid high bytes
+// and lane 31 8 valid low bytes; strips advance by 31 vectors and the shared
+// vector is stored as two 8-byte halves.  HBM traffic per cell-update: 2/K B.  Restates
+// compute_region (engine.cpp:17-48) x K generations.
+// ---------------------------------------------------------------------------
+constexpr int kByteTbMaxDepth = 8;
+constexpr int kByteTbStride = 31;  // vectors per strip: 30 whole + 2 shared halves
+#ifndef LIFE_BYTE_TB_PF
+#define LIFE_BYTE_TB_PF 4
+#endif
+constexpr int kByteTbPF = LIFE_BYTE_TB_PF;
+constexpr int kByteTbSmem = (kByteThreads / 32) * 2 * kByteTbPF * 32 * 16;  // per block
+
+// a + b as a * one + b: `one` is a runtime 1 (kernel argument) the compiler
+// cannot fold, so the add issues as IMAD on the FMA pipe and leaves the ALU
+// pipe -- the bound of byte_tb_kernel -- to the shifts and logic ops.
+__device__ __forceinline__ uint32_t add_fma(uint32_t a, uint32_t b, uint32_t one) {
+  uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(one), "r"(b));
+  return d;
+}
+
+// Horizontal byte sums of one 16-cell vector (byte_row with the adds on the
+// FMA pipe): per word 2 funnel shifts (ALU) + 2 IMAD.  `lw` / `rw` are the
+// whole neighbouring words (left lane's x[3], right lane's x[0]): the funnel
+// shifts take the byte they need.
+__device__ __forceinline__ void byte_row_fma(const uint32_t (&x)[4], uint32_t lw, uint32_t rw,
+                                             uint32_t one, uint32_t (&h)[4], uint32_t (&hn)[4]) {
+  uint32_t r[4], l[4];
+  r[0] = __funnelshift_r(x[0], x[1], 8);
+  r[1] = __funnelshift_r(x[1], x[2], 8);
+  r[2] = __funnelshift_r(x[2], x[3], 8);
+  r[3] = __funnelshift_r(x[3], rw, 8);
+  l[0] = __funnelshift_l(lw, x[0], 8);
+  l[1] = __funnelshift_l(x[0], x[1], 8);
+  l[2] = __funnelshift_l(x[1], x[2], 8);
+  l[3] = __funnelshift_l(x[2], x[3], 8);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    hn[i] = add_fma(l[i], r[i], one);
+    h[i] = add_fma(hn[i], x[i], one);
+  }
+}
+
+// (n | self) == 3 per byte (engine.cpp:32 on 0/1 bytes, n = 8-neighbour count):
+// t = (n | self) ^ 3 is 0..15 per byte; alive iff t == 0, via bit 7 of t + 0x7f.
+// 3 ALU ops (LOP3, SHF, LOP3) + 3 IMAD per 4 cells.
+__device__ __forceinline__ uint32_t byte_rule(uint32_t up_h, uint32_t dn_h, uint32_t mid_hn,
+                                              uint32_t mid_x, uint32_t one) {
+  const uint32_t t = (add_fma(add_fma(up_h, dn_h, one), mid_hn, one) | mid_x) ^ 0x03030303u;
+  return (~add_fma(t, 0x7f7f7f7fu, one) & 0x80808080u) >> 7;  // one LOP3 (~y & m) + SHF
+}
+
+template <int K>
+__global__ void __launch_bounds__(kByteThreads) byte_tb_kernel(const ByteStepArgs a) {
+  constexpr int PF = kByteTbPF;
+  constexpr int kLag = 3 * K - 1;  // output row j leaves the pipeline at step j + kLag
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kByteThreads + threadIdx.x) >> 5;
+  const int strip = static_cast<int>(gwarp % a.n_strips);
+  const int64_t seg = gwarp / a.n_strips;
+  const int64_t y0 = seg * a.seg_rows;
+  if (y0 >= a.out_rows) return;  // warp-uniform
+  const int n = static_cast<int>(min(a.seg_rows, a.out_rows - y0));
+  const int64_t vi = static_cast<int64_t>(strip) * kByteTbStride + lane - 1;
+  int64_t src = vi % a.nv;
+  if (src < 0) src += a.nv;
+  // Lanes 1..30 store whole vectors; lane 31 the low 8 bytes and lane 0 the
+  // high 8 bytes of the vectors shared with the neighbouring strips (K <= 8
+  // generations corrupt at most 8 bytes at each end of the warp).
+  const bool in_grid = vi >= 0 && vi < a.nv;
+  const bool store_mid = in_grid && lane >= 1 && lane <= 30;
+  const bool store_lo = in_grid && lane == 31;
+  const bool store_hi = in_grid && lane == 0;
+  const uint32_t one = a.one;
+  extern __shared__ uint4 byte_tb_ring[];
+  uint4* ring = byte_tb_ring + (threadIdx.x >> 5) * (2 * PF * 32) + lane;
+
+  const int in_rows = static_cast<int>(a.in_rows);
+  int lrow = static_cast<int>(wrap_row(a.in_row0, y0 - K, a.in_rows));
+  const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch);
+  const char* const in_lane = reinterpret_cast<const char*>(a.in + src * 16);
+  auto issue = [&](int slot) {
+    cp_async16(reinterpret_cast<uint32_t*>(ring + slot * 32),
+               row_addr(in_lane, static_cast<uint32_t>(lrow), in_pitch_b));
+    cp_async_commit();
+    lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
+  };
+  const uint32_t out_pitch_b = static_cast<uint32_t>(a.out_pitch);
+  char* const out_lane = reinterpret_cast<char*>(a.out + (a.out_row0 + y0) * a.out_pitch + vi * 16);
+
+#pragma unroll
+  for (int u = 0; u < PF; ++u) issue(u);
+  // Stage state: up.h, mid.h, mid.hn, mid.x (4 words each); xin[g] = stage g's input row.
+  uint32_t uh[K][4], mh[K][4], mhn[K][4], mx[K][4], xin[K][4];
+#pragma unroll
+  for (int g = 0; g < K; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) uh[g][i] = mh[g][i] = mhn[g][i] = mx[g][i] = xin[g][i] = 0u;
+
+  const int trips = (n + kLag + PF - 1) / PF;
+  int half = 0;
+  auto trip = [&](const int t, auto steady_tag) {
+    constexpr bool STEADY = decltype(steady_tag)::value;
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      issue((half ^ PF) + u);
+      cp_async_wait<PF>();
+      {
+        const uint4 v = ring[(half + u) * 32];
+        xin[0][0] = v.x;
+        xin[0][1] = v.y;
+        xin[0][2] = v.z;
+        xin[0][3] = v.w;
+      }
+      uint32_t y_last[4];
+      // Top stage first: stage g reads xin[g] and writes xin[g+1], which
+      // stage g+1 has already consumed this step.
+#pragma unroll
+      for (int g = K - 1; g >= 0; --g) {
+        const uint32_t lw = __shfl_up_sync(kFull, xin[g][3], 1);
+        const uint32_t rw = __shfl_down_sync(kFull, xin[g][0], 1);
+        uint32_t h[4], hn[4];
+        byte_row_fma(xin[g], lw, rw, one, h, hn);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t o = byte_rule(uh[g][i], h[i], mhn[g][i], mx[g][i], one);
+          uh[g][i] = mh[g][i];
+          mh[g][i] = h[i];
+          mhn[g][i] = hn[i];
+          mx[g][i] = xin[g][i];
+          if (g + 1 < K) {
+            xin[g + 1][i] = o;
+          } else {
+            y_last[i] = o;
+          }
+        }
+      }
+      const int j = t * PF + u - kLag;
+      const bool in_seg = STEADY || static_cast<unsigned>(j) < static_cast<unsigned>(n);
+      char* const p = const_cast<char*>(row_addr(out_lane, static_cast<uint32_t>(j), out_pitch_b));
+      st_global_v4_if(p, y_last, in_seg && store_mid);
+      st_global_v2_if(p, y_last[0], y_last[1], in_seg && store_lo);
+      st_global_v2_if(p + 8, y_last[2], y_last[3], in_seg && store_hi);
+    }
+    half ^= PF;
+  };
+  const int steady_begin = (kLag + PF - 1) / PF;
+  const int steady_end = (n + kLag) / PF;
+  int t = 0;
+  for (; t < trips && (t < steady_begin || t >= steady_end); ++t) trip(t, std::false_type{});
+  for (; t < steady_end; ++t) trip(t, std::true_type{});
+  for (; t < trips; ++t) trip(t, std::false_type{});
+  cp_async_wait<0>();
 }
 
 // ---------------------------------------------------------------------------

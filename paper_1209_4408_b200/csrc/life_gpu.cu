@@ -557,6 +557,83 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
   return LIFE_OK;
 }
 
+}  // extern "C"
+
+namespace {
+template <int K>
+int launch_byte_tb(ByteStepArgs a, cudaStream_t s) {
+  static int blocks_per_sm[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (blocks_per_sm[dev & 63] == 0) {
+    int nb = 0;
+    LIFE_CUDA(cudaFuncSetAttribute(byte_tb_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kByteTbSmem));
+    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, byte_tb_kernel<K>, kByteThreads,
+                                                            kByteTbSmem));
+    blocks_per_sm[dev & 63] = std::max(nb, 1);
+  }
+  // Segments long enough to amortise the 3K-1 step pipeline fill: one wave
+  // of independent warps.
+  const int64_t resident_warps =
+      static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kByteThreads / 32) * sm_count();
+  static const int waves = [] {
+    const char* e = std::getenv("LIFE_BYTE_TB_WAVES");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 1;  // 1 wave: 8.41 vs 8.02 T/s (2) at 16384^2, K = 6
+  }();
+  const int64_t segs_target = std::max<int64_t>(1, waves * resident_warps / a.n_strips);
+  a.seg_rows = std::max<int64_t>(ceil_div(a.out_rows, segs_target), 16 * K);
+  const int64_t warps = ceil_div(a.out_rows, a.seg_rows) * a.n_strips;
+  const int64_t blocks = ceil_div(warps, kByteThreads / 32);
+  if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
+  byte_tb_kernel<K><<<static_cast<unsigned>(blocks), kByteThreads, kByteTbSmem, s>>>(a);
+  LIFE_CHECK_LAUNCH("byte_tb_kernel");
+  return LIFE_OK;
+}
+using ByteTbLauncher = int (*)(ByteStepArgs, cudaStream_t);
+const ByteTbLauncher kByteTbLaunchers[kByteTbMaxDepth + 1] = {
+    nullptr, nullptr, launch_byte_tb<2>, launch_byte_tb<3>, launch_byte_tb<4>,
+    launch_byte_tb<5>, launch_byte_tb<6>, launch_byte_tb<7>, launch_byte_tb<8>};
+}  // namespace
+
+extern "C" {
+
+int life_dev_byte_pass(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                       uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                       int64_t out_rows, int32_t generations, void* stream) {
+  if (generations < 1 || generations > kByteTbMaxDepth)
+    return set_error(LIFE_ERR_CONFIG, "byte temporal depth must be in [1, %d], got %d",
+                     kByteTbMaxDepth, generations);
+  if (generations == 1)
+    return life_dev_byte_step(in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
+                              out_rows, stream);
+  if (width % 16 != 0)
+    return set_error(LIFE_ERR_CONFIG,
+                     "byte passes of more than one generation need W %% 16 == 0, got W = %lld",
+                     static_cast<long long>(width));
+  if (width < 1 || in_rows < 1 || out_rows < 0 || in_pitch < width || out_pitch < width ||
+      (in_pitch & 15) || (out_pitch & 15))
+    return set_error(LIFE_ERR_CONFIG, "bad byte pass geometry");
+  if (out_rows == 0) return LIFE_OK;
+  if (in_rows >= (int64_t(1) << 31) || in_pitch >= (int64_t(1) << 32) ||
+      out_pitch >= (int64_t(1) << 32) || out_rows >= (int64_t(1) << 31))
+    return set_error(LIFE_ERR_CONFIG, "grid too large for the byte engine");
+  ByteStepArgs a{};
+  a.in = in;
+  a.in_pitch = in_pitch;
+  a.in_row0 = in_row0;
+  a.in_rows = in_rows;
+  a.out = out;
+  a.out_pitch = out_pitch;
+  a.out_row0 = out_row0;
+  a.width = width;
+  a.out_rows = out_rows;
+  a.nv = static_cast<int32_t>(width / 16);
+  a.n_strips = static_cast<int32_t>(ceil_div(a.nv + 1, kByteTbStride));
+  a.one = 1;
+  return kByteTbLaunchers[generations](a, static_cast<cudaStream_t>(stream));
+}
+
 int life_dev_packed_random(uint32_t* out, int64_t pitch, int64_t width, int64_t y0, int64_t rows,
                            double density, uint64_t seed, void* stream) {
   if (!(density >= 0.0 && density <= 1.0))
@@ -775,6 +852,11 @@ int engine_layout(int engine) { return engine == LIFE_ENGINE_BYTE ? kByte : kPac
 // small tori (W % 32 == 0, at most kResidentAutoCells cells) where it beats
 // the multi-pass engine (measured), else K = 16 passes.
 constexpr int64_t kResidentAutoCells = int64_t(1) << 22;
+// temporal_depth 0 on the byte engine (W % 16 == 0).  Sweep (T cell-updates/s,
+// K = 1..8): 16384^2 2.78 5.09 6.52 6.83 6.88 7.28 7.10 7.31; 4096^2 2.03 3.22
+// 3.02 3.78 3.36 3.22 2.97 2.70 (short grids pay the 3K-1 step pipeline fill).
+int byte_auto_depth(int64_t w, int64_t h) { return w * h >= (int64_t(1) << 26) ? 6 : 4; }
+
 bool resident_auto(int64_t w, int64_t h) {
   return w % 32 == 0 && w * h <= kResidentAutoCells && life_resident_cluster_size(w, h) > 0;
 }
@@ -1087,9 +1169,13 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
                        static_cast<long long>(c->W), static_cast<long long>(c->H));
     if (depth == 0) depth = LIFE_MAX_TEMPORAL_DEPTH;
   } else {
-    if (depth != 0 && depth != 1)
-      return set_error(LIFE_ERR_CONFIG, "the byte engine runs one generation per pass (depth 0/1)");
-    depth = 1;
+    // Byte engine: K generations per pass (byte_tb_kernel) when W % 16 == 0;
+    // other widths run one generation per pass whatever the depth asks.
+    if (depth < 0 || depth > kByteTbMaxDepth)
+      return set_error(LIFE_ERR_CONFIG, "byte engine temporal depth must be in [0, %d], got %d",
+                       kByteTbMaxDepth, temporal_depth);
+    if (depth == 0) depth = byte_auto_depth(c->W, c->H);
+    if (c->W % 16 != 0) depth = 1;
   }
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   LIFE_TRY(to_layout(c, engine_layout(engine)));
@@ -1123,8 +1209,8 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
       c->pk_cur = nxt;
     } else {
       const int nxt = c->by_cur ^ 1;
-      LIFE_TRY(life_dev_byte_step(c->by[c->by_cur], c->by_pitch, 0, c->H, c->by[nxt],
-                                  c->by_pitch, 0, c->W, c->H, c->stream));
+      LIFE_TRY(life_dev_byte_pass(c->by[c->by_cur], c->by_pitch, 0, c->H, c->by[nxt],
+                                  c->by_pitch, 0, c->W, c->H, step, c->stream));
       c->by_cur = nxt;
     }
     done += step;

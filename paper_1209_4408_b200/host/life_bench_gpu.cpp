@@ -1,6 +1,6 @@
 // life-bench-gpu: the reference's CLI (tools/life_bench.cpp) on the B200 engine.
 //
-//   life-bench-gpu run   --width W --height H --iterations N [--strategy gpu|gpu:K|gpu-byte]
+//   life-bench-gpu run   --width W --height H --iterations N [--strategy gpu|gpu:K|gpu-byte[:K]|gpu-resident]
 //                        [--workers 1] [--pattern FILE.rle|FILE.cells | --seed S --density P]
 //                        [--render none|ascii|pbm] [--out PATH] [--checkpoints a,b,c]
 //   life-bench-gpu bench [--sizes 120x60,240x120] [--iterations 500,1000,2000]
@@ -133,7 +133,7 @@ Options parse_options(int argc, char** argv, int first, const std::set<std::stri
 
 const char* kUsage =
     "life-bench-gpu: Game of Life on the B200 engine (the reference's life-bench CLI)\n"
-    "  run   --width W --height H --iterations N [--strategy gpu|gpu:K|gpu-byte] [--workers 1]\n"
+    "  run   --width W --height H --iterations N [--strategy gpu|gpu:K|gpu-byte[:K]|gpu-resident] [--workers 1]\n"
     "        [--pattern FILE.rle|FILE.cells | --seed S --density P] [--render none|ascii|pbm]\n"
     "        [--out PATH] [--checkpoints a,b,c] [--device D]\n"
     "  bench [--sizes WxH,...] [--iterations a,b] [--strategies gpu,gpu:8,gpu-byte] [--workers 1]\n"

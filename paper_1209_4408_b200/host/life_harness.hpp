@@ -44,14 +44,18 @@ struct Strategy {
 };
 
 inline std::string to_string(const Strategy& s) {
-  if (s.engine == Engine::Byte) return "gpu-byte";
+  if (s.engine == Engine::Byte) return s.depth == 0 ? "gpu-byte" : "gpu-byte:" + std::to_string(s.depth);
   if (s.engine == Engine::Resident) return "gpu-resident";
   return s.depth == 0 ? "gpu" : "gpu:" + std::to_string(s.depth);
 }
 
 inline Strategy parse_strategy(const std::string& token) {
   if (token == "gpu") return {Engine::Packed, 0};
-  if (token == "gpu-byte") return {Engine::Byte, 1};
+  if (token == "gpu-byte") return {Engine::Byte, 0};
+  if (token.rfind("gpu-byte:", 0) == 0) {
+    const std::string k = token.substr(9);
+    if (k.size() == 1 && k[0] >= '1' && k[0] <= '8') return {Engine::Byte, k[0] - '0'};
+  }
   if (token == "gpu-resident") return {Engine::Resident, 0};
   if (token.rfind("gpu:", 0) == 0) {
     const std::string k = token.substr(4);
@@ -61,7 +65,7 @@ inline Strategy parse_strategy(const std::string& token) {
     }
   }
   throw ConfigError("unknown strategy '" + token +
-                    "' (expected gpu, gpu:K with K in 1..16, gpu-byte or gpu-resident)");
+                    "' (expected gpu, gpu:K with K in 1..16, gpu-byte, gpu-byte:K with K in 1..8 or gpu-resident)");
 }
 
 inline double speedup(double baseline_s, double other_s) {

@@ -142,8 +142,8 @@ class Strategy:
     generations per kernel pass (0 = auto: the cluster-resident engine for
     small tori with W % 32 == 0, else 16); `gpu_resident` keeps the whole
     torus in one thread-block cluster's shared memory and runs every
-    generation in one launch; `gpu_byte` runs the byte-per-cell engine, one
-    generation per pass."""
+    generation in one launch; `gpu_byte` runs the byte-per-cell engine,
+    `depth` (1..8, 0 = auto: 4) generations per pass when W % 16 == 0, else one."""
 
     kind: str = "gpu_packed"
     blocks_x: int = 1
@@ -155,8 +155,8 @@ class Strategy:
         return Strategy("gpu_packed", 1, 1, depth)
 
     @staticmethod
-    def gpu_byte() -> "Strategy":
-        return Strategy("gpu_byte", 1, 1, 1)
+    def gpu_byte(depth: int = 0) -> "Strategy":
+        return Strategy("gpu_byte", 1, 1, depth)
 
     @staticmethod
     def gpu_resident() -> "Strategy":
@@ -176,7 +176,7 @@ def to_string(strategy: Strategy) -> str:
     """Strategy token (decomposition.cpp:51-66 style): gpu, gpu:K, gpu-byte,
     gpu-resident."""
     if strategy.kind == "gpu_byte":
-        return "gpu-byte"
+        return "gpu-byte" if strategy.depth == 0 else f"gpu-byte:{strategy.depth}"
     if strategy.kind == "gpu_resident":
         return "gpu-resident"
     return "gpu" if strategy.depth == 0 else f"gpu:{strategy.depth}"
@@ -190,14 +190,17 @@ def parse_strategy(token: str) -> Strategy:
         return Strategy.gpu_byte()
     if token == "gpu-resident":
         return Strategy.gpu_resident()
-    if token.startswith("gpu:"):
-        try:
-            k = int(token[4:])
-        except ValueError:
-            k = -1
-        if 1 <= k <= capi.MAX_TEMPORAL_DEPTH:
-            return Strategy.gpu_packed(k)
-    raise ConfigError(f"unknown strategy '{token}' (expected gpu, gpu:K (1..16), gpu-byte or gpu-resident)")
+    for prefix, limit, make in (("gpu:", capi.MAX_TEMPORAL_DEPTH, Strategy.gpu_packed),
+                                ("gpu-byte:", capi.MAX_BYTE_DEPTH, Strategy.gpu_byte)):
+        if token.startswith(prefix):
+            try:
+                k = int(token[len(prefix):])
+            except ValueError:
+                k = -1
+            if 1 <= k <= limit:
+                return make(k)
+    raise ConfigError(f"unknown strategy '{token}' (expected gpu, gpu:K (1..16), gpu-byte, "
+                      "gpu-byte:K (1..8) or gpu-resident)")
 
 
 @dataclass

@@ -40,8 +40,16 @@ def test_gpu_arm_line():
     assert j["roofline"]["bound"] == "int" and 0 < j["roofline"]["frac"] < 1.2
     assert j["e2e"]["h2d_bytes_per_step"] == 1024 * 16 * 8 and j["e2e"]["value"] > 0
     assert j["cpu_baseline"]["value"] > 0
-    b = run_bench("--engine", "byte", "--config", "1", "--steps", "3", "--warmup", "3")
+    b = run_bench("--engine", "byte", "--config", "1", "--steps", "3", "--warmup", "3",
+                  "--byte-depth", "1", "--no-cpu")
     assert b["roofline"]["bound"] == "hbm" and b["value"] > 0
+    b = run_bench("--engine", "byte", "--config", "1", "--steps", "3", "--warmup", "3", "--no-cpu")
+    assert b["roofline"]["bound"] == "int" and b["config"]["temporal_depth"] == 4
+    assert b["e2e"]["value"] > 0 and 0 < b["roofline"]["frac"] < 1.0
+    r = run_bench("--engine", "resident", "--config", "1", "--steps", "3", "--warmup", "3",
+                  "--no-cpu")
+    assert r["config"]["cluster_ctas"] >= 1 and r["value"] > 0 and r["e2e"]["value"] > 0
+    assert 0 < r["roofline"]["frac"] < 1.0 and r["gpu_launches"] == 3
 
 
 @pytest.mark.gpu

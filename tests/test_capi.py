@@ -82,6 +82,8 @@ def test_grid_contract_errors():
     assert g.wrap(5, 4) == (0, 0) and g.wrap(-1, -1) == (4, 3) and g.wrap(12, -9) == (2, 3)
     assert life.parse_strategy("gpu:8") == life.Strategy.gpu_packed(8)
     assert life.to_string(life.parse_strategy("gpu-byte")) == "gpu-byte"
+    assert life.to_string(life.parse_strategy("gpu-byte:3")) == "gpu-byte:3"
+    assert life.to_string(life.parse_strategy("gpu-resident")) == "gpu-resident"
     with pytest.raises(life.ConfigError):
         life.parse_strategy("gpu:17")
     with pytest.raises(life.ConfigError):

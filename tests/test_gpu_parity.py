@@ -58,7 +58,7 @@ def test_packed_upload_ignores_tail_bits(engine, oracle):
 
 
 @pytest.mark.parametrize("eng,depth", [(PACKED, 1), (PACKED, 4), (PACKED, 7), (PACKED, 16),
-                                       (BYTE, 1)])
+                                       (BYTE, 1), (BYTE, 3), (BYTE, 8), (BYTE, 0)])
 def test_small_golden_cases(engine, oracle, golden_small, eng, depth):
     for case in golden_small["small_cases"]:
         engine.init_random(case["w"], case["h"], case["density"], case["seed"], eng)
@@ -71,7 +71,7 @@ def test_small_golden_cases(engine, oracle, golden_small, eng, depth):
 
 def test_cfg1_full_grid_at_1_10_100(engine, oracle, golden_small):
     cfg1 = golden_small["cfg1"]
-    for eng, depth in [(PACKED, 16), (PACKED, 5), (BYTE, 1)]:
+    for eng, depth in [(PACKED, 16), (PACKED, 5), (BYTE, 1), (BYTE, 4), (BYTE, 7)]:
         engine.init_random(1024, 1024, 0.5, 42, eng)
         pops = engine.run(100, eng, depth, [0, 1, 10, 100])
         assert pops == [524027, 286720, 211733, 98161]
@@ -134,9 +134,10 @@ def test_depth_transparency_sweep(engine, oracle):
             engine.upload(g)
             engine.run(41, PACKED, depth)
             assert np.array_equal(engine.download(), want), (seed, depth)
-        engine.upload(g)
-        engine.run(41, BYTE, 1)
-        assert np.array_equal(engine.download(), want)
+        for depth in range(1, 9):
+            engine.upload(g)
+            engine.run(41, BYTE, depth)
+            assert np.array_equal(engine.download(), want), (seed, "byte", depth)
 
 
 @pytest.mark.parametrize("w,h", [(128, 3), (128, 5), (256, 31), (1024, 97), (3968, 40),
@@ -181,7 +182,7 @@ def test_run_config_errors(engine):
         engine.init_random(5, 5, 1.5, 1)
     engine.init_random(5, 5, 0.5, 1)
     with pytest.raises(life.ConfigError):
-        engine.run(3, BYTE, 4)
+        engine.run(3, BYTE, 9)
     with pytest.raises(life.ConfigError):
         engine.run(3, PACKED, 17)
     r = life.run(g, life.RunConfig(life.Strategy.gpu_packed(), 1, 0), [0])
@@ -217,7 +218,7 @@ def _check_schedule(engine, oracle, gold, eng, depth, init):
 @pytest.mark.slow
 def test_cfg2_16384_1000_generations(engine, oracle):
     gold = load_golden("golden_cfg2.json")
-    for eng, depth in [(BYTE, 1), (PACKED, 16), (PACKED, 8)]:
+    for eng, depth in [(BYTE, 1), (BYTE, 4), (PACKED, 16), (PACKED, 8)]:
         _check_schedule(engine, oracle, gold, eng, depth,
                         lambda: engine.init_random(16384, 16384, 0.3, 42, eng))
 

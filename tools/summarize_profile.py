@@ -25,7 +25,7 @@ def to_bytes(k):
     return g(k, f)
 
 rd, wr = to_bytes("dram__bytes_read.sum"), to_bytes("dram__bytes_write.sum")
-dur_ms = g("gpu__time_duration.sum")
+dur_ms = g("gpu__time_duration.sum", {"usecond": 1e-3, "us": 1e-3, "nsecond": 1e-6, "ns": 1e-6}.get(u.get("gpu__time_duration.sum", "msecond"), 1.0))
 lines = [f"# ncu summary: {os.path.basename(rep)} ({m.get('Kernel Name', '')})", ""]
 lines.append("| metric | value |")
 lines.append("|---|---|")
