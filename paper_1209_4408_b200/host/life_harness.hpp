@@ -152,7 +152,7 @@ inline BenchRecord time_run(const TimingSpec& spec) {
     upload();  // outside the timed region, like the reference's grid copy
     // The first run on a byte upload converts to the packed layout inside
     // life_run; do that conversion outside the timer as well.
-    if (e == Engine::Packed) ctx.run(0, e, spec.strategy.depth, {});
+    if (e != Engine::Byte) ctx.run(0, e, spec.strategy.depth, {});
     const auto t0 = std::chrono::steady_clock::now();
     ctx.run(spec.iterations, e, spec.strategy.depth, {});
     rec.all_times_s.push_back(
@@ -275,9 +275,11 @@ inline std::string emit_csv(const std::vector<BenchRecord>& records) {
   return out;
 }
 
-// Roofline of a record: the packed engine is integer-bound (11 ops / 32
-// cell-updates against the measured LOP3 peak), the byte engine HBM-bound
-// (2 bytes per cell-update against the measured copy bandwidth).
+// Roofline of a record: the packed engines are integer-bound (11 ops / 32
+// cell-updates against the measured LOP3 peak of the whole GPU), the byte
+// engine HBM-bound at one generation per pass (2 bytes per cell-update
+// against the measured copy bandwidth) and instruction-bound when
+// temporally blocked.
 struct RooflinePeaks {
   double int_ops_per_s = 0.0;  // life_measure_int_peak
   double hbm_bytes_per_s = 6553.3e9;
@@ -285,7 +287,13 @@ struct RooflinePeaks {
 
 inline double roofline_fraction(const BenchRecord& r, const RooflinePeaks& p) {
   const double ups = r.gcups() * 1e9;
-  if (r.strategy.engine == Engine::Byte) return p.hbm_bytes_per_s > 0 ? ups * 2.0 / p.hbm_bytes_per_s : 0.0;
+  if (r.strategy.engine == Engine::Byte) {
+    // One generation per pass: HBM-bound (2 B per update); temporal-blocked
+    // passes (W % 16 == 0): 1.25 ALU + 1.25 FMA ops per update at 2x the LOP3 rate.
+    if (r.strategy.depth == 1 || r.width % 16 != 0)
+      return p.hbm_bytes_per_s > 0 ? ups * 2.0 / p.hbm_bytes_per_s : 0.0;
+    return p.int_ops_per_s > 0 ? ups * 2.5 / (2.0 * p.int_ops_per_s) : 0.0;
+  }
   return p.int_ops_per_s > 0 ? ups * (11.0 / 32.0) / p.int_ops_per_s : 0.0;
 }
 

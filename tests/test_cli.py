@@ -78,7 +78,11 @@ def test_run_reports_checkpoints_and_final_population(cli, oracle):
 def test_run_renders_glider_lap_to_stdout_with_summary_on_stderr(cli, tmp_path):
     p = tmp_path / "glider.rle"
     p.write_text("x = 3, y = 3\nbo$2bo$3o!")
-    for strat in ("gpu", "gpu-byte"):
+    # the cluster-resident engine needs W % 32 == 0: a 64x64 lap (256 generations)
+    r = run(cli, "run", "--width", "64", "--height", "64", "--iterations", "256",
+            "--strategy", "gpu-resident", "--pattern", p)
+    assert r.returncode == 0 and "final population 5 after 256 generations" in r.stdout + r.stderr
+    for strat in ("gpu", "gpu-byte", "gpu-byte:5"):
         r = run(cli, "run", "--width", "16", "--height", "16", "--iterations", "64",
                 "--strategy", strat, "--pattern", p, "--render", "ascii")
         assert r.returncode == 0
@@ -105,15 +109,16 @@ def test_run_writes_pbm_to_out(cli, tmp_path):
 @pytest.mark.gpu
 def test_bench_emits_pinned_csv(cli, tmp_path):
     csv = tmp_path / "m.csv"
-    r = run(cli, "bench", "--sizes", "64x32,40x40", "--iterations", "4,8", "--strategies",
-            "gpu,gpu:4,gpu-byte", "--repetitions", "2", "--warmup", "0", "--csv", csv)
+    r = run(cli, "bench", "--sizes", "64x32,96x40", "--iterations", "4,8", "--strategies",
+            "gpu,gpu:4,gpu-byte,gpu-byte:3,gpu-resident", "--repetitions", "2", "--warmup", "0",
+            "--csv", csv)
     assert r.returncode == 0, r.stderr
     lines = csv.read_text().strip().splitlines()
     assert lines[0] == ("width,height,iterations,strategy,workers,seed,density,repetitions,"
                         "median_s,speedup,hardware_threads,final_population")
     rows = [l.split(",") for l in lines[1:]]
-    assert len(rows) == 2 * 2 * 3
-    assert [r[3] for r in rows[:3]] == ["gpu", "gpu:4", "gpu-byte"]
+    assert len(rows) == 2 * 2 * 5
+    assert [r[3] for r in rows[:5]] == ["gpu", "gpu:4", "gpu-byte", "gpu-byte:3", "gpu-resident"]
     assert rows[0][9] == "1.00"                        # baseline row
     pops = {(r[0], r[1], r[2]) for r in rows}
     for key in pops:                                   # same final population for every engine
