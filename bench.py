@@ -837,12 +837,19 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
-    ap.add_argument("--engine", choices=["packed", "byte", "resident"], default="packed")
+    ap.add_argument("--engine", choices=["auto", "packed", "byte", "resident"], default="auto",
+                    help="auto: the cluster-resident engine for small W %% 32 == 0 tori on one "
+                         "GPU (config 1, as life_run's depth-0 auto mode), else packed")
     ap.add_argument("--byte-depth", type=int, default=0,
                     help="byte engine generations per pass (0 = auto, 1 = HBM-bound single step)")
     ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
                     help="multi-GPU halo: in-kernel NVLink peer reads or NCCL send/recv")
     args = ap.parse_args()
+    if args.engine == "auto":
+        c = CONFIGS[args.config]
+        small = c["w"] % 32 == 0 and c["w"] * c["h"] <= 2 ** 22
+        args.engine = "resident" if small and int(os.environ.get("WORLD_SIZE", "1")) == 1 \
+            else "packed"
     if args.impl == "reference":
         run_reference_arm(args)
     elif args.engine == "byte":

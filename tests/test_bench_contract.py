@@ -31,7 +31,8 @@ def test_reference_arm_line():
 
 @pytest.mark.gpu
 def test_gpu_arm_line():
-    j = run_bench("--config", "1", "--steps", "3", "--warmup", "3", "--cpu-budget", "1")
+    j = run_bench("--config", "1", "--engine", "packed", "--steps", "3", "--warmup", "3",
+                  "--cpu-budget", "1")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
               "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
               "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
@@ -46,8 +47,7 @@ def test_gpu_arm_line():
     b = run_bench("--engine", "byte", "--config", "1", "--steps", "3", "--warmup", "3", "--no-cpu")
     assert b["roofline"]["bound"] == "int" and b["config"]["temporal_depth"] == 4
     assert b["e2e"]["value"] > 0 and 0 < b["roofline"]["frac"] < 1.0
-    r = run_bench("--engine", "resident", "--config", "1", "--steps", "3", "--warmup", "3",
-                  "--no-cpu")
+    r = run_bench("--config", "1", "--steps", "3", "--warmup", "3", "--no-cpu")  # auto -> resident
     assert r["config"]["cluster_ctas"] >= 1 and r["value"] > 0 and r["e2e"]["value"] > 0
     assert 0 < r["roofline"]["frac"] < 1.0 and r["gpu_launches"] == 3
 
