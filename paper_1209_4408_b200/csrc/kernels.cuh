@@ -567,6 +567,12 @@ packed_tb_kernel(const PackedStepArgs a) {
 #endif
   extern __shared__ uint32_t ring_smem[];
   uint32_t* ring = ring_smem + (threadIdx.x >> 5) * (2 * PackedTraits<K>::kPrefetch * 96) + lane;
+  // Programmatic dependent launch: the previous pass's grid must be complete
+  // (and its writes visible) before the first read of our input rows; the
+  // next pass may be scheduled as soon as we start (it waits the same way).
+  // Both are no-ops for launches without the PDL attribute.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
   int trips = 0;
   if (n > 0) {
     // General path for W < 32 and (peer mode) tiles whose rows reach past
@@ -925,6 +931,8 @@ __global__ void __launch_bounds__(kByteThreads) byte_tb_kernel(const ByteStepArg
   const uint32_t one = a.one;
   extern __shared__ uint4 byte_tb_ring[];
   uint4* ring = byte_tb_ring + (threadIdx.x >> 5) * (2 * PF * 32) + lane;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: previous pass complete
+  asm volatile("griddepcontrol.launch_dependents;");
 
   const int in_rows = static_cast<int>(a.in_rows);
   int lrow = static_cast<int>(wrap_row(a.in_row0, y0 - K, a.in_rows));
@@ -1068,6 +1076,8 @@ __global__ void __launch_bounds__(kStep1Threads) packed_step1_kernel(const Step1
   const bool store = lane >= 1 && lane <= kStep1Stride && vi < a.nv;
   extern __shared__ uint4 step1_ring[];
   uint4* ring = step1_ring + (threadIdx.x >> 5) * (2 * PF * 32) + lane;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: previous pass complete
+  asm volatile("griddepcontrol.launch_dependents;");
 
   const int in_rows = static_cast<int>(a.in_rows);
   int lrow = static_cast<int>(wrap_row(a.in_row0, y0 - 1, a.in_rows));

@@ -92,6 +92,36 @@ uint64_t density_threshold(double density) {
 #endif
 constexpr int kSyncTrips = LIFE_SYNC_TRIPS;
 
+// Programmatic dependent launch (PDL): consecutive passes on a stream
+// overlap the next grid's launch with this one's tail; the kernels wait on
+// griddepcontrol.wait before their first read.  LIFE_PDL=0 disables it.
+// Measured with packed_tb_kernel<16> (T/s, 320 generations): 4096^2 9.45 ->
+// 10.0, 8192^2 23.1 -> 23.9, 16384^2 36.1 -> 36.7, 65536^2 unchanged.
+bool pdl_enabled() {
+  static const bool pdl = [] {
+    const char* e = std::getenv("LIFE_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return pdl;
+}
+
+template <typename Kernel, typename Args>
+int launch_pdl(Kernel kernel, unsigned blocks, unsigned threads, size_t smem, cudaStream_t s,
+               const Args& args) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  LIFE_CUDA(cudaLaunchKernelEx(&cfg, kernel, args));
+  return LIFE_OK;
+}
+
 template <int K>
 int launch_packed(PackedStepArgs a, cudaStream_t s) {
   // Per device: warps per block = every warp one SM holds (register-limited),
@@ -164,7 +194,8 @@ int launch_packed(PackedStepArgs a, cudaStream_t s) {
   a.sync_every = a.peer ? 1 : kSyncTrips;
   const int64_t blocks = ceil_div(tiles, wpb);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
-  packed_tb_kernel<K><<<static_cast<unsigned>(blocks), 32 * wpb, wpb * PackedTraits<K>::kRingBytes, s>>>(a);
+  LIFE_TRY(launch_pdl(packed_tb_kernel<K>, static_cast<unsigned>(blocks), 32 * wpb,
+                      static_cast<size_t>(wpb) * PackedTraits<K>::kRingBytes, s, a));
   LIFE_CHECK_LAUNCH("packed_tb_kernel");
   return LIFE_OK;
 }
@@ -257,7 +288,8 @@ int launch_step1(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t 
   const int64_t warps = ceil_div(out_rows, a.seg_rows) * a.n_strips;
   const int64_t blocks = ceil_div(warps, kStep1Threads / 32);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
-  packed_step1_kernel<<<static_cast<unsigned>(blocks), kStep1Threads, kStep1Smem, stream>>>(a);
+  LIFE_TRY(launch_pdl(packed_step1_kernel, static_cast<unsigned>(blocks), kStep1Threads,
+                      kStep1Smem, stream, a));
   LIFE_CHECK_LAUNCH("packed_step1_kernel");
   return LIFE_OK;
 }
@@ -586,7 +618,8 @@ int launch_byte_tb(ByteStepArgs a, cudaStream_t s) {
   const int64_t warps = ceil_div(a.out_rows, a.seg_rows) * a.n_strips;
   const int64_t blocks = ceil_div(warps, kByteThreads / 32);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
-  byte_tb_kernel<K><<<static_cast<unsigned>(blocks), kByteThreads, kByteTbSmem, s>>>(a);
+  LIFE_TRY(launch_pdl(byte_tb_kernel<K>, static_cast<unsigned>(blocks), kByteThreads,
+                      kByteTbSmem, s, a));
   LIFE_CHECK_LAUNCH("byte_tb_kernel");
   return LIFE_OK;
 }
