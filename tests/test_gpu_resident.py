@@ -98,3 +98,40 @@ def test_resident_rejects_unfit_tori(engine):
     engine.run(3, PACKED, 0)
     with pytest.raises(life.ConfigError):
         engine.run(3, RESIDENT, 17)
+
+
+def test_device_layer_entry_points(oracle):
+    """The device-buffer entry points of the two new engines: the resident run
+    in place (in == out), and byte passes of depth > 1 (W % 16 == 0 only)."""
+    import torch
+
+    from paper_1209_4408_b200 import capi, life
+    L = capi.lib()
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    W, H, G = 256, 48, 21
+    g = oracle.random_fill(W, H, 0.4, 3)
+    want, _ = oracle.run(g, G)
+    pitch = int(L.life_packed_pitch_words(W))
+    host = np.zeros((H, pitch), np.uint32)
+    host[:, : W // 32] = oracle.pack(g).view(np.uint32)[:, : W // 32]
+    buf = torch.from_numpy(host.view(np.int32)).to(dev)
+    life.check(L.life_dev_packed_run_resident(buf.data_ptr(), buf.data_ptr(), pitch, W, H, G,
+                                              stream))
+    torch.cuda.synchronize()
+    got = buf.cpu().numpy().view(np.uint32)[:, : W // 32].copy()
+    assert np.array_equal(got, oracle.pack(want).view(np.uint32)[:, : W // 32])
+    # byte passes: K = 5 in one launch == 5 oracle generations; W % 16 != 0 -> ConfigError
+    bp = int(L.life_byte_pitch(W))
+    hb = np.zeros((H, bp), np.uint8)
+    hb[:, :W] = g
+    a = torch.from_numpy(hb).to(dev)
+    b = torch.zeros_like(a)
+    life.check(L.life_dev_byte_pass(a.data_ptr(), bp, 0, H, b.data_ptr(), bp, 0, W, H, 5, stream))
+    torch.cuda.synchronize()
+    want5, _ = oracle.run(g, 5)
+    assert np.array_equal(b.cpu().numpy()[:, :W], want5)
+    assert L.life_dev_byte_pass(a.data_ptr(), bp, 0, H, b.data_ptr(), bp, 0, W - 8, H, 2,
+                                stream) == capi.ERR_CONFIG
+    assert L.life_dev_byte_pass(a.data_ptr(), bp, 0, H, b.data_ptr(), bp, 0, W, H, 9,
+                                stream) == capi.ERR_CONFIG
