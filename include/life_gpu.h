@@ -109,6 +109,11 @@ int life_grid_window_u8(life_ctx* ctx, int64_t x0, int64_t y0, int64_t w, int64_
 int life_grid_dims(life_ctx* ctx, int64_t* width, int64_t* height);
 /* Replaces population (grid.cpp:40-46), widened to uint64. */
 int life_population(life_ctx* ctx, uint64_t* out);
+/* Full-grid checksum for parity checks of grids too big to download (SURVEY
+ * 8(b) `grid_hash`): FNV-1a-64 over the H row hashes (8 little-endian bytes
+ * each), row hash = FNV-1a-64 over the row's ceil(W/64) packed uint64 words
+ * (little-endian bytes, tail bits zero).  Rows hash in parallel on the device. */
+int life_grid_hash(life_ctx* ctx, uint64_t* out);
 
 /* ---- the step loop ------------------------------------------------------ */
 /* Replaces run(Grid&&, RunConfig, checkpoints) (engine.cpp:162-214):
@@ -207,6 +212,13 @@ int life_dev_byte_random(uint8_t* out, int64_t pitch, int64_t width, int64_t y0,
 /* Adds the population of `rows` packed rows to *dev_count (device uint64). */
 int life_dev_packed_population(const uint32_t* grid, int64_t pitch, int64_t width,
                                int64_t rows, uint64_t* dev_count, void* stream);
+/* Row hashes of life_grid_hash for `rows` packed rows (into device memory);
+ * chain them on the host with life_fnv1a64 (bands: concatenate in row order). */
+int life_dev_packed_row_hashes(const uint32_t* grid, int64_t pitch, int64_t width,
+                               int64_t rows, uint64_t* dev_hashes, void* stream);
+/* FNV-1a-64 (offset 0xcbf29ce484222325, prime 0x100000001b3) of n host bytes,
+ * continuing from h (0 = start). */
+uint64_t life_fnv1a64(const void* bytes, int64_t n, uint64_t h);
 /* Packs byte rows (nonzero -> 1) into packed rows and back. */
 int life_dev_pack(const uint8_t* cells, int64_t cell_pitch, uint32_t* words, int64_t pitch,
                   int64_t width, int64_t rows, void* stream);

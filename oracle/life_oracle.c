@@ -281,6 +281,22 @@ uint64_t orc_fnv1a64(const uint8_t* bytes, int64_t n, uint64_t h) {
   return h;
 }
 
+/* life_grid_hash's definition (include/life_gpu.h; not a reference function:
+ * the checksum of row checksums that lets the device hash rows in
+ * parallel): FNV-1a-64 over the H row hashes (8 little-endian bytes each),
+ * row hash = FNV-1a-64 over the row's wpr packed uint64 words. */
+uint64_t orc_grid_hash(const uint64_t* words, int64_t wpr, int64_t height) {
+  uint8_t* rows = (uint8_t*)malloc((size_t)height * 8);
+  if (!rows) return 0;
+  for (int64_t y = 0; y < height; ++y) {
+    const uint64_t r = orc_fnv1a64((const uint8_t*)(words + y * wpr), wpr * 8, 0);
+    for (int i = 0; i < 8; ++i) rows[y * 8 + i] = (uint8_t)(r >> (8 * i));
+  }
+  const uint64_t h = orc_fnv1a64(rows, height * 8, 0);
+  free(rows);
+  return h;
+}
+
 /*
  * Packs a W x H byte grid into the packed exchange format of
  * include/life_gpu.h: row-major rows of ceil(W/64) little-endian uint64

@@ -57,6 +57,8 @@ class Oracle:
         L.orc_lightcone.argtypes = [_u8p, C.c_int64, C.c_int64, _u8p]
         L.orc_fnv1a64.argtypes = [C.c_void_p, C.c_int64, C.c_uint64]
         L.orc_fnv1a64.restype = C.c_uint64
+        L.orc_grid_hash.argtypes = [_u64p, C.c_int64, C.c_int64]
+        L.orc_grid_hash.restype = C.c_uint64
         L.orc_pack.argtypes = [_u8p, C.c_int64, C.c_int64, _u64p]
         L.orc_unpack.argtypes = [_u64p, C.c_int64, C.c_int64, _u8p]
         L.orc_band_bounds.argtypes = [C.c_int64, C.c_int32, _i64p]
@@ -129,6 +131,16 @@ class Oracle:
     def fnv1a64(self, data: np.ndarray) -> int:
         data = np.ascontiguousarray(data)
         return int(self.lib.orc_fnv1a64(data.ctypes.data, data.nbytes, 0))
+
+    def grid_hash(self, g: np.ndarray) -> int:
+        """life_grid_hash's definition on a byte grid (packs it first)."""
+        p = self.pack(g)
+        return int(self.lib.orc_grid_hash(p, p.shape[1], p.shape[0]))
+
+    def packed_hash(self, words: np.ndarray) -> int:
+        """The same on packed rows (uint64, ceil(W/64) words per row)."""
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        return int(self.lib.orc_grid_hash(words, words.shape[1], words.shape[0]))
 
     def pack(self, g: np.ndarray) -> np.ndarray:
         g = np.ascontiguousarray(g, dtype=np.uint8)

@@ -51,6 +51,7 @@ SIGNATURES = [
     ("life_grid_window_u8", C.c_int, [_vp, _i64, _i64, _i64, _i64, _vp]),
     ("life_grid_dims", C.c_int, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
     ("life_population", C.c_int, [_vp, C.POINTER(_u64)]),
+    ("life_grid_hash", C.c_int, [_vp, C.POINTER(_u64)]),
     ("life_run", C.c_int, [_vp, _i64, C.c_int, C.c_int, _vp, _i32, _vp]),
     ("life_step", C.c_int, [_vp, C.c_int]),
     ("life_run_batch", C.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _i64, C.c_int,
@@ -75,6 +76,8 @@ SIGNATURES = [
     ("life_dev_packed_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),
     ("life_dev_byte_random", C.c_int, [_vp, _i64, _i64, _i64, _i64, C.c_double, _u64, _vp]),
     ("life_dev_packed_population", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    ("life_dev_packed_row_hashes", C.c_int, [_vp, _i64, _i64, _i64, _vp, _vp]),
+    ("life_fnv1a64", _u64, [_vp, _i64, _u64]),
     ("life_dev_pack", C.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
     ("life_dev_unpack", C.c_int, [_vp, _i64, _vp, _i64, _i64, _i64, _vp]),
     ("life_measure_int_peak", C.c_int, [C.c_int, _i64, C.POINTER(C.c_double),

@@ -1561,6 +1561,31 @@ __global__ void byte_popcount_kernel(const uint8_t* __restrict__ cells, int64_t 
   block_add_u64(acc, count);
 }
 
+// FNV-1a-64 of every packed row's bytes (2*ceil(W/64) little-endian uint32
+// words of the device layout = the ceil(W/64) uint64 words of the exchange
+// format, tail bits zero): the per-row half of life_grid_hash, a checksum of
+// row checksums -- FNV itself is sequential, so rows hash in parallel and the
+// host chains the H row hashes.  One thread per row.
+__global__ void packed_row_hash_kernel(const uint32_t* __restrict__ words, int64_t pitch,
+                                       int32_t nwords, int64_t rows,
+                                       unsigned long long* __restrict__ out) {
+  for (int64_t r = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; r < rows;
+       r += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t* row = words + r * pitch;
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (int32_t k = 0; k < nwords; ++k) {
+      uint32_t v = __ldg(row + k);
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        h ^= (v & 0xffu);
+        h *= 0x100000001b3ULL;
+        v >>= 8;
+      }
+    }
+    out[r] = h;
+  }
+}
+
 // Wrapped window of a packed grid as 0/1 bytes.
 __global__ void packed_window_kernel(const uint32_t* __restrict__ words, int64_t pitch,
                                      int64_t width, int64_t height, int64_t x0, int64_t y0,

@@ -702,6 +702,28 @@ int life_dev_packed_population(const uint32_t* grid, int64_t pitch, int64_t widt
   return LIFE_OK;
 }
 
+int life_dev_packed_row_hashes(const uint32_t* grid, int64_t pitch, int64_t width, int64_t rows,
+                               uint64_t* dev_hashes, void* stream) {
+  if (!grid || !dev_hashes || width < 1 || rows < 0 || pitch < 2 * ceil_div(width, 64))
+    return set_error(LIFE_ERR_CONFIG, "bad row-hash geometry");
+  if (rows == 0) return LIFE_OK;
+  packed_row_hash_kernel<<<grid_stride_blocks(rows, 128), 128, 0, static_cast<cudaStream_t>(stream)>>>(
+      grid, pitch, static_cast<int32_t>(2 * ceil_div(width, 64)), rows,
+      reinterpret_cast<unsigned long long*>(dev_hashes));
+  LIFE_CHECK_LAUNCH("packed_row_hash_kernel");
+  return LIFE_OK;
+}
+
+uint64_t life_fnv1a64(const void* bytes, int64_t n, uint64_t h) {
+  const uint8_t* p = static_cast<const uint8_t*>(bytes);
+  if (h == 0) h = 0xcbf29ce484222325ULL;
+  for (int64_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 0x100000001b3ULL;
+  }
+  return h;
+}
+
 int life_dev_pack(const uint8_t* cells, int64_t cell_pitch, uint32_t* words, int64_t pitch,
                   int64_t width, int64_t rows, void* stream) {
   const int64_t warps = rows * ceil_div(pitch, 32);
@@ -768,6 +790,8 @@ struct life_ctx {
   int by_cur = 0;
   unsigned long long* counts = nullptr;
   int64_t counts_cap = 0;
+  uint64_t* row_hashes = nullptr;  // life_grid_hash scratch (H entries)
+  int64_t row_hashes_cap = 0;
   uint8_t* window = nullptr;
   int64_t window_cap = 0;
   // life_run_batch: 2 slots x (upload/ping, pong) buffers and copy streams
@@ -927,6 +951,7 @@ int life_ctx_destroy(life_ctx* c) {
   cudaStreamSynchronize(c->stream);
   free_buffers(c);
   if (c->counts) cudaFree(c->counts);
+  if (c->row_hashes) cudaFree(c->row_hashes);
   if (c->window) cudaFree(c->window);
   for (auto& b : c->batch)
     if (b) cudaFree(b);
@@ -1165,6 +1190,27 @@ int life_population(life_ctx* c, uint64_t* out) {
   LIFE_TRY(population_async(c, c->counts));
   LIFE_CUDA(cudaMemcpyAsync(out, c->counts, 8, cudaMemcpyDeviceToHost, c->stream));
   LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  return LIFE_OK;
+}
+
+int life_grid_hash(life_ctx* c, uint64_t* out) {
+  LIFE_TRY(activate(c));
+  if (!out) return set_error(LIFE_ERR_CONFIG, "null output pointer");
+  if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
+  LIFE_TRY(to_layout(c, kPacked));
+  if (c->H > c->row_hashes_cap) {
+    if (c->row_hashes) cudaFree(c->row_hashes);
+    c->row_hashes = nullptr;
+    LIFE_CUDA(cudaMalloc(&c->row_hashes, sizeof(uint64_t) * c->H));
+    c->row_hashes_cap = c->H;
+  }
+  LIFE_TRY(life_dev_packed_row_hashes(c->pk[c->pk_cur], c->pk_pitch, c->W, c->H, c->row_hashes,
+                                      c->stream));
+  std::vector<uint64_t> rows(static_cast<size_t>(c->H));
+  LIFE_CUDA(cudaMemcpyAsync(rows.data(), c->row_hashes, sizeof(uint64_t) * c->H,
+                            cudaMemcpyDeviceToHost, c->stream));
+  LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  *out = life_fnv1a64(rows.data(), static_cast<int64_t>(rows.size() * sizeof(uint64_t)), 0);
   return LIFE_OK;
 }
 

@@ -323,6 +323,12 @@ class Engine:
         check(self._lib.life_population(self._ctx, C.byref(v)))
         return int(v.value)
 
+    def hash(self) -> int:
+        """life_grid_hash: FNV-1a-64 of the packed rows' FNV-1a-64 hashes."""
+        v = C.c_uint64()
+        check(self._lib.life_grid_hash(self._ctx, C.byref(v)))
+        return int(v.value)
+
     # -- the step loop ----------------------------------------------------
     def run(self, generations: int, engine: int = capi.ENGINE_PACKED, depth: int = 0,
             checkpoints: Sequence[int] = ()) -> list[int]:

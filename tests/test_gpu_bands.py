@@ -131,3 +131,44 @@ def test_peer_driver_ipc_two_processes_one_gpu(oracle):
     want, pops = oracle.run(oracle.random_fill(W, H, 0.4, 5), gens, [gens])
     assert np.array_equal(got, want)
     assert parts[0][2] == pops[0]
+
+
+@pytest.mark.slow
+def test_cfg5_full_grid_hash_across_band_decompositions():
+    """the full 262144^2 grid hash after 32 generations
+    is the same for the whole torus (one context) and for 2 / 8 row bands
+    with in-kernel peer halos (emulated on one GPU), via life_grid_hash's row
+    hashes (life_dev_packed_row_hashes + life_fnv1a64)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1209_4408_b200 import capi, life
+    from paper_1209_4408_b200.bands import LocalPeerBands
+    W = H = 262144
+    G = 32
+    L = capi.lib()
+    with life.Engine(0) as e:
+        e.init_random(W, H, 0.4, 42)
+        e.run(G, capi.ENGINE_PACKED, 16)
+        want = e.hash()
+    torch.cuda.empty_cache()
+    dev = torch.device("cuda", 0)
+    for P in (2, 8):
+        lb = LocalPeerBands(W, H, P, 16, dev)
+        lb.init_random(0.4, 42)
+        lb.run(G)
+        rows = torch.empty(H, dtype=torch.int64, device=dev)
+        at = 0
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        for bb in lb.bufs:
+            band = bb[lb.cur]
+            n = band.shape[0]
+            life.check(L.life_dev_packed_row_hashes(band.data_ptr(), band.shape[1], W, n,
+                                                    rows[at:].data_ptr(), stream))
+            at += n
+        host = rows.cpu().numpy()
+        got = L.life_fnv1a64(host.ctypes.data, host.nbytes, 0)
+        assert got == want, P
+        del lb
+        torch.cuda.empty_cache()

@@ -340,3 +340,13 @@ def test_device_place_pattern(engine, oracle):
     engine.upload(np.zeros((5, 5), np.uint8))
     with pytest.raises(life.OutOfBounds):
         engine.place(np.ones((3, 3), np.uint8), 3, 0)
+
+
+def test_grid_hash_matches_oracle(engine, oracle):
+    for (w, h, p, s) in [(3, 3, 0.5, 1), (64, 9, 0.4, 2), (1000, 37, 0.3, 3), (4096, 64, 0.5, 4)]:
+        g = oracle.random_fill(w, h, p, s)
+        for eng in (PACKED, BYTE):
+            engine.upload(g)
+            engine.run(3, eng, 0)
+            want, _ = oracle.run(g, 3)
+            assert engine.hash() == oracle.grid_hash(want), (w, h, eng)

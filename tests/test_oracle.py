@@ -183,3 +183,24 @@ def test_place_pattern_vs_reference(oracle, reference):
         oracle.place_pattern(np.zeros((5, 5), np.uint8), np.ones((3, 3), np.uint8), 3, 0)
     with pytest.raises(RuntimeError):
         reference.place_pattern(np.zeros((5, 5), np.uint8), np.ones((3, 3), np.uint8), 3, 0)
+
+
+def test_grid_hash_definition(oracle):
+    """life_grid_hash's definition (checksum of packed-row FNV-1a-64 checksums)
+    restated in pure Python on small grids, including a tail word."""
+    import numpy as np
+
+    def fnv(bs, h=0xcbf29ce484222325):
+        for b in bs:
+            h = ((h ^ b) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+        return h
+    for (w, h, seed) in [(3, 3, 1), (64, 5, 2), (65, 7, 3), (130, 4, 4)]:
+        g = oracle.random_fill(w, h, 0.5, seed)
+        words = oracle.pack(g)
+        rows = b"".join(fnv(words[y].tobytes()).to_bytes(8, "little") for y in range(h))
+        assert oracle.grid_hash(g) == fnv(rows) == oracle.packed_hash(words)
+    # any single-cell change changes it
+    g = oracle.random_fill(100, 9, 0.5, 5)
+    g2 = g.copy()
+    g2[4, 77] ^= 1
+    assert oracle.grid_hash(g) != oracle.grid_hash(g2)
