@@ -120,6 +120,12 @@ class Context {
     check(life_population(ctx_, &p));
     return p;
   }
+  // Full-grid checksum (life_grid_hash) for grids too big to download.
+  uint64_t hash() {
+    uint64_t h = 0;
+    check(life_grid_hash(ctx_, &h));
+    return h;
+  }
   std::vector<uint8_t> window(int64_t x0, int64_t y0, int64_t w, int64_t h) {
     std::vector<uint8_t> out(static_cast<size_t>(w * h));
     check(life_grid_window_u8(ctx_, x0, y0, w, h, out.data()));

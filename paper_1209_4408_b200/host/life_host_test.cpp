@@ -153,6 +153,19 @@ int main() {
     return p > (uint64_t(1) << 30) && win.size() == 49;
   });
 
+  check_case("resident and byte engines agree with the packed engine (grid hash)", [] {
+    lifegpu::Context ctx(0);
+    uint64_t h[3];
+    const lifegpu::Engine engines[3] = {lifegpu::Engine::Packed, lifegpu::Engine::Resident,
+                                        lifegpu::Engine::Byte};
+    for (int i = 0; i < 3; ++i) {
+      ctx.init_random(512, 384, 0.4, 9, engines[i]);
+      ctx.run(77, engines[i], 0, {});
+      h[i] = ctx.hash();
+    }
+    return h[0] == h[1] && h[1] == h[2];
+  });
+
   std::printf("%d failure(s)\n", failures);
   return failures == 0 ? 0 : 1;
 }
