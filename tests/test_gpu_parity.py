@@ -350,3 +350,29 @@ def test_grid_hash_matches_oracle(engine, oracle):
             engine.run(3, eng, 0)
             want, _ = oracle.run(g, 3)
             assert engine.hash() == oracle.grid_hash(want), (w, h, eng)
+
+
+def test_random_shape_fuzz_all_engines(engine, oracle):
+    """Seeded fuzz over shapes, engines and depths (packed K = 0..16, byte
+    K = 0..8, resident where it fits), including word-boundary widths and
+    3-row tori: every case bit-exact against the oracle."""
+    from paper_1209_4408_b200 import capi
+    rng = np.random.default_rng(20261020)
+    RES = 2
+    widths = [3, 5, 31, 32, 33, 63, 64, 65, 95, 96, 127, 128, 129, 160, 255, 256, 257, 1000, 1024]
+    for case in range(160):
+        w = int(rng.choice(widths)) if case % 2 else int(rng.integers(3, 400))
+        h = int(rng.integers(3, 90))
+        gens = int(rng.integers(0, 60))
+        g = oracle.random_fill(w, h, float(rng.uniform(0.1, 0.7)), case)
+        want, _ = oracle.run(g, gens)
+        kind = case % 3
+        if kind == 0:
+            eng, depth = PACKED, int(rng.integers(0, 17))
+        elif kind == 1:
+            eng, depth = BYTE, int(rng.integers(0, 9))
+        else:
+            eng, depth = (RES, 0) if capi.lib().life_resident_cluster_size(w, h) else (PACKED, 0)
+        engine.upload(g)
+        engine.run(gens, eng, depth)
+        assert np.array_equal(engine.download(), want), (case, w, h, gens, eng, depth)
