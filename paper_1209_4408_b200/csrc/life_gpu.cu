@@ -1413,9 +1413,16 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   g.depth = depth;
   g.passes = static_cast<int>(ceil_div(generations, depth));
   // Chunked first/last grid when every chunk outlives its shrinking
-  // trapezoid with room to spare.
-  const bool trap = n >= 1 && generations > 0 &&
+  // trapezoid with room to spare and the chunks are tall enough for their
+  // passes to run near full speed (the schedule launches 2 x 16 small passes
+  // per pass): measured e2e / device value, 3 grids, with / without it:
+  // config 5 (16384-row chunks) 0.965 / 0.882, config 3 (4096-row chunks)
+  // 0.850 / 0.945.  LIFE_BATCH_TRAP=0 / 1 forces it off / on (when it fits).
+  const char* trap_var = std::getenv("LIFE_BATCH_TRAP");  // read per call (tests force it)
+  const int trap_env = trap_var ? std::atoi(trap_var) : -1;
+  const bool fits = n >= 1 && generations > 0 &&
                     height / kTrapChunks >= 2 * kShrink * g.passes + 1024;
+  const bool trap = fits && (trap_env == 1 || (trap_env != 0 && height / kTrapChunks >= 8192));
   if (trap) {
     LIFE_TRY(life_band_bounds(height, kTrapChunks, g.bounds));
     for (auto& st : c->cs)

@@ -287,7 +287,18 @@ def test_run_batch_pipelined(engine, oracle):
 def test_run_batch_banded(engine, oracle, W, H, G, depth):
     """life_run_batch on taller grids: several waves of row tiles per pass, W % 32 != 0,
     G not a multiple of the depth, G = 0, more grids than buffer slots; H >= 32768 runs
-    the first and last grid as 16 chunk trapezoids + boundary triangles."""
+    the first and last grid as 16 chunk trapezoids + boundary triangles (forced with
+    LIFE_BATCH_TRAP=1: by default only chunks of >= 8192 rows take it)."""
+    import os
+    if H >= 32768:
+        os.environ["LIFE_BATCH_TRAP"] = "1"
+    try:
+        _run_batch_banded(engine, oracle, W, H, G, depth)
+    finally:
+        os.environ.pop("LIFE_BATCH_TRAP", None)
+
+
+def _run_batch_banded(engine, oracle, W, H, G, depth):
     grids = [oracle.random_fill(W, H, 0.35, 100 + i) for i in range(3)]
     ins = [oracle.pack(g) for g in grids]
     outs = [np.zeros_like(p) for p in ins]
