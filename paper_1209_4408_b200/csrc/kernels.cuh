@@ -1131,22 +1131,25 @@ __global__ void __launch_bounds__(kStep1Threads) packed_step1_kernel(const Step1
 // 16 CTAs, one per SM) and a single launch runs every generation.  CTA k of
 // the cluster owns the row band band_bounds(H, C)[k] (decomposition.cpp:12-24,
 // the paper's 1-D row decomposition) plus one halo row above and below,
-// double-buffered in its shared memory.  Per generation:
-//   __syncthreads          (this CTA's generation-g rows are complete)
-//   interior rows 1..B-2   (own rows only; overlaps the cluster barrier)
-//   barrier.cluster.wait   (the neighbours have pushed our generation-g
-//                           halo rows, and finished reading generation g-1)
-//   edge rows 0 and B-1    (local reads; each result is also stored into
-//                           the neighbour's halo row over DSMEM)
-//   barrier.cluster.arrive (release: our pushes of generation g+1)
-// No load crosses the cluster on the critical path: pushes are fire-and-
-// forget stores ordered by the barrier.  This replaces the per-generation
-// WorkerTeam barrier (engine.cpp:79-96) with the hardware cluster barrier,
-// and the HBM round trip of every pass with shared memory: small grids
-// (config 1) are latency-bound in the multi-pass engine (one launch and a
-// grid-wide dependency per K generations), here they are bound by the
-// cluster barrier and the ALU work of 16 SMs.  Same rule network as
-// packed_tb_kernel; the torus column wrap is an index wrap (W % 32 == 0).
+// double-buffered in its shared memory.  Warp roles: edge warps compute band
+// rows 0 and B-1, interior warps rows 1..B-2.  Per generation g:
+//   __syncthreads            (this CTA's generation-g band rows are complete)
+//   interior warps: rows 1..B-2 from own rows only
+//   edge warps: mbarrier wait for the generation-g halo rows the neighbours
+//     pushed, then rows 0 and B-1; each result is also pushed into the
+//     neighbour's halo row of the next buffer with
+//     st.async.shared::cluster.mbarrier::complete_tx (a DSMEM store that
+//     completes the receiver's mbarrier transaction count)
+// Each mbarrier phase is armed two generations ahead, before the push that
+// lets the neighbours produce it; no CTA reads another's shared memory, so
+// the only cross-SM latency on the critical path is the push.  One cluster
+// barrier at the start (every CTA running before any push).  This replaces
+// the per-generation WorkerTeam barrier (engine.cpp:79-96) with point-to-point
+// DSMEM signalling, and the HBM round trip of every pass with shared memory:
+// small grids (config 1) are latency-bound in the multi-pass engine (a launch
+// and a grid-wide dependency per K generations); here the push chain and the
+// ALU work of 16 SMs bound them.  Same rule network as packed_tb_kernel; the
+// torus column wrap is an index wrap (W % 32 == 0).
 // ---------------------------------------------------------------------------
 struct ResidentArgs {
   const uint32_t* in;
