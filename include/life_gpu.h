@@ -134,7 +134,9 @@ int life_step(life_ctx* ctx, int engine);
  * engine and downloaded to outputs[i] (may alias inputs[i]).  The H2D copy of
  * grid i+1 and the D2H copy of grid i-1 overlap the compute of grid i (copy
  * engines); tall grids run their first and last grid as 16 row-chunk
- * trapezoids plus boundary triangles so those copies overlap compute too.
+ * trapezoids plus boundary triangles so those copies overlap compute too;
+ * temporal_depth 0 on a small W % 32 == 0 torus runs each grid on the
+ * cluster-resident engine (one launch per grid).
  * Use pinned host memory for the overlap.
  * *elapsed_ms (optional) = CUDA-event time from the first upload to the last
  * download.  The context's resident grid is not touched. */

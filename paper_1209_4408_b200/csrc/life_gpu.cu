@@ -1422,7 +1422,11 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   const int trap_env = trap_var ? std::atoi(trap_var) : -1;
   const bool fits = n >= 1 && generations > 0 &&
                     height / kTrapChunks >= 2 * kShrink * g.passes + 1024;
-  const bool trap = fits && (trap_env == 1 || (trap_env != 0 && height / kTrapChunks >= 8192));
+  // temporal_depth 0 on a small W % 32 == 0 torus: the cluster-resident engine
+  // (as life_run's auto mode), one launch per grid.
+  const bool resident = temporal_depth == 0 && resident_auto(width, height);
+  const bool trap = !resident && fits &&
+                    (trap_env == 1 || (trap_env != 0 && height / kTrapChunks >= 8192));
   if (trap) {
     LIFE_TRY(life_band_bounds(height, kTrapChunks, g.bounds));
     for (auto& st : c->cs)
@@ -1476,12 +1480,17 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
       packed_mask_tail_kernel<<<grid_stride_blocks(mask_n, 256), 256, 0, c->stream>>>(
           buf[0], pitch, nw, tail_mask(width), height);
       LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
-      for (int p = 0; p < P && rc == LIFE_OK; ++p) rc = pass_rows(g, buf, p, 0, height, c->stream);
+      if (resident) {  // small torus: every generation in one cluster-resident launch
+        rc = life_dev_packed_run_resident(buf[0], buf[1], pitch, width, height, generations,
+                                          c->stream);
+      } else {
+        for (int p = 0; p < P && rc == LIFE_OK; ++p) rc = pass_rows(g, buf, p, 0, height, c->stream);
+      }
       LIFE_CUDA(cudaEventRecord(comp[i], c->stream));
       // Download on the D2H stream.
       LIFE_CUDA(cudaStreamWaitEvent(c->d2h, comp[i], 0));
-      LIFE_CUDA(cudaMemcpy2DAsync(outputs[i], words_per_row * 8, buf[P & 1], pitch * 4, wpr * 8,
-                                  height, cudaMemcpyDeviceToHost, c->d2h));
+      LIFE_CUDA(cudaMemcpy2DAsync(outputs[i], words_per_row * 8, buf[resident ? 1 : (P & 1)],
+                                  pitch * 4, wpr * 8, height, cudaMemcpyDeviceToHost, c->d2h));
       LIFE_CUDA(cudaEventRecord(down[i], c->d2h));
       continue;
     }

@@ -135,3 +135,25 @@ def test_device_layer_entry_points(oracle):
                                 stream) == capi.ERR_CONFIG
     assert L.life_dev_byte_pass(a.data_ptr(), bp, 0, H, b.data_ptr(), bp, 0, W, H, 9,
                                 stream) == capi.ERR_CONFIG
+
+
+def test_run_batch_small_tori_take_the_resident_engine(engine, oracle):
+    """life_run_batch with temporal_depth 0 on small W % 32 == 0 tori: one
+    resident launch per grid, copies overlapped; every grid equals the oracle
+    (also G = 0 and in place)."""
+    from paper_1209_4408_b200 import capi
+    W, H = 1024, 96
+    grids = [oracle.random_fill(W, H, 0.3 + 0.1 * i, 50 + i) for i in range(4)]
+    ins = [oracle.pack(g) for g in grids]
+    for G in (0, 1, 45):
+        outs = [np.zeros_like(p) for p in ins]
+        before = capi.lib().life_kernel_launches()
+        engine.run_batch(ins, outs, W, G, 0)
+        assert capi.lib().life_kernel_launches() - before <= 2 * len(grids)  # mask + 1 launch per grid
+        for g, out in zip(grids, outs):
+            want, _ = oracle.run(g, G)
+            assert np.array_equal(oracle.unpack(out, W), want), G
+    engine.run_batch(ins, ins, W, 7, 0)
+    for g, out in zip(grids, ins):
+        want, _ = oracle.run(g, 7)
+        assert np.array_equal(oracle.unpack(out, W), want)
