@@ -88,7 +88,7 @@ uint64_t density_threshold(double density) {
 
 // ---- packed temporal-blocked step: template dispatch on K ----------------
 #ifndef LIFE_SYNC_TRIPS
-#define LIFE_SYNC_TRIPS 6
+#define LIFE_SYNC_TRIPS 48
 #endif
 constexpr int kSyncTrips = LIFE_SYNC_TRIPS;
 
@@ -187,9 +187,10 @@ int launch_packed(PackedStepArgs a, cudaStream_t s) {
   a.seg_rows = ceil_div(a.out_rows, best_segs);
   const int64_t tiles = static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, a.seg_rows);
   a.steps = static_cast<int32_t>(ceil_div(a.seg_rows + kLag, PF));
-  // Lockstep granularity: a block barrier every kSyncTrips trips (24 rows)
-  // keeps the warps of an SM together at a sixth of the barrier stalls of one
-  // per trip (measured +4 % on config 5, +2 % on config 4); peer-mode edge
+  // Lockstep granularity: a block barrier every kSyncTrips trips (192 rows).
+  // With the 12-op network one every 6 trips was +4 % over one per trip; the
+  // 11-op network gains another ~0.8 % from going to 48 (config 5 45.33 ->
+  // 45.70 T/s; 24: 45.65, none: 45.75, config 4 best at 48).  Peer-mode edge
   // strips (general fetch path, small launches) keep one per trip.
   a.sync_every = a.peer ? 1 : kSyncTrips;
   const int64_t blocks = ceil_div(tiles, wpb);
