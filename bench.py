@@ -410,7 +410,9 @@ def run_gpu_arm(args) -> None:
     step1 = depth == 1 and W % 128 == 0
     roofline = {
         "bound": "int",
-        "kernel": "packed_step1_kernel" if step1 else f"packed_tb_kernel<{depth}>",
+        "kernel": "packed_step1_kernel" if step1 else
+                  (f"packed_tb_fast_kernel<{depth}>" if W % 32 == 0 and W >= 64 and depth >= 4
+                   else f"packed_tb_kernel<{depth}>"),
         "achieved": achieved_ops / 1e12, "peak": int_ops / 1e12, "unit": "Tops/s",
         "frac": achieved_ops / int_ops if int_ops else None,
         "peak_source": "measured (life_measure_int_peak: LOP3 throughput, all SMs, this run)",

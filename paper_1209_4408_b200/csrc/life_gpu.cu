@@ -122,31 +122,30 @@ int launch_pdl(Kernel kernel, unsigned blocks, unsigned threads, size_t smem, cu
   return LIFE_OK;
 }
 
-template <int K>
-int launch_packed(PackedStepArgs a, cudaStream_t s) {
+template <int K, bool FAST>
+int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
+  const auto kernel = FAST ? packed_tb_fast_kernel<K> : packed_tb_kernel<K>;
+  constexpr int kRing = FAST ? PackedTraits<K>::kRingBytesFast : PackedTraits<K>::kRingBytes;
+  constexpr int kMaxWarps = (FAST ? PackedTraits<K>::kMaxThreadsFast : PackedTraits<K>::kMaxThreads) / 32;
   // Per device: warps per block = every warp one SM holds (register-limited),
   // one block per SM, so the block barrier keeps all of an SM's warps in
   // lockstep (LIFE_NO_LOCKSTEP builds use 4-warp blocks instead).
-  static int warps_per_block[64] = {0};
+  static int warps_per_block[64] = {0};  // per instantiation
   int dev = 0;
   cudaGetDevice(&dev);
   int& wpb = warps_per_block[dev & 63];
   if (wpb == 0) {
-    LIFE_CUDA(cudaFuncSetAttribute(packed_tb_kernel<K>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (PackedTraits<K>::kMaxThreads / 32) * PackedTraits<K>::kRingBytes));
+    LIFE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxWarps * kRing));
     int nb = 0;
-    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, packed_tb_kernel<K>,
-                                                            kPackedThreads,
-                                                            4 * PackedTraits<K>::kRingBytes));
-    int w = std::min(std::max(nb, 1) * (kPackedThreads / 32), PackedTraits<K>::kMaxThreads / 32);
+    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kPackedThreads, 4 * kRing));
+    int w = std::min(std::max(nb, 1) * (kPackedThreads / 32), kMaxWarps);
 #ifdef LIFE_NO_LOCKSTEP
     w = kPackedThreads / 32;
 #else
     for (; w > 1; --w) {
       int nb2 = 0;
-      LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, packed_tb_kernel<K>, 32 * w,
-                                                              w * PackedTraits<K>::kRingBytes));
+      LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, kernel, 32 * w, w * kRing));
       if (nb2 >= 1) break;
     }
 #endif
@@ -154,14 +153,14 @@ int launch_packed(PackedStepArgs a, cudaStream_t s) {
   }
   int blocks_per_sm = 1;
 #ifdef LIFE_NO_LOCKSTEP
-  LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, packed_tb_kernel<K>,
-                                                          32 * wpb, wpb * PackedTraits<K>::kRingBytes));
+  LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, 32 * wpb,
+                                                          wpb * kRing));
 #endif
   // Tiles of seg_rows rows x one strip; pick the segment count that
   // minimises (block waves) x (rows per tile + pipeline fill): blocks run
   // in lockstep internally, and the last wave's idle SMs are the loss.
   constexpr int kLag = PackedTraits<K>::kLag;
-  constexpr int PF = PackedTraits<K>::kPrefetch;
+  constexpr int PF = FAST ? PackedTraits<K>::kPrefetchFast : PackedTraits<K>::kPrefetch;
   if (a.out_rows >= (int64_t(1) << 31) || a.in_rows >= (int64_t(1) << 31) ||
       a.in_pitch * 4 >= (int64_t(1) << 32) || a.out_pitch * 4 >= (int64_t(1) << 32))
     return set_error(LIFE_ERR_CONFIG, "grid too large for one packed pass");
@@ -191,14 +190,25 @@ int launch_packed(PackedStepArgs a, cudaStream_t s) {
   // With the 12-op network one every 6 trips was +4 % over one per trip; the
   // 11-op network gains another ~0.8 % from going to 48 (config 5 45.33 ->
   // 45.70 T/s; 24: 45.65, none: 45.75, config 4 best at 48).  Peer-mode edge
-  // strips (general fetch path, small launches) keep one per trip.
-  a.sync_every = a.peer ? 1 : kSyncTrips;
+  // strips (general fetch path, small launches) keep one per trip; the
+  // fast-only kernel has no barrier.
+  a.sync_every = FAST ? 0 : (a.peer ? 1 : kSyncTrips);
   const int64_t blocks = ceil_div(tiles, wpb);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
-  LIFE_TRY(launch_pdl(packed_tb_kernel<K>, static_cast<unsigned>(blocks), 32 * wpb,
-                      static_cast<size_t>(wpb) * PackedTraits<K>::kRingBytes, s, a));
+  LIFE_TRY(launch_pdl(kernel, static_cast<unsigned>(blocks), 32 * wpb,
+                      static_cast<size_t>(wpb) * kRing, s, a));
   LIFE_CHECK_LAUNCH("packed_tb_kernel");
   return LIFE_OK;
+}
+
+// W % 32 == 0 tori outside peer mode take the fast-only kernel (every warp on
+// the fast fetch path, 6 rows per trip, no barrier); everything else the
+// all-paths kernel.
+template <int K>
+int launch_packed(PackedStepArgs a, cudaStream_t s) {
+  if (K >= 4 && !a.peer && a.width >= 64 && a.width % 32 == 0 && !a.trace)
+    return launch_packed_kernel<K, true>(a, s);
+  return launch_packed_kernel<K, false>(a, s);
 }
 
 using PackedLauncher = int (*)(PackedStepArgs, cudaStream_t);
