@@ -122,6 +122,16 @@ int launch_pdl(Kernel kernel, unsigned blocks, unsigned threads, size_t smem, cu
   return LIFE_OK;
 }
 
+// Block barrier interval of peer-mode (edge strip) launches; LIFE_PEER_SYNC
+// overrides (0 = none).
+int peer_sync_trips() {
+  static const int v = [] {
+    const char* e = std::getenv("LIFE_PEER_SYNC");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+
 template <int K, bool FAST>
 int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   const auto kernel = FAST ? packed_tb_fast_kernel<K> : packed_tb_kernel<K>;
@@ -192,7 +202,7 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   // 45.70 T/s; 24: 45.65, none: 45.75, config 4 best at 48).  Peer-mode edge
   // strips (general fetch path, small launches) keep one per trip; the
   // fast-only kernel has no barrier.
-  a.sync_every = FAST ? 0 : (a.peer ? 1 : kSyncTrips);
+  a.sync_every = FAST ? 0 : (a.peer ? peer_sync_trips() : kSyncTrips);
   const int64_t blocks = ceil_div(tiles, wpb);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
   LIFE_TRY(launch_pdl(kernel, static_cast<unsigned>(blocks), 32 * wpb,
