@@ -159,12 +159,20 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
       if (nb2 >= 1) break;
     }
 #endif
+    // The fast-only kernel has no block barrier: LIFE_FAST_WPB sets its
+    // warps per block (several blocks per SM), for measurement.
+    const char* e = FAST ? std::getenv("LIFE_FAST_WPB") : nullptr;
+    if (e && std::atoi(e) > 0) w = std::min(std::atoi(e), w);
     wpb = w;
   }
   int blocks_per_sm = 1;
 #ifdef LIFE_NO_LOCKSTEP
   LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, 32 * wpb,
                                                           wpb * kRing));
+#else
+  if (FAST)
+    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, 32 * wpb,
+                                                            wpb * kRing));
 #endif
   // Tiles of seg_rows rows x one strip; pick the segment count that
   // minimises (block waves) x (rows per tile + pipeline fill): blocks run
