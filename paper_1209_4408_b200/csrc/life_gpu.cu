@@ -122,6 +122,15 @@ int launch_pdl(Kernel kernel, unsigned blocks, unsigned threads, size_t smem, cu
   return LIFE_OK;
 }
 
+// LIFE_SPLIT=0: W % 32 != 0 tori run every strip in the all-paths kernel.
+bool split_disabled() {
+  static const bool v = [] {
+    const char* e = std::getenv("LIFE_SPLIT");
+    return e && std::atoi(e) == 0;
+  }();
+  return v;
+}
+
 // Block barrier interval of peer-mode (edge strip) launches; LIFE_PEER_SYNC
 // overrides (0 = none).
 int peer_sync_trips() {
@@ -222,11 +231,64 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
 // W % 32 == 0 tori outside peer mode take the fast-only kernel (every warp on
 // the fast fetch path, 6 rows per trip, no barrier); everything else the
 // all-paths kernel.
+// Side stream + fork/join events per (thread, device) for split launches.
+struct SplitStreams {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+int split_streams(SplitStreams** out) {
+  thread_local SplitStreams per_dev[64];
+  int dev = 0;
+  LIFE_CUDA(cudaGetDevice(&dev));
+  SplitStreams& ss = per_dev[dev & 63];
+  if (!ss.side) {
+    LIFE_CUDA(cudaStreamCreateWithFlags(&ss.side, cudaStreamNonBlocking));
+    LIFE_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    LIFE_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
+  return LIFE_OK;
+}
+
+// W % 32 == 0 tori outside peer mode take the fast-only kernel (every warp on
+// the fast fetch path, 6 rows per trip, no barrier).  Other widths split the
+// strips when the grid is several block waves deep: the two or three strips
+// that touch the torus seam (strip 0, which holds word -1, and the strips
+// holding words nw-1 and nw) run the all-paths kernel on a side stream,
+// launched first (short tiles: one quick wave), and the strips between run
+// the fast-only kernel beside and after them: 65535^2 41.4 -> 43.7 T/s,
+// 131071 x 65536 43.0 -> 45.9, 262143 x 8192 38.4 -> 40.5; one-wave grids
+// (config 4, 16383^2) keep the single all-paths launch (split: 37.5 -> 29.3).
 template <int K>
 int launch_packed(PackedStepArgs a, cudaStream_t s) {
-  if (K >= 4 && !a.peer && a.width >= 64 && a.width % 32 == 0 && !a.trace)
-    return launch_packed_kernel<K, true>(a, s);
-  return launch_packed_kernel<K, false>(a, s);
+  const bool fast_ok = K >= 4 && !a.peer && a.width >= 64 && !a.trace;
+  if (fast_ok && a.width % 32 == 0) return launch_packed_kernel<K, true>(a, s);
+  const int32_t total = a.n_strips;
+  // Strip s holds words [31s - 1, 31s + 30]: s_last is the first strip
+  // holding word nw-1 (the seam word); strips 1 .. s_last-1 hold only whole
+  // words inside [0, nw-1).
+  const int32_t s_last = (a.nw - 1) / kStripStride;
+  const bool many_waves = static_cast<int64_t>(total) * a.out_rows >= 2000000;  // ~3 waves of 512-row tiles
+  if (!fast_ok || a.strip0 != 0 || s_last < 2 || !many_waves || split_disabled())
+    return launch_packed_kernel<K, false>(a, s);
+  SplitStreams* ss = nullptr;
+  LIFE_TRY(split_streams(&ss));
+  LIFE_CUDA(cudaEventRecord(ss->fork, s));
+  LIFE_CUDA(cudaStreamWaitEvent(ss->side, ss->fork, 0));
+  PackedStepArgs seam = a;
+  seam.strip0 = 0;
+  seam.n_strips = 1;
+  LIFE_TRY((launch_packed_kernel<K, false>(seam, ss->side)));
+  seam.strip0 = s_last;
+  seam.n_strips = total - s_last;
+  LIFE_TRY((launch_packed_kernel<K, false>(seam, ss->side)));
+  LIFE_CUDA(cudaEventRecord(ss->join, ss->side));
+  PackedStepArgs mid = a;
+  mid.strip0 = 1;
+  mid.n_strips = s_last - 1;
+  LIFE_TRY((launch_packed_kernel<K, true>(mid, s)));
+  LIFE_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
+  return LIFE_OK;
 }
 
 using PackedLauncher = int (*)(PackedStepArgs, cudaStream_t);
