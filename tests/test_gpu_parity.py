@@ -387,3 +387,18 @@ def test_random_shape_fuzz_all_engines(engine, oracle):
         engine.upload(g)
         engine.run(gens, eng, depth)
         assert np.array_equal(engine.download(), want), (case, w, h, gens, eng, depth)
+
+
+@pytest.mark.slow
+def test_split_launch_seam_strips(engine):
+    """W % 32 != 0 tori several block waves deep run the seam strips on the
+    all-paths kernel beside the fast-only kernel (launch_packed's split):
+    its grid hash equals depth 2 (no split, no fast kernel) and the byte
+    engine (an independent implementation)."""
+    W, H, G = 2001, 700000, 32  # 3 strips x 700000 rows: over the split threshold
+    hashes = []
+    for eng, depth in [(PACKED, 16), (PACKED, 2), (BYTE, 1)]:
+        engine.init_random(W, H, 0.4, 2026, eng)
+        engine.run(G, eng, depth)
+        hashes.append(engine.hash())
+    assert hashes[0] == hashes[1] == hashes[2]
