@@ -133,7 +133,7 @@ int life_step(life_ctx* ctx, int engine);
  * `n` host grids inputs[i] is uploaded, run for `generations` on the packed
  * engine and downloaded to outputs[i] (may alias inputs[i]).  The H2D copy of
  * grid i+1 and the D2H copy of grid i-1 overlap the compute of grid i (copy
- * engines); tall grids run their first and last grid as 16 row-chunk
+ * engines); tall grids run their first and last grid as 32 row-chunk
  * trapezoids plus boundary triangles so those copies overlap compute too;
  * temporal_depth 0 on a small W % 32 == 0 torus runs each grid on the
  * cluster-resident engine (one launch per grid).

@@ -1413,7 +1413,14 @@ namespace {
 // B - kShrink*(p+2), exactly where triangle pass p stops reading; triangles
 // run after both neighbouring trapezoids.  Middle grids keep whole-grid
 // passes (their copies overlap the neighbouring grids' compute anyway).
-constexpr int kTrapChunks = 16;
+#ifndef LIFE_TRAP_CHUNKS
+#define LIFE_TRAP_CHUNKS 32  // e2e / value on config 5: 8 chunks 0.945, 16 0.953, 32 0.967, 48 0.955, 64 0.940
+#endif
+constexpr int kTrapChunks = LIFE_TRAP_CHUNKS;
+#ifndef LIFE_TRAP_MIN_ROWS
+#define LIFE_TRAP_MIN_ROWS 8192
+#endif
+constexpr int64_t kTrapMinChunkRows = LIFE_TRAP_MIN_ROWS;
 constexpr int64_t kShrink = 16;
 
 struct BatchGeom {
@@ -1517,7 +1524,7 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   // (as life_run's auto mode), one launch per grid.
   const bool resident = temporal_depth == 0 && resident_auto(width, height);
   const bool trap = !resident && fits &&
-                    (trap_env == 1 || (trap_env != 0 && height / kTrapChunks >= 8192));
+                    (trap_env == 1 || (trap_env != 0 && height / kTrapChunks >= kTrapMinChunkRows));
   if (trap) {
     LIFE_TRY(life_band_bounds(height, kTrapChunks, g.bounds));
     for (auto& st : c->cs)

@@ -283,11 +283,12 @@ def test_run_batch_pipelined(engine, oracle):
                                          (2048, 600, 16, 16), (96, 4099, 0, 16), (640, 1030, 5, 3),
                                          (96, 33001, 37, 8), (100, 40000, 20, 16),
                                          (64, 32768, 48, 16), (200, 36000, 1, 1),
-                                         (1024, 33000, 5, 1)])
+                                         (1024, 33000, 5, 1), (64, 80000, 48, 16),
+                                         (96, 66000, 37, 8)])
 def test_run_batch_banded(engine, oracle, W, H, G, depth):
     """life_run_batch on taller grids: several waves of row tiles per pass, W % 32 != 0,
     G not a multiple of the depth, G = 0, more grids than buffer slots; H >= 32768 runs
-    the first and last grid as 16 chunk trapezoids + boundary triangles (forced with
+    the first and last grid as 32 chunk trapezoids + boundary triangles (forced with
     LIFE_BATCH_TRAP=1: by default only chunks of >= 8192 rows take it)."""
     import os
     if H >= 32768:
