@@ -80,3 +80,23 @@ def test_multirank_path_on_one_gpu(halo):
     assert j["n_gpus"] == 2 and j["value"] > 0 and j["config"]["parallelism"] == "rowbands2"
     assert "peer" in j["config"]["halo"] or "NCCL" in j["config"]["halo"]
     assert j["e2e"]["value"] > 0 and j["cpu_baseline"] is None
+
+
+def test_reference_arm_under_torchrun_prints_once():
+    """`--impl reference` launched like the GPU arm at N > 1: rank 0 alone
+    runs the reference CPU engine and prints one JSON line; the others exit 0."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), "bench.py", "--impl", "reference", "--gpus", "2", "--config",
+                        "1", "--steps", "1", "--warmup", "0", "--cpu-budget", "0.3"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout
+    j = json.loads(lines[0])
+    assert j["impl"] == "reference" and j["value"] > 0 and j["e2e"]["d2h_bytes_per_step"] == 0
