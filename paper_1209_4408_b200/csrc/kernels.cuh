@@ -126,7 +126,8 @@ struct PackedStepArgs {
   int32_t sync_every; // loop trips per block barrier
   int32_t nw;         // ceil(width / 32): words holding cells
   int32_t n_strips;   // strips this launch covers (all: ceil((nw + 1) / 31))
-  int32_t strip0;     // first strip of this launch
+  int32_t strip0;     // first strip of this launch (strips wrap modulo strips_total)
+  int32_t strips_total;  // ceil((nw + 1) / 31)
   uint32_t tail_mask; // valid bits of word nw-1
   void* trace;        // LIFE_TRACE builds: per-warp (smid, start, end)
   // Peer mode (multi-GPU row bands over NVLink): input relative row r < 0 is
@@ -565,7 +566,8 @@ packed_tb_kernel(const PackedStepArgs a) {
   // neighbouring strips of the same rows, so the words they share (ghost
   // lanes, half-word stores) meet in L1/L2 at the same time.
   const int64_t tile = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int strip = a.strip0 + static_cast<int>(tile % a.n_strips);
+  const int strip = (a.strip0 + static_cast<int>(tile % a.n_strips)) %
+                    (a.strips_total > 0 ? a.strips_total : a.n_strips);
   const int64_t seg = tile / a.n_strips;
   const int64_t y0 = seg * a.seg_rows;
   const int64_t left = a.out_rows - y0;
@@ -642,7 +644,8 @@ __global__ void __launch_bounds__(PackedTraits<K>::kMaxThreadsFast)
 packed_tb_fast_kernel(const PackedStepArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t tile = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int strip = a.strip0 + static_cast<int>(tile % a.n_strips);
+  const int strip = (a.strip0 + static_cast<int>(tile % a.n_strips)) %
+                    (a.strips_total > 0 ? a.strips_total : a.n_strips);
   const int64_t seg = tile / a.n_strips;
   const int64_t y0 = seg * a.seg_rows;
   const int64_t left = a.out_rows - y0;

@@ -257,11 +257,11 @@ int split_streams(SplitStreams** out) {
 // the fast fetch path, 6 rows per trip, no barrier).  Other widths split the
 // strips when the grid is several block waves deep: the two or three strips
 // that touch the torus seam (strip 0, which holds word -1, and the strips
-// holding words nw-1 and nw) run the all-paths kernel on a side stream,
-// launched first (short tiles: one quick wave), and the strips between run
-// the fast-only kernel beside and after them: 65535^2 41.4 -> 43.7 T/s,
-// 131071 x 65536 43.0 -> 45.9, 262143 x 8192 38.4 -> 40.5; one-wave grids
-// (config 4, 16383^2) keep the single all-paths launch (split: 37.5 -> 29.3).
+// holding words nw-1 and nw) run the all-paths kernel in ONE launch on a side
+// stream (strips wrap modulo the strip count), launched first (short tiles:
+// one quick wave), and the strips between run the fast-only kernel beside
+// and after them: 65535^2 41.5 -> 44.4 T/s, 131071 x 65536 43.3 -> 46.3;
+// one-wave grids (config 4, 16383^2) keep the single all-paths launch.
 template <int K>
 int launch_packed(PackedStepArgs a, cudaStream_t s) {
   const bool fast_ok = K >= 4 && !a.peer && a.width >= 64 && !a.trace;
@@ -274,16 +274,20 @@ int launch_packed(PackedStepArgs a, cudaStream_t s) {
   const bool many_waves = static_cast<int64_t>(total) * a.out_rows >= 2000000;  // ~3 waves of 512-row tiles
   if (!fast_ok || a.strip0 != 0 || s_last < 2 || !many_waves || split_disabled())
     return launch_packed_kernel<K, false>(a, s);
+  const int32_t n_end = total - s_last;  // seam strips at the end (1 or 2)
+  // (Packing a one-wave grid's two launches into its single wave -- fast
+  // strips at the single launch's segment length, the seam strips in the
+  // blocks left over -- measured 2-10 % slower than one all-paths launch:
+  // config 4 37.6 -> 36.5, 4097^2 7.8 -> 7.1.)
   SplitStreams* ss = nullptr;
   LIFE_TRY(split_streams(&ss));
   LIFE_CUDA(cudaEventRecord(ss->fork, s));
   LIFE_CUDA(cudaStreamWaitEvent(ss->side, ss->fork, 0));
+  // One seam launch: strips s_last .. total-1 and (wrapping) strip 0.
   PackedStepArgs seam = a;
-  seam.strip0 = 0;
-  seam.n_strips = 1;
-  LIFE_TRY((launch_packed_kernel<K, false>(seam, ss->side)));
+  seam.strips_total = total;
   seam.strip0 = s_last;
-  seam.n_strips = total - s_last;
+  seam.n_strips = n_end + 1;
   LIFE_TRY((launch_packed_kernel<K, false>(seam, ss->side)));
   LIFE_CUDA(cudaEventRecord(ss->join, ss->side));
   PackedStepArgs mid = a;
@@ -417,6 +421,7 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
   a.out_rows = out_rows;
   a.nw = static_cast<int32_t>(nw32(width));
   a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
+  a.strips_total = a.n_strips;
   a.tail_mask = tail_mask(width);
   a.trace = g_trace;
   return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
@@ -449,6 +454,7 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
   a.out_rows = out_rows;
   a.nw = static_cast<int32_t>(nw32(width));
   a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
+  a.strips_total = a.n_strips;
   a.tail_mask = tail_mask(width);
   a.trace = g_trace;
   a.up = up;
