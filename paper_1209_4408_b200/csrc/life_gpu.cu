@@ -263,8 +263,8 @@ int split_streams(SplitStreams** out) {
 // and after them: 65535^2 41.5 -> 44.4 T/s, 131071 x 65536 43.3 -> 46.3;
 // one-wave grids (config 4, 16383^2) keep the single all-paths launch.
 template <int K>
-int launch_packed(PackedStepArgs a, cudaStream_t s) {
-  const bool fast_ok = K >= 4 && !a.peer && a.width >= 64 && !a.trace;
+int launch_packed_deep(PackedStepArgs a, cudaStream_t s) {
+  const bool fast_ok = !a.peer && a.width >= 64 && !a.trace;
   if (fast_ok && a.width % 32 == 0) return launch_packed_kernel<K, true>(a, s);
   const int32_t total = a.n_strips;
   // Strip s holds words [31s - 1, 31s + 30]: s_last is the first strip
@@ -296,6 +296,15 @@ int launch_packed(PackedStepArgs a, cudaStream_t s) {
   LIFE_TRY((launch_packed_kernel<K, true>(mid, s)));
   LIFE_CUDA(cudaStreamWaitEvent(s, ss->join, 0));
   return LIFE_OK;
+}
+
+template <int K>
+int launch_packed(PackedStepArgs a, cudaStream_t s) {
+  if constexpr (K < 4) {  // shallow passes keep the all-paths kernel (no fast-only instance)
+    return launch_packed_kernel<K, false>(a, s);
+  } else {
+    return launch_packed_deep<K>(a, s);
+  }
 }
 
 using PackedLauncher = int (*)(PackedStepArgs, cudaStream_t);
