@@ -2,7 +2,7 @@
 """Benchmark of the generation-step hot path (BASELINE.json metric:
 cell-updates/s at 1/2/4/8 B200, as a fraction of the int/HBM roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--depth 16]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--depth 0=auto]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference      # the reference's own CPU engine
     python bench.py --config 2 --engine byte       # byte engine (HBM-bound)
@@ -274,6 +274,9 @@ def run_gpu_arm(args) -> None:
     L = capi.lib()
     cfg = CONFIGS[args.config]
     W, H, gens, depth = cfg["w"], cfg["h"], args.gens or cfg["gens"], args.depth
+    if depth == 0:  # the engine's auto rule (life_gpu.cu packed_auto_depth)
+        strips = -(-((W + 31) // 32 + 1) // 31)
+        depth = 12 if W % 32 and strips * H < 2_000_000 else 16
 
     def barrier():
         if world > 1:
@@ -834,7 +837,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=5, choices=sorted(CONFIGS))
-    ap.add_argument("--depth", type=int, default=16)
+    ap.add_argument("--depth", type=int, default=0,
+                    help="generations per packed pass; 0 = the engine's auto rule (16; 12 for "
+                         "one-launch W %% 32 != 0 tori such as config 4)")
     ap.add_argument("--gens", type=int, default=0, help="override the config's generations")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
