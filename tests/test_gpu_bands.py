@@ -172,3 +172,35 @@ def test_cfg5_full_grid_hash_across_band_decompositions():
         assert got == want, P
         del lb
         torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_band_interiors_take_the_split_launch():
+    """Band interiors of a W % 32 != 0 torus deep enough for launch_packed's
+    split (seam strips on the all-paths kernel beside the fast-only kernel):
+    2 bands (ghost-copy and peer schemes) give the single context's
+    grid hash."""
+    import torch
+
+    from paper_1209_4408_b200 import capi, life
+    from paper_1209_4408_b200.bands import LocalBands, LocalPeerBands
+    W, H, G = 2001, 1_400_000, 32
+    L = capi.lib()
+    with life.Engine(0) as e:
+        e.init_random(W, H, 0.35, 77)
+        e.run(G, capi.ENGINE_PACKED, 16)
+        want = e.hash()
+    dev = torch.device("cuda", 0)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    for make in (lambda: LocalBands(W, H, 2, 16, dev), lambda: LocalPeerBands(W, H, 2, 16, dev)):
+        lb = make()
+        lb.init_random(0.35, 77)
+        lb.run(G)
+        grid = lb.gather()
+        rows = torch.empty(H, dtype=torch.int64, device=dev)
+        life.check(L.life_dev_packed_row_hashes(grid.data_ptr(), grid.shape[1], W, H,
+                                                rows.data_ptr(), stream))
+        host = rows.cpu().numpy()
+        assert L.life_fnv1a64(host.ctypes.data, host.nbytes, 0) == want
+        del lb, grid
+        torch.cuda.empty_cache()
