@@ -210,9 +210,11 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
       best_segs = segs;
     }
   }
-  if (const char* e = std::getenv("LIFE_SEGS")) {  // measurement knob: force the segment count
-    if (std::atoll(e) > 0) best_segs = std::min<int64_t>(std::atoll(e), a.out_rows);
-  }
+  static const int64_t forced_segs = [] {  // measurement knob: force the segment count
+    const char* e = std::getenv("LIFE_SEGS");
+    return e ? std::atoll(e) : 0LL;
+  }();
+  if (forced_segs > 0) best_segs = std::min<int64_t>(forced_segs, a.out_rows);
   a.seg_rows = ceil_div(a.out_rows, best_segs);
   const int64_t tiles = static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, a.seg_rows);
   a.steps = static_cast<int32_t>(ceil_div(a.seg_rows + kLag, PF));
