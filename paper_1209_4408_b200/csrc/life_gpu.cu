@@ -392,7 +392,11 @@ int launch_step1(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t 
   a.n_strips = static_cast<int32_t>(ceil_div(a.nv, kStep1Stride));
   const int64_t resident_warps =
       static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kStep1Threads / 32) * sm_count();
-  const int64_t segs_target = std::max<int64_t>(1, 8 * resident_warps / a.n_strips);
+  static const int waves = [] {  // LIFE_STEP1_WAVES: measurement knob
+    const char* e = std::getenv("LIFE_STEP1_WAVES");
+    return e && std::atoi(e) > 0 ? std::atoi(e) : 8;
+  }();
+  const int64_t segs_target = std::max<int64_t>(1, waves * resident_warps / a.n_strips);
   a.seg_rows = std::max<int64_t>(ceil_div(out_rows, segs_target), 32);
   const int64_t warps = ceil_div(out_rows, a.seg_rows) * a.n_strips;
   const int64_t blocks = ceil_div(warps, kStep1Threads / 32);
