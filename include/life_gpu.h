@@ -68,12 +68,58 @@ const char* life_last_error(void);
 const char* life_version(void);
 
 /* ---- context (owns device buffers and a stream on one GPU) ------------- */
+/* A context is used by one host thread at a time; distinct contexts may be
+ * used concurrently from different threads (the reference's run() is pure and
+ * safe to call from any thread). */
 int life_ctx_create(int device, life_ctx** out);
+/* Multi-device context: the torus is split into `n` row bands by band_bounds
+ * (decomposition.cpp:12-24 -- the paper's 1-D row decomposition, what
+ * run(..., RunConfig{Strategy::rows(), workers = n}) does with threads,
+ * engine.cpp:162-214), band i resident on GPU devices[i].  Repeated device
+ * ids are allowed (several bands on one GPU run the same code).  Owns the
+ * peer-access setup: neighbouring bands on different GPUs read each other's
+ * K halo rows inside the pass kernel over NVLink (LIFE_HALO_PEER), or, when
+ * peer access is unavailable, copy them into ghost rows first
+ * (LIFE_HALO_COPY).  Passes are ordered across bands by events between
+ * NEIGHBOURING bands only -- no global barrier.  Every grid / run entry point
+ * below accepts it (packed engine only: LIFE_ENGINE_BYTE / _RESIDENT and
+ * life_ctx_set_stream return LIFE_ERR_CONFIG); a loaded grid needs H >= n
+ * (LIFE_ERR_TOO_MANY_PARTS otherwise, decomposition.cpp:26-30). */
+int life_ctx_create_multi(int32_t n, const int* devices, life_ctx** out);
 int life_ctx_destroy(life_ctx* ctx);
 /* Orders the context's work on an external stream (e.g. torch's current
  * stream); NULL restores the context's own stream. */
 int life_ctx_set_stream(life_ctx* ctx, void* cuda_stream);
 int life_ctx_sync(life_ctx* ctx);
+/* Band layout: *n bands, bounds[0..n] row cut points, devices[0..n-1], *halo
+ * (LIFE_HALO_*, -1 for a single-device context).  NULL outputs are skipped;
+ * bounds needs n+1 entries (call with bounds = devices = NULL first). */
+int life_ctx_bands(life_ctx* ctx, int32_t* n, int64_t* bounds, int32_t* devices, int32_t* halo);
+
+/* Context options. */
+#define LIFE_OPT_PROFILE 1         /* 1: CUDA events around every pass of life_run (band stats) */
+#define LIFE_OPT_BATCH_TRAPEZOID 2 /* life_run_batch first/last-grid chunk schedule: -1 auto, 0, 1 */
+#define LIFE_OPT_HALO 3            /* multi-device halo scheme: LIFE_HALO_PEER / LIFE_HALO_COPY */
+#define LIFE_HALO_PEER 0           /* edge-strip kernels read neighbour rows over NVLink (P2P) */
+#define LIFE_HALO_COPY 1           /* neighbour rows copied into local ghost rows, then computed */
+int life_ctx_set_option(life_ctx* ctx, int32_t option, int64_t value);
+int life_ctx_get_option(life_ctx* ctx, int32_t option, int64_t* value);
+
+/* Per-band statistics of the last life_run (band 0 = the whole torus of a
+ * single-device context).  run_ms: CUDA-event time on the band's device from
+ * the run's first launch to its last; with LIFE_OPT_PROFILE, interior_ms /
+ * edge_ms are the summed per-pass times of the interior launches and of the
+ * edge strips (halo copies included), and wait_ms = run_ms - interior_ms -- the
+ * time the band's compute stream did not run interior rows (edges, neighbour
+ * waits, pass boundaries).  For a single-device context interior_ms is the
+ * whole pass. */
+typedef struct life_band_stats {
+  int32_t band, device;
+  int64_t y0, rows;
+  int64_t passes;
+  double run_ms, interior_ms, edge_ms, wait_ms;
+} life_band_stats;
+int life_ctx_band_stats(life_ctx* ctx, int32_t band, life_band_stats* out);
 
 /* ---- grid in / out (replaces constructing and reading life::Grid) ------ */
 /* Replaces `Grid` + `Grid::data()` writes (grid.hpp:29-35, :56-57).
@@ -144,6 +190,10 @@ int life_run_batch(life_ctx* ctx, const uint64_t* const* inputs, uint64_t* const
                    int32_t n, int64_t width, int64_t height, int64_t words_per_row,
                    int64_t generations, int temporal_depth, float* elapsed_ms);
 
+/* The depth life_run uses for temporal_depth 0 on the multi-pass packed
+ * engine (16; 12 for W % 32 != 0 tori less than ~3 block waves deep). */
+int life_packed_auto_depth(int64_t width, int64_t height);
+
 /* ---- row-band decomposition (multi-GPU) --------------------------------- */
 /* Mirrors band_bounds / partition_rows (decomposition.cpp:12-24, :93-104):
  * writes parts+1 cut points; LIFE_ERR_TOO_MANY_PARTS if parts > extent. */
@@ -156,7 +206,9 @@ int life_band_bounds(int64_t extent, int32_t parts, int64_t* bounds);
 int64_t life_packed_pitch_words(int64_t width);
 /* Byte layout pitch (>= W, a multiple of 16 B). */
 int64_t life_byte_pitch(int64_t width);
-/* `generations` (1..16) packed generations in one pass.  Output relative row
+/* `generations` (1..16) packed generations in one pass (W % 32 != 0 tori
+ * several block waves deep run their seam strips on a library-owned side
+ * stream per host thread and device, joined back into `stream`).  Output relative row
  * r (0 <= r < out_rows) is stored at out + (out_row0 + r) * out_pitch; input
  * relative row r (-generations <= r < out_rows + generations) is read from
  * physical row (in_row0 + r) mod in_rows of `in`.  The torus is the case

@@ -46,8 +46,9 @@ def build_lib(force: bool = False, verbose: bool = False, out: str = LIB,
     srcs = _sources()
     if not force and _newer(out, srcs + [os.path.abspath(__file__)]):
         return out
+    units = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cu")]
     cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-cudart", "static",
-           "-o", out + ".tmp", os.path.join(CSRC, "life_gpu.cu")]
+           "-o", out + ".tmp", *units]
     if verbose:
         cmd[1:1] = ["-Xptxas", "-v"]
         print(" ".join(cmd))

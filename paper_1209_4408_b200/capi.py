@@ -28,6 +28,22 @@ ENGINE_RESIDENT = 2
 MAX_TEMPORAL_DEPTH = 16
 MAX_BYTE_DEPTH = 8
 
+OPT_PROFILE = 1
+OPT_BATCH_TRAPEZOID = 2
+OPT_HALO = 3
+HALO_PEER = 0
+HALO_COPY = 1
+
+
+class BandStats(C.Structure):
+    """life_band_stats (include/life_gpu.h)."""
+    _fields_ = [("band", C.c_int32), ("device", C.c_int32), ("y0", C.c_int64),
+                ("rows", C.c_int64), ("passes", C.c_int64), ("run_ms", C.c_double),
+                ("interior_ms", C.c_double), ("edge_ms", C.c_double), ("wait_ms", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
 # Every function the header declares: (name, restype, argtypes).
 _vp = C.c_void_p
 _i64 = C.c_int64
@@ -37,9 +53,14 @@ SIGNATURES = [
     ("life_last_error", C.c_char_p, []),
     ("life_version", C.c_char_p, []),
     ("life_ctx_create", C.c_int, [C.c_int, C.POINTER(_vp)]),
+    ("life_ctx_create_multi", C.c_int, [_i32, C.POINTER(C.c_int), C.POINTER(_vp)]),
     ("life_ctx_destroy", C.c_int, [_vp]),
     ("life_ctx_set_stream", C.c_int, [_vp, _vp]),
     ("life_ctx_sync", C.c_int, [_vp]),
+    ("life_ctx_bands", C.c_int, [_vp, C.POINTER(_i32), _vp, _vp, C.POINTER(_i32)]),
+    ("life_ctx_set_option", C.c_int, [_vp, _i32, _i64]),
+    ("life_ctx_get_option", C.c_int, [_vp, _i32, C.POINTER(_i64)]),
+    ("life_ctx_band_stats", C.c_int, [_vp, _i32, C.POINTER(BandStats)]),
     ("life_grid_upload_u8", C.c_int, [_vp, _vp, _i64, _i64, _i64]),
     ("life_grid_upload_packed", C.c_int, [_vp, _vp, _i64, _i64, _i64]),
     ("life_grid_init_random", C.c_int, [_vp, _i64, _i64, C.c_double, _u64, C.c_int]),
@@ -56,6 +77,7 @@ SIGNATURES = [
     ("life_step", C.c_int, [_vp, C.c_int]),
     ("life_run_batch", C.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _i64, C.c_int,
                                  C.POINTER(C.c_float)]),
+    ("life_packed_auto_depth", C.c_int, [_i64, _i64]),
     ("life_band_bounds", C.c_int, [_i64, _i32, _vp]),
     ("life_packed_pitch_words", _i64, [_i64]),
     ("life_byte_pitch", _i64, [_i64]),

@@ -299,9 +299,9 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-// A warp's work is a range of the virtual row space strip*out_rows + y
-// (int32: the host checks n_strips*out_rows < 2^31): one or more segments
-// (strip, y, n), each a fresh pipeline of n + kLag steps.
+// A warp's work is one tile (strip, y, n): a fresh pipeline of n + kLag
+// steps (tile indices are int64; rows and trips are int32 -- the host
+// rejects passes with in_rows or out_rows >= 2^31).
 
 // One pipeline segment of a warp: strip `strip`, output rows [y, y+n).
 // Runs ceil((n + kLag) / PF) loop trips (a block barrier after every
@@ -614,8 +614,9 @@ packed_tb_kernel(const PackedStepArgs a) {
   }
 #ifndef LIFE_NO_LOCKSTEP
   // Shorter (last) segments and spare warps pad to the block's trip count.
-  for (; trips < a.steps; ++trips)
-    if ((trips + 1) % a.sync_every == 0) __syncthreads();
+  if (a.sync_every > 0)
+    for (; trips < a.steps; ++trips)
+      if ((trips + 1) % a.sync_every == 0) __syncthreads();
 #endif
 #ifdef LIFE_TRACE
   if (lane == 0) {

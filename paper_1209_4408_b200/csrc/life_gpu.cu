@@ -16,15 +16,20 @@
 #include <vector>
 
 #include "../../include/life_gpu.h"
+#include "internal.h"
 #include "kernels.cuh"
 
 using namespace lifegpu;
+using namespace lifegpu::detail;
 
 namespace {
-
 thread_local std::string g_error;
 std::atomic<uint64_t> g_launches{0};
-void* g_trace = nullptr;  // device buffer for LIFE_TRACE builds (life_debug_set_trace)
+std::atomic<void*> g_trace{nullptr};  // device buffer for LIFE_TRACE builds (life_debug_set_trace)
+}  // namespace
+
+namespace lifegpu {
+namespace detail {
 
 int set_error(int code, const char* fmt, ...) {
   char buf[512];
@@ -42,45 +47,87 @@ int cuda_fail(cudaError_t e, const char* what) {
   return set_error(LIFE_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-#define LIFE_CUDA(call)                                   \
-  do {                                                    \
-    cudaError_t e_ = (call);                              \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
-  } while (0)
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-#define LIFE_CHECK_LAUNCH(name)                                    \
-  do {                                                             \
-    g_launches.fetch_add(1, std::memory_order_relaxed);            \
-    cudaError_t e_ = cudaGetLastError();                           \
-    if (e_ != cudaSuccess) return cuda_fail(e_, "launch " name);   \
-  } while (0)
-
-#define LIFE_TRY(expr)             \
-  do {                             \
-    int rc_ = (expr);              \
-    if (rc_ != LIFE_OK) return rc_; \
-  } while (0)
-
-int sm_count() {
-  int dev = 0, n = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-  return n;
+int64_t knob(const char* name, int64_t dflt) {
+#ifdef LIFE_DEBUG_KNOBS
+  const char* e = std::getenv(name);
+  return e ? std::atoll(e) : dflt;
+#else
+  (void)name;
+  return dflt;
+#endif
 }
 
-int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int sm_count() {
+  static DeviceCache cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int n = cache.get(dev);
+  if (n == 0) {
+    n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cache.put(dev, n);
+  }
+  return n;
+}
 
 int grid_stride_blocks(int64_t n, int threads) {
   const int64_t want = ceil_div(std::max<int64_t>(n, 1), threads);
   return static_cast<int>(std::min<int64_t>(want, static_cast<int64_t>(sm_count()) * 16));
 }
 
-int64_t nw32(int64_t width) { return ceil_div(width, 32); }
-
-uint32_t tail_mask(int64_t width) {
-  const int r = static_cast<int>(width & 31);
-  return r == 0 ? 0xffffffffu : ((1u << r) - 1u);
+int check_dims(int64_t width, int64_t height) {
+  if (width < 3 || height < 3)
+    return set_error(LIFE_ERR_DIMENSION_TOO_SMALL,
+                     "grid dimensions must be at least 3x3, got %lldx%lld",
+                     static_cast<long long>(width), static_cast<long long>(height));
+  if (width > (int64_t(1) << 40) || height > (int64_t(1) << 40))
+    return set_error(LIFE_ERR_CONFIG, "grid dimensions too large");
+  return LIFE_OK;
 }
+
+int check_run_args(int64_t generations, const int64_t* checkpoints, int32_t n_checkpoints,
+                   const uint64_t* populations) {
+  // check_run_config (engine.cpp:127-148)
+  if (generations < 0)
+    return set_error(LIFE_ERR_CONFIG, "iteration count must be non-negative, got %lld",
+                     static_cast<long long>(generations));
+  if (n_checkpoints < 0 || (n_checkpoints > 0 && (!checkpoints || !populations)))
+    return set_error(LIFE_ERR_CONFIG, "bad checkpoint buffers");
+  int64_t prev = -1;
+  for (int32_t i = 0; i < n_checkpoints; ++i) {
+    const int64_t cp = checkpoints[i];
+    if (cp < 0 || cp > generations)
+      return set_error(LIFE_ERR_CONFIG, "checkpoint %lld is outside [0, iterations=%lld]",
+                       static_cast<long long>(cp), static_cast<long long>(generations));
+    if (cp <= prev) return set_error(LIFE_ERR_CONFIG, "checkpoints must be strictly ascending");
+    prev = cp;
+  }
+  return LIFE_OK;
+}
+
+int split_streams_init(SplitStreams* ss, int device) {
+  if (ss->side && ss->device == device) return LIFE_OK;
+  split_streams_destroy(ss);
+  LIFE_CUDA(cudaStreamCreateWithFlags(&ss->side, cudaStreamNonBlocking));
+  LIFE_CUDA(cudaEventCreateWithFlags(&ss->fork, cudaEventDisableTiming));
+  LIFE_CUDA(cudaEventCreateWithFlags(&ss->join, cudaEventDisableTiming));
+  ss->device = device;
+  return LIFE_OK;
+}
+
+void split_streams_destroy(SplitStreams* ss) {
+  if (ss->side) cudaStreamDestroy(ss->side);
+  if (ss->fork) cudaEventDestroy(ss->fork);
+  if (ss->join) cudaEventDestroy(ss->join);
+  *ss = SplitStreams{};
+}
+
+}  // namespace detail
+}  // namespace lifegpu
+
+namespace {
 
 uint64_t density_threshold(double density) {
   return static_cast<uint64_t>(std::ceil(density * 0x1.0p53));
@@ -94,14 +141,12 @@ constexpr int kSyncTrips = LIFE_SYNC_TRIPS;
 
 // Programmatic dependent launch (PDL): consecutive passes on a stream
 // overlap the next grid's launch with this one's tail; the kernels wait on
-// griddepcontrol.wait before their first read.  LIFE_PDL=0 disables it.
-// Measured with packed_tb_kernel<16> (T/s, 320 generations): 4096^2 9.45 ->
-// 10.0, 8192^2 23.1 -> 23.9, 16384^2 36.1 -> 36.7, 65536^2 unchanged.
+// griddepcontrol.wait before their first read (LIFE_PDL=0 in LIFE_DEBUG_KNOBS
+// builds disables it).  Measured with packed_tb_kernel<16> (T/s, 320
+// generations): 4096^2 9.45 -> 10.0, 8192^2 23.1 -> 23.9, 16384^2 36.1 ->
+// 36.7, 65536^2 unchanged.
 bool pdl_enabled() {
-  static const bool pdl = [] {
-    const char* e = std::getenv("LIFE_PDL");
-    return !(e && std::atoi(e) == 0);
-  }();
+  static const bool pdl = knob("LIFE_PDL", 1) != 0;
   return pdl;
 }
 
@@ -122,22 +167,17 @@ int launch_pdl(Kernel kernel, unsigned blocks, unsigned threads, size_t smem, cu
   return LIFE_OK;
 }
 
-// LIFE_SPLIT=0: W % 32 != 0 tori run every strip in the all-paths kernel.
+// LIFE_SPLIT=0 (debug builds): W % 32 != 0 tori run every strip in the
+// all-paths kernel.
 bool split_disabled() {
-  static const bool v = [] {
-    const char* e = std::getenv("LIFE_SPLIT");
-    return e && std::atoi(e) == 0;
-  }();
+  static const bool v = knob("LIFE_SPLIT", 1) == 0;
   return v;
 }
 
-// Block barrier interval of peer-mode (edge strip) launches; LIFE_PEER_SYNC
-// overrides (0 = none).
+// Block barrier interval of peer-mode (edge strip) launches (one per loop
+// trip; LIFE_PEER_SYNC in debug builds, 0 = none).
 int peer_sync_trips() {
-  static const int v = [] {
-    const char* e = std::getenv("LIFE_PEER_SYNC");
-    return e ? std::atoi(e) : 1;
-  }();
+  static const int v = static_cast<int>(std::max<int64_t>(knob("LIFE_PEER_SYNC", 1), 0));
   return v;
 }
 
@@ -149,10 +189,10 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   // Per device: warps per block = every warp one SM holds (register-limited),
   // one block per SM, so the block barrier keeps all of an SM's warps in
   // lockstep (LIFE_NO_LOCKSTEP builds use 4-warp blocks instead).
-  static int warps_per_block[64] = {0};  // per instantiation
+  static DeviceCache warps_per_block;  // per instantiation
   int dev = 0;
   cudaGetDevice(&dev);
-  int& wpb = warps_per_block[dev & 63];
+  int wpb = warps_per_block.get(dev);
   if (wpb == 0) {
     LIFE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kMaxWarps * kRing));
@@ -168,11 +208,12 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
       if (nb2 >= 1) break;
     }
 #endif
-    // The fast-only kernel has no block barrier: LIFE_FAST_WPB sets its
-    // warps per block (several blocks per SM), for measurement.
-    const char* e = FAST ? std::getenv("LIFE_FAST_WPB") : nullptr;
-    if (e && std::atoi(e) > 0) w = std::min(std::atoi(e), w);
+    // The fast-only kernel has no block barrier: LIFE_FAST_WPB (debug builds)
+    // sets its warps per block (several blocks per SM), for measurement.
+    const int64_t forced = FAST ? knob("LIFE_FAST_WPB", 0) : 0;
+    if (forced > 0) w = std::min(static_cast<int>(forced), w);
     wpb = w;
+    warps_per_block.put(dev, wpb);
   }
   int blocks_per_sm = 1;
 #ifdef LIFE_NO_LOCKSTEP
@@ -210,10 +251,7 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
       best_segs = segs;
     }
   }
-  static const int64_t forced_segs = [] {  // measurement knob: force the segment count
-    const char* e = std::getenv("LIFE_SEGS");
-    return e ? std::atoll(e) : 0LL;
-  }();
+  static const int64_t forced_segs = knob("LIFE_SEGS", 0);  // debug builds: force the segment count
   if (forced_segs > 0) best_segs = std::min<int64_t>(forced_segs, a.out_rows);
   a.seg_rows = ceil_div(a.out_rows, best_segs);
   const int64_t tiles = static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, a.seg_rows);
@@ -233,24 +271,21 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   return LIFE_OK;
 }
 
-// W % 32 == 0 tori outside peer mode take the fast-only kernel (every warp on
-// the fast fetch path, 6 rows per trip, no barrier); everything else the
-// all-paths kernel.
-// Side stream + fork/join events per (thread, device) for split launches.
-struct SplitStreams {
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
-};
-int split_streams(SplitStreams** out) {
-  thread_local SplitStreams per_dev[64];
+// Library-owned side stream per (thread, device) for split launches of the
+// device-buffer layer (life_dev_packed_step has no context to own one; see
+// include/life_gpu.h).  Contexts pass their own SplitStreams instead.
+int thread_split_streams(SplitStreams** out) {
+  struct PerThread {
+    SplitStreams s[64];
+    ~PerThread() {
+      for (auto& x : s) split_streams_destroy(&x);
+    }
+  };
+  thread_local PerThread per;
   int dev = 0;
   LIFE_CUDA(cudaGetDevice(&dev));
-  SplitStreams& ss = per_dev[dev & 63];
-  if (!ss.side) {
-    LIFE_CUDA(cudaStreamCreateWithFlags(&ss.side, cudaStreamNonBlocking));
-    LIFE_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
-    LIFE_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
-  }
+  SplitStreams& ss = per.s[dev & 63];
+  LIFE_TRY(split_streams_init(&ss, dev));
   *out = &ss;
   return LIFE_OK;
 }
@@ -265,7 +300,7 @@ int split_streams(SplitStreams** out) {
 // and after them: 65535^2 41.5 -> 44.4 T/s, 131071 x 65536 43.3 -> 46.3;
 // one-wave grids (config 4, 16383^2) keep the single all-paths launch.
 template <int K>
-int launch_packed_deep(PackedStepArgs a, cudaStream_t s) {
+int launch_packed_deep(PackedStepArgs a, cudaStream_t s, SplitStreams* ss) {
   const bool fast_ok = !a.peer && a.width >= 64 && !a.trace;
   if (fast_ok && a.width % 32 == 0) return launch_packed_kernel<K, true>(a, s);
   const int32_t total = a.n_strips;
@@ -281,8 +316,7 @@ int launch_packed_deep(PackedStepArgs a, cudaStream_t s) {
   // strips at the single launch's segment length, the seam strips in the
   // blocks left over -- measured 2-10 % slower than one all-paths launch:
   // config 4 37.6 -> 36.5, 4097^2 7.8 -> 7.1.)
-  SplitStreams* ss = nullptr;
-  LIFE_TRY(split_streams(&ss));
+  if (!ss) LIFE_TRY(thread_split_streams(&ss));
   LIFE_CUDA(cudaEventRecord(ss->fork, s));
   LIFE_CUDA(cudaStreamWaitEvent(ss->side, ss->fork, 0));
   // One seam launch: strips s_last .. total-1 and (wrapping) strip 0.
@@ -301,31 +335,22 @@ int launch_packed_deep(PackedStepArgs a, cudaStream_t s) {
 }
 
 template <int K>
-int launch_packed(PackedStepArgs a, cudaStream_t s) {
+int launch_packed(PackedStepArgs a, cudaStream_t s, SplitStreams* ss) {
   if constexpr (K < 4) {  // shallow passes keep the all-paths kernel (no fast-only instance)
+    (void)ss;
     return launch_packed_kernel<K, false>(a, s);
   } else {
-    return launch_packed_deep<K>(a, s);
+    return launch_packed_deep<K>(a, s, ss);
   }
 }
 
-using PackedLauncher = int (*)(PackedStepArgs, cudaStream_t);
+using PackedLauncher = int (*)(PackedStepArgs, cudaStream_t, SplitStreams*);
 const PackedLauncher kPackedLaunchers[LIFE_MAX_TEMPORAL_DEPTH + 1] = {
     nullptr,           launch_packed<1>,  launch_packed<2>,  launch_packed<3>,
     launch_packed<4>,  launch_packed<5>,  launch_packed<6>,  launch_packed<7>,
     launch_packed<8>,  launch_packed<9>,  launch_packed<10>, launch_packed<11>,
     launch_packed<12>, launch_packed<13>, launch_packed<14>, launch_packed<15>,
     launch_packed<16>};
-
-int check_dims(int64_t width, int64_t height) {
-  if (width < 3 || height < 3)
-    return set_error(LIFE_ERR_DIMENSION_TOO_SMALL,
-                     "grid dimensions must be at least 3x3, got %lldx%lld",
-                     static_cast<long long>(width), static_cast<long long>(height));
-  if (width > (int64_t(1) << 40) || height > (int64_t(1) << 40))
-    return set_error(LIFE_ERR_CONFIG, "grid dimensions too large");
-  return LIFE_OK;
-}
 
 }  // namespace
 
@@ -339,7 +364,7 @@ const char* life_version(void) { return "life-b200 0.1 (sm_100a)"; }
 uint64_t life_kernel_launches(void) { return g_launches.load(); }
 // Debug hook (not in the public header): LIFE_TRACE builds record per-warp
 // (smid, start ns, end ns) of packed passes into this device buffer.
-void life_debug_set_trace(void* dev_buf) { g_trace = dev_buf; }
+void life_debug_set_trace(void* dev_buf) { g_trace.store(dev_buf); }
 
 int64_t life_packed_pitch_words(int64_t width) {
   return ceil_div(2 * ceil_div(width, 64), 32) * 32;
@@ -368,16 +393,17 @@ namespace {
 int launch_step1(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
                  uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
                  int64_t out_rows, cudaStream_t stream) {
-  static int blocks_per_sm[64] = {0};
+  static DeviceCache blocks_per_sm;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (blocks_per_sm[dev & 63] == 0) {
-    int nb = 0;
+  int nb = blocks_per_sm.get(dev);
+  if (nb == 0) {
     LIFE_CUDA(cudaFuncSetAttribute(packed_step1_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, kStep1Smem));
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, packed_step1_kernel,
                                                             kStep1Threads, kStep1Smem));
-    blocks_per_sm[dev & 63] = std::max(nb, 1);
+    nb = std::max(nb, 1);
+    blocks_per_sm.put(dev, nb);
   }
   Step1Args a{};
   a.in = in;
@@ -391,11 +417,8 @@ int launch_step1(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t 
   a.nv = static_cast<int32_t>(width / 128);
   a.n_strips = static_cast<int32_t>(ceil_div(a.nv, kStep1Stride));
   const int64_t resident_warps =
-      static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kStep1Threads / 32) * sm_count();
-  static const int waves = [] {  // LIFE_STEP1_WAVES: measurement knob
-    const char* e = std::getenv("LIFE_STEP1_WAVES");
-    return e && std::atoi(e) > 0 ? std::atoi(e) : 8;
-  }();
+      static_cast<int64_t>(nb) * (kStep1Threads / 32) * sm_count();
+  static const int64_t waves = std::max<int64_t>(knob("LIFE_STEP1_WAVES", 8), 1);
   const int64_t segs_target = std::max<int64_t>(1, waves * resident_warps / a.n_strips);
   a.seg_rows = std::max<int64_t>(ceil_div(out_rows, segs_target), 32);
   const int64_t warps = ceil_div(out_rows, a.seg_rows) * a.n_strips;
@@ -408,9 +431,13 @@ int launch_step1(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t 
 }
 }  // namespace
 
-int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
-                         uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
-                         int64_t out_rows, int32_t generations, void* stream) {
+}  // extern "C"
+
+namespace lifegpu {
+namespace detail {
+int packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                int64_t out_rows, int32_t generations, cudaStream_t stream, SplitStreams* ss) {
   if (generations < 1 || generations > LIFE_MAX_TEMPORAL_DEPTH)
     return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [1, %d], got %d",
                      LIFE_MAX_TEMPORAL_DEPTH, generations);
@@ -421,9 +448,9 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
   if (generations == 1 && width % 128 == 0 && in_pitch % 4 == 0 && out_pitch % 4 == 0 &&
       reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
       in_rows < (int64_t(1) << 31) && in_pitch * 4 < (int64_t(1) << 32) &&
-      out_pitch * 4 < (int64_t(1) << 32) && !g_trace)
+      out_pitch * 4 < (int64_t(1) << 32) && !g_trace.load(std::memory_order_relaxed))
     return launch_step1(in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
-                        out_rows, static_cast<cudaStream_t>(stream));
+                        out_rows, stream);
   PackedStepArgs a{};
   a.in = in;
   a.in_pitch = in_pitch;
@@ -438,8 +465,19 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
   a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
   a.strips_total = a.n_strips;
   a.tail_mask = tail_mask(width);
-  a.trace = g_trace;
-  return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
+  a.trace = g_trace.load(std::memory_order_relaxed);
+  return kPackedLaunchers[generations](a, stream, ss);
+}
+}  // namespace detail
+}  // namespace lifegpu
+
+extern "C" {
+
+int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                         uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                         int64_t out_rows, int32_t generations, void* stream) {
+  return packed_step(in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width, out_rows,
+                     generations, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
@@ -471,13 +509,13 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
   a.n_strips = static_cast<int32_t>(ceil_div(a.nw + 1, kStripStride));
   a.strips_total = a.n_strips;
   a.tail_mask = tail_mask(width);
-  a.trace = g_trace;
+  a.trace = g_trace.load(std::memory_order_relaxed);
   a.up = up;
   a.down = down;
   a.up_rows = up_rows;
   a.down_rows = down_rows;
-  a.peer = 1;
-  return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream));
+  a.peer = 1;  // peer launches never split (no side stream)
+  return kPackedLaunchers[generations](a, static_cast<cudaStream_t>(stream), nullptr);
 }
 
 namespace {
@@ -497,10 +535,7 @@ struct ResidentPlan {
 // Sweep (T cell-updates/s, 800 generations): 1024^2 at 256/512/1024
 // threads 1.78/1.91/1.57; 2048^2 2.48/3.00/3.04; 2048x4096 2.71/3.33/3.53.
 int resident_target_threads(int nw) {
-  static int v = [] {
-    const char* e = std::getenv("LIFE_RESIDENT_THREADS");
-    return e ? std::atoi(e) : 0;
-  }();
+  static const int v = static_cast<int>(knob("LIFE_RESIDENT_THREADS", 0));  // debug builds
   return v > 0 ? v : (nw <= 32 ? 512 : kResidentMaxThreads);
 }
 
@@ -510,8 +545,8 @@ int plan_resident(int64_t width, int64_t height, ResidentPlan* plan) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   LIFE_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  static int max_dyn[64] = {0};  // dynamic shared memory bytes per CTA (opt-in max - static)
-  if (max_dyn[dev & 63] == 0) {
+  static DeviceCache max_dyn;  // dynamic shared memory bytes per CTA (opt-in max - static)
+  if (max_dyn.get(dev) == 0) {
     cudaFuncAttributes fa{};
     LIFE_CUDA(cudaFuncGetAttributes(&fa, packed_resident_kernel));
     const int dyn = optin - static_cast<int>(fa.sharedSizeBytes);
@@ -519,9 +554,9 @@ int plan_resident(int64_t width, int64_t height, ResidentPlan* plan) {
                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     LIFE_CUDA(cudaFuncSetAttribute(packed_resident_kernel,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
-    max_dyn[dev & 63] = dyn;
+    max_dyn.put(dev, dyn);
   }
-  optin = max_dyn[dev & 63];
+  optin = max_dyn.get(dev);
   const int nw = static_cast<int>(width / 32);
   for (int C : {16, 8, 4, 2, 1}) {
     if (height < 2 * C) continue;
@@ -661,16 +696,17 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
       out_pitch < ceil_div(width, 16) * 16 || (in_pitch & 15) || (out_pitch & 15))
     return set_error(LIFE_ERR_CONFIG, "bad byte step geometry");
   if (out_rows == 0) return LIFE_OK;
-  static int blocks_per_sm[64] = {0};
+  static DeviceCache blocks_per_sm;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (blocks_per_sm[dev & 63] == 0) {
-    int nb = 0;
+  int nb = blocks_per_sm.get(dev);
+  if (nb == 0) {
     LIFE_CUDA(cudaFuncSetAttribute(byte_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kByteSmem));
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, byte_step_kernel,
                                                             kByteThreads, kByteSmem));
-    blocks_per_sm[dev & 63] = std::max(nb, 1);
+    nb = std::max(nb, 1);
+    blocks_per_sm.put(dev, nb);
   }
   ByteStepArgs a{};
   a.in = in;
@@ -688,7 +724,7 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
       out_pitch >= (int64_t(1) << 32) || out_rows >= (int64_t(1) << 31))
     return set_error(LIFE_ERR_CONFIG, "grid too large for the byte engine");
   const int64_t resident_warps =
-      static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kByteThreads / 32) * sm_count();
+      static_cast<int64_t>(nb) * (kByteThreads / 32) * sm_count();
   // Many short segments (>= 32 rows; the 2 halo rows are L2 hits) so the
   // independent warps balance across SMs: 8 waves measured +3 % over 2.
 #ifndef LIFE_BYTE_WAVES
@@ -709,25 +745,24 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
 namespace {
 template <int K>
 int launch_byte_tb(ByteStepArgs a, cudaStream_t s) {
-  static int blocks_per_sm[64] = {0};
+  static DeviceCache blocks_per_sm;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (blocks_per_sm[dev & 63] == 0) {
-    int nb = 0;
+  int nb = blocks_per_sm.get(dev);
+  if (nb == 0) {
     LIFE_CUDA(cudaFuncSetAttribute(byte_tb_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kByteTbSmem));
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, byte_tb_kernel<K>, kByteThreads,
                                                             kByteTbSmem));
-    blocks_per_sm[dev & 63] = std::max(nb, 1);
+    nb = std::max(nb, 1);
+    blocks_per_sm.put(dev, nb);
   }
   // Segments long enough to amortise the 3K-1 step pipeline fill: one wave
   // of independent warps.
   const int64_t resident_warps =
-      static_cast<int64_t>(blocks_per_sm[dev & 63]) * (kByteThreads / 32) * sm_count();
-  static const int waves = [] {
-    const char* e = std::getenv("LIFE_BYTE_TB_WAVES");
-    return e && std::atoi(e) > 0 ? std::atoi(e) : 1;  // 1 wave: 8.41 vs 8.02 T/s (2) at 16384^2, K = 6
-  }();
+      static_cast<int64_t>(nb) * (kByteThreads / 32) * sm_count();
+  // 1 wave: 8.41 vs 8.02 T/s (2) at 16384^2, K = 6 (LIFE_BYTE_TB_WAVES, debug builds)
+  static const int64_t waves = std::max<int64_t>(knob("LIFE_BYTE_TB_WAVES", 1), 1);
   const int64_t segs_target = std::max<int64_t>(1, waves * resident_warps / a.n_strips);
   a.seg_rows = std::max<int64_t>(ceil_div(a.out_rows, segs_target), 16 * K);
   const int64_t warps = ceil_div(a.out_rows, a.seg_rows) * a.n_strips;
@@ -914,6 +949,18 @@ struct life_ctx {
   size_t batch_bytes = 0;
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaStream_t cs[4] = {};  // life_run_batch chunk streams (first / last grid)
+  // Side streams of split launches: [0] for `stream`, [1..4] for cs[0..3].
+  SplitStreams split[5];
+  // Options (life_ctx_set_option).
+  int batch_trap = -1;   // LIFE_OPT_BATCH_TRAPEZOID
+  bool profile = false;  // LIFE_OPT_PROFILE
+  // Statistics of the last life_run (life_ctx_band_stats, band 0).
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  double run_ms = 0.0, pass_ms = 0.0;
+  int64_t passes = 0;
+  // Multi-device contexts (life_ctx_create_multi): every grid / run entry
+  // point dispatches to life_multi.cu; the fields above are unused.
+  MultiState* multi = nullptr;
 };
 
 namespace {
@@ -1029,22 +1076,27 @@ constexpr int64_t kResidentAutoCells = int64_t(1) << 22;
 // 3.02 3.78 3.36 3.22 2.97 2.70 (short grids pay the 3K-1 step pipeline fill).
 int byte_auto_depth(int64_t w, int64_t h) { return w * h >= (int64_t(1) << 26) ? 6 : 4; }
 
-// temporal_depth 0 on the multi-pass packed engine: K = 16, except tori whose
-// passes run as one all-paths launch (W % 32 != 0, less than ~3 block waves
-// deep), where K = 12 fits 12 warps per SM instead of 8 (config 4: 37.5 ->
-// 38.6 T/s; kbench depth sweep, DESIGN.md section 4.1).
-int packed_auto_depth(int64_t w, int64_t h) {
-  const int64_t strips = ceil_div(nw32(w) + 1, kStripStride);
-  return (w % 32 != 0 && strips * h < 2000000) ? 12 : LIFE_MAX_TEMPORAL_DEPTH;
-}
-
 bool resident_auto(int64_t w, int64_t h) {
   return w % 32 == 0 && w * h <= kResidentAutoCells && life_resident_cluster_size(w, h) > 0;
 }
 
 }  // namespace
 
+// temporal_depth 0 on the multi-pass packed engine: K = 16, except tori whose
+// passes run as one all-paths launch (W % 32 != 0, less than ~3 block waves
+// deep), where K = 12 fits 12 warps per SM instead of 8 (config 4: 37.5 ->
+// 38.6 T/s; kbench depth sweep, DESIGN.md section 4.1).
+int lifegpu::detail::packed_auto_depth(int64_t w, int64_t h) {
+  const int64_t strips = ceil_div(nw32(w) + 1, kStripStride);
+  return (w % 32 != 0 && strips * h < 2000000) ? 12 : LIFE_MAX_TEMPORAL_DEPTH;
+}
+
 extern "C" {
+
+int life_packed_auto_depth(int64_t width, int64_t height) {
+  if (width < 1 || height < 1) return LIFE_MAX_TEMPORAL_DEPTH;
+  return packed_auto_depth(width, height);
+}
 
 int life_ctx_create(int device, life_ctx** out) {
   if (!out) return set_error(LIFE_ERR_CONFIG, "null output pointer");
@@ -1069,8 +1121,25 @@ int life_ctx_create(int device, life_ctx** out) {
   return LIFE_OK;
 }
 
+int life_ctx_create_multi(int32_t n, const int* devices, life_ctx** out) {
+  if (!out) return set_error(LIFE_ERR_CONFIG, "null output pointer");
+  *out = nullptr;
+  MultiState* m = nullptr;
+  LIFE_TRY(multi_create(n, devices, &m));
+  life_ctx* c = new life_ctx();
+  c->device = devices[0];
+  c->multi = m;
+  *out = c;
+  return LIFE_OK;
+}
+
 int life_ctx_destroy(life_ctx* c) {
   if (!c) return LIFE_OK;
+  if (c->multi) {
+    multi_destroy(c->multi);
+    delete c;
+    return LIFE_OK;
+  }
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   free_buffers(c);
@@ -1080,7 +1149,16 @@ int life_ctx_destroy(life_ctx* c) {
   for (auto& b : c->batch)
     if (b) cudaFree(b);
   for (auto& st : c->cs)
-    if (st) cudaStreamDestroy(st);
+    if (st) {
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    }
+  for (auto& ss : c->split) {
+    if (ss.side) cudaStreamSynchronize(ss.side);
+    split_streams_destroy(&ss);
+  }
+  if (c->t0) cudaEventDestroy(c->t0);
+  if (c->t1) cudaEventDestroy(c->t1);
   if (c->h2d) cudaStreamDestroy(c->h2d);
   if (c->d2h) cudaStreamDestroy(c->d2h);
   if (c->own) cudaStreamDestroy(c->own);
@@ -1089,6 +1167,9 @@ int life_ctx_destroy(life_ctx* c) {
 }
 
 int life_ctx_set_stream(life_ctx* c, void* stream) {
+  if (c && c->multi)
+    return set_error(LIFE_ERR_CONFIG,
+                     "a multi-device context orders its work on its own per-band streams");
   LIFE_TRY(activate(c));
   LIFE_CUDA(cudaStreamSynchronize(c->stream));
   c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
@@ -1096,12 +1177,73 @@ int life_ctx_set_stream(life_ctx* c, void* stream) {
 }
 
 int life_ctx_sync(life_ctx* c) {
+  if (c && c->multi) return multi_sync(c->multi);
   LIFE_TRY(activate(c));
   LIFE_CUDA(cudaStreamSynchronize(c->stream));
   return LIFE_OK;
 }
 
+int life_ctx_set_option(life_ctx* c, int32_t option, int64_t value) {
+  if (!c) return set_error(LIFE_ERR_STATE, "null context");
+  if (c->multi) return multi_set_option(c->multi, option, value);
+  switch (option) {
+    case LIFE_OPT_PROFILE:
+      c->profile = value != 0;
+      return LIFE_OK;
+    case LIFE_OPT_BATCH_TRAPEZOID:
+      if (value < -1 || value > 1)
+        return set_error(LIFE_ERR_CONFIG, "LIFE_OPT_BATCH_TRAPEZOID must be -1, 0 or 1");
+      c->batch_trap = static_cast<int>(value);
+      return LIFE_OK;
+    case LIFE_OPT_HALO:
+      return set_error(LIFE_ERR_CONFIG, "LIFE_OPT_HALO applies to multi-device contexts");
+    default:
+      return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
+  }
+}
+
+int life_ctx_get_option(life_ctx* c, int32_t option, int64_t* value) {
+  if (!c || !value) return set_error(LIFE_ERR_STATE, "null context or output");
+  if (c->multi) return multi_get_option(c->multi, option, value);
+  switch (option) {
+    case LIFE_OPT_PROFILE: *value = c->profile ? 1 : 0; return LIFE_OK;
+    case LIFE_OPT_BATCH_TRAPEZOID: *value = c->batch_trap; return LIFE_OK;
+    default: return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
+  }
+}
+
+int life_ctx_bands(life_ctx* c, int32_t* n, int64_t* bounds, int32_t* devices, int32_t* halo) {
+  if (!c) return set_error(LIFE_ERR_STATE, "null context");
+  if (c->multi) return multi_bands(c->multi, n, bounds, devices, halo);
+  if (n) *n = 1;
+  if (bounds) {
+    bounds[0] = 0;
+    bounds[1] = c->H;
+  }
+  if (devices) devices[0] = c->device;
+  if (halo) *halo = -1;
+  return LIFE_OK;
+}
+
+int life_ctx_band_stats(life_ctx* c, int32_t band, life_band_stats* out) {
+  if (!c || !out) return set_error(LIFE_ERR_STATE, "null context or output");
+  if (c->multi) return multi_band_stats(c->multi, band, out);
+  if (band != 0) return set_error(LIFE_ERR_CONFIG, "band %d out of range [0, 1)", band);
+  *out = life_band_stats{};
+  out->band = 0;
+  out->device = c->device;
+  out->y0 = 0;
+  out->rows = c->H;
+  out->passes = c->passes;
+  out->run_ms = c->run_ms;
+  out->interior_ms = c->pass_ms;
+  out->edge_ms = 0.0;
+  out->wait_ms = c->profile ? c->run_ms - c->pass_ms : 0.0;
+  return LIFE_OK;
+}
+
 int life_grid_dims(life_ctx* c, int64_t* w, int64_t* h) {
+  if (c && c->multi) return multi_dims(c->multi, w, h);
   if (!c) return set_error(LIFE_ERR_STATE, "null context");
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   *w = c->W;
@@ -1111,6 +1253,7 @@ int life_grid_dims(life_ctx* c, int64_t* w, int64_t* h) {
 
 int life_grid_upload_u8(life_ctx* c, const uint8_t* cells, int64_t width, int64_t height,
                         int64_t row_stride) {
+  if (c && c->multi) return multi_upload_u8(c->multi, cells, width, height, row_stride);
   LIFE_TRY(activate(c));
   if (!cells) return set_error(LIFE_ERR_CONFIG, "null cell buffer");
   LIFE_TRY(set_dims(c, width, height));
@@ -1130,6 +1273,7 @@ int life_grid_upload_u8(life_ctx* c, const uint8_t* cells, int64_t width, int64_
 
 int life_grid_upload_packed(life_ctx* c, const uint64_t* words, int64_t width, int64_t height,
                             int64_t words_per_row) {
+  if (c && c->multi) return multi_upload_packed(c->multi, words, width, height, words_per_row);
   LIFE_TRY(activate(c));
   if (!words) return set_error(LIFE_ERR_CONFIG, "null word buffer");
   LIFE_TRY(set_dims(c, width, height));
@@ -1151,6 +1295,10 @@ int life_grid_upload_packed(life_ctx* c, const uint64_t* words, int64_t width, i
 
 int life_grid_init_random(life_ctx* c, int64_t width, int64_t height, double density,
                           uint64_t seed, int engine) {
+  if (c && c->multi) {
+    LIFE_TRY(check_engine(engine));
+    return multi_init_random(c->multi, width, height, density, seed);
+  }
   LIFE_TRY(activate(c));
   LIFE_TRY(check_engine(engine));
   if (!(density >= 0.0 && density <= 1.0))
@@ -1175,6 +1323,10 @@ int life_grid_init_random(life_ctx* c, int64_t width, int64_t height, double den
 
 int life_grid_init_soup(life_ctx* c, int64_t width, int64_t height, double coverage,
                         int32_t block_size, double density, uint64_t seed, int engine) {
+  if (c && c->multi) {
+    LIFE_TRY(check_engine(engine));
+    return multi_init_soup(c->multi, width, height, coverage, block_size, density, seed);
+  }
   LIFE_TRY(activate(c));
   LIFE_TRY(check_engine(engine));
   if (!(density >= 0.0 && density <= 1.0))
@@ -1215,6 +1367,7 @@ int life_grid_init_soup(life_ctx* c, int64_t width, int64_t height, double cover
 
 int life_grid_place_u8(life_ctx* c, const uint8_t* pattern, int64_t pw, int64_t ph, int64_t x0,
                        int64_t y0) {
+  if (c && c->multi) return multi_place_u8(c->multi, pattern, pw, ph, x0, y0);
   LIFE_TRY(activate(c));
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   if (pw < 0 || ph < 0 || (pw * ph > 0 && !pattern))
@@ -1244,6 +1397,7 @@ int life_grid_place_u8(life_ctx* c, const uint8_t* pattern, int64_t pw, int64_t 
 }
 
 int life_grid_download_u8(life_ctx* c, uint8_t* cells, int64_t row_stride) {
+  if (c && c->multi) return multi_download_u8(c->multi, cells, row_stride);
   LIFE_TRY(activate(c));
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   if (!cells || row_stride < c->W) return set_error(LIFE_ERR_CONFIG, "bad output buffer");
@@ -1263,6 +1417,7 @@ int life_grid_download_u8(life_ctx* c, uint8_t* cells, int64_t row_stride) {
 }
 
 int life_grid_download_packed(life_ctx* c, uint64_t* words, int64_t words_per_row) {
+  if (c && c->multi) return multi_download_packed(c->multi, words, words_per_row);
   LIFE_TRY(activate(c));
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   const int64_t wpr = ceil_div(c->W, 64);
@@ -1283,6 +1438,7 @@ int life_grid_download_packed(life_ctx* c, uint64_t* words, int64_t words_per_ro
 }
 
 int life_grid_window_u8(life_ctx* c, int64_t x0, int64_t y0, int64_t w, int64_t h, uint8_t* out) {
+  if (c && c->multi) return multi_window_u8(c->multi, x0, y0, w, h, out);
   LIFE_TRY(activate(c));
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   if (w < 0 || h < 0 || !out) return set_error(LIFE_ERR_CONFIG, "bad window");
@@ -1308,6 +1464,7 @@ int life_grid_window_u8(life_ctx* c, int64_t x0, int64_t y0, int64_t w, int64_t 
 }
 
 int life_population(life_ctx* c, uint64_t* out) {
+  if (c && c->multi) return multi_population(c->multi, out);
   LIFE_TRY(activate(c));
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   LIFE_TRY(ensure_counts(c, 1));
@@ -1318,6 +1475,7 @@ int life_population(life_ctx* c, uint64_t* out) {
 }
 
 int life_grid_hash(life_ctx* c, uint64_t* out) {
+  if (c && c->multi) return multi_hash(c->multi, out);
   LIFE_TRY(activate(c));
   if (!out) return set_error(LIFE_ERR_CONFIG, "null output pointer");
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
@@ -1340,23 +1498,14 @@ int life_grid_hash(life_ctx* c, uint64_t* out) {
 
 int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
              const int64_t* checkpoints, int32_t n_checkpoints, uint64_t* populations) {
+  if (c && c->multi) {
+    LIFE_TRY(check_engine(engine));
+    return multi_run(c->multi, generations, engine, temporal_depth, checkpoints, n_checkpoints,
+                     populations);
+  }
   LIFE_TRY(activate(c));
   LIFE_TRY(check_engine(engine));
-  // check_run_config (engine.cpp:127-148)
-  if (generations < 0)
-    return set_error(LIFE_ERR_CONFIG, "iteration count must be non-negative, got %lld",
-                     static_cast<long long>(generations));
-  if (n_checkpoints < 0 || (n_checkpoints > 0 && (!checkpoints || !populations)))
-    return set_error(LIFE_ERR_CONFIG, "bad checkpoint buffers");
-  int64_t prev = -1;
-  for (int32_t i = 0; i < n_checkpoints; ++i) {
-    const int64_t cp = checkpoints[i];
-    if (cp < 0 || cp > generations)
-      return set_error(LIFE_ERR_CONFIG, "checkpoint %lld is outside [0, iterations=%lld]",
-                       static_cast<long long>(cp), static_cast<long long>(generations));
-    if (cp <= prev) return set_error(LIFE_ERR_CONFIG, "checkpoints must be strictly ascending");
-    prev = cp;
-  }
+  LIFE_TRY(check_run_args(generations, checkpoints, n_checkpoints, populations));
   int depth = temporal_depth;
   if (engine != LIFE_ENGINE_BYTE) {
     if (depth < 0 || depth > LIFE_MAX_TEMPORAL_DEPTH)
@@ -1383,6 +1532,24 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   LIFE_TRY(to_layout(c, engine_layout(engine)));
   if (n_checkpoints > 0) LIFE_TRY(ensure_counts(c, n_checkpoints));
+  LIFE_TRY(split_streams_init(&c->split[0], c->device));
+  if (!c->t0) LIFE_CUDA(cudaEventCreate(&c->t0));
+  if (!c->t1) LIFE_CUDA(cudaEventCreate(&c->t1));
+  // LIFE_OPT_PROFILE: CUDA events around every pass (life_ctx_band_stats).
+  struct PassEvents {
+    std::vector<cudaEvent_t> v;
+    ~PassEvents() {
+      for (cudaEvent_t e : v) cudaEventDestroy(e);
+    }
+  } prof;
+  auto prof_mark = [&]() -> int {
+    if (!c->profile) return LIFE_OK;
+    cudaEvent_t e;
+    LIFE_CUDA(cudaEventCreate(&e));
+    prof.v.push_back(e);
+    LIFE_CUDA(cudaEventRecord(e, c->stream));
+    return LIFE_OK;
+  };
 
   int32_t ci = 0;
   auto record = [&](int64_t gen) -> int {
@@ -1393,22 +1560,27 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
     return LIFE_OK;
   };
   LIFE_TRY(record(0));
+  c->passes = 0;
+  LIFE_CUDA(cudaEventRecord(c->t0, c->stream));
   int64_t done = 0;
   while (done < generations) {
     const int64_t stop = ci < n_checkpoints ? checkpoints[ci] : generations;
+    LIFE_TRY(prof_mark());
     if (engine == LIFE_ENGINE_RESIDENT) {  // every generation up to the next stop in one launch
       LIFE_TRY(life_dev_packed_run_resident(c->pk[c->pk_cur], c->pk[c->pk_cur ^ 1], c->pk_pitch,
                                             c->W, c->H, stop - done, c->stream));
       c->pk_cur ^= 1;
       done = stop;
+      ++c->passes;
+      LIFE_TRY(prof_mark());
       LIFE_TRY(record(done));
       continue;
     }
     const int step = static_cast<int>(std::min<int64_t>(depth, stop - done));
     if (engine == LIFE_ENGINE_PACKED) {
       const int nxt = c->pk_cur ^ 1;
-      LIFE_TRY(life_dev_packed_step(c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt],
-                                    c->pk_pitch, 0, c->W, c->H, step, c->stream));
+      LIFE_TRY(packed_step(c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt], c->pk_pitch, 0,
+                           c->W, c->H, step, c->stream, &c->split[0]));
       c->pk_cur = nxt;
     } else {
       const int nxt = c->by_cur ^ 1;
@@ -1417,13 +1589,24 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
       c->by_cur = nxt;
     }
     done += step;
+    ++c->passes;
+    LIFE_TRY(prof_mark());
     LIFE_TRY(record(done));
   }
+  LIFE_CUDA(cudaEventRecord(c->t1, c->stream));
   if (n_checkpoints > 0) {
     LIFE_CUDA(cudaMemcpyAsync(populations, c->counts, sizeof(uint64_t) * n_checkpoints,
                               cudaMemcpyDeviceToHost, c->stream));
   }
   LIFE_CUDA(cudaStreamSynchronize(c->stream));
+  float ms = 0.0f;
+  LIFE_CUDA(cudaEventElapsedTime(&ms, c->t0, c->t1));
+  c->run_ms = ms;
+  c->pass_ms = 0.0;
+  for (size_t i = 0; i + 1 < prof.v.size(); i += 2) {
+    LIFE_CUDA(cudaEventElapsedTime(&ms, prof.v[i], prof.v[i + 1]));
+    c->pass_ms += ms;
+  }
   return LIFE_OK;
 }
 
@@ -1464,14 +1647,14 @@ struct BatchGeom {
 
 // out rows [r0, r0 + rows) (mod H) of pass p: one launch per contiguous piece.
 int pass_rows(const BatchGeom& g, uint32_t* const* buf, int p, int64_t r0, int64_t rows,
-              cudaStream_t s) {
+              cudaStream_t s, SplitStreams* ss) {
   const int k = static_cast<int>(std::min<int64_t>(g.depth, g.generations - int64_t(p) * g.depth));
   r0 %= g.height;
   if (r0 < 0) r0 += g.height;
   while (rows > 0) {
     const int64_t piece = std::min(rows, g.height - r0);
-    LIFE_TRY(life_dev_packed_step(buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch, r0,
-                                  g.width, piece, k, s));
+    LIFE_TRY(packed_step(buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch, r0,
+                         g.width, piece, k, s, ss));
     rows -= piece;
     r0 = 0;
   }
@@ -1503,6 +1686,9 @@ int copy_rows(const BatchGeom& g, void* host, const uint32_t* dev, int64_t r0, i
 int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* outputs, int32_t n,
                    int64_t width, int64_t height, int64_t words_per_row, int64_t generations,
                    int temporal_depth, float* elapsed_ms) {
+  if (c && c->multi)
+    return multi_run_batch(c->multi, inputs, outputs, n, width, height, words_per_row,
+                           generations, temporal_depth, elapsed_ms);
   LIFE_TRY(activate(c));
   LIFE_TRY(check_dims(width, height));
   if (n < 0 || (n > 0 && (!inputs || !outputs)))
@@ -1532,6 +1718,7 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
     c->batch_bytes = bytes;
     LIFE_CUDA(cudaStreamSynchronize(c->stream));
   }
+  for (auto& ss : c->split) LIFE_TRY(split_streams_init(&ss, c->device));
   if (!c->h2d) LIFE_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   if (!c->d2h) LIFE_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
   BatchGeom g{};
@@ -1548,9 +1735,8 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   // passes to run near full speed (the schedule launches 2 x 16 small passes
   // per pass): measured e2e / device value, 3 grids, with / without it:
   // config 5 (16384-row chunks) 0.965 / 0.882, config 3 (4096-row chunks)
-  // 0.850 / 0.945.  LIFE_BATCH_TRAP=0 / 1 forces it off / on (when it fits).
-  const char* trap_var = std::getenv("LIFE_BATCH_TRAP");  // read per call (tests force it)
-  const int trap_env = trap_var ? std::atoi(trap_var) : -1;
+  // 0.850 / 0.945.  LIFE_OPT_BATCH_TRAPEZOID 0 / 1 forces it off / on (when it fits).
+  const int trap_env = c->batch_trap;
   const bool fits = n >= 1 && generations > 0 &&
                     height / kTrapChunks >= 2 * kShrink * g.passes + 1024;
   // temporal_depth 0 on a small W % 32 == 0 torus: the cluster-resident engine
@@ -1615,7 +1801,7 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
         rc = life_dev_packed_run_resident(buf[0], buf[1], pitch, width, height, generations,
                                           c->stream);
       } else {
-        for (int p = 0; p < P && rc == LIFE_OK; ++p) rc = pass_rows(g, buf, p, 0, height, c->stream);
+        for (int p = 0; p < P && rc == LIFE_OK; ++p) rc = pass_rows(g, buf, p, 0, height, c->stream, &c->split[0]);
       }
       LIFE_CUDA(cudaEventRecord(comp[i], c->stream));
       // Download on the D2H stream.
@@ -1645,7 +1831,8 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
           buf[0] + y0 * pitch, pitch, nw, tail_mask(width), rows);
       LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
       for (int p = 0; p < P && rc == LIFE_OK; ++p)
-        rc = pass_rows(g, buf, p, y0 + kShrink * (p + 1), rows - 2 * kShrink * (p + 1), st);
+        rc = pass_rows(g, buf, p, y0 + kShrink * (p + 1), rows - 2 * kShrink * (p + 1), st,
+                       &c->split[1 + ch % 2]);
       LIFE_CUDA(cudaEventRecord(trap_done[ch], st));
     }
     // Triangles at boundary b (row bounds[b]) between chunks b-1 and b.
@@ -1655,7 +1842,8 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
       LIFE_CUDA(cudaStreamWaitEvent(st, trap_done[(b + nc - 1) % nc], 0));
       LIFE_CUDA(cudaStreamWaitEvent(st, trap_done[b], 0));
       for (int p = 0; p < P && rc == LIFE_OK; ++p)
-        rc = pass_rows(g, buf, p, g.bounds[b] - kShrink * (p + 1), 2 * kShrink * (p + 1), st);
+        rc = pass_rows(g, buf, p, g.bounds[b] - kShrink * (p + 1), 2 * kShrink * (p + 1), st,
+                       &c->split[3 + bi % 2]);
       LIFE_CUDA(cudaEventRecord(tri_done[b], st));
     }
     // Downloads: each chunk's interior when its trapezoid is done, then the
@@ -1688,3 +1876,42 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
 }
 
 }  // extern "C"
+
+// ---- small launchers shared with life_multi.cu ------------------------------
+namespace lifegpu {
+namespace detail {
+
+int launch_mask_tail(uint32_t* words, int64_t pitch, int64_t width, int64_t rows,
+                     cudaStream_t s) {
+  const int32_t nw = static_cast<int32_t>(nw32(width));
+  const int64_t n = rows * (pitch - nw + 1);
+  if (n <= 0) return LIFE_OK;
+  packed_mask_tail_kernel<<<grid_stride_blocks(n, 256), 256, 0, s>>>(words, pitch, nw,
+                                                                      tail_mask(width), rows);
+  LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
+  return LIFE_OK;
+}
+
+int launch_place_packed(uint32_t* words, int64_t pitch, const uint8_t* dev_pattern, int64_t pw,
+                        int64_t ph, int64_t x0, int64_t y0, cudaStream_t s) {
+  if (pw * ph == 0) return LIFE_OK;
+  const int64_t n = (((x0 + pw - 1) >> 5) - (x0 >> 5) + 1) * ph;
+  place_packed_kernel<<<grid_stride_blocks(n, 256), 256, 0, s>>>(words, pitch, dev_pattern, pw,
+                                                                  ph, x0, y0);
+  LIFE_CHECK_LAUNCH("place_packed_kernel");
+  return LIFE_OK;
+}
+
+int launch_window_packed(const uint32_t* words, int64_t pitch, int64_t width, int64_t height,
+                         int64_t x0, int64_t y0, int64_t w, int64_t h, uint8_t* dev_out,
+                         cudaStream_t s) {
+  const int64_t n = w * h;
+  if (n == 0) return LIFE_OK;
+  packed_window_kernel<<<grid_stride_blocks(n, 256), 256, 0, s>>>(words, pitch, width, height,
+                                                                   x0, y0, w, h, dev_out);
+  LIFE_CHECK_LAUNCH("packed_window_kernel");
+  return LIFE_OK;
+}
+
+}  // namespace detail
+}  // namespace lifegpu

@@ -14,6 +14,8 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -69,10 +71,17 @@ enum class Engine { Packed = LIFE_ENGINE_PACKED, Byte = LIFE_ENGINE_BYTE, Reside
 // RunConfig (engine.hpp:11-15) with the GPU strategy fields.
 struct RunConfig {
   Engine engine = Engine::Packed;
-  int temporal_depth = 0;  // generations per packed kernel pass, 0 = 16
-  int workers = 1;         // validated like the reference (>= 1, <= rows)
+  // Generations per kernel pass; 0 = auto: the cluster-resident engine for
+  // small W % 32 == 0 tori (<= 2^22 cells, one GPU), else 16 -- 12 for
+  // W % 32 != 0 tori less than ~3 block waves deep (life_packed_auto_depth).
+  int temporal_depth = 0;
+  int workers = 1;  // validated like the reference (>= 1, <= rows)
   int64_t iterations = 0;
   int device = 0;
+  // Row bands over several GPUs (life_ctx_create_multi, band_bounds of
+  // decomposition.cpp:12-24): one band per entry, ids may repeat.  Empty =
+  // the single GPU `device`.  The packed engine only.
+  std::vector<int> devices;
 };
 
 // RunStats (engine.hpp:17-22) with uint64 populations.
@@ -91,6 +100,10 @@ struct RunResult {
 class Context {
  public:
   explicit Context(int device = 0) { check(life_ctx_create(device, &ctx_)); }
+  // Row bands over `devices` (repeats allowed).
+  explicit Context(const std::vector<int>& devices) {
+    check(life_ctx_create_multi(static_cast<int32_t>(devices.size()), devices.data(), &ctx_));
+  }
   ~Context() { life_ctx_destroy(ctx_); }
   Context(const Context&) = delete;
   Context& operator=(const Context&) = delete;
@@ -131,11 +144,39 @@ class Context {
     check(life_grid_window_u8(ctx_, x0, y0, w, h, out.data()));
     return out;
   }
+  std::vector<life_band_stats> band_stats() {
+    int32_t n = 0;
+    check(life_ctx_bands(ctx_, &n, nullptr, nullptr, nullptr));
+    std::vector<life_band_stats> out(static_cast<size_t>(n));
+    for (int32_t i = 0; i < n; ++i) check(life_ctx_band_stats(ctx_, i, &out[i]));
+    return out;
+  }
   life_ctx* handle() const { return ctx_; }
 
  private:
   life_ctx* ctx_ = nullptr;
 };
+
+// One cached context per host thread and device set: a drop-in run() call
+// reuses its device buffers instead of creating a context and allocating
+// two grid buffers every time (contexts are single-thread objects, hence
+// thread_local).  release_cached_contexts() frees this thread's.
+inline std::map<std::vector<int>, std::unique_ptr<Context>>& cached_contexts() {
+  thread_local std::map<std::vector<int>, std::unique_ptr<Context>> cache;
+  return cache;
+}
+inline Context& cached_context(const RunConfig& cfg) {
+  const std::vector<int> key = cfg.devices.empty() ? std::vector<int>{cfg.device} : cfg.devices;
+  auto& cache = cached_contexts();
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    std::unique_ptr<Context> c = cfg.devices.empty() ? std::make_unique<Context>(cfg.device)
+                                                     : std::make_unique<Context>(cfg.devices);
+    it = cache.emplace(key, std::move(c)).first;
+  }
+  return *it->second;
+}
+inline void release_cached_contexts() { cached_contexts().clear(); }
 
 // run (engine.cpp:157-214): check_run_config's rules (:127-148) and
 // partition_rows' TooManyParts (decomposition.cpp:26-30) on `workers`, then
@@ -161,7 +202,7 @@ RunResult<GridT> run(GridT initial, const RunConfig& cfg,
     if (cp <= prev) throw ConfigError("checkpoints must be strictly ascending");
     prev = cp;
   }
-  Context ctx(cfg.device);
+  Context& ctx = cached_context(cfg);
   ctx.upload(initial);
   const std::vector<uint64_t> pops = ctx.run(cfg.iterations, cfg.engine, cfg.temporal_depth, checkpoints);
   ctx.download(initial);

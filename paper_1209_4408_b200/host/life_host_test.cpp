@@ -8,6 +8,7 @@
 #include <functional>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "life_gpu.hpp"
@@ -164,6 +165,52 @@ int main() {
       h[i] = ctx.hash();
     }
     return h[0] == h[1] && h[1] == h[2];
+  });
+
+  check_case("row bands over several devices equal the serial step (run(), devices = {0,0,0})", [] {
+    for (int seed = 0; seed < 3; ++seed) {
+      const int w = 70 + 33 * seed, h = 41 + 10 * seed;
+      Grid g = lifegpu::random_fill<Grid>(w, h, 0.35, 100 + seed);
+      Grid want = g;
+      for (int i = 0; i < 37; ++i) want = serial_step(want);
+      for (std::vector<int> devs : {std::vector<int>{0, 0}, std::vector<int>{0, 0, 0},
+                                    std::vector<int>(7, 0)}) {
+        RunConfig c;
+        c.iterations = 37;
+        c.workers = static_cast<int>(devs.size());
+        c.devices = devs;
+        auto r = lifegpu::run(g, c, {0, 5, 37});
+        if (!(r.grid == want)) return false;
+        uint64_t pop = 0;
+        for (int i = 0; i < w * h; ++i) pop += want.data()[i];
+        if (r.stats.population_checkpoints.back().second != pop) return false;
+      }
+    }
+    return true;
+  });
+
+  check_case("two host threads run concurrently (SPEC.md:112: run() is thread-safe)", [] {
+    bool ok[2] = {false, false};
+    auto job = [&](int t) {
+      try {
+        for (int rep = 0; rep < 4; ++rep) {
+          const int w = 200 + 64 * t + rep, h = 150 + rep;
+          Grid g = lifegpu::random_fill<Grid>(w, h, 0.4, 7 * t + rep);
+          Grid want = g;
+          for (int i = 0; i < 25; ++i) want = serial_step(want);
+          RunConfig c;
+          c.iterations = 25;
+          c.temporal_depth = t == 0 ? 16 : 5;
+          if (!(lifegpu::run(g, c).grid == want)) return;
+        }
+        ok[t] = true;
+      } catch (...) {
+      }
+    };
+    std::thread a(job, 0), b(job, 1);
+    a.join();
+    b.join();
+    return ok[0] && ok[1];
   });
 
   std::printf("%d failure(s)\n", failures);

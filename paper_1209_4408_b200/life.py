@@ -211,6 +211,9 @@ class RunConfig:
     workers: int = 1
     iterations: int = 0
     device: int = 0
+    # Row bands over several GPUs (life_ctx_create_multi): one band per entry,
+    # ids may repeat.  Empty = one GPU (`device`).
+    devices: tuple = ()
 
 
 @dataclass
@@ -228,13 +231,22 @@ class RunResult:
 
 
 class Engine:
-    """One C-ABI context: a grid resident on one GPU."""
+    """One C-ABI context: a grid resident on one GPU, or -- with `devices` --
+    split into row bands over several GPUs (life_ctx_create_multi; repeated
+    device ids put several bands on one GPU)."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, devices: Sequence[int] | None = None):
         self._lib = capi.lib()
         self._ctx = C.c_void_p()
-        check(self._lib.life_ctx_create(device, C.byref(self._ctx)))
-        self.device = device
+        if devices is not None:
+            devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+            check(self._lib.life_ctx_create_multi(len(devices), devs, C.byref(self._ctx)))
+            self.device = int(devices[0]) if len(devices) else device
+            self.devices = [int(d) for d in devices]
+        else:
+            check(self._lib.life_ctx_create(device, C.byref(self._ctx)))
+            self.device = device
+            self.devices = [device]
 
     def close(self) -> None:
         if self._ctx:
@@ -262,6 +274,35 @@ class Engine:
 
     def sync(self) -> None:
         check(self._lib.life_ctx_sync(self._ctx))
+
+    def set_option(self, option: int, value: int) -> None:
+        check(self._lib.life_ctx_set_option(self._ctx, option, value))
+
+    def get_option(self, option: int) -> int:
+        v = C.c_int64()
+        check(self._lib.life_ctx_get_option(self._ctx, option, C.byref(v)))
+        return int(v.value)
+
+    def bands(self) -> dict:
+        """Band layout: {'bounds': [...n+1 row cuts], 'devices': [...], 'halo': int}."""
+        n, halo = C.c_int32(), C.c_int32()
+        check(self._lib.life_ctx_bands(self._ctx, C.byref(n), None, None, C.byref(halo)))
+        bounds = np.zeros(n.value + 1, np.int64)
+        devs = np.zeros(n.value, np.int32)
+        check(self._lib.life_ctx_bands(self._ctx, None, bounds.ctypes.data, devs.ctypes.data, None))
+        return {"bounds": [int(x) for x in bounds], "devices": [int(x) for x in devs],
+                "halo": int(halo.value)}
+
+    def band_stats(self) -> list[dict]:
+        """life_band_stats of every band for the last run()."""
+        n = C.c_int32()
+        check(self._lib.life_ctx_bands(self._ctx, C.byref(n), None, None, None))
+        out = []
+        for i in range(n.value):
+            s = capi.BandStats()
+            check(self._lib.life_ctx_band_stats(self._ctx, i, C.byref(s)))
+            out.append(s.as_dict())
+        return out
 
     # -- grid in / out ----------------------------------------------------
     def upload(self, cells: np.ndarray) -> None:
@@ -375,11 +416,13 @@ def run(initial: Grid, config: RunConfig, checkpoints: Iterable[int] = ()) -> Ru
     """run (engine.cpp:157-214) on the GPU: `config.iterations` generations,
     populations at the strictly ascending checkpoints (0 = initial grid).
     `workers` is validated like the reference's row bands (engine.cpp:127-131,
-    decomposition.cpp:26-30); a single process drives one GPU."""
+    decomposition.cpp:26-30); `config.devices` spreads the torus over row
+    bands on several GPUs (band_bounds, decomposition.cpp:12-24) in this one
+    call, as the reference's Strategy::rows() does over threads."""
     checkpoints = list(checkpoints)
     _check_workers(config, initial.height())
     engine = config.strategy.engine()
-    with Engine(config.device) as e:
+    with (Engine(devices=list(config.devices)) if config.devices else Engine(config.device)) as e:
         e.upload(initial.cells)
         pops = e.run(config.iterations, engine, config.strategy.depth, checkpoints)
         out = e.download()

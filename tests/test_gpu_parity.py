@@ -9,6 +9,7 @@ import numpy as np
 import pytest
 
 from conftest import load_golden
+from paper_1209_4408_b200 import capi
 
 pytestmark = pytest.mark.gpu
 
@@ -289,14 +290,13 @@ def test_run_batch_banded(engine, oracle, W, H, G, depth):
     """life_run_batch on taller grids: several waves of row tiles per pass, W % 32 != 0,
     G not a multiple of the depth, G = 0, more grids than buffer slots; H >= 32768 runs
     the first and last grid as 32 chunk trapezoids + boundary triangles (forced with
-    LIFE_BATCH_TRAP=1: by default only chunks of >= 8192 rows take it)."""
-    import os
+    LIFE_OPT_BATCH_TRAPEZOID=1: by default only chunks of >= 8192 rows take it)."""
     if H >= 32768:
-        os.environ["LIFE_BATCH_TRAP"] = "1"
+        engine.set_option(capi.OPT_BATCH_TRAPEZOID, 1)
     try:
         _run_batch_banded(engine, oracle, W, H, G, depth)
     finally:
-        os.environ.pop("LIFE_BATCH_TRAP", None)
+        engine.set_option(capi.OPT_BATCH_TRAPEZOID, -1)
 
 
 def _run_batch_banded(engine, oracle, W, H, G, depth):
