@@ -243,6 +243,144 @@ def run_reference_arm(args) -> None:
 
 
 # ---------------------------------------------------------------------------
+# Parity after the timed region: the run is repeated from the initial grid
+# and compared with fixtures the REFERENCE generated (tests/golden/, written
+# by tests/golden/make_golden.py from oracle/_ref): light-cone windows for
+# config 5 (they include the 2/4/8-band seams and the wrap corners), the
+# full-grid packed FNV-1a-64 for the others.  Only the committed JSON is read
+# here; nothing under oracle/ is imported.
+# ---------------------------------------------------------------------------
+GOLDEN_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+def golden_for(config: int, gens: int):
+    def load(name):
+        try:
+            with open(os.path.join(GOLDEN_DIR, name)) as f:
+                return json.load(f)
+        except OSError:
+            return None
+    if config == 5:
+        g = load("golden_cfg5_windows.json")
+        if g:
+            for key in ("windows_500", "windows_16"):
+                ws = [w for w in g.get(key, []) if w["T"] == gens]
+                if ws:
+                    return {"kind": "windows", "windows": ws, "source": "golden_cfg5_windows.json"}
+        return None
+    name = {1: "golden_small.json", 2: "golden_cfg2.json", 3: "golden_cfg3.json",
+            4: "golden_cfg4.json"}[config]
+    g = load(name)
+    if g is None:
+        return None
+    sched = g["cfg1"] if config == 1 else g["gens"]
+    if str(gens) in sched:
+        return {"kind": "hash", "fnv_packed": sched[str(gens)]["fnv_packed"],
+                "population": sched[str(gens)]["population"], "source": name}
+    return None
+
+
+def band_window_rows(band, y0b: int, H: int, W: int, x0: int, y0: int, S: int) -> dict:
+    """Rows of the wrapped S x S window at (x0, y0) (Grid::wrap, grid.hpp:48-54)
+    that lie in this band ([y0b, y0b + rows) of the torus), as 0/1 bytes keyed
+    by window row; `band` is the band's packed uint32 rows on the device."""
+    import numpy as np
+    import torch
+    rows = (y0 + np.arange(S)) % H
+    sel = np.nonzero((rows >= y0b) & (rows < y0b + band.shape[0]))[0]
+    if not len(sel):
+        return {}
+    cols = (x0 + np.arange(S)) % W
+    widx = np.unique(cols // 32)
+    ri = torch.as_tensor(rows[sel] - y0b, device=band.device)
+    wi = torch.as_tensor(widx, device=band.device)
+    sub = band.index_select(0, ri).index_select(1, wi).cpu().numpy().view(np.uint32)
+    pos = np.searchsorted(widx, cols // 32)
+    bits = ((sub[:, pos] >> (cols % 32).astype(np.uint32)) & 1).astype(np.uint8)
+    return {int(i): bits[j].tobytes() for j, i in enumerate(sel)}
+
+
+def fnv(data: bytes, h: int = 0) -> int:
+    from paper_1209_4408_b200 import capi
+    return int(capi.lib().life_fnv1a64(data, len(data), h))
+
+
+def check_windows(gold: dict, rows_of) -> dict:
+    """rows_of(x0, y0, S) -> {window row: bytes} for the whole window."""
+    bad = []
+    for w in gold["windows"]:
+        rows = rows_of(w["x0"], w["y0"], w["S"])
+        data = b"".join(rows[i] for i in range(w["S"]))
+        got = f"{fnv(data):016x}"
+        pop = sum(data)
+        if got != w["fnv_bytes"] or pop != w["population"]:
+            bad.append({"x0": w["x0"], "y0": w["y0"], "got": got, "want": w["fnv_bytes"]})
+    return {"ok": not bad, "kind": f"{len(gold['windows'])} light-cone windows "
+                                    f"{gold['windows'][0]['S']}^2 at T={gold['windows'][0]['T']}",
+            "mismatches": bad}
+
+
+def parity_bands(drv, geo, cfg: dict, config: int, gens: int, world: int, rank: int,
+                 soup_host) -> dict:
+    """Re-runs the configuration on the band driver(s) from the initial grid
+    and compares with the reference-generated golden fixture."""
+    import torch
+    import torch.distributed as dist
+    gold = golden_for(config, gens)
+    if gold is None:
+        return {"ok": None, "reason": f"no reference golden for config {config} at {gens} generations"}
+    if soup_host is not None:
+        drv.load_rows(soup_host)
+    else:
+        drv.init_random(cfg["p"], 42)
+    drv.run(gens)
+    torch.cuda.synchronize()
+    band = drv.band()
+    W, H = geo.width, geo.height
+    if gold["kind"] == "windows":
+        mine = {(w["x0"], w["y0"]): band_window_rows(band, geo.y0, H, W, w["x0"], w["y0"], w["S"])
+                for w in gold["windows"]}
+        if world > 1:
+            allp = [None] * world
+            dist.all_gather_object(allp, mine)
+            merged = {}
+            for part in allp:
+                for key, rows in part.items():
+                    merged.setdefault(key, {}).update(rows)
+        else:
+            merged = mine
+        res = check_windows(gold, lambda x0, y0, S: merged[(x0, y0)]) if rank == 0 else {}
+    else:
+        # fnv_packed: FNV-1a-64 over the packed exchange format (rows of
+        # ceil(W/64) little-endian uint64), chained band by band in row order.
+        wpr = -(-W // 64)
+        data = band[:, :2 * wpr].contiguous().cpu().numpy().tobytes()
+        cdev = band.device if world > 1 and dist.get_backend() == "nccl" else torch.device("cpu")
+
+        def as_t(v):  # uint64 hash state in an int64 tensor
+            return torch.tensor([v - (1 << 64) if v >= 1 << 63 else v], dtype=torch.int64,
+                                device=cdev)
+        h = as_t(0)
+        if rank > 0:
+            dist.recv(h, rank - 1)
+        hv = fnv(data, int(h.item()) & (2 ** 64 - 1))
+        if rank + 1 < world:
+            dist.send(as_t(hv), rank + 1)
+        if world > 1:  # the last band holds the whole-grid hash
+            t = as_t(hv)
+            dist.broadcast(t, world - 1)
+            hv = int(t.item()) & (2 ** 64 - 1)
+        pop = drv.population()
+        got = f"{hv:016x}"
+        res = {"ok": got == gold["fnv_packed"] and pop == gold["population"],
+               "kind": "full-grid packed FNV-1a-64 + population", "got": got,
+               "want": gold["fnv_packed"], "population": pop}
+    res["source"] = "tests/golden/" + gold["source"] + " (written by the reference, oracle/_ref)"
+    res["generations"] = gens
+    return res
+
+
+# ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
 def run_gpu_arm(args) -> None:
@@ -256,13 +394,17 @@ def run_gpu_arm(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.gpus != world and world > 1:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.gpus != world:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     # LIFE_BENCH_DEVICE / LIFE_BENCH_BACKEND exist for the single-GPU test of
     # the multi-rank path (ranks sharing cuda:0 over gloo, host barriers only,
     # so no kernel ever waits on another rank): tests/test_bench_contract.py.
-    if os.environ.get("LIFE_BENCH_DEVICE"):
+    emulated = bool(os.environ.get("LIFE_BENCH_DEVICE"))
+    if emulated:
         local = int(os.environ["LIFE_BENCH_DEVICE"])
+    elif torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} CUDA "
+                         f"device(s) visible -- refusing to measure fewer GPUs than requested")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -271,12 +413,18 @@ def run_gpu_arm(args) -> None:
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        # Communicator evidence for the log: every rank names its GPU.
+        props = torch.cuda.get_device_properties(dev)
+        print(f"[bench rank {rank}/{dist.get_world_size()}] backend {dist.get_backend()} "
+              f"cuda:{local} {props.name} pci {getattr(props, 'pci_bus_id', '?')} "
+              f"uuid {getattr(props, 'uuid', '?')}", file=sys.stderr, flush=True)
     L = capi.lib()
     cfg = CONFIGS[args.config]
-    W, H, gens, depth = cfg["w"], cfg["h"], args.gens or cfg["gens"], args.depth
-    if depth == 0:  # the engine's auto rule (life_gpu.cu packed_auto_depth)
-        strips = -(-((W + 31) // 32 + 1) // 31)
-        depth = 12 if W % 32 and strips * H < 2_000_000 else 16
+    W, H, gens = cfg["w"], cfg["h"], args.gens or cfg["gens"]
+    bounds0 = [H * r // world for r in range(world + 1)]
+    band_rows_max = max(b - a for a, b in zip(bounds0, bounds0[1:])) + 1
+    # depth 0: the engine's own auto rule (life_packed_auto_depth)
+    depth = args.depth or int(L.life_packed_auto_depth(W, H if world == 1 else band_rows_max))
 
     def barrier():
         if world > 1:
@@ -290,15 +438,16 @@ def run_gpu_arm(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    int_ops, int_s = (0.0, 0.0)
+    int_ops = 0.0
     import ctypes as C
     o, s = C.c_double(), C.c_double()
     if L.life_measure_int_peak(local, 4000, C.byref(o), C.byref(s)) == 0:
         int_ops = o.value
 
     geo = make_geometry(W, H, rank, world, depth)
-    # Launch timing of every kernel pass in the timed region (events on the
-    # stream the kernels are launched on).
+    # Per-launch CUDA events are recorded only in one extra PROFILED step after
+    # the timed region (events between launches serialise programmatic
+    # dependent launch, so the timed steps carry none).
     launches = []
     from paper_1209_4408_b200.bands import cuda_stepper
     base_step = cuda_stepper(W)
@@ -317,42 +466,29 @@ def run_gpu_arm(args) -> None:
 
     halo = "none" if world == 1 else args.halo
     drv = None
+    peer = False
     if halo == "peer":
         # Fused halo: the pass kernels read the neighbour bands' rows over
-        # NVLink (CUDA IPC); NCCL is only the per-pass barrier.
+        # NVLink (CUDA IPC); a neighbour-only NCCL token orders the passes.
         from paper_1209_4408_b200.bands import PeerBandDriver
         err = None
         try:
-            drv = PeerBandDriver(geo, dev)
+            drv = PeerBandDriver(geo, dev, sync=args.pass_sync)
         except Exception as exc:  # no IPC / peer access on this rank
             err, drv = exc, None
         # Collective decision: every rank falls back if any rank could not open
         # its neighbours' buffers (mixed halo schemes would deadlock).
         ok = torch.tensor([0 if drv is None else 1], dtype=torch.int32, device=dev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if int(ok.item()) == 0 and drv is not None:
-            drv.close()
+        if int(ok.item()) == 0:
+            if drv is not None:
+                drv.close()
             drv = None
-        try:
-            if drv is None:
-                raise RuntimeError(f"peer halo unavailable on some rank ({err!r})")
-            inner = drv.compute
-
-            def timed_compute(k):
-                if record["on"]:
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record()
-                    inner(k)
-                    e1.record()
-                    launches.append((e0, e1, geo.band_rows * W * k, k, geo.band_rows))
-                else:
-                    inner(k)
-            drv.compute = timed_compute
-        except Exception as exc:  # no IPC / peer access: NCCL send/recv halos
-            print(f"peer halo unavailable ({exc!r}); using NCCL send/recv", file=sys.stderr)
+            print(f"peer halo unavailable on some rank ({err!r}); using NCCL send/recv",
+                  file=sys.stderr)
             halo = "nccl"
-            drv = None
+        else:
+            peer = True
     if drv is None:
         drv = BandDriver(geo, dev, stepper=timed_step)
     soup_host = None
@@ -373,7 +509,6 @@ def run_gpu_arm(args) -> None:
     barrier()
     step_ms = []
     l0 = L.life_kernel_launches()
-    record["on"] = True
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             if flush is not None:
@@ -386,36 +521,76 @@ def run_gpu_arm(args) -> None:
             e1.record()
             torch.cuda.synchronize()
             step_ms.append(e0.elapsed_time(e1))
-    record["on"] = False
     gpu_launches = int(L.life_kernel_launches() - l0)
     barrier()
     total_ms = max_over_ranks(sum(step_ms))
     cells = W * H * gens * args.steps
     value = cells / (total_ms * 1e-3) / 1e9
 
-    # Dominant kernel: the depth-`depth` packed pass over the whole band (the
-    # interior launch when N > 1; the k-row edge launches run beside it on a
-    # side stream).  Algorithmic int ops per launch / mean launch duration.
-    full = max((r for (_, _, _, k, r) in launches if k == depth), default=0)
-    main = [(a.elapsed_time(b), n) for (a, b, n, k, r) in launches if k == depth and r == full]
-    kern_ms = sum(t for t, _ in main)
-    kern_cells = sum(n for _, n in main)
-    all_kern_ms = sum(a.elapsed_time(b) for (a, b, _, _, r) in launches if r == full or world == 1)
+    # ---- one profiled step: per-launch events on the launching stream ----
+    if flush is not None:
+        flush.fill_(1)
+    barrier()
+    record["on"] = True
+    if peer:
+        drv.profile = True
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record()
+    drv.run(gens)
+    p1.record()
+    torch.cuda.synchronize()
+    record["on"] = False
+    prof_ms = p0.elapsed_time(p1)
+    rank_stats = {"rank": rank, "device": local, "y0": geo.y0, "rows": geo.band_rows,
+                  "timed_ms": sum(step_ms), "profiled_step_ms": prof_ms}
+    if peer:
+        drv.profile = False
+        st = drv.stats()
+        # the interior launch of each full-depth pass is the dominant kernel
+        rank_stats.update({"interior_ms": st["interior_ms"], "pass_ms": st["pass_ms"],
+                           "barrier_ms": st["barrier_ms"], "passes": st["passes"],
+                           "pass_sync": drv.sync})
+        n_full = sum(1 for k in st["ks"] if k == depth)
+        kern_ms = st["interior_full_ms"]
+        kern_cells = n_full * (geo.band_rows - 2 * depth if geo.band_rows > 2 * depth
+                               else geo.band_rows) * W * depth
+        all_kern_ms = st["interior_ms"]
+        n_main = max(n_full, 1)
+    else:
+        full = max((r for (_, _, _, k, r) in launches if k == depth), default=0)
+        main = [(a.elapsed_time(b), n) for (a, b, n, k, r) in launches if k == depth and r == full]
+        kern_ms = sum(t for t, _ in main)
+        kern_cells = sum(n for _, n in main)
+        all_kern_ms = sum(a.elapsed_time(b) for (a, b, _, _, r) in launches)
+        n_main = max(len(main), 1)
+        rank_stats.update({"interior_ms": kern_ms, "kernel_ms": all_kern_ms,
+                           "launches": len(launches)})
+        if world > 1:
+            rank_stats["halo_wait_ms"] = prof_ms - all_kern_ms
+    launches.clear()
+    if world > 1:
+        allst = [None] * world
+        dist.all_gather_object(allst, rank_stats)
+    else:
+        allst = [rank_stats]
+
     achieved_ops = kern_cells * OPS_PER_UPDATE / (kern_ms * 1e-3) if kern_ms else 0.0
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     alg_bytes_per_update = 0.25 / depth
     hbm_achieved = kern_cells * alg_bytes_per_update / (kern_ms * 1e-3) / 1e9 if kern_ms else 0.0
     traffic = ncu_traffic(args.config, depth)
-    n_main = max(len(main), 1)
-    # Depth 1 on a W % 128 == 0 torus runs packed_step1_kernel (16-B vectors),
-    # HBM-bound: 0.25 B per cell-update against the copy bandwidth.
-    step1 = depth == 1 and W % 128 == 0
+    kind = int(L.life_packed_launch_kind(W, geo.band_rows if world > 1 else H, depth))
+    kname = {capi.LAUNCH_STEP1: "packed_step1_kernel",
+             capi.LAUNCH_FAST: f"packed_tb_fast_kernel<{depth}>",
+             capi.LAUNCH_ALL_PATHS: f"packed_tb_kernel<{depth}>",
+             capi.LAUNCH_SPLIT: f"split: packed_tb_fast_kernel<{depth}> (inner strips) + "
+                                f"packed_tb_kernel<{depth}> (seam strips, side stream)"}.get(kind, "?")
+    step1 = kind == capi.LAUNCH_STEP1
     roofline = {
         "bound": "int",
-        "kernel": "packed_step1_kernel" if step1 else
-                  (f"packed_tb_fast_kernel<{depth}>" if W % 32 == 0 and W >= 64 and depth >= 4
-                   else f"packed_tb_kernel<{depth}>"),
+        "kernel": kname,
         "achieved": achieved_ops / 1e12, "peak": int_ops / 1e12, "unit": "Tops/s",
         "frac": achieved_ops / int_ops if int_ops else None,
         "peak_source": "measured (life_measure_int_peak: LOP3 throughput, all SMs, this run)",
@@ -424,7 +599,11 @@ def run_gpu_arm(args) -> None:
                                    "int_ops": kern_cells / n_main * OPS_PER_UPDATE,
                                    "hbm_bytes": kern_cells / n_main * alg_bytes_per_update},
         "mean_launch_ms": kern_ms / n_main,
-        "kernel_share_of_step": all_kern_ms / sum(step_ms) if step_ms else None,
+        "timing": "per-launch CUDA events on the launching stream over one profiled step "
+                  "right after the timed steps (same work; the timed steps carry no "
+                  "per-launch events, which would serialise programmatic dependent launch)",
+        "kernel_share_of_step": all_kern_ms / prof_ms if prof_ms else None,
+        "step_frac": (value * 1e9 * OPS_PER_UPDATE / world) / int_ops if int_ops else None,
         "traffic": traffic,
         "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": hbm_achieved / hbm_peak, "bytes_per_cell_update": alg_bytes_per_update,
@@ -439,6 +618,11 @@ def run_gpu_arm(args) -> None:
                          "int": {"achieved": achieved_ops / 1e12, "peak": int_ops / 1e12,
                                  "unit": "Tops/s",
                                  "frac": achieved_ops / int_ops if int_ops else None}})
+
+    # ---- parity: the same run again, against the reference's golden -------
+    parity = {"ok": None, "reason": "--no-parity"}
+    if not args.no_parity:
+        parity = parity_bands(drv, geo, cfg, args.config, gens, world, rank, soup_host)
     if hasattr(drv, "close"):
         drv.close()
     del drv
@@ -449,9 +633,9 @@ def run_gpu_arm(args) -> None:
     if not args.no_e2e:
         steps_e2e = max(2, args.steps)
         if world == 1:
-            # life_run_batch: every step uploads its 8 GiB packed grid from
-            # pinned memory, runs the generations and downloads the result;
-            # step i's copies overlap step i+-1's compute (copy engines).
+            # life_run_batch: every step uploads its packed grid from pinned
+            # memory, runs the generations and downloads the result; step i's
+            # copies overlap step i+-1's compute (copy engines).
             eng = Engine(local)
             wpr = math.ceil(W / 64)
             host_in = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
@@ -465,65 +649,30 @@ def run_gpu_arm(args) -> None:
             eng.download_packed(hin)
             eng.run_batch([hin], [hout], W, gens, depth)  # warm-up (allocates buffers)
             e2e_ms = eng.run_batch([hin] * steps_e2e, [hout] * steps_e2e, W, gens, depth)
+            # Drop-in latency: one synchronous run() per call -- upload, run,
+            # download, nothing overlapped across calls (what lifegpu::run
+            # does for one caller), host-timed.
+            eng.upload_packed(hin, W)
+            eng.run(gens, capi.ENGINE_PACKED, depth)
+            eng.download_packed(hout)
+            sync_s = []
+            for _ in range(steps_e2e):
+                t0 = time.perf_counter()
+                eng.upload_packed(hin, W)
+                eng.run(gens, capi.ENGINE_PACKED, depth)
+                eng.download_packed(hout)
+                sync_s.append(time.perf_counter() - t0)
             eng.close()
             bi = bo = H * wpr * 8
+            sync = {"value": W * H * gens / statistics.median(sync_s) / 1e9, "unit": UNIT,
+                    "ms_per_call": 1e3 * statistics.median(sync_s),
+                    "api": "C-ABI life_grid_upload_packed + life_run + life_grid_download_packed "
+                           "per call from/to pinned host memory, serial (drop-in latency; "
+                           "host-timed median)"}
         else:
-            if halo == "peer":
-                from paper_1209_4408_b200.bands import PeerBandDriver
-                drv = PeerBandDriver(geo, dev)
-            else:
-                drv = BandDriver(geo, dev)
-            host = torch.empty(tuple(drv.band().shape), dtype=torch.int32, pin_memory=True)
-            if soup_host is not None:
-                drv.load_rows(soup_host)
-            else:
-                drv.init_random(cfg["p"], 42)
-            host.copy_(drv.band())
-            # Step i's band upload (pinned host -> staging buffer) and step
-            # i-1's download (staging -> pinned host) run on a copy stream
-            # while the band computes; the band itself is only touched by two
-            # on-device copies per step.  Timed from the first upload to the
-            # last download, max over ranks.
-            stage_in = torch.empty_like(drv.band())
-            stage_out = torch.empty_like(drv.band())
-            copy = torch.cuda.Stream(dev)
-            main = torch.cuda.current_stream(dev)
-            up_done = [torch.cuda.Event() for _ in range(steps_e2e)]
-            for warm in (True, False):
-                n_steps = 1 if warm else steps_e2e
-                barrier()
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record()
-                copy.wait_stream(main)
-                with torch.cuda.stream(copy):
-                    stage_in.copy_(host, non_blocking=True)
-                    up_done[0].record(copy)
-                for i in range(n_steps):
-                    main.wait_event(up_done[i])
-                    drv.band().copy_(stage_in)          # on-device, after upload i
-                    if i + 1 < n_steps:                 # upload i+1 overlaps compute i
-                        copy.wait_stream(main)
-                        with torch.cuda.stream(copy):
-                            stage_in.copy_(host, non_blocking=True)
-                            up_done[i + 1].record(copy)
-                    drv.run(gens)
-                    stage_out.copy_(drv.band())         # on-device
-                    copy.wait_stream(main)
-                    with torch.cuda.stream(copy):       # download i overlaps compute i+1
-                        host.copy_(stage_out, non_blocking=True)
-                main.wait_stream(copy)
-                e1.record()
-                torch.cuda.synchronize()
-                if not warm:
-                    e2e_ms = max_over_ranks(e0.elapsed_time(e1))
-            del stage_in, stage_out
-            t = torch.tensor([host.numel() * 4], dtype=torch.int64, device=dev)
-            dist.all_reduce(t)
-            bi = bo = int(t.item())
-            if hasattr(drv, "close"):
-                drv.close()
-            del drv
+            e2e_ms, bi, bo = e2e_bands(args, geo, dev, halo, cfg, gens, soup_host, steps_e2e,
+                                       barrier, max_over_ranks)
+            sync = None
         e2e = {"value": W * H * gens * steps_e2e / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo,
                "api": "C-ABI life_run_batch (per step: H2D packed grid, run, D2H; copies "
@@ -532,6 +681,8 @@ def run_gpu_arm(args) -> None:
                       "band driver per rank: pinned-host band upload / run / download, "
                       "copies overlapped with the neighbouring steps' compute",
                "steps": steps_e2e}
+        if sync:
+            e2e["sync_call"] = sync
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -550,20 +701,214 @@ def run_gpu_arm(args) -> None:
             "config": {"workload": cfg["desc"], "width": W, "height": H, "generations": gens,
                        "temporal_depth": depth, "global_cells": W * H,
                        "parallelism": f"rowbands{world}" if world > 1 else "single-gpu",
-                       "halo": {"peer": "in-kernel NVLink peer reads (CUDA IPC) + NCCL barrier",
+                       "halo": {"peer": "in-kernel NVLink peer reads (CUDA IPC) + "
+                                        f"{args.pass_sync} pass ordering",
                                 "nccl": "NCCL send/recv of k ghost rows, interior overlapped",
                                 "none": "torus wraps inside the kernel"}[halo],
+                       "emulated_ranks_on_one_gpu": emulated,
                        "l2": ("inputs larger than L2" if flush is None else
                               "L2 flushed (256 MiB write) between steps")},
             "roofline": roofline,
+            "parity": parity,
+            "ranks": allst,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
+    ok = parity.get("ok") is not False
     if world > 1:
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        ok = bool(t.item())
         dist.destroy_process_group()
+    if not ok:
+        print("bench.py: PARITY MISMATCH against the reference golden", file=sys.stderr)
+        sys.exit(3)
+
+
+def e2e_bands(args, geo, dev, halo, cfg, gens, soup_host, steps_e2e, barrier, max_over_ranks):
+    """N > 1 e2e: each rank uploads its band from pinned host memory, runs,
+    downloads; step i's copies overlap step i+-1's compute."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1209_4408_b200.bands import BandDriver, PeerBandDriver
+    if halo == "peer":
+        drv = PeerBandDriver(geo, dev, sync=args.pass_sync)
+    else:
+        drv = BandDriver(geo, dev)
+    host = torch.empty(tuple(drv.band().shape), dtype=torch.int32, pin_memory=True)
+    if soup_host is not None:
+        drv.load_rows(soup_host)
+    else:
+        drv.init_random(cfg["p"], 42)
+    host.copy_(drv.band())
+    # Step i's band upload (pinned host -> staging buffer) and step i-1's
+    # download (staging -> pinned host) run on a copy stream while the band
+    # computes; the band itself is only touched by two on-device copies per
+    # step.  Timed from the first upload to the last download, max over ranks.
+    stage_in = torch.empty_like(drv.band())
+    stage_out = torch.empty_like(drv.band())
+    copy = torch.cuda.Stream(dev)
+    main = torch.cuda.current_stream(dev)
+    up_done = [torch.cuda.Event() for _ in range(steps_e2e)]
+    e2e_ms = 0.0
+    for warm in (True, False):
+        n_steps = 1 if warm else steps_e2e
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        copy.wait_stream(main)
+        with torch.cuda.stream(copy):
+            stage_in.copy_(host, non_blocking=True)
+            up_done[0].record(copy)
+        for i in range(n_steps):
+            main.wait_event(up_done[i])
+            drv.band().copy_(stage_in)          # on-device, after upload i
+            if i + 1 < n_steps:                 # upload i+1 overlaps compute i
+                copy.wait_stream(main)
+                with torch.cuda.stream(copy):
+                    stage_in.copy_(host, non_blocking=True)
+                    up_done[i + 1].record(copy)
+            drv.run(gens)
+            stage_out.copy_(drv.band())         # on-device
+            copy.wait_stream(main)
+            with torch.cuda.stream(copy):       # download i overlaps compute i+1
+                host.copy_(stage_out, non_blocking=True)
+        main.wait_stream(copy)
+        e1.record()
+        torch.cuda.synchronize()
+        if not warm:
+            e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+    del stage_in, stage_out
+    t = torch.tensor([host.numel() * 4], dtype=torch.int64, device=dev)
+    dist.all_reduce(t)
+    if hasattr(drv, "close"):
+        drv.close()
+    return e2e_ms, int(t.item()), int(t.item())
+
+
+def run_ctx_arm(args) -> None:
+    """--single-process: ONE process drives all N GPUs through the multi-device
+    C-ABI context (life_ctx_create_multi: row bands by band_bounds, in-kernel
+    NVLink halos, neighbour-only event ordering) -- the drop-in run() of the
+    reference over N workers (engine.cpp:162-214).  Time = max over the bands
+    of the CUDA-event time on each band's device (life_band_stats.run_ms)."""
+    import torch
+
+    from paper_1209_4408_b200 import capi
+    from paper_1209_4408_b200.life import Engine
+    n = args.gpus
+    emulated = bool(os.environ.get("LIFE_BENCH_DEVICE"))
+    if emulated:
+        devices = [int(os.environ["LIFE_BENCH_DEVICE"])] * n
+    else:
+        if torch.cuda.device_count() < n:
+            raise SystemExit(f"bench.py: --gpus {n} but only {torch.cuda.device_count()} CUDA "
+                             f"device(s) visible")
+        devices = list(range(n))
+    L = capi.lib()
+    cfg = CONFIGS[args.config]
+    W, H, gens = cfg["w"], cfg["h"], args.gens or cfg["gens"]
+    import ctypes as C
+    o, s = C.c_double(), C.c_double()
+    int_ops = o.value if L.life_measure_int_peak(devices[0], 4000, C.byref(o), C.byref(s)) == 0 \
+        else 0.0
+    e = Engine(devices=devices)
+
+    def init():
+        if cfg.get("soup"):
+            e.init_soup(W, H, 0.02, 5, cfg["p"], 42, capi.ENGINE_PACKED)
+        else:
+            e.init_random(W, H, cfg["p"], 42, capi.ENGINE_PACKED)
+    init()
+    b = e.bands()
+    depth = args.depth or 0
+    for _ in range(args.warmup):
+        e.run(gens, capi.ENGINE_PACKED, depth)
+    l0 = L.life_kernel_launches()
+    ms = []
+    with ClockSampler(devices[0]) as clocks:
+        for _ in range(args.steps):
+            e.run(gens, capi.ENGINE_PACKED, depth)
+            ms.append(max(st["run_ms"] for st in e.band_stats()))
+    gpu_launches = int(L.life_kernel_launches() - l0)
+    e.set_option(capi.OPT_PROFILE, 1)
+    e.run(gens, capi.ENGINE_PACKED, depth)
+    stats = e.band_stats()
+    e.set_option(capi.OPT_PROFILE, 0)
+    value = W * H * gens * args.steps / (sum(ms) * 1e-3) / 1e9
+    parity = {"ok": None, "reason": "--no-parity"}
+    gold = None if args.no_parity else golden_for(args.config, gens)
+    if not args.no_parity and gold is None:
+        parity = {"ok": None, "reason": f"no reference golden for config {args.config} at {gens}"}
+    elif gold is not None:
+        init()
+        e.run(gens, capi.ENGINE_PACKED, depth)
+        if gold["kind"] == "windows":
+            parity = check_windows(gold, lambda x0, y0, S: {
+                i: r.tobytes() for i, r in enumerate(e.window(x0, y0, S, S))})
+        else:
+            got = f"{fnv(e.download_packed().tobytes()):016x}"
+            pop = e.population()
+            parity = {"ok": got == gold["fnv_packed"] and pop == gold["population"],
+                      "kind": "full-grid packed FNV-1a-64 + population", "got": got,
+                      "want": gold["fnv_packed"], "population": pop}
+        parity["source"] = "tests/golden/" + gold["source"]
+    e.close()
+    eff_depth = depth or int(L.life_packed_auto_depth(W, max(y - x for x, y in zip(b["bounds"], b["bounds"][1:]))))
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sum(ms) / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32 bit-sliced (32 cells/word, exact integer)", "data": "synthetic",
+        "config": {"workload": cfg["desc"], "width": W, "height": H, "generations": gens,
+                   "temporal_depth": eff_depth, "parallelism": f"rowbands{n} (one process, "
+                   "multi-device C-ABI context)", "devices": devices,
+                   "bounds": b["bounds"], "halo": {0: "peer", 1: "copy"}.get(b["halo"], "none"),
+                   "emulated_ranks_on_one_gpu": emulated},
+        "roofline": {"bound": "int", "achieved": value * 1e9 * OPS_PER_UPDATE / n / 1e12,
+                     "peak": int_ops / 1e12, "unit": "Tops/s",
+                     "frac": value * 1e9 * OPS_PER_UPDATE / n / int_ops if int_ops else None,
+                     "basis": "whole step per GPU (band_stats run_ms, max over bands)",
+                     "traffic": None},
+        "parity": parity, "bands": stats, "cpu_baseline": None, "e2e": None,
+        "gpu_launches": gpu_launches, "clocks": clocks.summary()}
+    print(json.dumps(line), flush=True)
+    if parity.get("ok") is False:
+        print("bench.py: PARITY MISMATCH against the reference golden", file=sys.stderr)
+        sys.exit(3)
+
+
+def self_launch(args) -> int:
+    """`python bench.py --gpus N` without torchrun: refuse if fewer than N
+    GPUs are visible, else re-run this command as N ranks under
+    torch.distributed.run (one process per GPU)."""
+    if not os.environ.get("LIFE_BENCH_DEVICE"):
+        try:
+            import torch
+            n = torch.cuda.device_count()
+        except Exception:  # noqa: BLE001
+            n = 0
+        if n < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} but only {n} CUDA device(s) visible -- "
+                  f"refusing to measure fewer GPUs than requested", file=sys.stderr)
+            return 2
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 # byte_tb_kernel per 4-cell word (csrc/kernels.cuh byte_row_fma / byte_rule): ALU pipe --
@@ -851,7 +1196,18 @@ def main() -> None:
                     help="byte engine generations per pass (0 = auto, 1 = HBM-bound single step)")
     ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
                     help="multi-GPU halo: in-kernel NVLink peer reads or NCCL send/recv")
+    ap.add_argument("--pass-sync", choices=["neighbour", "allreduce"], default="neighbour",
+                    help="peer halo: order passes by a token with the two neighbour ranks "
+                         "(default) or by an all-rank NCCL all-reduce")
+    ap.add_argument("--single-process", action="store_true",
+                    help="N GPUs from ONE process through the multi-device C-ABI context "
+                         "(life_ctx_create_multi) instead of one rank per GPU")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-run comparison with the reference's golden fixture")
     args = ap.parse_args()
+    ranked = "WORLD_SIZE" in os.environ
+    if args.impl == "ours" and args.gpus > 1 and not ranked and not args.single_process:
+        sys.exit(self_launch(args))
     if args.engine == "auto":
         c = CONFIGS[args.config]
         small = c["w"] % 32 == 0 and c["w"] * c["h"] <= 2 ** 22
@@ -859,6 +1215,8 @@ def main() -> None:
             else "packed"
     if args.impl == "reference":
         run_reference_arm(args)
+    elif args.single_process:
+        run_ctx_arm(args)
     elif args.engine == "byte":
         run_byte_arm(args)
     elif args.engine == "resident":

@@ -194,6 +194,19 @@ int life_run_batch(life_ctx* ctx, const uint64_t* const* inputs, uint64_t* const
  * engine (16; 12 for W % 32 != 0 tori less than ~3 block waves deep). */
 int life_packed_auto_depth(int64_t width, int64_t height);
 
+/* Which kernel(s) one torus pass of `generations` over `out_rows` rows of a
+ * W-wide packed grid launches (device-buffer layer and life_run alike):
+ * LIFE_LAUNCH_STEP1 packed_step1_kernel (one generation, W % 128 == 0, 16-B
+ * vectors); LIFE_LAUNCH_FAST packed_tb_fast_kernel<K> (W % 32 == 0, K >= 4);
+ * LIFE_LAUNCH_ALL_PATHS packed_tb_kernel<K>; LIFE_LAUNCH_SPLIT the seam strips
+ * on packed_tb_kernel<K> beside packed_tb_fast_kernel<K> for the rest (W % 32
+ * != 0 tori several block waves deep); -1 for a bad argument. */
+#define LIFE_LAUNCH_STEP1 0
+#define LIFE_LAUNCH_FAST 1
+#define LIFE_LAUNCH_ALL_PATHS 2
+#define LIFE_LAUNCH_SPLIT 3
+int life_packed_launch_kind(int64_t width, int64_t out_rows, int32_t generations);
+
 /* ---- row-band decomposition (multi-GPU) --------------------------------- */
 /* Mirrors band_bounds / partition_rows (decomposition.cpp:12-24, :93-104):
  * writes parts+1 cut points; LIFE_ERR_TOO_MANY_PARTS if parts > extent. */

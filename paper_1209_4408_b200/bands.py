@@ -293,9 +293,11 @@ class LocalBands:
 # ---------------------------------------------------------------------------
 # Fused halo over NVLink: the pass kernel reads the neighbour bands' rows
 # straight from their HBM (CUDA IPC peer mappings), so a pass is ONE launch
-# per GPU and there is no separate exchange step; a stream-ordered barrier
-# (a 1-element NCCL all-reduce) between passes keeps neighbours from
-# overwriting rows that are still being read.
+# per GPU and there is no separate exchange step.  Between passes a band only
+# has to wait for its two NEIGHBOURS (the rows it reads next pass are theirs,
+# and the buffer it overwrites next pass is the one they read this pass):
+# a stream-ordered NCCL send/recv of a 4-byte token with the band above and
+# the band below, no global collective.
 # ---------------------------------------------------------------------------
 class DeviceBuffer:
     """cudaMalloc'd packed rows (IPC-shareable), exposed to torch zero-copy."""
@@ -339,7 +341,8 @@ def open_peer(handle: bytes) -> int:
 
 def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows: int,
               pitch: int, band_rows: int, dst: int, k: int, device: torch.device,
-              edge_stream: Optional["torch.cuda.Stream"] = None) -> None:
+              edge_stream: Optional["torch.cuda.Stream"] = None,
+              interior_done: Optional["torch.cuda.Event"] = None) -> None:
     """One depth-k pass of a band with in-kernel NVLink halos: the interior
     rows [k, band-k) read only the band's own rows (the branch-free kernel
     path); the two k-row edge strips read the neighbours' rows through peer
@@ -349,11 +352,15 @@ def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows:
     if band_rows <= 2 * k:
         check(L.life_dev_packed_step_peer(src, up, up_rows, down, down_rows, pitch, band_rows,
                                           dst, 0, band_rows, width, k, main.cuda_stream))
+        if interior_done is not None:
+            interior_done.record(main)
         return
     if edge_stream is not None:
         edge_stream.wait_stream(main)
     check(L.life_dev_packed_step(src, pitch, k, band_rows, dst, pitch, k, width,
                                  band_rows - 2 * k, k, main.cuda_stream))
+    if interior_done is not None:
+        interior_done.record(main)
     es = edge_stream.cuda_stream if edge_stream is not None else main.cuda_stream
     for r0 in (0, band_rows - k):
         check(L.life_dev_packed_step_peer(src, up, up_rows, down, down_rows, pitch, band_rows,
@@ -363,11 +370,19 @@ def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows:
 
 
 class PeerBandDriver:
-    """One rank's band for the fused NVLink halo (see above).  `barrier`
-    defaults to a stream-ordered NCCL all-reduce; a host barrier
-    (synchronize + dist.barrier) is used with non-NCCL process groups."""
+    """One rank's band for the fused NVLink halo (see above).
 
-    def __init__(self, geo: BandGeometry, device: torch.device, group=None):
+    `sync` orders passes across ranks: "neighbour" (default with NCCL) -- a
+    4-byte token sent to and received from the bands above and below,
+    stream-ordered on the compute stream (the reference's per-generation
+    barrier, engine.cpp:79-96, narrowed to the two ranks whose rows a band
+    touches); "allreduce" -- a 1-element NCCL all-reduce over every rank;
+    "host" (forced with non-NCCL groups) -- synchronize + dist.barrier.
+    With `profile` on, CUDA events around each pass's interior launch and
+    barrier give per-rank interior / barrier times (stats())."""
+
+    def __init__(self, geo: BandGeometry, device: torch.device, group=None,
+                 sync: str = "neighbour", profile: bool = False):
         if geo.world < 2:
             raise ConfigError("PeerBandDriver needs at least two ranks")
         self.geo = geo
@@ -400,35 +415,82 @@ class PeerBandDriver:
             self.down_rows, self.down_ptrs = (self.up_rows, self.up_ptrs) if down == up \
                 else peer_ptrs(down)
         self._flag = torch.zeros(1, dtype=torch.int32, device=device)
+        self._tok_in = torch.zeros(2, dtype=torch.int32, device=device)
         self._nccl = dist.get_backend(group) == "nccl"
+        if sync not in ("neighbour", "allreduce", "host"):
+            raise ConfigError(f"unknown pass sync {sync!r}")
+        self.sync = sync if self._nccl else "host"
         self.edge_stream = torch.cuda.Stream(device)
+        self.profile = profile
+        self._events = []  # (start, interior done, pass done, barrier done) per pass
 
     def band(self) -> torch.Tensor:
         return self.buf[self.cur].tensor
 
     def barrier(self) -> None:
-        if self._nccl:
+        if self.sync == "neighbour":
+            # Same issue order on every rank (send up, send down, recv down,
+            # recv up) so the i-th send to a peer matches its i-th receive,
+            # also when up == down (two ranks).  wait() orders the current
+            # stream after the NCCL kernels; the host does not block.
+            g = self.geo
+            up, down = (g.rank - 1) % g.world, (g.rank + 1) % g.world
+            ops = [dist.P2POp(dist.isend, self._flag, up, self.group),
+                   dist.P2POp(dist.isend, self._flag, down, self.group),
+                   dist.P2POp(dist.irecv, self._tok_in[1:], down, self.group),
+                   dist.P2POp(dist.irecv, self._tok_in[:1], up, self.group)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        elif self.sync == "allreduce":
             dist.all_reduce(self._flag, group=self.group)  # ordered on the current stream
         else:
             torch.cuda.synchronize(self.device)
             dist.barrier(group=self.group)
 
-    def compute(self, k: int) -> None:
+    def compute(self, k: int, interior_done=None) -> None:
         """The pass's kernels (interior + peer edge strips), no barrier."""
         g = self.geo
         c = self.cur
         peer_pass(g.width, self.buf[c].ptr.value, self.up_ptrs[c], self.up_rows,
                   self.down_ptrs[c], self.down_rows, g.pitch, g.band_rows,
-                  self.buf[c ^ 1].ptr.value, k, self.device, self.edge_stream)
+                  self.buf[c ^ 1].ptr.value, k, self.device, self.edge_stream,
+                  interior_done=interior_done)
 
     def pass_(self, k: int) -> None:
         g = self.geo
         if not 1 <= k <= g.depth:
             raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
-        self.compute(k)
-        self.barrier()
+        if self.profile:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev[0].record()
+            self.compute(k, interior_done=ev[1])
+            ev[2].record()
+            self.barrier()
+            ev[3].record()
+            self._events.append((k, ev))
+        else:
+            self.compute(k)
+            self.barrier()
         self.cur ^= 1
         self.generations += k
+
+    def stats(self, reset: bool = True) -> dict:
+        """Summed per-pass times (ms) of the profiled passes on this rank:
+        interior launch, pass (interior + edge strips joined) and barrier."""
+        torch.cuda.synchronize(self.device)
+        out = {"passes": len(self._events), "interior_ms": 0.0, "pass_ms": 0.0,
+               "barrier_ms": 0.0, "interior_full_ms": 0.0,
+               "ks": [k for k, _ in self._events]}
+        for k, ev in self._events:
+            t = ev[0].elapsed_time(ev[1])
+            out["interior_ms"] += t
+            if k == self.geo.depth:
+                out["interior_full_ms"] += t
+            out["pass_ms"] += ev[0].elapsed_time(ev[2])
+            out["barrier_ms"] += ev[2].elapsed_time(ev[3])
+        if reset:
+            self._events = []
+        return out
 
     def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None) -> None:
         if generations < 0:

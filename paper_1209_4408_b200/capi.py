@@ -34,6 +34,11 @@ OPT_HALO = 3
 HALO_PEER = 0
 HALO_COPY = 1
 
+LAUNCH_STEP1 = 0
+LAUNCH_FAST = 1
+LAUNCH_ALL_PATHS = 2
+LAUNCH_SPLIT = 3
+
 
 class BandStats(C.Structure):
     """life_band_stats (include/life_gpu.h)."""
@@ -78,6 +83,7 @@ SIGNATURES = [
     ("life_run_batch", C.c_int, [_vp, _vp, _vp, _i32, _i64, _i64, _i64, _i64, C.c_int,
                                  C.POINTER(C.c_float)]),
     ("life_packed_auto_depth", C.c_int, [_i64, _i64]),
+    ("life_packed_launch_kind", C.c_int, [_i64, _i64, _i32]),
     ("life_band_bounds", C.c_int, [_i64, _i32, _vp]),
     ("life_packed_pitch_words", _i64, [_i64]),
     ("life_byte_pitch", _i64, [_i64]),

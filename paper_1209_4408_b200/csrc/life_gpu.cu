@@ -220,9 +220,13 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, 32 * wpb,
                                                           wpb * kRing));
 #else
-  if (FAST)
+  if (FAST) {
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, 32 * wpb,
                                                             wpb * kRing));
+    // LIFE_FAST_BPS (debug builds): blocks per SM the segment model plans for.
+    static const int64_t bps = knob("LIFE_FAST_BPS", 0);
+    if (bps > 0) blocks_per_sm = static_cast<int>(bps);
+  }
 #endif
   // Tiles of seg_rows rows x one strip; pick the segment count that
   // minimises (block waves) x (rows per tile + pipeline fill): blocks run
@@ -308,6 +312,7 @@ int launch_packed_deep(PackedStepArgs a, cudaStream_t s, SplitStreams* ss) {
   // holding word nw-1 (the seam word); strips 1 .. s_last-1 hold only whole
   // words inside [0, nw-1).
   const int32_t s_last = (a.nw - 1) / kStripStride;
+  // (life_packed_launch_kind restates this choice for callers.)
   const bool many_waves = static_cast<int64_t>(total) * a.out_rows >= 2000000;  // ~3 waves of 512-row tiles
   if (!fast_ok || a.strip0 != 0 || s_last < 2 || !many_waves || split_disabled())
     return launch_packed_kernel<K, false>(a, s);
@@ -1096,6 +1101,22 @@ extern "C" {
 int life_packed_auto_depth(int64_t width, int64_t height) {
   if (width < 1 || height < 1) return LIFE_MAX_TEMPORAL_DEPTH;
   return packed_auto_depth(width, height);
+}
+
+int life_packed_launch_kind(int64_t width, int64_t out_rows, int32_t generations) {
+  if (width < 1 || out_rows < 1 || generations < 1 || generations > LIFE_MAX_TEMPORAL_DEPTH)
+    return -1;
+  // Mirrors packed_step (aligned buffers, no trace) -> launch_packed ->
+  // launch_packed_deep for a torus pass outside peer mode.
+  if (generations == 1 && width % 128 == 0) return LIFE_LAUNCH_STEP1;
+  if (generations < 4 || width < 64) return LIFE_LAUNCH_ALL_PATHS;
+  if (width % 32 == 0) return LIFE_LAUNCH_FAST;
+  const int64_t nw = nw32(width);
+  const int64_t strips = ceil_div(nw + 1, kStripStride);
+  const int64_t s_last = (nw - 1) / kStripStride;
+  const bool many_waves = strips * out_rows >= 2000000;
+  if (s_last < 2 || !many_waves || split_disabled()) return LIFE_LAUNCH_ALL_PATHS;
+  return LIFE_LAUNCH_SPLIT;
 }
 
 int life_ctx_create(int device, life_ctx** out) {

@@ -7,6 +7,7 @@ UNMODIFIED reference core (oracle/_ref/liblife_ref.so, built from
     python tests/golden/make_golden.py cfg4       # ~10 min   (12289 x 40961 x 5000)
     python tests/golden/make_golden.py cfg3       # ~20 min   (65536^2 x 1000, 12 GiB RAM)
     python tests/golden/make_golden.py cfg5       # light-cone windows of 262144^2 x 500
+    python tests/golden/make_golden.py split      # windows of split-launch W % 32 != 0 tori
 
 Hash conventions (tests/golden/README.md):
   fnv_bytes  = FNV-1a-64 over the row-major W*H bytes (0/1);
@@ -183,6 +184,28 @@ def cfg5() -> None:
            "windows_500": windows(W, H, 0.4, 42, 500, S, spots),
            "windows_16": windows(W, H, 0.4, 42, 16, 256, spots[:6])}
     dump("golden_cfg5_windows.json", res)
+
+
+def split() -> None:
+    """Light-cone windows of W % 32 != 0 tori deep enough for the split launch
+    (seam strips on the all-paths kernel beside the fast-only kernel,
+    life_packed_launch_kind == LIFE_LAUNCH_SPLIT): windows straddle the column
+    seam and both wrap corners, the boundary between the last fast strip and
+    the first seam strip (column 32*(31*s_last - 1)) and the strip-0 / strip-1
+    boundary (column 960); shapes with nw % 31 == 0 (three seam strips) and
+    W % 32 == 1 as well as 65535^2 and 131071 x 65536."""
+    S = 256
+    res = {}
+    for (W, H, T, p, seed) in [(65535, 65535, 64, 0.5, 42), (131071, 65536, 48, 0.4, 7),
+                               (2975, 700000, 32, 0.4, 2026), (2049, 700000, 32, 0.4, 11)]:
+        nw = -(-W // 32)
+        s_last = (nw - 1) // 31
+        seam_col = 32 * (31 * s_last - 1)
+        spots = [(W - S // 2, H - S // 2), (W - 100, 7), (0, H // 3), (seam_col - S // 2, H // 2),
+                 (960 - S // 2, 2 * H // 3), (W // 2, 12345)]
+        res[f"{W}x{H}"] = {"w": W, "h": H, "density": p, "seed": seed, "T": T,
+                           "windows": windows(W, H, p, seed, T, S, spots)}
+    dump("golden_split_windows.json", res)
 
 
 def cfg3w() -> None:

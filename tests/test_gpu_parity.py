@@ -219,7 +219,10 @@ def _check_schedule(engine, oracle, gold, eng, depth, init):
 @pytest.mark.slow
 def test_cfg2_16384_1000_generations(engine, oracle):
     gold = load_golden("golden_cfg2.json")
-    for eng, depth in [(BYTE, 1), (BYTE, 4), (PACKED, 16), (PACKED, 8)]:
+    # depth 0 = what life_run / bench.py run: byte auto K=6, packed auto K=16
+    assert capi.lib().life_packed_auto_depth(16384, 16384) == 16
+    for eng, depth in [(BYTE, 1), (BYTE, 4), (BYTE, 0), (BYTE, 6), (PACKED, 16), (PACKED, 8),
+                       (PACKED, 0)]:
         _check_schedule(engine, oracle, gold, eng, depth,
                         lambda: engine.init_random(16384, 16384, 0.3, 42, eng))
 
@@ -246,8 +249,32 @@ def test_cfg3_windows(engine, oracle):
 def test_cfg4_nonpow2_sparse_soup(engine, oracle):
     gold = load_golden("golden_cfg4.json")
     soup = oracle.sparse_soup(40961, 12289, seed=42)
-    for eng, depth in [(BYTE, 1), (PACKED, 16)]:
+    # depth 0 = the engine's auto rule: K = 12 on this one-wave W % 32 != 0 torus
+    assert capi.lib().life_packed_auto_depth(40961, 12289) == 12
+    assert capi.lib().life_packed_launch_kind(40961, 12289, 12) == capi.LAUNCH_ALL_PATHS
+    for eng, depth in [(BYTE, 1), (PACKED, 16), (PACKED, 0), (PACKED, 12)]:
         _check_schedule(engine, oracle, gold, eng, depth, lambda: engine.upload(soup))
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("shape", ["65535x65535", "131071x65536", "2975x700000", "2049x700000"])
+def test_split_launch_reference_windows(engine, oracle, shape):
+    """W % 32 != 0 tori that take the split launch (seam strips on the
+    all-paths kernel beside the fast-only kernel) against light-cone windows
+    the REFERENCE computed (make_golden.py split): column seam, both wrap
+    corners, the fast/seam strip boundary, nw % 31 == 0 (three seam strips)
+    and W % 32 == 1."""
+    gold = load_golden("golden_split_windows.json")[shape]
+    W, H, T = gold["w"], gold["h"], gold["T"]
+    for depth in (0, 16, 11):
+        k = depth or capi.lib().life_packed_auto_depth(W, H)
+        assert capi.lib().life_packed_launch_kind(W, H, k) == capi.LAUNCH_SPLIT, (shape, k)
+        engine.init_random(W, H, gold["density"], gold["seed"], PACKED)
+        engine.run(T, PACKED, depth)
+        for w in gold["windows"]:
+            got = engine.window(w["x0"], w["y0"], w["S"], w["S"])
+            assert fnv(oracle, got) == w["fnv_bytes"], (shape, depth, w)
+            assert int(got.sum()) == w["population"]
 
 
 @pytest.mark.slow
