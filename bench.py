@@ -489,7 +489,12 @@ def run_gpu_arm(args) -> None:
             halo = "nccl"
         else:
             peer = True
-    if drv is None:
+    torus = None
+    if drv is None and world == 1:
+        # One GPU: the whole torus, one life_dev_packed_run per step.
+        from paper_1209_4408_b200.bands import TorusDriver
+        drv = torus = TorusDriver(geo, dev)
+    elif drv is None:
         drv = BandDriver(geo, dev, stepper=timed_step)
     soup_host = None
     if cfg.get("soup"):
@@ -534,6 +539,16 @@ def run_gpu_arm(args) -> None:
     record["on"] = True
     if peer:
         drv.profile = True
+    if torus is not None:
+        def on_launch(kind, g, fn):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            n = g // depth if kind == "full" else 1  # kernel passes inside the call
+            launches.append((e0, e1, H * W * g, depth if kind == "full" else g, H, n))
+        torus.on_launch = on_launch
     p0 = torch.cuda.Event(enable_timing=True)
     p1 = torch.cuda.Event(enable_timing=True)
     p0.record()
@@ -558,12 +573,16 @@ def run_gpu_arm(args) -> None:
         all_kern_ms = st["interior_ms"]
         n_main = max(n_full, 1)
     else:
-        full = max((r for (_, _, _, k, r) in launches if k == depth), default=0)
-        main = [(a.elapsed_time(b), n) for (a, b, n, k, r) in launches if k == depth and r == full]
-        kern_ms = sum(t for t, _ in main)
-        kern_cells = sum(n for _, n in main)
-        all_kern_ms = sum(a.elapsed_time(b) for (a, b, _, _, r) in launches)
-        n_main = max(len(main), 1)
+        if torus is not None:
+            torus.on_launch = None
+        launches[:] = [x if len(x) == 6 else (*x, 1) for x in launches]
+        full = max((r for (_, _, _, k, r, _) in launches if k == depth), default=0)
+        main = [(a.elapsed_time(b), n, m) for (a, b, n, k, r, m) in launches
+                if k == depth and r == full]
+        kern_ms = sum(t for t, _, _ in main)
+        kern_cells = sum(n for _, n, _ in main)
+        all_kern_ms = sum(a.elapsed_time(b) for (a, b, _, _, _, _) in launches)
+        n_main = max(sum(m for _, _, m in main), 1)
         rank_stats.update({"interior_ms": kern_ms, "kernel_ms": all_kern_ms,
                            "launches": len(launches)})
         if world > 1:
@@ -1041,11 +1060,38 @@ def run_byte_arm(args) -> None:
                 eng.run(gens, capi.ENGINE_BYTE, depth)
                 eng.download(hout)
             e2e_s = time.perf_counter() - t0
+            byte_final = hout.copy()
         e2e = {"value": W * H * gens * steps_e2e / e2e_s / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": W * H, "d2h_bytes_per_step": W * H,
                "api": "C-ABI life_grid_upload_u8 + life_run(LIFE_ENGINE_BYTE) + "
                       "life_grid_download_u8 from/to pinned host memory (host-timed)",
                "steps": steps_e2e}
+        # The same byte-per-cell API with the packed engine behind it: the
+        # uint8 grid is packed on the device at upload (warp ballots), runs
+        # the temporal-blocked packed passes and is unpacked at download --
+        # north_star's "converted at the API boundary".
+        with life.Engine(0) as eng:
+            eng.upload(host)
+            eng.run(1, capi.ENGINE_PACKED, 0)
+            eng.download(hout)
+            eng.upload(host)
+            eng.run(gens, capi.ENGINE_PACKED, 0)
+            eng.download(hout)
+            ok = fnv(hout.tobytes()) == fnv(byte_final.tobytes()) if byte_final is not None \
+                else None
+            t0 = time.perf_counter()
+            for _ in range(steps_e2e):
+                eng.upload(host)
+                eng.run(gens, capi.ENGINE_PACKED, 0)
+                eng.download(hout)
+            pk_s = time.perf_counter() - t0
+        e2e["packed_behind_byte_api"] = {
+            "value": W * H * gens * steps_e2e / pk_s / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": W * H, "d2h_bytes_per_step": W * H,
+            "api": "C-ABI life_grid_upload_u8 (device pack) + life_run(LIFE_ENGINE_PACKED, "
+                   "depth auto) + life_grid_download_u8 (device unpack), pinned host memory, "
+                   "host-timed",
+            "same_result_as_byte_engine": ok, "steps": steps_e2e}
     cpu = None
     if not args.no_cpu:
         try:

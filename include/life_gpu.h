@@ -230,6 +230,15 @@ int64_t life_byte_pitch(int64_t width);
 int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0,
                          int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0,
                          int64_t width, int64_t out_rows, int32_t generations, void* stream);
+/* `generations` of a W x H packed torus (rows of `pitch` words) ping-ponging
+ * between buf_a (holding the input) and buf_b, `depth` (1..16) generations
+ * per pass (one life_dev_packed_step launch each, then the remainder): the
+ * result is in buf_b if *result_in_b = 1, else in buf_a.  (A persistent
+ * single-launch form with per-tile neighbour flags between passes was
+ * measured 11-23 % slower on one-wave tori and is not used.) */
+int life_dev_packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width,
+                        int64_t height, int64_t generations, int32_t depth, int32_t* result_in_b,
+                        void* stream);
 /* The same pass for one row band of a torus split across GPUs, with the
  * halo read IN the kernel over NVLink: input rows above the band come from
  * `up` (the last rows of the band above, up_rows tall -- a peer GPU's buffer

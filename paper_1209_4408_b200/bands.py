@@ -245,6 +245,72 @@ class BandDriver:
         return int(acc.item())
 
 
+class TorusDriver:
+    """The single-GPU case of the band drivers (one band = the whole torus,
+    no halo): run() is ONE life_dev_packed_run call (the full-depth passes,
+    then the remainder).  `on_launch(kind, generations, fn)` (optional)
+    splits it into the full-pass call and the remainder call and wraps each,
+    so a profiler can put events around them."""
+
+    def __init__(self, geo: BandGeometry, device: torch.device):
+        if geo.world != 1:
+            raise ConfigError("TorusDriver is the one-band case")
+        self.geo = geo
+        self.device = device
+        shape = (geo.height, geo.pitch)
+        self.buf = [torch.zeros(shape, dtype=torch.int32, device=device) for _ in range(2)]
+        self.cur = 0
+        self.generations = 0
+        self.on_launch = None
+
+    def band(self) -> torch.Tensor:
+        return self.buf[self.cur]
+
+    def _call(self, gens: int) -> None:
+        import ctypes as C
+        g = self.geo
+        a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
+        flip = C.c_int32(0)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_run(a.data_ptr(), b.data_ptr(), g.pitch, g.width,
+                                             g.height, gens, g.depth, C.byref(flip), stream))
+        self.cur ^= flip.value
+        self.generations += gens
+
+    def run(self, generations: int) -> None:
+        if generations < 0:
+            raise ConfigError(f"iteration count must be non-negative, got {generations}")
+        k = self.geo.depth
+        if self.on_launch is None:
+            self._call(generations)
+            return
+        full = generations // k * k
+        if full:
+            self.on_launch("full", full, lambda: self._call(full))
+        if generations - full:
+            self.on_launch("rem", generations - full, lambda: self._call(generations - full))
+
+    def init_random(self, density: float, seed: int) -> None:
+        g = self.geo
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_random(self.band().data_ptr(), g.pitch, g.width, 0,
+                                                g.height, density, seed, stream))
+        self.generations = 0
+
+    def load_rows(self, words) -> None:
+        src = torch.from_numpy(words.view("int32").copy())
+        self.band()[:, :src.shape[1]].copy_(src)
+        self.generations = 0
+
+    def population(self) -> int:
+        g = self.geo
+        acc = torch.zeros(1, dtype=torch.int64, device=self.device)
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_population(self.band().data_ptr(), g.pitch, g.width,
+                                                    g.height, acc.data_ptr(), stream))
+        return int(acc.item())
+
+
 class LocalBands:
     """P row bands of one torus on ONE device, halos exchanged by device
     copies instead of NCCL: exercises the band seams, ghost addressing and

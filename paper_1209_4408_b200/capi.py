@@ -84,6 +84,8 @@ SIGNATURES = [
                                  C.POINTER(C.c_float)]),
     ("life_packed_auto_depth", C.c_int, [_i64, _i64]),
     ("life_packed_launch_kind", C.c_int, [_i64, _i64, _i32]),
+    ("life_dev_packed_run", C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32,
+                                      C.POINTER(_i32), _vp]),
     ("life_band_bounds", C.c_int, [_i64, _i32, _vp]),
     ("life_packed_pitch_words", _i64, [_i64]),
     ("life_byte_pitch", _i64, [_i64]),

@@ -83,6 +83,11 @@ int packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t i
 // temporal_depth 0 on the multi-pass packed engine (exported as
 // life_packed_auto_depth).
 int packed_auto_depth(int64_t width, int64_t height);
+// `generations` of a packed torus ping-ponging between buf_a (input) and
+// buf_b: whole passes of `depth`, then the remainder; *result_in_b = 1 if the result is in buf_b.
+int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, int64_t height,
+               int64_t generations, int32_t depth, cudaStream_t stream, SplitStreams* ss,
+               int* result_in_b);
 
 // Small kernels the multi-device context launches on band buffers.
 int launch_mask_tail(uint32_t* words, int64_t pitch, int64_t width, int64_t rows,

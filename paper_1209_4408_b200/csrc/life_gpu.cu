@@ -181,6 +181,9 @@ int peer_sync_trips() {
   return v;
 }
 
+// Tiles up to this many rows run the fast kernel's single-loop-body variant.
+constexpr int64_t kUniMaxRows = 1024;
+
 template <int K, bool FAST>
 int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   const auto kernel = FAST ? packed_tb_fast_kernel<K> : packed_tb_kernel<K>;
@@ -196,6 +199,10 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   if (wpb == 0) {
     LIFE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    kMaxWarps * kRing));
+    if (FAST)
+      LIFE_CUDA(cudaFuncSetAttribute(packed_tb_fast_kernel<K, true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kMaxWarps * kRing));
     int nb = 0;
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kPackedThreads, 4 * kRing));
     int w = std::min(std::max(nb, 1) * (kPackedThreads / 32), kMaxWarps);
@@ -210,7 +217,7 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
 #endif
     // The fast-only kernel has no block barrier: LIFE_FAST_WPB (debug builds)
     // sets its warps per block (several blocks per SM), for measurement.
-    const int64_t forced = FAST ? knob("LIFE_FAST_WPB", 0) : 0;
+    const int64_t forced = knob(FAST ? "LIFE_FAST_WPB" : "LIFE_WPB", 0);
     if (forced > 0) w = std::min(static_cast<int>(forced), w);
     wpb = w;
     warps_per_block.put(dev, wpb);
@@ -269,7 +276,10 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   a.sync_every = FAST ? 0 : (a.peer ? peer_sync_trips() : kSyncTrips);
   const int64_t blocks = ceil_div(tiles, wpb);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
-  LIFE_TRY(launch_pdl(kernel, static_cast<unsigned>(blocks), 32 * wpb,
+  // Short tiles of the fast kernel run the single-loop-body variant (UNI).
+  const auto launch_kernel = (FAST && a.seg_rows <= kUniMaxRows) ? packed_tb_fast_kernel<K, true>
+                                                                  : kernel;
+  LIFE_TRY(launch_pdl(launch_kernel, static_cast<unsigned>(blocks), 32 * wpb,
                       static_cast<size_t>(wpb) * kRing, s, a));
   LIFE_CHECK_LAUNCH("packed_tb_kernel");
   return LIFE_OK;
@@ -473,6 +483,33 @@ int packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t i
   a.trace = g_trace.load(std::memory_order_relaxed);
   return kPackedLaunchers[generations](a, stream, ss);
 }
+
+int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, int64_t height,
+               int64_t generations, int32_t depth, cudaStream_t stream, SplitStreams* ss,
+               int* result_in_b) {
+  if (depth < 1 || depth > LIFE_MAX_TEMPORAL_DEPTH)
+    return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [1, %d], got %d",
+                     LIFE_MAX_TEMPORAL_DEPTH, depth);
+  if (generations < 0) return set_error(LIFE_ERR_CONFIG, "generations must be >= 0");
+  if (width < 1 || height < 1 || pitch < 2 * ceil_div(width, 64) || buf_a == buf_b)
+    return set_error(LIFE_ERR_CONFIG, "bad packed run geometry");
+  uint32_t* cur = buf_a;
+  uint32_t* nxt = buf_b;
+  int flip = 0;
+  const int64_t full = generations / depth;
+  const int rem = static_cast<int>(generations % depth);
+  for (int64_t i = 0; i < full; ++i) {
+    LIFE_TRY(packed_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, depth, stream, ss));
+    std::swap(cur, nxt);
+    flip ^= 1;
+  }
+  if (rem > 0) {
+    LIFE_TRY(packed_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, rem, stream, ss));
+    flip ^= 1;
+  }
+  if (result_in_b) *result_in_b = flip;
+  return LIFE_OK;
+}
 }  // namespace detail
 }  // namespace lifegpu
 
@@ -483,6 +520,16 @@ int life_dev_packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, 
                          int64_t out_rows, int32_t generations, void* stream) {
   return packed_step(in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width, out_rows,
                      generations, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int life_dev_packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width,
+                        int64_t height, int64_t generations, int32_t depth, int32_t* result_in_b,
+                        void* stream) {
+  int flip = 0;
+  LIFE_TRY(packed_run(buf_a, buf_b, pitch, width, height, generations, depth,
+                      static_cast<cudaStream_t>(stream), nullptr, &flip));
+  if (result_in_b) *result_in_b = flip;
+  return LIFE_OK;
 }
 
 int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
@@ -1593,6 +1640,19 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
       c->pk_cur ^= 1;
       done = stop;
       ++c->passes;
+      LIFE_TRY(prof_mark());
+      LIFE_TRY(record(done));
+      continue;
+    }
+    if (engine == LIFE_ENGINE_PACKED && !c->profile && stop - done >= 2 * int64_t(depth)) {
+      // Every generation up to the next stop (packed_run: full passes, then
+      // the remainder).
+      int flip = 0;
+      LIFE_TRY(packed_run(c->pk[c->pk_cur], c->pk[c->pk_cur ^ 1], c->pk_pitch, c->W, c->H,
+                          stop - done, depth, c->stream, &c->split[0], &flip));
+      c->pk_cur ^= flip;
+      c->passes += ceil_div(stop - done, int64_t(depth));
+      done = stop;
       LIFE_TRY(prof_mark());
       LIFE_TRY(record(done));
       continue;

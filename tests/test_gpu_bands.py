@@ -204,3 +204,37 @@ def test_band_interiors_take_the_split_launch():
         assert L.life_fnv1a64(host.ctypes.data, host.nbytes, 0) == want
         del lb, grid
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("W,H,depth,gens", [
+    (2048, 6400, 16, 16 * 3 + 5),   # odd passes + remainder
+    (2048, 6400, 16, 16 * 4),       # even passes, no remainder
+    (4096, 3800, 8, 8 * 5 + 3),
+    (8192, 1536, 12, 12 * 2 + 1),
+    (2047, 6400, 16, 40),           # W % 32 != 0
+    (2048, 100, 16, 7),             # remainder only
+])
+def test_dev_packed_run_matches_oracle(oracle, W, H, depth, gens):
+    """life_dev_packed_run (full passes then the remainder, ping-pong) equals
+    the oracle, result buffer as reported."""
+    import ctypes as C
+
+    import torch
+    from paper_1209_4408_b200 import capi
+    from paper_1209_4408_b200.life import check
+    L = capi.lib()
+    pitch = int(L.life_packed_pitch_words(W))
+    dev = torch.device("cuda", 0)
+    a = torch.zeros((H, pitch), dtype=torch.int32, device=dev)
+    b = torch.zeros_like(a)
+    s = torch.cuda.current_stream(dev).cuda_stream
+    check(L.life_dev_packed_random(a.data_ptr(), pitch, W, 0, H, 0.4, 77, s))
+    flip = C.c_int32(-1)
+    check(L.life_dev_packed_run(a.data_ptr(), b.data_ptr(), pitch, W, H, gens, depth,
+                                C.byref(flip), s))
+    torch.cuda.synchronize()
+    passes = gens // depth + (1 if gens % depth else 0)
+    assert flip.value == passes % 2
+    got = words_to_cells((b if flip.value else a).cpu().numpy(), W)
+    want, _ = oracle.run(oracle.random_fill(W, H, 0.4, 77), gens)
+    assert np.array_equal(got, want)
