@@ -107,7 +107,7 @@ def test_run_writes_pbm_to_out(cli, tmp_path):
 
 
 @pytest.mark.gpu
-def test_bench_emits_pinned_csv(cli, tmp_path):
+def test_bench_emits_pinned_csv(cli, tmp_path, oracle):
     csv = tmp_path / "m.csv"
     r = run(cli, "bench", "--sizes", "64x32,96x40", "--iterations", "4,8", "--strategies",
             "gpu,gpu:4,gpu-byte,gpu-byte:3,gpu-resident", "--repetitions", "2", "--warmup", "0",
@@ -121,8 +121,11 @@ def test_bench_emits_pinned_csv(cli, tmp_path):
     assert [r[3] for r in rows[:5]] == ["gpu", "gpu:4", "gpu-byte", "gpu-byte:3", "gpu-resident"]
     assert rows[0][9] == "1.00"                        # baseline row
     pops = {(r[0], r[1], r[2]) for r in rows}
-    for key in pops:                                   # same final population for every engine
-        assert len({r[11] for r in rows if (r[0], r[1], r[2]) == key}) == 1
+    for key in pops:                                   # every engine: the oracle's population
+        w, h, it = map(int, key)
+        seed, dens = [(int(r[5]), float(r[6])) for r in rows if (r[0], r[1], r[2]) == key][0]
+        want, _ = oracle.run(oracle.random_fill(w, h, dens, seed), it)
+        assert {r[11] for r in rows if (r[0], r[1], r[2]) == key} == {str(int(want.sum()))}
     r2 = run(cli, "bench", "--sizes", "64x32", "--iterations", "4", "--strategies", "gpu",
              "--repetitions", "1", "--warmup", "0", "--gpu-columns")
     assert r2.returncode == 0
