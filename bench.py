@@ -71,54 +71,87 @@ def ncu_traffic(config: int, depth, engine: str = ""):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 50 ms.  Started
+    before the warm-up (nvidia-smi takes ~0.2 s to emit its first sample);
+    mark() brackets the timed region and summary() keeps the samples whose
+    timestamps fall inside it (the closest ones if the region is shorter
+    than the sampling interval)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown")
 
     def __init__(self, device: int):
         self.device = device
         self.proc = None
+        self.window = [None, None]
 
     def __enter__(self):
+        import threading
+        self.lines = []
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.device)],
+                 "-lms", "50", "-i", str(self.device)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def reader():
+            for line in self.proc.stdout:
+                if line.strip():
+                    self.lines.append(line)
+                    first.set()
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        first.wait(5.0)  # the first sample is out before the measured work starts
         return self
 
+    def mark(self, which: int) -> None:
+        self.window[which] = time.time()
+
     def __exit__(self, *exc):
-        self.lines = []
         if self.proc:
+            time.sleep(0.06)  # one more sample after the region
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [l for l in out.splitlines() if l.strip()]
+            self.thread.join(timeout=5)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], None, set()
+        import datetime
         names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        rows = []
         for line in getattr(self, "lines", []):
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 7:
                 continue
             try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                rows.append((ts, float(parts[1]), float(parts[2]), parts[3:7]))
             except ValueError:
                 continue
-            for n, v in zip(names, parts[2:6]):
+        t0, t1 = self.window
+        inside = rows
+        if t0 is not None and t1 is not None and rows:
+            inside = [r for r in rows if t0 <= r[0] <= t1]
+            if not inside:  # region shorter than the interval: the nearest samples
+                mid = 0.5 * (t0 + t1)
+                inside = sorted(rows, key=lambda r: abs(r[0] - mid))[:2]
+        reasons = set()
+        for r in inside:
+            for n, v in zip(names, r[3]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [r[1] for r in inside]
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": inside[-1][2] if inside else None,
+                "reasons": sorted(reasons), "samples": len(sm),
+                "window_s": round(t1 - t0, 3) if t0 and t1 else None}
 
 
 def blocks_shape(n: int) -> tuple[int, int]:
@@ -509,23 +542,26 @@ def run_gpu_arm(args) -> None:
     if grid_bytes * 2 < 4 * L2_BYTES:
         flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev)
 
+    clocks = ClockSampler(local).__enter__()  # running through warm-up and timed steps
     for _ in range(args.warmup):
         drv.run(gens)
     barrier()
     step_ms = []
     l0 = L.life_kernel_launches()
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            if flush is not None:
-                flush.fill_(1)
-            barrier()
-            e0 = torch.cuda.Event(enable_timing=True)
-            e1 = torch.cuda.Event(enable_timing=True)
-            e0.record()
-            drv.run(gens)
-            e1.record()
-            torch.cuda.synchronize()
-            step_ms.append(e0.elapsed_time(e1))
+    clocks.mark(0)
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        drv.run(gens)
+        e1.record()
+        torch.cuda.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    clocks.mark(1)
+    clocks.__exit__(None, None, None)
     gpu_launches = int(L.life_kernel_launches() - l0)
     barrier()
     total_ms = max_over_ranks(sum(step_ms))
@@ -846,14 +882,17 @@ def run_ctx_arm(args) -> None:
     init()
     b = e.bands()
     depth = args.depth or 0
+    clocks = ClockSampler(devices[0]).__enter__()  # running through warm-up and timed steps
     for _ in range(args.warmup):
         e.run(gens, capi.ENGINE_PACKED, depth)
     l0 = L.life_kernel_launches()
     ms = []
-    with ClockSampler(devices[0]) as clocks:
-        for _ in range(args.steps):
-            e.run(gens, capi.ENGINE_PACKED, depth)
-            ms.append(max(st["run_ms"] for st in e.band_stats()))
+    clocks.mark(0)
+    for _ in range(args.steps):
+        e.run(gens, capi.ENGINE_PACKED, depth)
+        ms.append(max(st["run_ms"] for st in e.band_stats()))
+    clocks.mark(1)
+    clocks.__exit__(None, None, None)
     gpu_launches = int(L.life_kernel_launches() - l0)
     e.set_option(capi.OPT_PROFILE, 1)
     e.run(gens, capi.ENGINE_PACKED, depth)
@@ -1010,23 +1049,48 @@ def run_byte_arm(args) -> None:
             cur[0] ^= 1
             done += k
 
+    clocks = ClockSampler(0).__enter__()  # running through warm-up and timed steps
     for _ in range(args.warmup):
         step(False)
     torch.cuda.synchronize()
     l0 = L.life_kernel_launches()
     ms = []
-    with ClockSampler(0) as clocks:
-        for _ in range(args.steps):
-            if flush is not None:
-                flush.fill_(1)
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            step(True)
-            e1.record()
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
+    clocks.mark(0)
+    for _ in range(args.steps):
+        if flush is not None:
+            flush.fill_(1)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step(False)
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    clocks.mark(1)
+    clocks.__exit__(None, None, None)
     n_launch = int(L.life_kernel_launches() - l0)
+    # One profiled step after the timed ones: per-launch events (they would
+    # serialise programmatic dependent launch inside the timed steps).
+    if flush is not None:
+        flush.fill_(1)
+    torch.cuda.synchronize()
+    step(True)
+    torch.cuda.synchronize()
+    # Parity: the configuration again from the initial grid, against the
+    # reference's golden (FNV-1a-64 over the W*H 0/1 bytes).
+    parity = {"ok": None, "reason": "--no-parity"}
+    gold = None if args.no_parity else golden_for(args.config, gens)
+    if gold is not None and gold["kind"] == "hash" and not cfg.get("soup"):
+        with open(os.path.join(GOLDEN_DIR, gold["source"])) as f:
+            gj = json.load(f)
+        want = (gj["cfg1"] if args.config == 1 else gj["gens"])[str(gens)]
+        check(L.life_dev_byte_random(bufs[cur[0]].data_ptr(), pitch, W, 0, H, cfg["p"], 42, stream))
+        step(False)
+        torch.cuda.synchronize()
+        got = f"{fnv(bufs[cur[0]][:, :W].contiguous().cpu().numpy().tobytes()):016x}"
+        parity = {"ok": got == want["fnv_bytes"], "kind": "full-grid byte FNV-1a-64",
+                  "got": got, "want": want["fnv_bytes"], "generations": gens,
+                  "source": "tests/golden/" + gold["source"]}
     full = [(a.elapsed_time(b), k) for a, b, k in launches if k == depth] or \
         [(a.elapsed_time(b), k) for a, b, k in launches]
     kern_ms = sum(t for t, _ in full) / len(full)
@@ -1107,8 +1171,11 @@ def run_byte_arm(args) -> None:
                    "l2": "inputs larger than L2" if flush is None else "L2 flushed between steps"},
         "roofline": byte_roofline(W * H * k_main, k_main, kern_ms, hbm_peak, int_ops,
                                   ncu_traffic(args.config, k_main, "byte")),
-        "cpu_baseline": cpu, "e2e": e2e,
+        "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": n_launch, "clocks": clocks.summary()}), flush=True)
+    if parity.get("ok") is False:
+        print("bench.py: PARITY MISMATCH against the reference golden", file=sys.stderr)
+        sys.exit(3)
 
 
 def run_resident_arm(args) -> None:
@@ -1150,22 +1217,37 @@ def run_resident_arm(args) -> None:
         check(L.life_dev_packed_run_resident(a.data_ptr(), b.data_ptr(), pitch, W, H, gens, stream))
         cur[0] ^= 1
 
+    clocks = ClockSampler(0).__enter__()  # running through warm-up and timed steps
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     l0 = L.life_kernel_launches()
     ms = []
-    with ClockSampler(0) as clocks:
-        for _ in range(args.steps):
-            flush.fill_(1)  # the grid fits in L2: flush between steps
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            step()
-            e1.record()
-            torch.cuda.synchronize()
-            ms.append(e0.elapsed_time(e1))
+    clocks.mark(0)
+    for _ in range(args.steps):
+        flush.fill_(1)  # the grid fits in L2: flush between steps
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    clocks.mark(1)
+    clocks.__exit__(None, None, None)
     n_launch = int(L.life_kernel_launches() - l0)
+    parity = {"ok": None, "reason": "--no-parity"}
+    gold = None if args.no_parity else golden_for(args.config, gens)
+    if gold is not None and gold["kind"] == "hash" and not cfg.get("soup"):
+        check(L.life_dev_packed_random(bufs[cur[0]].data_ptr(), pitch, W, 0, H, cfg["p"], 42,
+                                       stream))
+        step()
+        torch.cuda.synchronize()
+        wpr = (W + 63) // 64
+        got = f"{fnv(bufs[cur[0]][:, :2 * wpr].contiguous().cpu().numpy().tobytes()):016x}"
+        parity = {"ok": got == gold["fnv_packed"], "kind": "full-grid packed FNV-1a-64",
+                  "got": got, "want": gold["fnv_packed"], "generations": gens,
+                  "source": "tests/golden/" + gold["source"]}
     step_ms = sum(ms) / len(ms)
     value = W * H * gens * args.steps / (sum(ms) * 1e-3) / 1e9
     achieved = W * H * gens * OPS_PER_UPDATE / (step_ms * 1e-3) / 1e12
@@ -1217,8 +1299,11 @@ def run_resident_arm(args) -> None:
                      "frac_of_gpu": achieved / (int_ops / 1e12) if int_ops else None,
                      "ops_per_cell_update": OPS_PER_UPDATE, "mean_launch_ms": step_ms,
                      "traffic": None},
-        "cpu_baseline": cpu, "e2e": e2e,
+        "parity": parity, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": n_launch, "clocks": clocks.summary()}), flush=True)
+    if parity.get("ok") is False:
+        print("bench.py: PARITY MISMATCH against the reference golden", file=sys.stderr)
+        sys.exit(3)
 
 
 def main() -> None:
