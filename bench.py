@@ -969,36 +969,41 @@ def self_launch(args) -> int:
     return subprocess.call(cmd, env=env)
 
 
-# byte_tb_kernel per 4-cell word (csrc/kernels.cuh byte_row_fma / byte_rule): ALU pipe --
-# 2 funnel shifts, (n|x)^3, ~y & m, >>7; FMA pipe (IMAD a*one+b) -- the adds h, hn, the
-# 3-way neighbour sum (2) and +0x7f7f7f7f.
-BYTE_ALU_OPS_PER_UPDATE = 5 / 4.0
-BYTE_FMA_OPS_PER_UPDATE = 5 / 4.0
+# byte_tb2_kernel per 32-bit word = 4 columns x 2 row streams = 8 cell-updates
+# (csrc/kernels.cuh byte_row_fma / nib_rule): ALU pipe -- 2 funnel shifts, n & 7,
+# (n|x)^3, ~y & m, >>3; FMA pipe (IMAD a*one+b) -- the adds hn, h, the two
+# vertical adds and +0x77777777.  (Round 1's one-stream byte_tb_kernel: 5 + 5
+# per 4 cells.)
+BYTE_ALU_OPS_PER_UPDATE = 6 / 8.0
+BYTE_FMA_OPS_PER_UPDATE = 5 / 8.0
 
 
 def byte_roofline(cell_updates: float, k: int, kern_ms: float, hbm_peak: float, int_ops: float,
                   traffic) -> dict:
     """Roofline of one byte-engine pass of depth k: HBM-bound at k = 1 (2 B per
-    cell-update); for k >= 2 instruction-bound: 1.25 ALU-pipe + 1.25 FMA-pipe
-    ops per cell-update, each pipe at the measured LOP3 lane rate P and one
-    instruction issued per cycle per sub-partition, so the peak of the mix is
-    2P lane-ops/s (bound P / 1.25 cell-updates/s)."""
+    cell-update); for k >= 2 instruction-bound: 0.75 ALU-pipe + 0.625 FMA-pipe
+    ops per cell-update (two row streams per word), each pipe at the measured
+    LOP3 lane rate P and one instruction issued per cycle per sub-partition:
+    the ALU pipe binds: achieved = ALU-pipe ops/s of the kernel, peak = P,
+    bound P / 0.75 cell-updates/s."""
     t = kern_ms * 1e-3
     hbm = {"achieved": 2.0 / k * cell_updates / t / 1e9, "peak": hbm_peak, "unit": "GB/s",
            "bytes_per_cell_update": 2.0 / k}
     hbm["frac"] = hbm["achieved"] / hbm_peak
     if k == 1 or not int_ops:
-        return {"bound": "hbm", "kernel": "byte_step_kernel" if k == 1 else f"byte_tb_kernel<{k}>",
+        return {"bound": "hbm", "kernel": "byte_step_kernel" if k == 1 else f"byte_tb2_kernel<{k}>",
                 **hbm, "mean_launch_ms": kern_ms, "traffic": traffic}
     ops = BYTE_ALU_OPS_PER_UPDATE + BYTE_FMA_OPS_PER_UPDATE
-    ach = cell_updates * ops / t / 1e12
-    peak = 2 * int_ops / 1e12
-    return {"bound": "int", "kernel": f"byte_tb_kernel<{k}>", "achieved": ach, "peak": peak,
+    ach = cell_updates * BYTE_ALU_OPS_PER_UPDATE / t / 1e12
+    peak = int_ops / 1e12
+    return {"bound": "int", "kernel": f"byte_tb2_kernel<{k}>", "achieved": ach, "peak": peak,
             "unit": "Tops/s", "frac": ach / peak, "ops_per_cell_update": ops,
             "alu_ops_per_cell_update": BYTE_ALU_OPS_PER_UPDATE,
             "fma_ops_per_cell_update": BYTE_FMA_OPS_PER_UPDATE,
-            "peak_source": "2 x measured LOP3 lane rate (ALU + FMA pipes, one issue per cycle)",
+            "peak_source": "measured LOP3 lane rate (the ALU pipe, which binds)",
             "roofline_updates_per_s": int_ops / BYTE_ALU_OPS_PER_UPDATE,
+            "issue_frac": cell_updates * ops / t / (2 * int_ops),
+            "vs_one_stream_bound": cell_updates / t / (int_ops / 1.25),
             "hbm": hbm, "mean_launch_ms": kern_ms, "traffic": traffic}
 
 
@@ -1029,7 +1034,7 @@ def run_byte_arm(args) -> None:
     launches = []
     cur = [0]
 
-    depth = args.byte_depth or (6 if W * H >= 2 ** 26 else 4)
+    depth = args.byte_depth or (8 if W * H >= 2 ** 26 else 4)  # life_run's byte auto rule
     if W % 16:
         depth = 1
 

@@ -1087,6 +1087,151 @@ __global__ void __launch_bounds__(kByteThreads) byte_tb_kernel(const ByteStepArg
 }
 
 // ---------------------------------------------------------------------------
+// byte_tb_kernel with TWO row streams per register word (nibble SWAR).  A
+// warp's tile of n rows is split into two halves that run through the same
+// K-stage pipeline side by side: stream A (rows [y, y+nA)) in the low nibble
+// of every byte, stream B (rows [y+nA, y+n)) in the high nibble.  Counts stay
+// <= 9 < 16, so no add carries between nibbles, and the horizontal neighbour
+// is still one byte away, so the funnel shifts serve both streams at once:
+// one instruction sequence updates 8 cells per 32-bit word instead of 4.
+// HBM layout and traffic are unchanged (one byte per cell; stage 0 packs A |
+// B << 4 from the two rows it loads, the last stage unpacks and stores both).
+// Rule per nibble: n' = n & 7 (n = 8 -> 0: dead either way, and it keeps t <=
+// 7 so t + 7 cannot carry), t = (n' | self) ^ 3, alive iff t == 0, i.e. bit 3
+// of t + 7 clear.  Per word and stage: ALU 2 SHF (neighbours) + 2 LOP3 + 1
+// LOP3 + 1 SHF, FMA 5 IMAD (hn, h, two vertical adds, t + 7) -- 11
+// instructions per 8 cell-updates vs 10 per 4 in byte_tb_kernel.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t nib_rule(uint32_t up_h, uint32_t dn_h, uint32_t mid_hn,
+                                             uint32_t mid_x, uint32_t one) {
+  const uint32_t n = add_fma(add_fma(up_h, dn_h, one), mid_hn, one) & 0x77777777u;
+  const uint32_t t = (n | mid_x) ^ 0x33333333u;
+  return (~add_fma(t, 0x77777777u, one) & 0x88888888u) >> 3;
+}
+
+constexpr int kByteTb2PF = 4;
+constexpr int kByteTb2Smem = (kByteThreads / 32) * 2 * kByteTb2PF * 64 * 16;  // per block
+
+template <int K>
+__global__ void __launch_bounds__(kByteThreads) byte_tb2_kernel(const ByteStepArgs a) {
+  constexpr int PF = kByteTb2PF;
+  constexpr int kLag = 3 * K - 1;  // output row j leaves the pipeline at step j + kLag
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kByteThreads + threadIdx.x) >> 5;
+  const int strip = static_cast<int>(gwarp % a.n_strips);
+  const int64_t seg = gwarp / a.n_strips;
+  const int64_t y0 = seg * a.seg_rows;
+  if (y0 >= a.out_rows) return;  // warp-uniform
+  const int n = static_cast<int>(min(a.seg_rows, a.out_rows - y0));
+  const int nA = (n + 1) >> 1, nB = n - nA;
+  const int64_t vi = static_cast<int64_t>(strip) * kByteTbStride + lane - 1;
+  int64_t src = vi % a.nv;
+  if (src < 0) src += a.nv;
+  const bool in_grid = vi >= 0 && vi < a.nv;
+  const bool store_mid = in_grid && lane >= 1 && lane <= 30;
+  const bool store_lo = in_grid && lane == 31;
+  const bool store_hi = in_grid && lane == 0;
+  const uint32_t one = a.one;
+  extern __shared__ uint4 byte_tb2_ring[];
+  uint4* ring = byte_tb2_ring + (threadIdx.x >> 5) * (2 * PF * 64) + lane;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: previous pass complete
+  asm volatile("griddepcontrol.launch_dependents;");
+
+  const int in_rows = static_cast<int>(a.in_rows);
+  int rowA = static_cast<int>(wrap_row(a.in_row0, y0 - K, a.in_rows));
+  int rowB = static_cast<int>(wrap_row(a.in_row0, y0 + nA - K, a.in_rows));
+  const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch);
+  const char* const in_lane = reinterpret_cast<const char*>(a.in + src * 16);
+  auto issue = [&](int slot) {
+    cp_async16(reinterpret_cast<uint32_t*>(ring + slot * 64),
+               row_addr(in_lane, static_cast<uint32_t>(rowA), in_pitch_b));
+    cp_async16(reinterpret_cast<uint32_t*>(ring + slot * 64 + 32),
+               row_addr(in_lane, static_cast<uint32_t>(rowB), in_pitch_b));
+    cp_async_commit();
+    rowA = (rowA + 1 == in_rows) ? 0 : rowA + 1;
+    rowB = (rowB + 1 == in_rows) ? 0 : rowB + 1;
+  };
+  const uint32_t out_pitch_b = static_cast<uint32_t>(a.out_pitch);
+  char* const out_A = reinterpret_cast<char*>(a.out + (a.out_row0 + y0) * a.out_pitch + vi * 16);
+  char* const out_B =
+      reinterpret_cast<char*>(a.out + (a.out_row0 + y0 + nA) * a.out_pitch + vi * 16);
+
+#pragma unroll
+  for (int u = 0; u < PF; ++u) issue(u);
+  uint32_t uh[K][4], mh[K][4], mhn[K][4], mx[K][4], xin[K][4];
+#pragma unroll
+  for (int g = 0; g < K; ++g)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) uh[g][i] = mh[g][i] = mhn[g][i] = mx[g][i] = xin[g][i] = 0u;
+
+  const int trips = (nA + kLag + PF - 1) / PF;
+  int half = 0;
+  auto trip = [&](const int t, auto steady_tag) {
+    constexpr bool STEADY = decltype(steady_tag)::value;
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      issue((half ^ PF) + u);
+      cp_async_wait<PF>();
+      {
+        const uint4 va = ring[(half + u) * 64];
+        const uint4 vb = ring[(half + u) * 64 + 32];
+        // Both streams in one word: A | B << 4 (bytes are 0/1), on the FMA pipe.
+        xin[0][0] = vb.x * 16u + va.x;
+        xin[0][1] = vb.y * 16u + va.y;
+        xin[0][2] = vb.z * 16u + va.z;
+        xin[0][3] = vb.w * 16u + va.w;
+      }
+      uint32_t y_last[4];
+#pragma unroll
+      for (int g = K - 1; g >= 0; --g) {
+        const uint32_t lw = __shfl_up_sync(kFull, xin[g][3], 1);
+        const uint32_t rw = __shfl_down_sync(kFull, xin[g][0], 1);
+        uint32_t h[4], hn[4];
+        byte_row_fma(xin[g], lw, rw, one, h, hn);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const uint32_t o = nib_rule(uh[g][i], h[i], mhn[g][i], mx[g][i], one);
+          uh[g][i] = mh[g][i];
+          mh[g][i] = h[i];
+          mhn[g][i] = hn[i];
+          mx[g][i] = xin[g][i];
+          if (g + 1 < K) {
+            xin[g + 1][i] = o;
+          } else {
+            y_last[i] = o;
+          }
+        }
+      }
+      const int j = t * PF + u - kLag;
+      uint32_t ya[4], yb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        ya[i] = y_last[i] & 0x0f0f0f0fu;
+        yb[i] = (y_last[i] >> 4) & 0x0f0f0f0fu;
+      }
+      const bool segA = STEADY || static_cast<unsigned>(j) < static_cast<unsigned>(nA);
+      const bool segB = static_cast<unsigned>(j) < static_cast<unsigned>(nB);
+      char* const pa = const_cast<char*>(row_addr(out_A, static_cast<uint32_t>(j), out_pitch_b));
+      char* const pb = const_cast<char*>(row_addr(out_B, static_cast<uint32_t>(j), out_pitch_b));
+      st_global_v4_if(pa, ya, segA && store_mid);
+      st_global_v2_if(pa, ya[0], ya[1], segA && store_lo);
+      st_global_v2_if(pa + 8, ya[2], ya[3], segA && store_hi);
+      st_global_v4_if(pb, yb, segB && store_mid);
+      st_global_v2_if(pb, yb[0], yb[1], segB && store_lo);
+      st_global_v2_if(pb + 8, yb[2], yb[3], segB && store_hi);
+    }
+    half ^= PF;
+  };
+  const int steady_begin = (kLag + PF - 1) / PF;
+  const int steady_end = (nA + kLag) / PF;
+  int t = 0;
+  for (; t < trips && (t < steady_begin || t >= steady_end); ++t) trip(t, std::false_type{});
+  for (; t < steady_end; ++t) trip(t, std::true_type{});
+  for (; t < trips; ++t) trip(t, std::false_type{});
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
 // Packed single-generation step (K = 1, W % 128 == 0): the HBM-bound end of
 // the temporal-depth range.  Each lane owns one 16-byte vector (4 words =
 // 128 cells) of a row and walks a segment of rows with the 3-row window of

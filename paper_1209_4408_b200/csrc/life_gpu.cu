@@ -800,15 +800,17 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
 namespace {
 template <int K>
 int launch_byte_tb(ByteStepArgs a, cudaStream_t s) {
+  // Two row streams per word (byte_tb2_kernel) unless LIFE_BYTE_TB2=0 (debug builds).
+  static const bool two = knob("LIFE_BYTE_TB2", 1) != 0;
+  const auto kernel = two ? byte_tb2_kernel<K> : byte_tb_kernel<K>;
+  const int smem = two ? kByteTb2Smem : kByteTbSmem;
   static DeviceCache blocks_per_sm;
   int dev = 0;
   cudaGetDevice(&dev);
   int nb = blocks_per_sm.get(dev);
   if (nb == 0) {
-    LIFE_CUDA(cudaFuncSetAttribute(byte_tb_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   kByteTbSmem));
-    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, byte_tb_kernel<K>, kByteThreads,
-                                                            kByteTbSmem));
+    LIFE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kByteThreads, smem));
     nb = std::max(nb, 1);
     blocks_per_sm.put(dev, nb);
   }
@@ -823,8 +825,7 @@ int launch_byte_tb(ByteStepArgs a, cudaStream_t s) {
   const int64_t warps = ceil_div(a.out_rows, a.seg_rows) * a.n_strips;
   const int64_t blocks = ceil_div(warps, kByteThreads / 32);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
-  LIFE_TRY(launch_pdl(byte_tb_kernel<K>, static_cast<unsigned>(blocks), kByteThreads,
-                      kByteTbSmem, s, a));
+  LIFE_TRY(launch_pdl(kernel, static_cast<unsigned>(blocks), kByteThreads, smem, s, a));
   LIFE_CHECK_LAUNCH("byte_tb_kernel");
   return LIFE_OK;
 }
@@ -1126,10 +1127,12 @@ int engine_layout(int engine) { return engine == LIFE_ENGINE_BYTE ? kByte : kPac
 // small tori (W % 32 == 0, at most kResidentAutoCells cells) where it beats
 // the multi-pass engine (measured), else K = 16 passes.
 constexpr int64_t kResidentAutoCells = int64_t(1) << 22;
-// temporal_depth 0 on the byte engine (W % 16 == 0).  Sweep (T cell-updates/s,
-// K = 1..8): 16384^2 2.78 5.09 6.52 6.83 6.88 7.28 7.10 7.31; 4096^2 2.03 3.22
-// 3.02 3.78 3.36 3.22 2.97 2.70 (short grids pay the 3K-1 step pipeline fill).
-int byte_auto_depth(int64_t w, int64_t h) { return w * h >= (int64_t(1) << 26) ? 6 : 4; }
+// temporal_depth 0 on the byte engine (W % 16 == 0).  Two-stream kernel
+// (byte_tb2_kernel), T cell-updates/s at K = 4 / 6 / 8: 16384^2 10.0 / 12.7 /
+// 13.1, 32768 x 16384 10.0 / 13.8 / 13.7, 4096^2 4.6 / 4.1 / 3.6 (short grids
+// pay the 3K-1 step pipeline fill).  (One stream per word, round 1: 16384^2
+// 8.1 / 8.8 / 8.1.)
+int byte_auto_depth(int64_t w, int64_t h) { return w * h >= (int64_t(1) << 26) ? 8 : 4; }
 
 bool resident_auto(int64_t w, int64_t h) {
   return w % 32 == 0 && w * h <= kResidentAutoCells && life_resident_cluster_size(w, h) > 0;
