@@ -26,13 +26,52 @@ world-size-2 gloo tests on CPU with a test-only stepper.
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import Callable, Optional
+from typing import Callable, Optional, Sequence
 
 import torch
 import torch.distributed as dist
 
 from . import capi
 from .life import ConfigError, TooManyParts, band_bounds, check
+
+
+def run_schedule(drv, generations: int, checkpoints: Sequence[int] = (),
+                 on_pass: Optional[Callable[[int], None]] = None) -> list[int]:
+    """The pass loop of run() (engine.cpp:162-214) for a band driver: passes
+    of up to `depth` generations, split at the checkpoints, whose uint64
+    populations (summed over every rank's band, engine.cpp:179-186; checkpoint
+    0 = the initial grid) are returned in order.  check_run_config's rules
+    (engine.cpp:127-148) on generations and checkpoints."""
+    if generations < 0:
+        raise ConfigError(f"iteration count must be non-negative, got {generations}")
+    cps = [int(c) for c in checkpoints]
+    prev = -1
+    for c in cps:
+        if c < 0 or c > generations:
+            raise ConfigError(f"checkpoint {c} is outside [0, iterations={generations}]")
+        if c <= prev:
+            raise ConfigError("checkpoints must be strictly ascending")
+        prev = c
+    pops: list[int] = []
+    ci = 0
+
+    def record(gen: int) -> None:
+        nonlocal ci
+        while ci < len(cps) and cps[ci] == gen:
+            pops.append(drv.population())
+            ci += 1
+    record(0)
+    depth = drv.geo.depth
+    done = 0
+    while done < generations:
+        stop = cps[ci] if ci < len(cps) else generations
+        k = min(depth, stop - done)
+        drv.pass_(k)
+        done += k
+        if on_pass:
+            on_pass(k)
+        record(done)
+    return pops
 
 
 @dataclass
@@ -92,12 +131,14 @@ class BandDriver:
     """One rank's band, ping-pong buffers and pass loop."""
 
     def __init__(self, geo: BandGeometry, device: torch.device, stepper: Optional[Stepper] = None,
-                 group=None, overlap: bool = True):
+                 group=None, overlap: bool = True,
+                 counter: Optional[Callable[[torch.Tensor], int]] = None):
         self.geo = geo
         self.device = device
         self.group = group
         self.overlap = overlap
         self.stepper = stepper or cuda_stepper(geo.width)
+        self.counter = counter  # test hook: band rows -> live cells (default: CUDA popcount)
         shape = (geo.buf_rows, geo.pitch)
         self.buf = [torch.zeros(shape, dtype=torch.int32, device=device) for _ in range(2)]
         # CUDA: the k-row edge strips run on a side stream as soon as the
@@ -204,16 +245,11 @@ class BandDriver:
             main.wait_event(done)
         self.finish_pass(k)
 
-    def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None) -> None:
-        if generations < 0:
-            raise ConfigError(f"iteration count must be non-negative, got {generations}")
-        done = 0
-        while done < generations:
-            k = min(self.geo.depth, generations - done)
-            self.pass_(k)
-            done += k
-            if on_pass:
-                on_pass(k)
+    def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None,
+            checkpoints: Sequence[int] = ()) -> list[int]:
+        """`generations` in passes of up to `depth`; populations at the
+        checkpoints (summed over ranks), see run_schedule."""
+        return run_schedule(self, generations, checkpoints, on_pass)
 
     # -- init / reductions (CUDA) ----------------------------------------
     def init_random(self, density: float, seed: int) -> None:
@@ -234,12 +270,16 @@ class BandDriver:
         self.generations = 0
 
     def population(self) -> int:
-        """Band population (CUDA popcount), summed over ranks when distributed."""
+        """Band population (CUDA popcount, or the injected `counter`), summed
+        over ranks when distributed (uint64 semantics; grid.cpp:40-46)."""
         g = self.geo
-        acc = torch.zeros(1, dtype=torch.int64, device=self.device)
-        stream = torch.cuda.current_stream(self.device).cuda_stream
-        check(capi.lib().life_dev_packed_population(self.band().data_ptr(), g.pitch, g.width,
-                                                    g.band_rows, acc.data_ptr(), stream))
+        if self.counter is not None:
+            acc = torch.tensor([int(self.counter(self.band()))], dtype=torch.int64)
+        else:
+            acc = torch.zeros(1, dtype=torch.int64, device=self.device)
+            stream = torch.cuda.current_stream(self.device).cuda_stream
+            check(capi.lib().life_dev_packed_population(self.band().data_ptr(), g.pitch, g.width,
+                                                        g.band_rows, acc.data_ptr(), stream))
         if g.world > 1:
             dist.all_reduce(acc, group=self.group)
         return int(acc.item())
@@ -277,18 +317,30 @@ class TorusDriver:
         self.cur ^= flip.value
         self.generations += gens
 
-    def run(self, generations: int) -> None:
+    def pass_(self, k: int) -> None:
+        g = self.geo
+        a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_step(a.data_ptr(), g.pitch, 0, g.height, b.data_ptr(),
+                                              g.pitch, 0, g.width, g.height, k, stream))
+        self.cur ^= 1
+        self.generations += k
+
+    def run(self, generations: int, checkpoints: Sequence[int] = ()) -> list[int]:
+        if checkpoints:
+            return run_schedule(self, generations, checkpoints)
         if generations < 0:
             raise ConfigError(f"iteration count must be non-negative, got {generations}")
         k = self.geo.depth
         if self.on_launch is None:
             self._call(generations)
-            return
+            return []
         full = generations // k * k
         if full:
             self.on_launch("full", full, lambda: self._call(full))
         if generations - full:
             self.on_launch("rem", generations - full, lambda: self._call(generations - full))
+        return []
 
     def init_random(self, density: float, seed: int) -> None:
         g = self.geo
@@ -558,17 +610,10 @@ class PeerBandDriver:
             self._events = []
         return out
 
-    def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None) -> None:
-        if generations < 0:
-            raise ConfigError(f"iteration count must be non-negative, got {generations}")
+    def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None,
+            checkpoints: Sequence[int] = ()) -> list[int]:
         self.barrier()  # every rank's initial band is in place
-        done = 0
-        while done < generations:
-            k = min(self.geo.depth, generations - done)
-            self.pass_(k)
-            done += k
-            if on_pass:
-                on_pass(k)
+        return run_schedule(self, generations, checkpoints, on_pass)
 
     def init_random(self, density: float, seed: int) -> None:
         g = self.geo

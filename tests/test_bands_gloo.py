@@ -52,7 +52,7 @@ def oracle_stepper(width: int):
     return step
 
 
-def _worker(rank, world, port, W, H, depth, gens, overlap, result_q):
+def _worker(rank, world, port, W, H, depth, gens, overlap, result_q, checkpoints=()):
     import sys
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -63,15 +63,16 @@ def _worker(rank, world, port, W, H, depth, gens, overlap, result_q):
         from paper_1209_4408_b200.bands import BandDriver, make_geometry
         O = Oracle()
         geo = make_geometry(W, H, rank, world, depth)
-        drv = BandDriver(geo, torch.device("cpu"), stepper=oracle_stepper(W), overlap=overlap)
+        drv = BandDriver(geo, torch.device("cpu"), stepper=oracle_stepper(W), overlap=overlap,
+                         counter=lambda b: int(np.unpackbits(b.numpy().view(np.uint8)).sum()))
         init = O.random_window(W, H, 0.4, 7, 0, geo.y0, W, geo.band_rows)
         drv.band().copy_(torch.from_numpy(to_words(init, geo.pitch)))
-        drv.run(gens)
+        pops = drv.run(gens, checkpoints=checkpoints)
         band = from_words(drv.band().numpy(), W)
         parts = [None] * world
         dist.all_gather_object(parts, (geo.y0, band))
         if rank == 0:
-            result_q.put(parts)
+            result_q.put((parts, pops))
     finally:
         dist.destroy_process_group()
 
@@ -83,20 +84,51 @@ def _worker(rank, world, port, W, H, depth, gens, overlap, result_q):
     (2, 100, 12, 6, 6, True),
 ])
 def test_band_driver_matches_full_torus(oracle, world, W, H, depth, gens, overlap):
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, W, H, depth, gens, overlap, q))
-             for r in range(world)]
-    for p in procs:
-        p.start()
-    parts = q.get(timeout=240)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    parts, _ = _run_world(world, W, H, depth, gens, overlap)
     got = np.concatenate([b for _, b in sorted(parts, key=lambda t: t[0])], axis=0)
     want, _ = oracle.run(oracle.random_fill(W, H, 0.4, 7), gens)
     assert np.array_equal(got, want)
+
+
+def _run_world(world, W, H, depth, gens, overlap, checkpoints=()):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, W, H, depth, gens, overlap, q,
+                                               tuple(checkpoints)))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+@pytest.mark.parametrize("world,depth,cps", [(2, 4, (0, 3, 9, 13)), (3, 3, (1, 2, 13))])
+def test_band_driver_checkpoint_populations(oracle, world, depth, cps):
+    """run(..., checkpoints) on N ranks: passes split at the checkpoints, the
+    populations summed over every rank's band (engine.cpp:179-186) equal the
+    oracle's at every checkpoint, and the final torus is unchanged."""
+    W, H, gens = 70, 37, 13
+    parts, pops = _run_world(world, W, H, depth, gens, True, cps)
+    want, want_pops = oracle.run(oracle.random_fill(W, H, 0.4, 7), gens, list(cps))
+    assert pops == want_pops
+    got = np.concatenate([b for _, b in sorted(parts, key=lambda t: t[0])], axis=0)
+    assert np.array_equal(got, want)
+
+
+def test_run_schedule_rejects_bad_checkpoints():
+    from paper_1209_4408_b200.bands import run_schedule
+    from paper_1209_4408_b200.life import ConfigError
+
+    class Dummy:
+        class geo:
+            depth = 4
+    for gens, cps in [(-1, ()), (5, (6,)), (5, (2, 2)), (5, (3, 1))]:
+        with pytest.raises(ConfigError):
+            run_schedule(Dummy(), gens, cps)
 
 
 def test_geometry_follows_partition_rows(golden_small):

@@ -94,11 +94,12 @@ def _ipc_worker(rank, world, port, W, H, depth, gens, q):
         torch.cuda.set_device(dev)
         drv = PeerBandDriver(make_geometry(W, H, rank, world, depth), dev)
         drv.init_random(0.4, 5)
-        drv.run(gens)  # gloo => host barrier per pass: no kernel waits on another
+        # gloo => host barrier per pass: no kernel waits on another
+        cps = drv.run(gens, checkpoints=[0, 5, 11, gens])  # passes split at 5 and 11
         band = drv.band().cpu().numpy()
         pop = drv.population()
         parts = [None] * world
-        dist.all_gather_object(parts, (drv.geo.y0, band, pop))
+        dist.all_gather_object(parts, (drv.geo.y0, band, pop, cps))
         drv.close()
         if rank == 0:
             q.put(parts)
@@ -127,10 +128,27 @@ def test_peer_driver_ipc_two_processes_one_gpu(oracle):
         p.join(timeout=60)
         assert p.exitcode == 0
     parts.sort(key=lambda t: t[0])
-    got = words_to_cells(np.concatenate([b for _, b, _ in parts], axis=0), W)
-    want, pops = oracle.run(oracle.random_fill(W, H, 0.4, 5), gens, [gens])
+    got = words_to_cells(np.concatenate([b for _, b, _, _ in parts], axis=0), W)
+    want, pops = oracle.run(oracle.random_fill(W, H, 0.4, 5), gens, [0, 5, 11, gens])
     assert np.array_equal(got, want)
-    assert parts[0][2] == pops[0]
+    assert parts[0][2] == pops[-1]
+    assert parts[0][3] == parts[1][3] == pops  # checkpoint populations summed over ranks
+
+
+def test_torus_driver_checkpoints(oracle):
+    """TorusDriver (the one-GPU band driver bench.py uses): whole run and
+    checkpointed run equal the oracle."""
+    import torch
+    from paper_1209_4408_b200.bands import TorusDriver, make_geometry
+    W, H, gens = 1000, 301, 45
+    want, pops = oracle.run(oracle.random_fill(W, H, 0.4, 21), gens, [0, 7, 30, gens])
+    for cps in ([], [0, 7, 30, gens]):
+        drv = TorusDriver(make_geometry(W, H, 0, 1, 16), torch.device("cuda", 0))
+        drv.init_random(0.4, 21)
+        got_pops = drv.run(gens, checkpoints=cps)
+        torch.cuda.synchronize()
+        assert np.array_equal(words_to_cells(drv.band().cpu().numpy(), W), want)
+        assert got_pops == (pops if cps else [])
 
 
 @pytest.mark.slow
