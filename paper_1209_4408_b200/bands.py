@@ -487,6 +487,24 @@ def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows:
         main.wait_stream(edge_stream)
 
 
+def neighbour_token(token: torch.Tensor, inbox: torch.Tensor, rank: int, world: int,
+                    group=None) -> None:
+    """Pass ordering with the two neighbouring ranks only: send `token` (one
+    element) to the rank above and the rank below, receive theirs into
+    inbox[0] (from above) and inbox[1] (from below).  Same issue order on every
+    rank (send up, send down, recv down, recv up) so the i-th send to a peer
+    matches its i-th receive, also when up == down (two ranks).  With NCCL,
+    wait() orders the current stream after the transfers (the host does not
+    block); with gloo it blocks the host."""
+    up, down = (rank - 1) % world, (rank + 1) % world
+    ops = [dist.P2POp(dist.isend, token, up, group),
+           dist.P2POp(dist.isend, token, down, group),
+           dist.P2POp(dist.irecv, inbox[1:2], down, group),
+           dist.P2POp(dist.irecv, inbox[0:1], up, group)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
+
+
 class PeerBandDriver:
     """One rank's band for the fused NVLink halo (see above).
 
@@ -547,18 +565,7 @@ class PeerBandDriver:
 
     def barrier(self) -> None:
         if self.sync == "neighbour":
-            # Same issue order on every rank (send up, send down, recv down,
-            # recv up) so the i-th send to a peer matches its i-th receive,
-            # also when up == down (two ranks).  wait() orders the current
-            # stream after the NCCL kernels; the host does not block.
-            g = self.geo
-            up, down = (g.rank - 1) % g.world, (g.rank + 1) % g.world
-            ops = [dist.P2POp(dist.isend, self._flag, up, self.group),
-                   dist.P2POp(dist.isend, self._flag, down, self.group),
-                   dist.P2POp(dist.irecv, self._tok_in[1:], down, self.group),
-                   dist.P2POp(dist.irecv, self._tok_in[:1], up, self.group)]
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
+            neighbour_token(self._flag, self._tok_in, self.geo.rank, self.geo.world, self.group)
         elif self.sync == "allreduce":
             dist.all_reduce(self._flag, group=self.group)  # ordered on the current stream
         else:

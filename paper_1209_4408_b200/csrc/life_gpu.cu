@@ -816,8 +816,10 @@ int launch_byte_tb(ByteStepArgs a, cudaStream_t s) {
   }
   // Segments long enough to amortise the 3K-1 step pipeline fill: one wave
   // of independent warps.
+  // LIFE_BYTE_TB_WPS (debug builds): warps per SM to plan the segments for.
+  static const int64_t wps = knob("LIFE_BYTE_TB_WPS", 0);
   const int64_t resident_warps =
-      static_cast<int64_t>(nb) * (kByteThreads / 32) * sm_count();
+      (wps > 0 ? wps : static_cast<int64_t>(nb) * (kByteThreads / 32)) * sm_count();
   // 1 wave: 8.41 vs 8.02 T/s (2) at 16384^2, K = 6 (LIFE_BYTE_TB_WAVES, debug builds)
   static const int64_t waves = std::max<int64_t>(knob("LIFE_BYTE_TB_WAVES", 1), 1);
   const int64_t segs_target = std::max<int64_t>(1, waves * resident_warps / a.n_strips);

@@ -145,3 +145,44 @@ def test_geometry_follows_partition_rows(golden_small):
         make_geometry(64, 20, 0, 4, 8)  # 5-row bands < depth 8
     with pytest.raises(ConfigError):
         make_geometry(64, 64, 0, 2, 17)
+
+
+def _token_worker(rank, world, port, rounds, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1209_4408_b200.bands import neighbour_token
+        got = []
+        for p in range(rounds):
+            tok = torch.tensor([1000 * p + rank], dtype=torch.int32)
+            inbox = torch.full((2,), -1, dtype=torch.int32)
+            neighbour_token(tok, inbox, rank, world)
+            got.append([int(inbox[0]), int(inbox[1])])
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_neighbour_token_pairs_with_both_neighbours(world):
+    """The peer band driver's pass ordering (neighbour_token): every rank
+    receives, each pass, the token of the rank above and of the rank below --
+    no deadlock in the up == down case (two ranks) or around the ring."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    rounds = 5
+    procs = [ctx.Process(target=_token_worker, args=(r, world, port, rounds, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        up, down = (r - 1) % world, (r + 1) % world
+        assert res[r] == [[1000 * p + up, 1000 * p + down] for p in range(rounds)]
