@@ -183,6 +183,8 @@ int peer_sync_trips() {
 
 // Tiles up to this many rows run the fast kernel's single-loop-body variant.
 constexpr int64_t kUniMaxRows = 1024;
+// One-wave fast-kernel tiles shorter than this run at half the warps per SM.
+constexpr int64_t kShortTileRows = 128;
 
 template <int K, bool FAST>
 int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
@@ -265,6 +267,21 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   static const int64_t forced_segs = knob("LIFE_SEGS", 0);  // debug builds: force the segment count
   if (forced_segs > 0) best_segs = std::min<int64_t>(forced_segs, a.out_rows);
   a.seg_rows = ceil_div(a.out_rows, best_segs);
+  // Very short one-wave tiles (< kShortTileRows rows at a full SM of warps):
+  // half the warps per SM, each tile twice as tall -- one warp of K
+  // independent stage chains per SMSP still fills its ALU pipe, and the
+  // pipeline fill is paid on twice as many rows (8192^2 at K = 16: 23.4 ->
+  // 24.9 T/s; 16384^2, 238-row tiles, loses 5 % that way and keeps 8).
+  if (FAST && forced_segs == 0 && wpb >= 8 && blocks_per_sm == 1 && a.seg_rows < kShortTileRows &&
+      static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, a.seg_rows) <= slots * wpb) {
+    const int64_t half = wpb / 2;
+    const int64_t segs2 = std::max<int64_t>(1, (slots * half) / a.n_strips);  // one wave, 1 block/SM
+    const int64_t rows2 = ceil_div(a.out_rows, segs2);
+    if (rows2 > a.seg_rows) {
+      wpb = static_cast<int>(half);
+      a.seg_rows = rows2;
+    }
+  }
   const int64_t tiles = static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, a.seg_rows);
   a.steps = static_cast<int32_t>(ceil_div(a.seg_rows + kLag, PF));
   // Lockstep granularity: a block barrier every kSyncTrips trips (192 rows).
