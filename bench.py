@@ -1029,13 +1029,22 @@ def run_byte_arm(args) -> None:
     bufs = [torch.zeros((H, pitch), dtype=torch.uint8, device=dev) for _ in range(2)]
     stream = torch.cuda.current_stream(dev).cuda_stream
     from paper_1209_4408_b200.life import check
-    check(L.life_dev_byte_random(bufs[0].data_ptr(), pitch, W, 0, H, cfg["p"], 42, stream))
+    def init_grid(buf):
+        if cfg.get("soup"):  # config 4: the device soup, byte layout
+            from paper_1209_4408_b200.life import Engine
+            with Engine(0) as e:
+                e.init_soup(W, H, 0.02, 5, cfg["p"], 42, capi.ENGINE_BYTE)
+                cells = e.download()
+            buf[:, :W].copy_(torch.from_numpy(cells))
+        else:
+            check(L.life_dev_byte_random(buf.data_ptr(), pitch, W, 0, H, cfg["p"], 42, stream))
+    init_grid(bufs[0])
     flush = torch.empty(2 * L2_BYTES, dtype=torch.uint8, device=dev) if 2 * pitch * H < 4 * L2_BYTES else None
     launches = []
     cur = [0]
 
     depth = args.byte_depth or (8 if W * H >= 2 ** 26 else 4)  # life_run's byte auto rule
-    if W % 16:
+    if W % 16 and W < 33:
         depth = 1
 
     def step(record: bool):
@@ -1085,11 +1094,11 @@ def run_byte_arm(args) -> None:
     # reference's golden (FNV-1a-64 over the W*H 0/1 bytes).
     parity = {"ok": None, "reason": "--no-parity"}
     gold = None if args.no_parity else golden_for(args.config, gens)
-    if gold is not None and gold["kind"] == "hash" and not cfg.get("soup"):
+    if gold is not None and gold["kind"] == "hash":
         with open(os.path.join(GOLDEN_DIR, gold["source"])) as f:
             gj = json.load(f)
         want = (gj["cfg1"] if args.config == 1 else gj["gens"])[str(gens)]
-        check(L.life_dev_byte_random(bufs[cur[0]].data_ptr(), pitch, W, 0, H, cfg["p"], 42, stream))
+        init_grid(bufs[cur[0]])
         step(False)
         torch.cuda.synchronize()
         got = f"{fnv(bufs[cur[0]][:, :W].contiguous().cpu().numpy().tobytes()):016x}"

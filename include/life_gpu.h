@@ -165,7 +165,7 @@ int life_grid_hash(life_ctx* ctx, uint64_t* out);
 /* Replaces run(Grid&&, RunConfig, checkpoints) (engine.cpp:162-214):
  *   `generations` >= 0 (ConfigError otherwise, engine.cpp:133-136);
  *   `temporal_depth`: generations per kernel pass, 0 = auto; packed 1..16,
- *     byte 1..8 (W % 16 == 0; other widths run one generation per pass);
+ *     byte 1..8 (W % 16 == 0 or W >= 33; narrower tori run one generation per pass);
  *   `checkpoints`: strictly ascending in [0, generations] (engine.cpp:137-147);
  *     `populations[i]` receives the population after checkpoints[i]
  *     generations (checkpoint 0 = the initial grid, engine.cpp:186).
@@ -217,7 +217,8 @@ int life_band_bounds(int64_t extent, int32_t parts, int64_t* bounds);
 /* Device row pitch, in uint32 words, of the packed layout for width W
  * (>= 2*ceil(W/64), a multiple of 32 words = 128 B). */
 int64_t life_packed_pitch_words(int64_t width);
-/* Byte layout pitch (>= W, a multiple of 16 B). */
+/* Byte layout pitch (>= W, a multiple of 128 B; W % 16 != 0 rows keep 48
+ * bytes of padding after the last 16-byte vector, see life_dev_byte_pass). */
 int64_t life_byte_pitch(int64_t width);
 /* `generations` (1..16) packed generations in one pass (W % 32 != 0 tori
  * several block waves deep run their seam strips on a library-owned side
@@ -274,7 +275,9 @@ int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
                        uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
                        int64_t out_rows, void* stream);
 /* `generations` (1..8) byte-engine generations in one pass (temporal blocking;
- * more than one needs W % 16 == 0), same addressing as life_dev_byte_step;
+ * more than one needs W % 16 == 0 or W >= 33), same addressing as life_dev_byte_step;
+ * for W % 16 != 0 the 48 bytes after each input row's last vector (in_pitch >=
+ * life_byte_pitch(W)) are overwritten with the row's seam vectors;
  * input relative rows -generations .. out_rows + generations are read. */
 int life_dev_byte_pass(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
                        uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,

@@ -934,6 +934,9 @@ __global__ void __launch_bounds__(kByteThreads) byte_step_kernel(const ByteStepA
 // compute_region (engine.cpp:17-48) x K generations.
 // ---------------------------------------------------------------------------
 constexpr int kByteTbMaxDepth = 8;
+// Narrowest W % 16 != 0 torus the temporal-blocked byte pass takes (three
+// vectors per row, byte_seam_plan); narrower ones run one generation per pass.
+constexpr int kByteTbMinSeamWidth = 33;
 constexpr int kByteTbStride = 31;  // vectors per strip: 30 whole + 2 shared halves
 #ifndef LIFE_BYTE_TB_PF
 #define LIFE_BYTE_TB_PF 4
@@ -1112,40 +1115,103 @@ __device__ __forceinline__ uint32_t nib_rule(uint32_t up_h, uint32_t dn_h, uint3
 constexpr int kByteTb2PF = 4;
 constexpr int kByteTb2Smem = (kByteThreads / 32) * 2 * kByteTb2PF * 64 * 16;  // per block
 
-template <int K>
-__global__ void __launch_bounds__(kByteThreads) byte_tb2_kernel(const ByteStepArgs a) {
+// W % 16 != 0 byte tori (r = W % 16, nv = ceil(W/16) >= 3 vectors per row,
+// the bytes of vector nv-1 past column W zero): the lanes next to the column
+// seam need vectors of the infinitely repeated row that are not aligned
+// vectors of the stored row.  byte_seam_prep_kernel writes them, per row,
+// into three padding vectors after the row (life_byte_pitch reserves them)
+// before every pass, so the pass kernel only maps those lanes' loads there:
+//   vector nv   : columns 16nv .. 16nv+15 of the next period  = bytes 16-r.. of [v0, v1]
+//   vector nv+1 : columns W-16 .. W-1 (lane vi = -1)           = bytes r.. of [v(nv-2), v(nv-1)]
+//   vector nv+2 : vi = nv-1 with the row start after column W  = v(nv-1) | bytes 16-r.. of [0, v0]
+// Lanes further out only ever feed the ghost bytes K <= 8 generations
+// corrupt, so they may load anything.
+__device__ __forceinline__ int64_t byte_seam_src(int64_t vi, int64_t nv) {
+  if (vi >= 0 && vi <= nv - 2) return vi;
+  if (vi == nv - 1) return nv + 2;
+  if (vi == -1) return nv + 1;
+  return nv;
+}
+// Bytes o .. o+15 (o in 0..16) of the 32-byte concatenation [p, q].
+__device__ __forceinline__ uint4 byte_extract(const uint4 p, const uint4 q, int o) {
+  const uint32_t c[9] = {p.x, p.y, p.z, p.w, q.x, q.y, q.z, q.w, 0u};
+  const int wo = o >> 2;
+  const uint32_t sh = static_cast<uint32_t>(o & 3) * 8u;
+  uint32_t w[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i)
+    w[i] = wo == 0 ? c[i] : wo == 1 ? c[i + 1] : wo == 2 ? c[i + 2] : wo == 3 ? c[i + 3] : c[i + 4];
+  return make_uint4(__funnelshift_r(w[0], w[1], sh), __funnelshift_r(w[1], w[2], sh),
+                    __funnelshift_r(w[2], w[3], sh), __funnelshift_r(w[3], w[4], sh));
+}
+__device__ __forceinline__ void byte_tail_mask(int r, uint32_t (&m)[4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int valid = r - 4 * i;  // bytes of word i inside the row
+    m[i] = valid >= 4 ? ~0u : (valid <= 0 ? 0u : (1u << (8 * valid)) - 1u);
+  }
+}
+
+struct SeamPrepArgs {
+  uint8_t* rows;
+  int64_t pitch, n_rows, width;
+};
+__global__ void __launch_bounds__(128) byte_seam_prep_kernel(const SeamPrepArgs a) {
+  uint8_t* const rows = a.rows;
+  const int64_t pitch = a.pitch, n_rows = a.n_rows, width = a.width;
+  const int64_t nv = (width + 15) / 16;
+  const int r = static_cast<int>(width & 15);
+  uint32_t m[4];
+  byte_tail_mask(r, m);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: previous pass complete
+  for (int64_t y = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; y < n_rows;
+       y += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint4* row = reinterpret_cast<uint4*>(rows + y * pitch);
+    const uint4 v0 = row[0], v1 = row[1], vm2 = row[nv - 2];
+    uint4 vm1 = row[nv - 1];
+    vm1 = make_uint4(vm1.x & m[0], vm1.y & m[1], vm1.z & m[2], vm1.w & m[3]);
+    const uint4 zero = make_uint4(0u, 0u, 0u, 0u);
+    const uint4 s = byte_extract(zero, v0, 16 - r);
+    row[nv] = byte_extract(v0, v1, 16 - r);
+    row[nv + 1] = byte_extract(vm2, vm1, r);
+    row[nv + 2] = make_uint4(vm1.x | s.x, vm1.y | s.y, vm1.z | s.z, vm1.w | s.w);
+  }
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
+// One warp's tile of the two-stream kernel.  SEAMW: a W % 16 != 0 torus (the
+// lanes next to the column seam load the padding vectors byte_seam_prep_kernel
+// wrote, and the partial last vector is stored with its tail bytes zero).
+template <int K, bool SEAMW>
+__device__ __forceinline__ void byte_tb2_body(const ByteStepArgs& a, const int lane,
+                                              const int64_t vi, const int64_t y0, const int n,
+                                              uint4* ring) {
   constexpr int PF = kByteTb2PF;
   constexpr int kLag = 3 * K - 1;  // output row j leaves the pipeline at step j + kLag
-  const int lane = threadIdx.x & 31;
-  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kByteThreads + threadIdx.x) >> 5;
-  const int strip = static_cast<int>(gwarp % a.n_strips);
-  const int64_t seg = gwarp / a.n_strips;
-  const int64_t y0 = seg * a.seg_rows;
-  if (y0 >= a.out_rows) return;  // warp-uniform
-  const int n = static_cast<int>(min(a.seg_rows, a.out_rows - y0));
   const int nA = (n + 1) >> 1, nB = n - nA;
-  const int64_t vi = static_cast<int64_t>(strip) * kByteTbStride + lane - 1;
-  int64_t src = vi % a.nv;
-  if (src < 0) src += a.nv;
-  const bool in_grid = vi >= 0 && vi < a.nv;
+  const int64_t nv = a.nv;
+  int64_t src = vi % nv;
+  if (src < 0) src += nv;
+  if (SEAMW) src = byte_seam_src(vi, nv);
+  const bool in_grid = vi >= 0 && vi < nv;
   const bool store_mid = in_grid && lane >= 1 && lane <= 30;
   const bool store_lo = in_grid && lane == 31;
   const bool store_hi = in_grid && lane == 0;
+  // The partial last vector keeps its bytes past column W zero.
+  uint32_t tail_mask[4] = {~0u, ~0u, ~0u, ~0u};
+  if (SEAMW && vi == nv - 1) byte_tail_mask(static_cast<int>(a.width & 15), tail_mask);
   const uint32_t one = a.one;
-  extern __shared__ uint4 byte_tb2_ring[];
-  uint4* ring = byte_tb2_ring + (threadIdx.x >> 5) * (2 * PF * 64) + lane;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: previous pass complete
-  asm volatile("griddepcontrol.launch_dependents;");
 
   const int in_rows = static_cast<int>(a.in_rows);
   int rowA = static_cast<int>(wrap_row(a.in_row0, y0 - K, a.in_rows));
   int rowB = static_cast<int>(wrap_row(a.in_row0, y0 + nA - K, a.in_rows));
   const uint32_t in_pitch_b = static_cast<uint32_t>(a.in_pitch);
-  const char* const in_lane = reinterpret_cast<const char*>(a.in + src * 16);
+  const char* const in_lane = reinterpret_cast<const char*>(a.in) + src * 16;
   auto issue = [&](int slot) {
-    cp_async16(reinterpret_cast<uint32_t*>(ring + slot * 64),
+    uint4* sl = ring + slot * 64;
+    cp_async16(reinterpret_cast<uint32_t*>(sl),
                row_addr(in_lane, static_cast<uint32_t>(rowA), in_pitch_b));
-    cp_async16(reinterpret_cast<uint32_t*>(ring + slot * 64 + 32),
+    cp_async16(reinterpret_cast<uint32_t*>(sl + 32),
                row_addr(in_lane, static_cast<uint32_t>(rowB), in_pitch_b));
     cp_async_commit();
     rowA = (rowA + 1 == in_rows) ? 0 : rowA + 1;
@@ -1208,6 +1274,10 @@ __global__ void __launch_bounds__(kByteThreads) byte_tb2_kernel(const ByteStepAr
       for (int i = 0; i < 4; ++i) {
         ya[i] = y_last[i] & 0x0f0f0f0fu;
         yb[i] = (y_last[i] >> 4) & 0x0f0f0f0fu;
+        if (SEAMW) {
+          ya[i] &= tail_mask[i];
+          yb[i] &= tail_mask[i];
+        }
       }
       const bool segA = STEADY || static_cast<unsigned>(j) < static_cast<unsigned>(nA);
       const bool segB = static_cast<unsigned>(j) < static_cast<unsigned>(nB);
@@ -1229,6 +1299,23 @@ __global__ void __launch_bounds__(kByteThreads) byte_tb2_kernel(const ByteStepAr
   for (; t < steady_end; ++t) trip(t, std::true_type{});
   for (; t < trips; ++t) trip(t, std::false_type{});
   cp_async_wait<0>();
+}
+
+template <int K, bool SEAMW>
+__global__ void __launch_bounds__(kByteThreads) byte_tb2_kernel(const ByteStepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gwarp = (static_cast<int64_t>(blockIdx.x) * kByteThreads + threadIdx.x) >> 5;
+  const int strip = static_cast<int>(gwarp % a.n_strips);
+  const int64_t seg = gwarp / a.n_strips;
+  const int64_t y0 = seg * a.seg_rows;
+  if (y0 >= a.out_rows) return;  // warp-uniform
+  const int n = static_cast<int>(min(a.seg_rows, a.out_rows - y0));
+  const int64_t vi = static_cast<int64_t>(strip) * kByteTbStride + lane - 1;
+  extern __shared__ uint4 byte_tb2_ring[];
+  uint4* ring = byte_tb2_ring + (threadIdx.x >> 5) * (2 * kByteTb2PF * 64) + lane;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: previous pass complete
+  asm volatile("griddepcontrol.launch_dependents;");
+  byte_tb2_body<K, SEAMW>(a, lane, vi, y0, n, ring);
 }
 
 // ---------------------------------------------------------------------------
@@ -1770,14 +1857,19 @@ __global__ void packed_popcount_kernel(const uint32_t* __restrict__ words, int64
   block_add_u64(acc, count);
 }
 
+// Live cells of the W columns of `rows` byte rows: the first nv = ceil(W/16)
+// vectors of every row (bytes past column W inside vector nv-1 are zero; the
+// row padding after it is scratch, see byte_seam_prep_kernel).
 __global__ void byte_popcount_kernel(const uint8_t* __restrict__ cells, int64_t pitch,
-                                     int64_t rows, unsigned long long* count) {
+                                     int64_t rows, int64_t nv, unsigned long long* count) {
   uint64_t acc = 0;
-  const int64_t n = rows * pitch / 16;
+  const int64_t per_row = pitch / 16;
+  const int64_t n = rows * nv;
   const uint4* v = reinterpret_cast<const uint4*>(cells);
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const uint4 q = __ldg(v + t);
+    const int64_t r = t / nv;
+    const uint4 q = __ldg(v + r * per_row + (t - r * nv));
     acc += __popc(q.x) + __popc(q.y) + __popc(q.z) + __popc(q.w);  // bytes are 0/1
   }
   block_add_u64(acc, count);

@@ -402,7 +402,12 @@ int64_t life_packed_pitch_words(int64_t width) {
   return ceil_div(2 * ceil_div(width, 64), 32) * 32;
 }
 
-int64_t life_byte_pitch(int64_t width) { return ceil_div(width, 128) * 128; }
+// W % 16 != 0 rows get three padding vectors after the row for the seam
+// vectors of the temporal-blocked byte pass (byte_seam_prep_kernel).
+int64_t life_byte_pitch(int64_t width) {
+  const int64_t need = width % 16 ? ceil_div(width, 16) * 16 + 48 : width;
+  return ceil_div(need, 128) * 128;
+}
 
 int life_band_bounds(int64_t extent, int32_t parts, int64_t* bounds) {
   if (parts < 1 || parts > extent)
@@ -818,18 +823,23 @@ namespace {
 template <int K>
 int launch_byte_tb(ByteStepArgs a, cudaStream_t s) {
   // Two row streams per word (byte_tb2_kernel) unless LIFE_BYTE_TB2=0 (debug builds).
-  static const bool two = knob("LIFE_BYTE_TB2", 1) != 0;
-  const auto kernel = two ? byte_tb2_kernel<K> : byte_tb_kernel<K>;
+  // W % 16 != 0 tori need the two-stream kernel's seam path.
+  static const bool two_knob = knob("LIFE_BYTE_TB2", 1) != 0;
+  const bool seam = (a.width & 15) != 0;
+  const bool two = two_knob || seam;
+  const auto kernel = !two ? byte_tb_kernel<K>
+                           : (seam ? byte_tb2_kernel<K, true> : byte_tb2_kernel<K, false>);
   const int smem = two ? kByteTb2Smem : kByteTbSmem;
-  static DeviceCache blocks_per_sm;
+  static DeviceCache blocks_per_sm[3];  // [one-stream, two-stream, two-stream seam]
+  const int variant = !two ? 0 : (seam ? 2 : 1);
   int dev = 0;
   cudaGetDevice(&dev);
-  int nb = blocks_per_sm.get(dev);
+  int nb = blocks_per_sm[variant].get(dev);
   if (nb == 0) {
     LIFE_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, kByteThreads, smem));
     nb = std::max(nb, 1);
-    blocks_per_sm.put(dev, nb);
+    blocks_per_sm[variant].put(dev, nb);
   }
   // Segments long enough to amortise the 3K-1 step pipeline fill: one wave
   // of independent warps.
@@ -844,6 +854,14 @@ int launch_byte_tb(ByteStepArgs a, cudaStream_t s) {
   const int64_t warps = ceil_div(a.out_rows, a.seg_rows) * a.n_strips;
   const int64_t blocks = ceil_div(warps, kByteThreads / 32);
   if (blocks > 0x7fffffff) return set_error(LIFE_ERR_CONFIG, "grid too large");
+  if (seam) {  // the seam vectors of every input row, into the row padding
+    const SeamPrepArgs pa{const_cast<uint8_t*>(a.in), a.in_pitch, a.in_rows, a.width};
+    LIFE_TRY(launch_pdl(byte_seam_prep_kernel,
+                        static_cast<unsigned>(std::min<int64_t>(ceil_div(a.in_rows, 128),
+                                                                4 * sm_count())),
+                        128, 0, s, pa));
+    LIFE_CHECK_LAUNCH("byte_seam_prep_kernel");
+  }
   LIFE_TRY(launch_pdl(kernel, static_cast<unsigned>(blocks), kByteThreads, smem, s, a));
   LIFE_CHECK_LAUNCH("byte_tb_kernel");
   return LIFE_OK;
@@ -865,13 +883,18 @@ int life_dev_byte_pass(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
   if (generations == 1)
     return life_dev_byte_step(in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
                               out_rows, stream);
-  if (width % 16 != 0)
+  if (width % 16 != 0 && width < kByteTbMinSeamWidth)
     return set_error(LIFE_ERR_CONFIG,
-                     "byte passes of more than one generation need W %% 16 == 0, got W = %lld",
-                     static_cast<long long>(width));
+                     "byte passes of more than one generation need W %% 16 == 0 or W >= %d, "
+                     "got W = %lld", kByteTbMinSeamWidth, static_cast<long long>(width));
   if (width < 1 || in_rows < 1 || out_rows < 0 || in_pitch < width || out_pitch < width ||
       (in_pitch & 15) || (out_pitch & 15))
     return set_error(LIFE_ERR_CONFIG, "bad byte pass geometry");
+  if (width % 16 != 0 && in_pitch < ceil_div(width, 16) * 16 + 48)
+    return set_error(LIFE_ERR_CONFIG,
+                     "byte passes of W %% 16 != 0 tori need 48 bytes of row padding "
+                     "(in_pitch >= life_byte_pitch(W)), got in_pitch = %lld",
+                     static_cast<long long>(in_pitch));
   if (out_rows == 0) return LIFE_OK;
   if (in_rows >= (int64_t(1) << 31) || in_pitch >= (int64_t(1) << 32) ||
       out_pitch >= (int64_t(1) << 32) || out_rows >= (int64_t(1) << 31))
@@ -886,7 +909,7 @@ int life_dev_byte_pass(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int
   a.out_row0 = out_row0;
   a.width = width;
   a.out_rows = out_rows;
-  a.nv = static_cast<int32_t>(width / 16);
+  a.nv = static_cast<int32_t>(ceil_div(width, 16));
   a.n_strips = static_cast<int32_t>(ceil_div(a.nv + 1, kByteTbStride));
   a.one = 1;
   return kByteTbLaunchers[generations](a, static_cast<cudaStream_t>(stream));
@@ -1126,9 +1149,9 @@ int population_async(life_ctx* c, unsigned long long* slot) {
     return life_dev_packed_population(c->pk[c->pk_cur], c->pk_pitch, c->W, c->H,
                                       reinterpret_cast<uint64_t*>(slot), c->stream);
   }
-  const int64_t n = c->H * c->by_pitch / 16;
-  byte_popcount_kernel<<<grid_stride_blocks(n / 4, 256), 256, 0, c->stream>>>(
-      c->by[c->by_cur], c->by_pitch, c->H, slot);
+  const int64_t nv = ceil_div(c->W, 16);
+  byte_popcount_kernel<<<grid_stride_blocks(c->H * nv / 4, 256), 256, 0, c->stream>>>(
+      c->by[c->by_cur], c->by_pitch, c->H, nv, slot);
   LIFE_CHECK_LAUNCH("byte_popcount_kernel");
   return LIFE_OK;
 }
@@ -1146,7 +1169,7 @@ int engine_layout(int engine) { return engine == LIFE_ENGINE_BYTE ? kByte : kPac
 // small tori (W % 32 == 0, at most kResidentAutoCells cells) where it beats
 // the multi-pass engine (measured), else K = 16 passes.
 constexpr int64_t kResidentAutoCells = int64_t(1) << 22;
-// temporal_depth 0 on the byte engine (W % 16 == 0).  Two-stream kernel
+// temporal_depth 0 on the byte engine (W % 16 == 0 or W >= 33).  Two-stream kernel
 // (byte_tb2_kernel), T cell-updates/s at K = 4 / 6 / 8: 16384^2 10.0 / 12.7 /
 // 13.1, 32768 x 16384 10.0 / 13.8 / 13.7, 4096^2 4.6 / 4.1 / 3.6 (short grids
 // pay the 3K-1 step pipeline fill).  (One stream per word, round 1: 16384^2
@@ -1614,13 +1637,14 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
                        static_cast<long long>(c->W), static_cast<long long>(c->H));
     if (depth == 0) depth = packed_auto_depth(c->W, c->H);
   } else {
-    // Byte engine: K generations per pass (byte_tb_kernel) when W % 16 == 0;
+    // Byte engine: K generations per pass (byte_tb2_kernel) when W % 16 == 0 or
+    // W >= 33 (the seam path);
     // other widths run one generation per pass whatever the depth asks.
     if (depth < 0 || depth > kByteTbMaxDepth)
       return set_error(LIFE_ERR_CONFIG, "byte engine temporal depth must be in [0, %d], got %d",
                        kByteTbMaxDepth, temporal_depth);
     if (depth == 0) depth = byte_auto_depth(c->W, c->H);
-    if (c->W % 16 != 0) depth = 1;
+    if (c->W % 16 != 0 && c->W < kByteTbMinSeamWidth) depth = 1;
   }
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   LIFE_TRY(to_layout(c, engine_layout(engine)));

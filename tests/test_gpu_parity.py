@@ -252,8 +252,27 @@ def test_cfg4_nonpow2_sparse_soup(engine, oracle):
     # depth 0 = the engine's auto rule: K = 12 on this one-wave W % 32 != 0 torus
     assert capi.lib().life_packed_auto_depth(40961, 12289) == 12
     assert capi.lib().life_packed_launch_kind(40961, 12289, 12) == capi.LAUNCH_ALL_PATHS
-    for eng, depth in [(BYTE, 1), (PACKED, 16), (PACKED, 0), (PACKED, 12)]:
+    # BYTE 0 / 8: the two-stream byte kernel's seam path (W % 16 == 1)
+    for eng, depth in [(BYTE, 1), (BYTE, 0), (BYTE, 8), (PACKED, 16), (PACKED, 0), (PACKED, 12)]:
         _check_schedule(engine, oracle, gold, eng, depth, lambda: engine.upload(soup))
+
+
+@pytest.mark.parametrize("W", [33, 40, 47, 50, 100, 127, 1000, 1001, 2047, 2049])
+def test_byte_passes_on_widths_not_multiple_of_16(engine, oracle, W):
+    """Temporal-blocked byte passes on W % 16 != 0 tori: the seam lanes build
+    their 16 columns from two or three vectors of the row (byte_seam_plan),
+    the partial last vector keeps its bytes past W zero; equal to the oracle
+    for depths 2..8, remainders and checkpoint splits."""
+    rng = np.random.default_rng(W)
+    H = int(rng.integers(20, 90))
+    g = oracle.random_fill(W, H, 0.35, int(rng.integers(1 << 30)))
+    gens = 29
+    want, pops = oracle.run(g, gens, [0, 11, gens])
+    for depth in (2, 3, 5, 8, 0):
+        engine.upload(g)
+        got_pops = engine.run(gens, BYTE, depth, [0, 11, gens])
+        assert np.array_equal(engine.download(), want), (W, H, depth)
+        assert got_pops == pops
 
 
 @pytest.mark.slow
