@@ -213,6 +213,28 @@ int main() {
     return ok[0] && ok[1];
   });
 
+  check_case("run_packed on host packed rows equals run() on bytes", [] {
+    for (int rep = 0; rep < 3; ++rep) {
+      const int w = 300 + 97 * rep, h = 120 + 31 * rep;
+      Grid g = lifegpu::random_fill<Grid>(w, h, 0.35, 40 + rep);
+      RunConfig c;
+      c.iterations = 37;
+      c.temporal_depth = rep == 0 ? 0 : 7;
+      const Grid want = lifegpu::run(g, c).grid;
+      const int64_t wpr = (w + 63) / 64;
+      std::vector<uint64_t> words(static_cast<size_t>(wpr) * h, 0);
+      for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+          if (g.at(x, y)) words[static_cast<size_t>(y) * wpr + x / 64] |= uint64_t(1) << (x % 64);
+      lifegpu::run_packed(words.data(), words.data(), w, h, wpr, c);  // in place
+      for (int y = 0; y < h; ++y)
+        for (int x = 0; x < w; ++x)
+          if (((words[static_cast<size_t>(y) * wpr + x / 64] >> (x % 64)) & 1) != want.at(x, y))
+            return false;
+    }
+    return true;
+  });
+
   std::printf("%d failure(s)\n", failures);
   return failures == 0 ? 0 : 1;
 }
