@@ -929,6 +929,25 @@ def run_ctx_arm(args) -> None:
                       "kind": "full-grid packed FNV-1a-64 + population", "got": got,
                       "want": gold["fnv_packed"], "population": pop}
         parity["source"] = "tests/golden/" + gold["source"]
+    e2e = None
+    if not args.no_e2e:
+        # life_run_batch on the multi-device context: every step's packed grid
+        # from pinned host memory to the bands and back, copies overlapped with
+        # the neighbouring steps' compute; CUDA-event time (life_run_batch's
+        # elapsed_ms, max over the bands' devices).
+        wpr = (W + 63) // 64
+        hin = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True).numpy().view("uint64")
+        hout = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True).numpy().view("uint64")
+        init()
+        e.download_packed(hin)
+        steps_e2e = max(2, args.steps)
+        e.run_batch([hin], [hout], W, gens, depth)  # warm-up (allocates buffers)
+        e2e_ms = e.run_batch([hin] * steps_e2e, [hout] * steps_e2e, W, gens, depth)
+        e2e = {"value": W * H * gens * steps_e2e / (e2e_ms * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": H * wpr * 8, "d2h_bytes_per_step": H * wpr * 8,
+               "api": "C-ABI life_run_batch on the multi-device context (per step: H2D of "
+                      "every band, run, D2H; copies overlapped with the neighbouring steps)",
+               "steps": steps_e2e}
     e.close()
     eff_depth = depth or int(L.life_packed_auto_depth(W, max(y - x for x, y in zip(b["bounds"], b["bounds"][1:]))))
     line = {
@@ -946,7 +965,7 @@ def run_ctx_arm(args) -> None:
                      "frac": value * 1e9 * OPS_PER_UPDATE / n / int_ops if int_ops else None,
                      "basis": "whole step per GPU (band_stats run_ms, max over bands)",
                      "traffic": None},
-        "parity": parity, "bands": stats, "cpu_baseline": None, "e2e": None,
+        "parity": parity, "bands": stats, "cpu_baseline": None, "e2e": e2e,
         "gpu_launches": gpu_launches, "clocks": clocks.summary()}
     print(json.dumps(line), flush=True)
     if parity.get("ok") is False:

@@ -105,6 +105,7 @@ def test_single_process_multi_device_context_line():
     assert r.returncode == 0, r.stderr[-3000:]
     j = json.loads([l for l in r.stdout.splitlines() if l.strip().startswith("{")][0])
     assert j["n_gpus"] == 3 and j["parity"]["ok"] is True and len(j["bands"]) == 3
+    assert j["e2e"]["value"] > 0 and j["e2e"]["h2d_bytes_per_step"] == 12289 * 641 * 8
     assert j["config"]["bounds"] == [0, 4097, 8193, 12289]
 
 
