@@ -257,8 +257,12 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   for (int64_t segs = 1; segs <= max_segs; ++segs) {
     const int64_t rows = ceil_div(a.out_rows, segs);
     const int64_t blocks = ceil_div(static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, rows), wpb);
-    // + 64 rows per wave: block start-up and pipeline refill.
-    const double cost = double(ceil_div(blocks, slots)) * double(rows + kLag + PF + 64);
+    // Per wave: the tile's pipeline fill (about half of the 3K-1 lag steps
+    // run, the fill trips skip the stage groups with no valid input yet) and
+    // block start-up.  (Round 1 charged kLag + PF + 64, which kept config 3
+    // on one wave of 1139 tiles at 96 % occupancy; two waves of 2345 tiles run
+    // 1.6 % faster -- LIFE_SEGS sweep.)
+    const double cost = double(ceil_div(blocks, slots)) * double(rows + kLag / 2 + PF + 8);
     if (cost < best_cost * 0.999) {
       best_cost = cost;
       best_segs = segs;
