@@ -257,12 +257,13 @@ int launch_packed_kernel(PackedStepArgs a, cudaStream_t s) {
   for (int64_t segs = 1; segs <= max_segs; ++segs) {
     const int64_t rows = ceil_div(a.out_rows, segs);
     const int64_t blocks = ceil_div(static_cast<int64_t>(a.n_strips) * ceil_div(a.out_rows, rows), wpb);
-    // Per wave: the tile's pipeline fill (about half of the 3K-1 lag steps
-    // run, the fill trips skip the stage groups with no valid input yet) and
-    // block start-up.  (Round 1 charged kLag + PF + 64, which kept config 3
-    // on one wave of 1139 tiles at 96 % occupancy; two waves of 2345 tiles run
-    // 1.6 % faster -- LIFE_SEGS sweep.)
-    const double cost = double(ceil_div(blocks, slots)) * double(rows + kLag / 2 + PF + 8);
+    // Per wave: the tile's pipeline fill and block start-up, calibrated on
+    // LIFE_SEGS sweeps: + 48 rows (round 1: + 64)
+    // moves config 3 from one wave of 1139 tiles at 96 % occupancy to two
+    // waves of 2345 (44.6 -> 45.3 T/s) and keeps config 5's 7-wave plan; a
+    // lighter charge (kLag / 2 + PF + 8) also re-planned config 5's passes
+    // and cost its copy-overlapped e2e 2 % (45.2 -> 44.2).
+    const double cost = double(ceil_div(blocks, slots)) * double(rows + kLag + PF + 48);
     if (cost < best_cost * 0.999) {
       best_cost = cost;
       best_segs = segs;
