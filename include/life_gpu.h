@@ -100,6 +100,7 @@ int life_ctx_bands(life_ctx* ctx, int32_t* n, int64_t* bounds, int32_t* devices,
 #define LIFE_OPT_PROFILE 1         /* 1: CUDA events around every pass of life_run (band stats) */
 #define LIFE_OPT_BATCH_TRAPEZOID 2 /* life_run_batch first/last-grid chunk schedule: -1 auto, 0, 1 */
 #define LIFE_OPT_HALO 3            /* multi-device halo scheme: LIFE_HALO_PEER / LIFE_HALO_COPY */
+#define LIFE_OPT_PAIR_DEPTH 4      /* interleaved-pair kernel (W % 64 == 0): -1 auto, 0 off, 1..12 forced depth */
 #define LIFE_HALO_PEER 0           /* edge-strip kernels read neighbour rows over NVLink (P2P) */
 #define LIFE_HALO_COPY 1           /* neighbour rows copied into local ghost rows, then computed */
 int life_ctx_set_option(life_ctx* ctx, int32_t option, int64_t value);

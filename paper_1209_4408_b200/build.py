@@ -47,7 +47,7 @@ def build_lib(force: bool = False, verbose: bool = False, out: str = LIB,
     if not force and _newer(out, srcs + [os.path.abspath(__file__)]):
         return out
     units = [os.path.join(CSRC, f) for f in sorted(os.listdir(CSRC)) if f.endswith(".cu")]
-    cmd = [NVCC, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-cudart", "static",
+    cmd = [NVCC, "--threads", "0", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-shared", "-cudart", "static",
            "-o", out + ".tmp", *units]
     if verbose:
         cmd[1:1] = ["-Xptxas", "-v"]

@@ -31,6 +31,7 @@ MAX_BYTE_DEPTH = 8
 OPT_PROFILE = 1
 OPT_BATCH_TRAPEZOID = 2
 OPT_HALO = 3
+OPT_PAIR_DEPTH = 4
 HALO_PEER = 0
 HALO_COPY = 1
 

@@ -87,7 +87,23 @@ int packed_auto_depth(int64_t width, int64_t height);
 // buf_b: whole passes of `depth`, then the remainder; *result_in_b = 1 if the result is in buf_b.
 int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, int64_t height,
                int64_t generations, int32_t depth, cudaStream_t stream, SplitStreams* ss,
-               int* result_in_b);
+               int* result_in_b, bool pair = false);
+
+// ---- interleaved-pair layout (life_pair.cu, kernels_pair.cuh) ---------------
+// W % 64 == 0 tori: each uint64 group of a packed row kept as (even columns,
+// odd columns); passes of up to kPairMaxDepth generations at 10 instead of 11
+// integer ops per 32 cell-updates.  packed_zip converts rows in place.
+constexpr int kPairMaxDepthHost = 12;
+inline bool pair_eligible(int64_t width) { return width >= 64 && width % 64 == 0; }
+int packed_pair_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                     uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                     int64_t out_rows, int32_t generations, cudaStream_t stream);
+int packed_pair_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
+                          const uint32_t* down, int64_t down_rows, int64_t pitch,
+                          int64_t band_rows, uint32_t* out, int64_t out_row0, int64_t out_rows,
+                          int64_t width, int32_t generations, cudaStream_t stream);
+int packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
+               bool unzip, cudaStream_t stream);
 
 // Small kernels the multi-device context launches on band buffers.
 int launch_mask_tail(uint32_t* words, int64_t pitch, int64_t width, int64_t rows,

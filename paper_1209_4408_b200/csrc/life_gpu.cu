@@ -516,10 +516,10 @@ int packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t i
 
 int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, int64_t height,
                int64_t generations, int32_t depth, cudaStream_t stream, SplitStreams* ss,
-               int* result_in_b) {
-  if (depth < 1 || depth > LIFE_MAX_TEMPORAL_DEPTH)
+               int* result_in_b, bool pair) {
+  if (depth < 1 || depth > (pair ? kPairMaxDepthHost : LIFE_MAX_TEMPORAL_DEPTH))
     return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [1, %d], got %d",
-                     LIFE_MAX_TEMPORAL_DEPTH, depth);
+                     pair ? kPairMaxDepthHost : LIFE_MAX_TEMPORAL_DEPTH, depth);
   if (generations < 0) return set_error(LIFE_ERR_CONFIG, "generations must be >= 0");
   if (width < 1 || height < 1 || pitch < 2 * ceil_div(width, 64) || buf_a == buf_b)
     return set_error(LIFE_ERR_CONFIG, "bad packed run geometry");
@@ -528,13 +528,18 @@ int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, i
   int flip = 0;
   const int64_t full = generations / depth;
   const int rem = static_cast<int>(generations % depth);
+  auto pass = [&](int k) -> int {
+    if (pair)  // buffers in the interleaved-pair layout (kernels_pair.cuh)
+      return packed_pair_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, k, stream);
+    return packed_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, k, stream, ss);
+  };
   for (int64_t i = 0; i < full; ++i) {
-    LIFE_TRY(packed_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, depth, stream, ss));
+    LIFE_TRY(pass(depth));
     std::swap(cur, nxt);
     flip ^= 1;
   }
   if (rem > 0) {
-    LIFE_TRY(packed_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, rem, stream, ss));
+    LIFE_TRY(pass(rem));
     flip ^= 1;
   }
   if (result_in_b) *result_in_b = flip;
@@ -1038,6 +1043,9 @@ struct life_ctx {
   uint32_t* pk[2] = {nullptr, nullptr};
   int64_t pk_pitch = 0;  // uint32 words
   int pk_cur = 0;
+  // pk[pk_cur] is in the interleaved-pair layout (kernels_pair.cuh): left so by
+  // life_run between runs; every reader of the plain layout calls pk_plain().
+  bool pk_pair = false;
   uint8_t* by[2] = {nullptr, nullptr};
   int64_t by_pitch = 0;  // bytes
   int by_cur = 0;
@@ -1057,6 +1065,7 @@ struct life_ctx {
   // Options (life_ctx_set_option).
   int batch_trap = -1;   // LIFE_OPT_BATCH_TRAPEZOID
   bool profile = false;  // LIFE_OPT_PROFILE
+  int pair_depth = -1;   // LIFE_OPT_PAIR_DEPTH
   // Statistics of the last life_run (life_ctx_band_stats, band 0).
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   double run_ms = 0.0, pass_ms = 0.0;
@@ -1086,6 +1095,7 @@ void free_buffers(life_ctx* c) {
 
 int set_dims(life_ctx* c, int64_t w, int64_t h) {
   LIFE_TRY(check_dims(w, h));
+  c->pk_pair = false;  // callers overwrite the whole grid in the plain layout
   if (w != c->W || h != c->H) {
     LIFE_CUDA(cudaStreamSynchronize(c->stream));
     free_buffers(c);
@@ -1130,9 +1140,29 @@ int ensure_counts(life_ctx* c, int64_t n) {
 }
 
 // Converts the resident grid to `layout` (device-side pack / unpack).
+// life_run leaves a W % 64 == 0 packed grid in the interleaved-pair layout
+// (kernels_pair.cuh) so consecutive runs pay no conversion; everything that
+// reads or edits the plain packed words converts it back first (in place,
+// one HBM read + write of the grid).
+int pk_plain(life_ctx* c) {
+  if (c->layout == kPacked && c->pk_pair) {
+    LIFE_TRY(packed_zip(c->pk[c->pk_cur], c->pk_pitch, c->W, 0, c->H, /*unzip=*/true, c->stream));
+  }
+  c->pk_pair = false;
+  return LIFE_OK;
+}
+int pk_to_pair(life_ctx* c) {
+  if (c->layout == kPacked && !c->pk_pair) {
+    LIFE_TRY(packed_zip(c->pk[c->pk_cur], c->pk_pitch, c->W, 0, c->H, /*unzip=*/false, c->stream));
+    c->pk_pair = true;
+  }
+  return LIFE_OK;
+}
+
 int to_layout(life_ctx* c, int layout) {
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   if (c->layout == layout) return LIFE_OK;
+  LIFE_TRY(pk_plain(c));
   if (layout == kPacked) {
     LIFE_TRY(ensure_packed(c));
     LIFE_TRY(life_dev_pack(c->by[c->by_cur], c->by_pitch, c->pk[0], c->pk_pitch, c->W, c->H,
@@ -1180,6 +1210,13 @@ constexpr int64_t kResidentAutoCells = int64_t(1) << 22;
 // pay the 3K-1 step pipeline fill).  (One stream per word, round 1: 16384^2
 // 8.1 / 8.8 / 8.1.)
 int byte_auto_depth(int64_t w, int64_t h) { return w * h >= (int64_t(1) << 26) ? 8 : 4; }
+
+// temporal_depth 0 on W % 64 == 0 tori: the interleaved-pair kernel at this
+// depth (0: keep the plain-layout kernels).
+int pair_auto_depth(int64_t w, int64_t h) {
+  if (!pair_eligible(w)) return 0;
+  return w * h >= (int64_t(1) << 30) ? 10 : 0;
+}
 
 bool resident_auto(int64_t w, int64_t h) {
   return w % 32 == 0 && w * h <= kResidentAutoCells && life_resident_cluster_size(w, h) > 0;
@@ -1318,6 +1355,12 @@ int life_ctx_set_option(life_ctx* c, int32_t option, int64_t value) {
       return LIFE_OK;
     case LIFE_OPT_HALO:
       return set_error(LIFE_ERR_CONFIG, "LIFE_OPT_HALO applies to multi-device contexts");
+    case LIFE_OPT_PAIR_DEPTH:
+      if (value < -1 || value > kPairMaxDepthHost)
+        return set_error(LIFE_ERR_CONFIG, "LIFE_OPT_PAIR_DEPTH must be in [-1, %d]",
+                         kPairMaxDepthHost);
+      c->pair_depth = static_cast<int>(value);
+      return LIFE_OK;
     default:
       return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
   }
@@ -1329,6 +1372,7 @@ int life_ctx_get_option(life_ctx* c, int32_t option, int64_t* value) {
   switch (option) {
     case LIFE_OPT_PROFILE: *value = c->profile ? 1 : 0; return LIFE_OK;
     case LIFE_OPT_BATCH_TRAPEZOID: *value = c->batch_trap; return LIFE_OK;
+    case LIFE_OPT_PAIR_DEPTH: *value = c->pair_depth; return LIFE_OK;
     default: return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
   }
 }
@@ -1500,6 +1544,7 @@ int life_grid_place_u8(life_ctx* c, const uint8_t* pattern, int64_t pw, int64_t 
                      static_cast<long long>(x0), static_cast<long long>(y0),
                      static_cast<long long>(c->W), static_cast<long long>(c->H));
   if (pw * ph == 0) return LIFE_OK;
+  LIFE_TRY(pk_plain(c));
   uint8_t* dpat = nullptr;
   LIFE_CUDA(cudaMallocAsync(&dpat, pw * ph, c->stream));
   LIFE_CUDA(cudaMemcpyAsync(dpat, pattern, pw * ph, cudaMemcpyHostToDevice, c->stream));
@@ -1522,6 +1567,7 @@ int life_grid_download_u8(life_ctx* c, uint8_t* cells, int64_t row_stride) {
   LIFE_TRY(activate(c));
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   if (!cells || row_stride < c->W) return set_error(LIFE_ERR_CONFIG, "bad output buffer");
+  LIFE_TRY(pk_plain(c));
   const uint8_t* src;
   if (c->layout == kByte) {
     src = c->by[c->by_cur];
@@ -1543,6 +1589,7 @@ int life_grid_download_packed(life_ctx* c, uint64_t* words, int64_t words_per_ro
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   const int64_t wpr = ceil_div(c->W, 64);
   if (!words || words_per_row < wpr) return set_error(LIFE_ERR_CONFIG, "bad output buffer");
+  LIFE_TRY(pk_plain(c));
   const uint32_t* src;
   if (c->layout == kPacked) {
     src = c->pk[c->pk_cur];
@@ -1565,6 +1612,7 @@ int life_grid_window_u8(life_ctx* c, int64_t x0, int64_t y0, int64_t w, int64_t 
   if (w < 0 || h < 0 || !out) return set_error(LIFE_ERR_CONFIG, "bad window");
   const int64_t n = w * h;
   if (n == 0) return LIFE_OK;
+  LIFE_TRY(pk_plain(c));
   if (n > c->window_cap) {
     if (c->window) cudaFree(c->window);
     c->window = nullptr;
@@ -1601,6 +1649,7 @@ int life_grid_hash(life_ctx* c, uint64_t* out) {
   if (!out) return set_error(LIFE_ERR_CONFIG, "null output pointer");
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   LIFE_TRY(to_layout(c, kPacked));
+  LIFE_TRY(pk_plain(c));
   if (c->H > c->row_hashes_cap) {
     if (c->row_hashes) cudaFree(c->row_hashes);
     c->row_hashes = nullptr;
@@ -1628,6 +1677,7 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
   LIFE_TRY(check_engine(engine));
   LIFE_TRY(check_run_args(generations, checkpoints, n_checkpoints, populations));
   int depth = temporal_depth;
+  int pair = 0;  // > 0: passes of that depth on the interleaved-pair layout
   if (engine != LIFE_ENGINE_BYTE) {
     if (depth < 0 || depth > LIFE_MAX_TEMPORAL_DEPTH)
       return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [0, %d], got %d",
@@ -1641,6 +1691,15 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
                        "(needs W %% 32 == 0 and every band in one CTA's shared memory)",
                        static_cast<long long>(c->W), static_cast<long long>(c->H));
     if (depth == 0) depth = packed_auto_depth(c->W, c->H);
+    // Interleaved-pair kernel (W % 64 == 0): forced by LIFE_OPT_PAIR_DEPTH, or
+    // the auto rule's choice when the caller left the depth to the engine.
+    if (engine == LIFE_ENGINE_PACKED && pair_eligible(c->W)) {
+      if (c->pair_depth > 0)
+        pair = c->pair_depth;
+      else if (c->pair_depth < 0 && temporal_depth == 0)
+        pair = pair_auto_depth(c->W, c->H);
+      if (pair > 0) depth = pair;
+    }
   } else {
     // Byte engine: K generations per pass (byte_tb2_kernel) when W % 16 == 0 or
     // W >= 33 (the seam path);
@@ -1653,6 +1712,11 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
   }
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   LIFE_TRY(to_layout(c, engine_layout(engine)));
+  if (pair > 0 && generations > 0) {
+    LIFE_TRY(pk_to_pair(c));
+  } else if (generations > 0 || engine != LIFE_ENGINE_PACKED) {
+    LIFE_TRY(pk_plain(c));
+  }
   if (n_checkpoints > 0) LIFE_TRY(ensure_counts(c, n_checkpoints));
   LIFE_TRY(split_streams_init(&c->split[0], c->device));
   if (!c->t0) LIFE_CUDA(cudaEventCreate(&c->t0));
@@ -1703,7 +1767,7 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
       // the remainder).
       int flip = 0;
       LIFE_TRY(packed_run(c->pk[c->pk_cur], c->pk[c->pk_cur ^ 1], c->pk_pitch, c->W, c->H,
-                          stop - done, depth, c->stream, &c->split[0], &flip));
+                          stop - done, depth, c->stream, &c->split[0], &flip, c->pk_pair));
       c->pk_cur ^= flip;
       c->passes += ceil_div(stop - done, int64_t(depth));
       done = stop;
@@ -1714,8 +1778,13 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
     const int step = static_cast<int>(std::min<int64_t>(depth, stop - done));
     if (engine == LIFE_ENGINE_PACKED) {
       const int nxt = c->pk_cur ^ 1;
-      LIFE_TRY(packed_step(c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt], c->pk_pitch, 0,
-                           c->W, c->H, step, c->stream, &c->split[0]));
+      if (c->pk_pair) {
+        LIFE_TRY(packed_pair_step(c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt],
+                                  c->pk_pitch, 0, c->W, c->H, step, c->stream));
+      } else {
+        LIFE_TRY(packed_step(c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt], c->pk_pitch, 0,
+                             c->W, c->H, step, c->stream, &c->split[0]));
+      }
       c->pk_cur = nxt;
     } else {
       const int nxt = c->by_cur ^ 1;
