@@ -32,6 +32,23 @@ METRIC = "cell-updates/sec (GCUPS) at 1/2/4/8 B200 and % of HBM/int roofline"
 UNIT = "GCUPS"
 OPS_PER_WORD = 11            # bit-sliced rule network (2 SHF + 9 LOP3), csrc/kernels.cuh
 OPS_PER_UPDATE = OPS_PER_WORD / 32.0
+PAIR_OPS_PER_WORD = 10       # interleaved-pair layout (1 SHF + 9 LOP3), csrc/kernels_pair.cuh
+PAIR_OPS_PER_UPDATE = PAIR_OPS_PER_WORD / 32.0
+
+
+def pick_depth(L, args, W: int, rows: int):
+    """(depth, pair) as life_run picks them for `--depth` / `--pair-depth` on
+    a W-wide torus (or band) of `rows` rows: the interleaved-pair kernel when
+    forced, or when both are left to the engine and life_pair_auto_depth says
+    so; else the plain-layout kernels at --depth or life_packed_auto_depth."""
+    pair = 0
+    if W % 64 == 0:
+        if args.pair_depth > 0:
+            pair = args.pair_depth
+        elif args.pair_depth < 0 and args.depth == 0:
+            pair = int(L.life_pair_auto_depth(W, rows))
+    depth = pair or args.depth or int(L.life_packed_auto_depth(W, rows))
+    return depth, bool(pair)
 
 CONFIGS = {
     1: dict(w=1024, h=1024, p=0.5, gens=100,
@@ -456,8 +473,9 @@ def run_gpu_arm(args) -> None:
     W, H, gens = cfg["w"], cfg["h"], args.gens or cfg["gens"]
     bounds0 = [H * r // world for r in range(world + 1)]
     band_rows_max = max(b - a for a, b in zip(bounds0, bounds0[1:])) + 1
-    # depth 0: the engine's own auto rule (life_packed_auto_depth)
-    depth = args.depth or int(L.life_packed_auto_depth(W, H if world == 1 else band_rows_max))
+    # depth 0: the engine's own auto rule (life_pair_auto_depth / life_packed_auto_depth)
+    depth, pair = pick_depth(L, args, W, H if world == 1 else band_rows_max)
+    ops_per_update = PAIR_OPS_PER_UPDATE if pair else OPS_PER_UPDATE
 
     def barrier():
         if world > 1:
@@ -477,13 +495,13 @@ def run_gpu_arm(args) -> None:
     if L.life_measure_int_peak(local, 4000, C.byref(o), C.byref(s)) == 0:
         int_ops = o.value
 
-    geo = make_geometry(W, H, rank, world, depth)
+    geo = make_geometry(W, H, rank, world, depth, pair)
     # Per-launch CUDA events are recorded only in one extra PROFILED step after
     # the timed region (events between launches serialise programmatic
     # dependent launch, so the timed steps carry none).
     launches = []
     from paper_1209_4408_b200.bands import cuda_stepper
-    base_step = cuda_stepper(W)
+    base_step = cuda_stepper(W, pair)
     record = {"on": False}
 
     def timed_step(inp, in_row0, in_rows, out, out_row0, out_rows, k):
@@ -630,14 +648,16 @@ def run_gpu_arm(args) -> None:
     else:
         allst = [rank_stats]
 
-    achieved_ops = kern_cells * OPS_PER_UPDATE / (kern_ms * 1e-3) if kern_ms else 0.0
+    achieved_ops = kern_cells * ops_per_update / (kern_ms * 1e-3) if kern_ms else 0.0
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     alg_bytes_per_update = 0.25 / depth
     hbm_achieved = kern_cells * alg_bytes_per_update / (kern_ms * 1e-3) / 1e9 if kern_ms else 0.0
-    traffic = ncu_traffic(args.config, depth)
-    kind = int(L.life_packed_launch_kind(W, geo.band_rows if world > 1 else H, depth))
-    kname = {capi.LAUNCH_STEP1: "packed_step1_kernel",
+    traffic = ncu_traffic(args.config, depth, "pair" if pair else "")
+    kind = -2 if pair else int(L.life_packed_launch_kind(W, geo.band_rows if world > 1 else H,
+                                                         depth))
+    kname = {-2: f"packed_pair_kernel<{depth}>",
+             capi.LAUNCH_STEP1: "packed_step1_kernel",
              capi.LAUNCH_FAST: f"packed_tb_fast_kernel<{depth}>",
              capi.LAUNCH_ALL_PATHS: f"packed_tb_kernel<{depth}>",
              capi.LAUNCH_SPLIT: f"split: packed_tb_fast_kernel<{depth}> (inner strips) + "
@@ -649,21 +669,21 @@ def run_gpu_arm(args) -> None:
         "achieved": achieved_ops / 1e12, "peak": int_ops / 1e12, "unit": "Tops/s",
         "frac": achieved_ops / int_ops if int_ops else None,
         "peak_source": "measured (life_measure_int_peak: LOP3 throughput, all SMs, this run)",
-        "ops_per_cell_update": OPS_PER_UPDATE,
+        "ops_per_cell_update": ops_per_update,
         "algorithmic_per_launch": {"cell_updates": kern_cells / n_main,
-                                   "int_ops": kern_cells / n_main * OPS_PER_UPDATE,
+                                   "int_ops": kern_cells / n_main * ops_per_update,
                                    "hbm_bytes": kern_cells / n_main * alg_bytes_per_update},
         "mean_launch_ms": kern_ms / n_main,
         "timing": "per-launch CUDA events on the launching stream over one profiled step "
                   "right after the timed steps (same work; the timed steps carry no "
                   "per-launch events, which would serialise programmatic dependent launch)",
         "kernel_share_of_step": all_kern_ms / prof_ms if prof_ms else None,
-        "step_frac": (value * 1e9 * OPS_PER_UPDATE / world) / int_ops if int_ops else None,
+        "step_frac": (value * 1e9 * ops_per_update / world) / int_ops if int_ops else None,
         "traffic": traffic,
         "hbm": {"achieved": hbm_achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": hbm_achieved / hbm_peak, "bytes_per_cell_update": alg_bytes_per_update,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback"},
-        "roofline_updates_per_s": min(int_ops / OPS_PER_UPDATE if int_ops else float("inf"),
+        "roofline_updates_per_s": min(int_ops / ops_per_update if int_ops else float("inf"),
                                       hbm_peak * 1e9 / alg_bytes_per_update),
     }
     if step1:
@@ -692,6 +712,9 @@ def run_gpu_arm(args) -> None:
             # memory, runs the generations and downloads the result; step i's
             # copies overlap step i+-1's compute (copy engines).
             eng = Engine(local)
+            if args.pair_depth >= 0:
+                eng.set_option(capi.OPT_PAIR_DEPTH, args.pair_depth)
+            api_depth = args.depth  # 0: the engine's auto rule (the same choice as `depth`)
             wpr = math.ceil(W / 64)
             host_in = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
             host_out = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
@@ -702,19 +725,19 @@ def run_gpu_arm(args) -> None:
             hin = host_in.numpy().view("uint64")
             hout = host_out.numpy().view("uint64")
             eng.download_packed(hin)
-            eng.run_batch([hin], [hout], W, gens, depth)  # warm-up (allocates buffers)
-            e2e_ms = eng.run_batch([hin] * steps_e2e, [hout] * steps_e2e, W, gens, depth)
+            eng.run_batch([hin], [hout], W, gens, api_depth)  # warm-up (allocates buffers)
+            e2e_ms = eng.run_batch([hin] * steps_e2e, [hout] * steps_e2e, W, gens, api_depth)
             # Drop-in latency: one synchronous run() per call -- upload, run,
             # download, nothing overlapped across calls (what lifegpu::run
             # does for one caller), host-timed.
             eng.upload_packed(hin, W)
-            eng.run(gens, capi.ENGINE_PACKED, depth)
+            eng.run(gens, capi.ENGINE_PACKED, api_depth)
             eng.download_packed(hout)
             sync_s = []
             for _ in range(steps_e2e):
                 t0 = time.perf_counter()
                 eng.upload_packed(hin, W)
-                eng.run(gens, capi.ENGINE_PACKED, depth)
+                eng.run(gens, capi.ENGINE_PACKED, api_depth)
                 eng.download_packed(hout)
                 sync_s.append(time.perf_counter() - t0)
             # The same single-grid call through life_run_batch(n = 1): its
@@ -723,7 +746,7 @@ def run_gpu_arm(args) -> None:
             one_s = []
             for _ in range(steps_e2e):
                 t0 = time.perf_counter()
-                eng.run_batch([hin], [hout], W, gens, depth)
+                eng.run_batch([hin], [hout], W, gens, api_depth)
                 one_s.append(time.perf_counter() - t0)
             eng.close()
             bi = bo = H * wpr * 8
@@ -767,7 +790,8 @@ def run_gpu_arm(args) -> None:
             "scaling": "strong", "vs_baseline": None,
             "dtype": "u32 bit-sliced (32 cells/word, exact integer)", "data": "synthetic",
             "config": {"workload": cfg["desc"], "width": W, "height": H, "generations": gens,
-                       "temporal_depth": depth, "global_cells": W * H,
+                       "temporal_depth": depth, "layout": "interleaved-pair" if pair else "plain",
+                       "global_cells": W * H,
                        "parallelism": f"rowbands{world}" if world > 1 else "single-gpu",
                        "halo": {"peer": "in-kernel NVLink peer reads (CUDA IPC) + "
                                         f"{args.pass_sync} pass ordering",
@@ -835,7 +859,7 @@ def e2e_bands(args, geo, dev, halo, cfg, gens, soup_host, steps_e2e, barrier, ma
             up_done[0].record(copy)
         for i in range(n_steps):
             main.wait_event(up_done[i])
-            drv.band().copy_(stage_in)          # on-device, after upload i
+            drv.set_band(stage_in)              # on-device, after upload i
             if i + 1 < n_steps:                 # upload i+1 overlaps compute i
                 copy.wait_stream(main)
                 with torch.cuda.stream(copy):
@@ -886,6 +910,8 @@ def run_ctx_arm(args) -> None:
     int_ops = o.value if L.life_measure_int_peak(devices[0], 4000, C.byref(o), C.byref(s)) == 0 \
         else 0.0
     e = Engine(devices=devices)
+    if args.pair_depth >= 0:
+        e.set_option(capi.OPT_PAIR_DEPTH, args.pair_depth)
 
     def init():
         if cfg.get("soup"):
@@ -949,20 +975,24 @@ def run_ctx_arm(args) -> None:
                       "every band, run, D2H; copies overlapped with the neighbouring steps)",
                "steps": steps_e2e}
     e.close()
-    eff_depth = depth or int(L.life_packed_auto_depth(W, max(y - x for x, y in zip(b["bounds"], b["bounds"][1:]))))
+    eff_depth, pair = pick_depth(L, args, W, max(y - x for x, y in zip(b["bounds"], b["bounds"][1:])))
+    ops_per_update = PAIR_OPS_PER_UPDATE if pair else OPS_PER_UPDATE
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sum(ms) / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None,
         "dtype": "u32 bit-sliced (32 cells/word, exact integer)", "data": "synthetic",
         "config": {"workload": cfg["desc"], "width": W, "height": H, "generations": gens,
-                   "temporal_depth": eff_depth, "parallelism": f"rowbands{n} (one process, "
+                   "temporal_depth": eff_depth,
+                   "layout": "interleaved-pair" if pair else "plain",
+                   "parallelism": f"rowbands{n} (one process, "
                    "multi-device C-ABI context)", "devices": devices,
                    "bounds": b["bounds"], "halo": {0: "peer", 1: "copy"}.get(b["halo"], "none"),
                    "emulated_ranks_on_one_gpu": emulated},
-        "roofline": {"bound": "int", "achieved": value * 1e9 * OPS_PER_UPDATE / n / 1e12,
+        "roofline": {"bound": "int", "achieved": value * 1e9 * ops_per_update / n / 1e12,
                      "peak": int_ops / 1e12, "unit": "Tops/s",
-                     "frac": value * 1e9 * OPS_PER_UPDATE / n / int_ops if int_ops else None,
+                     "ops_per_cell_update": ops_per_update,
+                     "frac": value * 1e9 * ops_per_update / n / int_ops if int_ops else None,
                      "basis": "whole step per GPU (band_stats run_ms, max over bands)",
                      "traffic": None},
         "parity": parity, "bands": stats, "cpu_baseline": None, "e2e": e2e,
@@ -1362,6 +1392,9 @@ def main() -> None:
     ap.add_argument("--depth", type=int, default=0,
                     help="generations per packed pass; 0 = the engine's auto rule (16; 12 for "
                          "one-launch W %% 32 != 0 tori such as config 4)")
+    ap.add_argument("--pair-depth", type=int, default=-1,
+                    help="interleaved-pair kernel (W %% 64 == 0 tori): -1 = the engine's auto "
+                         "rule when --depth is 0 too, 0 = off, 1..12 = forced depth")
     ap.add_argument("--gens", type=int, default=0, help="override the config's generations")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

@@ -195,6 +195,12 @@ int life_run_batch(life_ctx* ctx, const uint64_t* const* inputs, uint64_t* const
  * engine (16; 12 for W % 32 != 0 tori less than ~3 block waves deep). */
 int life_packed_auto_depth(int64_t width, int64_t height);
 
+/* The depth life_run / life_run_batch use for temporal_depth 0 on the
+ * interleaved-pair kernel (packed_pair_kernel<K>: W % 64 == 0 tori of 2^30
+ * cells or more, 10 instead of 11 integer ops per 32 cell-updates), or 0 when
+ * the plain-layout kernels run (LIFE_OPT_PAIR_DEPTH overrides per context). */
+int life_pair_auto_depth(int64_t width, int64_t height);
+
 /* Which kernel(s) one torus pass of `generations` over `out_rows` rows of a
  * W-wide packed grid launches (device-buffer layer and life_run alike):
  * LIFE_LAUNCH_STEP1 packed_step1_kernel (one generation, W % 128 == 0, 16-B
@@ -255,6 +261,27 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
                               int64_t band_rows, uint32_t* out, int64_t out_row0,
                               int64_t out_rows, int64_t width, int32_t generations,
                               void* stream);
+/* ---- the interleaved-pair layout at the device-buffer layer (W % 64 == 0):
+ * each uint64 group of a packed row kept as (even columns, odd columns), the
+ * layout packed_pair_kernel<K> steps at 10 integer ops per 32 cell-updates.
+ * life_dev_packed_zip converts rows [row0, row0 + rows) in place (to_pair 1:
+ * plain -> pair, 0: pair -> plain).  The _pair step / run / step_peer calls
+ * are life_dev_packed_step / _run / _step_peer on buffers in that layout,
+ * `generations` / `depth` in 1..12.  Populations (popcounts) are layout-
+ * independent; everything else reads the plain layout. */
+int life_dev_packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
+                        int32_t to_pair, void* stream);
+int life_dev_packed_step_pair(const uint32_t* in, int64_t in_pitch, int64_t in_row0,
+                              int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0,
+                              int64_t width, int64_t out_rows, int32_t generations, void* stream);
+int life_dev_packed_run_pair(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width,
+                             int64_t height, int64_t generations, int32_t depth,
+                             int32_t* result_in_b, void* stream);
+int life_dev_packed_step_pair_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
+                                   const uint32_t* down, int64_t down_rows, int64_t pitch,
+                                   int64_t band_rows, uint32_t* out, int64_t out_row0,
+                                   int64_t out_rows, int64_t width, int32_t generations,
+                                   void* stream);
 /* `generations` packed generations of a whole W x H torus (rows of `pitch`
  * words, in == out allowed) through the cluster-resident engine
  * (LIFE_ENGINE_RESIDENT), one launch per 2^30 generations. */

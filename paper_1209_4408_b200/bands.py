@@ -84,6 +84,10 @@ class BandGeometry:
     y0: int
     y1: int
     pitch: int  # uint32 words per row
+    # Passes run packed_pair_kernel on the interleaved-pair layout (W % 64 == 0,
+    # depth <= 12; kernels_pair.cuh): the drivers convert their band in place
+    # before the first pass and back before anything reads the plain words.
+    pair: bool = False
 
     @property
     def band_rows(self) -> int:
@@ -98,17 +102,52 @@ class BandGeometry:
         return self.band_rows + 2 * self.ghost
 
 
-def make_geometry(width: int, height: int, rank: int, world: int, depth: int) -> BandGeometry:
+def make_geometry(width: int, height: int, rank: int, world: int, depth: int,
+                  pair: bool = False) -> BandGeometry:
     if width < 3 or height < 3:
         raise ConfigError(f"grid dimensions must be at least 3x3, got {width}x{height}")
     if not 1 <= depth <= capi.MAX_TEMPORAL_DEPTH:
         raise ConfigError(f"temporal depth must be in [1, {capi.MAX_TEMPORAL_DEPTH}]")
+    if pair and (width % 64 != 0 or depth > capi.PAIR_MAX_DEPTH):
+        raise ConfigError(f"the pair layout needs W % 64 == 0 and depth <= {capi.PAIR_MAX_DEPTH}, "
+                          f"got W = {width}, depth {depth}")
     bounds = band_bounds(height, world)  # TooManyParts like partition_rows
     y0, y1 = bounds[rank], bounds[rank + 1]
     if world > 1 and (y1 - y0) < depth:
         raise TooManyParts(f"band of {y1 - y0} rows is thinner than the temporal depth {depth}")
     return BandGeometry(width, height, rank, world, depth, y0, y1,
-                        int(capi.lib().life_packed_pitch_words(width)))
+                        int(capi.lib().life_packed_pitch_words(width)), pair)
+
+
+class PairLayout:
+    """Mixin of the band drivers: which layout the current band is in.  A
+    driver names its band rows with _band_raw() (a view of `band_rows` rows of
+    `pitch` words); passes call _to_pair() first when the geometry asks for
+    the pair kernel, readers of the plain layout call _to_plain()."""
+
+    in_pair = False
+
+    def _zip(self, to_pair: bool) -> None:
+        g = self.geo
+        raw = self._band_raw()
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        check(capi.lib().life_dev_packed_zip(raw.data_ptr(), g.pitch, g.width, 0, g.band_rows,
+                                             1 if to_pair else 0, stream))
+
+    def set_band(self, rows: torch.Tensor) -> None:
+        """Overwrites the band with `rows` (plain packed layout)."""
+        self.in_pair = False
+        self._band_raw().copy_(rows)
+
+    def _to_pair(self) -> None:
+        if self.geo.pair and not self.in_pair:
+            self._zip(True)
+            self.in_pair = True
+
+    def _to_plain(self) -> None:
+        if self.in_pair:
+            self._zip(False)
+            self.in_pair = False
 
 
 # Stepper(in, in_row0, in_rows, out, out_row0, out_rows, k): one k-generation
@@ -116,18 +155,19 @@ def make_geometry(width: int, height: int, rank: int, world: int, depth: int) ->
 Stepper = Callable[[torch.Tensor, int, int, torch.Tensor, int, int, int], None]
 
 
-def cuda_stepper(width: int) -> Stepper:
+def cuda_stepper(width: int, pair: bool = False) -> Stepper:
     L = capi.lib()
+    fn = L.life_dev_packed_step_pair if pair else L.life_dev_packed_step
 
     def step(inp, in_row0, in_rows, out, out_row0, out_rows, k):
         pitch = inp.shape[1]
         stream = torch.cuda.current_stream(inp.device).cuda_stream
-        check(L.life_dev_packed_step(inp.data_ptr(), pitch, in_row0, in_rows, out.data_ptr(),
-                                     out.shape[1], out_row0, width, out_rows, k, stream))
+        check(fn(inp.data_ptr(), pitch, in_row0, in_rows, out.data_ptr(), out.shape[1], out_row0,
+                 width, out_rows, k, stream))
     return step
 
 
-class BandDriver:
+class BandDriver(PairLayout):
     """One rank's band, ping-pong buffers and pass loop."""
 
     def __init__(self, geo: BandGeometry, device: torch.device, stepper: Optional[Stepper] = None,
@@ -137,7 +177,9 @@ class BandDriver:
         self.device = device
         self.group = group
         self.overlap = overlap
-        self.stepper = stepper or cuda_stepper(geo.width)
+        if geo.pair and stepper is not None:
+            raise ConfigError("the pair layout runs on the CUDA stepper")
+        self.stepper = stepper or cuda_stepper(geo.width, geo.pair)
         self.counter = counter  # test hook: band rows -> live cells (default: CUDA popcount)
         shape = (geo.buf_rows, geo.pitch)
         self.buf = [torch.zeros(shape, dtype=torch.int32, device=device) for _ in range(2)]
@@ -149,7 +191,13 @@ class BandDriver:
         self.exchange_bytes = 0  # per pass, both directions, this rank
 
     # -- views ---------------------------------------------------------
+    def _band_raw(self) -> torch.Tensor:
+        return self.buf[self.cur][self.geo.ghost:self.geo.ghost + self.geo.band_rows]
+
     def band(self, which: Optional[int] = None) -> torch.Tensor:
+        """This rank's band rows in the plain packed layout."""
+        if which is None or which == self.cur:
+            self._to_plain()
         b = self.buf[self.cur if which is None else which]
         return b[self.geo.ghost:self.geo.ghost + self.geo.band_rows]
 
@@ -222,6 +270,7 @@ class BandDriver:
         g = self.geo
         if not 1 <= k <= g.depth:
             raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
+        self._to_pair()
         if g.world == 1:
             a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
             self.stepper(a, 0, g.height, b, 0, g.height, k)
@@ -254,6 +303,7 @@ class BandDriver:
     # -- init / reductions (CUDA) ----------------------------------------
     def init_random(self, density: float, seed: int) -> None:
         g = self.geo
+        self.in_pair = False  # overwritten whole, in the plain layout
         band = self.band()
         stream = torch.cuda.current_stream(self.device).cuda_stream
         check(capi.lib().life_dev_packed_random(band.data_ptr(), g.pitch, g.width, g.y0,
@@ -266,6 +316,7 @@ class BandDriver:
         g = self.geo
         rows = words[g.y0:g.y1]
         src = torch.from_numpy(rows.view("int32").copy())
+        self.in_pair = False
         self.band()[:, :src.shape[1]].copy_(src)
         self.generations = 0
 
@@ -275,17 +326,18 @@ class BandDriver:
         g = self.geo
         if self.counter is not None:
             acc = torch.tensor([int(self.counter(self.band()))], dtype=torch.int64)
-        else:
+        else:  # a popcount: the same in either layout
             acc = torch.zeros(1, dtype=torch.int64, device=self.device)
             stream = torch.cuda.current_stream(self.device).cuda_stream
-            check(capi.lib().life_dev_packed_population(self.band().data_ptr(), g.pitch, g.width,
-                                                        g.band_rows, acc.data_ptr(), stream))
+            check(capi.lib().life_dev_packed_population(self._band_raw().data_ptr(), g.pitch,
+                                                        g.width, g.band_rows, acc.data_ptr(),
+                                                        stream))
         if g.world > 1:
             dist.all_reduce(acc, group=self.group)
         return int(acc.item())
 
 
-class TorusDriver:
+class TorusDriver(PairLayout):
     """The single-GPU case of the band drivers (one band = the whole torus,
     no halo): run() is ONE life_dev_packed_run call (the full-depth passes,
     then the remainder).  `on_launch(kind, generations, fn)` (optional)
@@ -303,26 +355,37 @@ class TorusDriver:
         self.generations = 0
         self.on_launch = None
 
+    def _band_raw(self) -> torch.Tensor:
+        return self.buf[self.cur]
+
     def band(self) -> torch.Tensor:
+        """The torus in the plain packed layout."""
+        self._to_plain()
         return self.buf[self.cur]
 
     def _call(self, gens: int) -> None:
         import ctypes as C
         g = self.geo
+        self._to_pair()
         a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
         flip = C.c_int32(0)
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        check(capi.lib().life_dev_packed_run(a.data_ptr(), b.data_ptr(), g.pitch, g.width,
-                                             g.height, gens, g.depth, C.byref(flip), stream))
+        L = capi.lib()
+        fn = L.life_dev_packed_run_pair if g.pair else L.life_dev_packed_run
+        check(fn(a.data_ptr(), b.data_ptr(), g.pitch, g.width, g.height, gens, g.depth,
+                 C.byref(flip), stream))
         self.cur ^= flip.value
         self.generations += gens
 
     def pass_(self, k: int) -> None:
         g = self.geo
+        self._to_pair()
         a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        check(capi.lib().life_dev_packed_step(a.data_ptr(), g.pitch, 0, g.height, b.data_ptr(),
-                                              g.pitch, 0, g.width, g.height, k, stream))
+        L = capi.lib()
+        fn = L.life_dev_packed_step_pair if g.pair else L.life_dev_packed_step
+        check(fn(a.data_ptr(), g.pitch, 0, g.height, b.data_ptr(), g.pitch, 0, g.width, g.height,
+                 k, stream))
         self.cur ^= 1
         self.generations += k
 
@@ -344,6 +407,7 @@ class TorusDriver:
 
     def init_random(self, density: float, seed: int) -> None:
         g = self.geo
+        self.in_pair = False
         stream = torch.cuda.current_stream(self.device).cuda_stream
         check(capi.lib().life_dev_packed_random(self.band().data_ptr(), g.pitch, g.width, 0,
                                                 g.height, density, seed, stream))
@@ -351,6 +415,7 @@ class TorusDriver:
 
     def load_rows(self, words) -> None:
         src = torch.from_numpy(words.view("int32").copy())
+        self.in_pair = False
         self.band()[:, :src.shape[1]].copy_(src)
         self.generations = 0
 
@@ -358,7 +423,7 @@ class TorusDriver:
         g = self.geo
         acc = torch.zeros(1, dtype=torch.int64, device=self.device)
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        check(capi.lib().life_dev_packed_population(self.band().data_ptr(), g.pitch, g.width,
+        check(capi.lib().life_dev_packed_population(self._band_raw().data_ptr(), g.pitch, g.width,
                                                     g.height, acc.data_ptr(), stream))
         return int(acc.item())
 
@@ -370,8 +435,8 @@ class LocalBands:
     (no rank ever waits on another)."""
 
     def __init__(self, width: int, height: int, parts: int, depth: int, device: torch.device,
-                 overlap: bool = True):
-        self.drivers = [BandDriver(make_geometry(width, height, r, parts, depth), device,
+                 overlap: bool = True, pair: bool = False):
+        self.drivers = [BandDriver(make_geometry(width, height, r, parts, depth, pair), device,
                                    overlap=overlap) for r in range(parts)]
 
     def init_random(self, density: float, seed: int) -> None:
@@ -384,6 +449,8 @@ class LocalBands:
         if p == 1:
             ds[0].pass_(k)
             return
+        for d in ds:
+            d._to_pair()
         views = [d.halo_views(k) for d in ds]
         done = [d.compute_interior(k) for d in ds]
         for r in range(p):
@@ -460,29 +527,32 @@ def open_peer(handle: bytes) -> int:
 def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows: int,
               pitch: int, band_rows: int, dst: int, k: int, device: torch.device,
               edge_stream: Optional["torch.cuda.Stream"] = None,
-              interior_done: Optional["torch.cuda.Event"] = None) -> None:
+              interior_done: Optional["torch.cuda.Event"] = None, pair: bool = False) -> None:
     """One depth-k pass of a band with in-kernel NVLink halos: the interior
     rows [k, band-k) read only the band's own rows (the branch-free kernel
     path); the two k-row edge strips read the neighbours' rows through peer
-    pointers and run on `edge_stream` (if given) beside the interior."""
+    pointers and run on `edge_stream` (if given) beside the interior.
+    `pair`: every buffer is in the interleaved-pair layout (packed_pair_kernel)."""
     L = capi.lib()
+    step = L.life_dev_packed_step_pair if pair else L.life_dev_packed_step
+    step_peer = L.life_dev_packed_step_pair_peer if pair else L.life_dev_packed_step_peer
     main = torch.cuda.current_stream(device)
     if band_rows <= 2 * k:
-        check(L.life_dev_packed_step_peer(src, up, up_rows, down, down_rows, pitch, band_rows,
-                                          dst, 0, band_rows, width, k, main.cuda_stream))
+        check(step_peer(src, up, up_rows, down, down_rows, pitch, band_rows, dst, 0, band_rows,
+                        width, k, main.cuda_stream))
         if interior_done is not None:
             interior_done.record(main)
         return
     if edge_stream is not None:
         edge_stream.wait_stream(main)
-    check(L.life_dev_packed_step(src, pitch, k, band_rows, dst, pitch, k, width,
-                                 band_rows - 2 * k, k, main.cuda_stream))
+    check(step(src, pitch, k, band_rows, dst, pitch, k, width, band_rows - 2 * k, k,
+               main.cuda_stream))
     if interior_done is not None:
         interior_done.record(main)
     es = edge_stream.cuda_stream if edge_stream is not None else main.cuda_stream
     for r0 in (0, band_rows - k):
-        check(L.life_dev_packed_step_peer(src, up, up_rows, down, down_rows, pitch, band_rows,
-                                          dst, r0, k, width, k, es))
+        check(step_peer(src, up, up_rows, down, down_rows, pitch, band_rows, dst, r0, k, width,
+                        k, es))
     if edge_stream is not None:
         main.wait_stream(edge_stream)
 
@@ -505,7 +575,7 @@ def neighbour_token(token: torch.Tensor, inbox: torch.Tensor, rank: int, world: 
         w.wait()
 
 
-class PeerBandDriver:
+class PeerBandDriver(PairLayout):
     """One rank's band for the fused NVLink halo (see above).
 
     `sync` orders passes across ranks: "neighbour" (default with NCCL) -- a
@@ -560,7 +630,13 @@ class PeerBandDriver:
         self.profile = profile
         self._events = []  # (start, interior done, pass done, barrier done) per pass
 
+    def _band_raw(self) -> torch.Tensor:
+        return self.buf[self.cur].tensor
+
     def band(self) -> torch.Tensor:
+        """This rank's band in the plain packed layout (converted in place
+        after the last pass's barrier, so no neighbour still reads it)."""
+        self._to_plain()
         return self.buf[self.cur].tensor
 
     def barrier(self) -> None:
@@ -579,12 +655,15 @@ class PeerBandDriver:
         peer_pass(g.width, self.buf[c].ptr.value, self.up_ptrs[c], self.up_rows,
                   self.down_ptrs[c], self.down_rows, g.pitch, g.band_rows,
                   self.buf[c ^ 1].ptr.value, k, self.device, self.edge_stream,
-                  interior_done=interior_done)
+                  interior_done=interior_done, pair=g.pair)
 
     def pass_(self, k: int) -> None:
         g = self.geo
         if not 1 <= k <= g.depth:
             raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
+        if g.pair and not self.in_pair:
+            raise ConfigError("band in the plain layout: pair-layout passes start through run() "
+                              "(conversion, then a barrier with the neighbours)")
         if self.profile:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
@@ -619,11 +698,13 @@ class PeerBandDriver:
 
     def run(self, generations: int, on_pass: Optional[Callable[[int], None]] = None,
             checkpoints: Sequence[int] = ()) -> list[int]:
+        self._to_pair()  # before the barrier: the neighbours read this band in that layout
         self.barrier()  # every rank's initial band is in place
         return run_schedule(self, generations, checkpoints, on_pass)
 
     def init_random(self, density: float, seed: int) -> None:
         g = self.geo
+        self.in_pair = False
         stream = torch.cuda.current_stream(self.device).cuda_stream
         check(capi.lib().life_dev_packed_random(self.band().data_ptr(), g.pitch, g.width, g.y0,
                                                 g.band_rows, density, seed, stream))
@@ -632,6 +713,7 @@ class PeerBandDriver:
     def load_rows(self, words) -> None:
         g = self.geo
         src = torch.from_numpy(words[g.y0:g.y1].view("int32").copy())
+        self.in_pair = False
         self.band()[:, :src.shape[1]].copy_(src)
         self.generations = 0
 
@@ -639,7 +721,7 @@ class PeerBandDriver:
         g = self.geo
         acc = torch.zeros(1, dtype=torch.int64, device=self.device)
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        check(capi.lib().life_dev_packed_population(self.band().data_ptr(), g.pitch, g.width,
+        check(capi.lib().life_dev_packed_population(self._band_raw().data_ptr(), g.pitch, g.width,
                                                     g.band_rows, acc.data_ptr(), stream))
         dist.all_reduce(acc, group=self.group)
         return int(acc.item())
@@ -659,10 +741,13 @@ class LocalPeerBands:
     peers): exercises the in-kernel cross-band row addressing with no
     cross-GPU waits."""
 
-    def __init__(self, width: int, height: int, parts: int, depth: int, device: torch.device):
+    def __init__(self, width: int, height: int, parts: int, depth: int, device: torch.device,
+                 pair: bool = False):
         if parts < 2:
             raise ConfigError("LocalPeerBands needs at least two bands")
-        self.geos = [make_geometry(width, height, r, parts, depth) for r in range(parts)]
+        self.geos = [make_geometry(width, height, r, parts, depth, pair) for r in range(parts)]
+        self.pair = pair
+        self.in_pair = False
         self.device = device
         self.bufs = [[torch.zeros((g.band_rows, g.pitch), dtype=torch.int32, device=device)
                       for _ in range(2)] for g in self.geos]
@@ -671,19 +756,30 @@ class LocalPeerBands:
 
     def init_random(self, density: float, seed: int) -> None:
         stream = torch.cuda.current_stream(self.device).cuda_stream
+        self.in_pair = False
         for g, b in zip(self.geos, self.bufs):
             check(capi.lib().life_dev_packed_random(b[self.cur].data_ptr(), g.pitch, g.width, g.y0,
                                                     g.band_rows, density, seed, stream))
 
+    def _zip(self, to_pair: bool) -> None:
+        stream = torch.cuda.current_stream(self.device).cuda_stream
+        for g, b in zip(self.geos, self.bufs):
+            check(capi.lib().life_dev_packed_zip(b[self.cur].data_ptr(), g.pitch, g.width, 0,
+                                                 g.band_rows, 1 if to_pair else 0, stream))
+        self.in_pair = to_pair
+
     def pass_(self, k: int) -> None:
         p = len(self.geos)
+        if self.pair and not self.in_pair:
+            self._zip(True)
         c = self.cur
         for r, g in enumerate(self.geos):
             up, down = (r - 1) % p, (r + 1) % p
             peer_pass(g.width, self.bufs[r][c].data_ptr(), self.bufs[up][c].data_ptr(),
                       self.geos[up].band_rows, self.bufs[down][c].data_ptr(),
                       self.geos[down].band_rows, g.pitch, g.band_rows,
-                      self.bufs[r][c ^ 1].data_ptr(), k, self.device, self.edge_stream)
+                      self.bufs[r][c ^ 1].data_ptr(), k, self.device, self.edge_stream,
+                      pair=self.pair)
         self.cur ^= 1
 
     def run(self, generations: int) -> None:
@@ -695,4 +791,7 @@ class LocalPeerBands:
             done += k
 
     def gather(self) -> torch.Tensor:
+        """The whole torus as packed uint32 rows (device), plain layout."""
+        if self.in_pair:
+            self._zip(False)
         return torch.cat([b[self.cur] for b in self.bufs], dim=0)

@@ -26,6 +26,7 @@ ENGINE_PACKED = 0
 ENGINE_BYTE = 1
 ENGINE_RESIDENT = 2
 MAX_TEMPORAL_DEPTH = 16
+PAIR_MAX_DEPTH = 12  # packed_pair_kernel<K> (W % 64 == 0)
 MAX_BYTE_DEPTH = 8
 
 OPT_PROFILE = 1
@@ -94,6 +95,14 @@ SIGNATURES = [
                                        _vp]),
     ("life_dev_packed_step_peer", C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64,
                                             _i64, _i64, _i32, _vp]),
+    ("life_pair_auto_depth", C.c_int, [_i64, _i64]),
+    ("life_dev_packed_zip", C.c_int, [_vp, _i64, _i64, _i64, _i64, _i32, _vp]),
+    ("life_dev_packed_step_pair", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64,
+                                            _i32, _vp]),
+    ("life_dev_packed_run_pair", C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32,
+                                           C.POINTER(_i32), _vp]),
+    ("life_dev_packed_step_pair_peer", C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp,
+                                                 _i64, _i64, _i64, _i32, _vp]),
     ("life_dev_packed_run_resident", C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     ("life_resident_cluster_size", C.c_int, [_i64, _i64]),
     ("life_dev_alloc", C.c_int, [_i64, C.POINTER(_vp)]),

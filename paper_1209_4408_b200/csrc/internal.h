@@ -104,6 +104,9 @@ int packed_pair_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_row
                           int64_t width, int32_t generations, cudaStream_t stream);
 int packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
                bool unzip, cudaStream_t stream);
+// temporal_depth 0: the pair kernel's depth for a W-wide torus (or band) of
+// `height` rows, 0 = keep the plain-layout kernels (exported as life_pair_auto_depth).
+int pair_auto_depth(int64_t width, int64_t height);
 
 // Small kernels the multi-device context launches on band buffers.
 int launch_mask_tail(uint32_t* words, int64_t pitch, int64_t width, int64_t rows,

@@ -567,6 +567,41 @@ int life_dev_packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t
   return LIFE_OK;
 }
 
+int life_dev_packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
+                        int32_t to_pair, void* stream) {
+  return packed_zip(words, pitch, width, row0, rows, /*unzip=*/to_pair == 0,
+                    static_cast<cudaStream_t>(stream));
+}
+
+int life_dev_packed_step_pair(const uint32_t* in, int64_t in_pitch, int64_t in_row0,
+                              int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0,
+                              int64_t width, int64_t out_rows, int32_t generations, void* stream) {
+  return packed_pair_step(in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
+                          out_rows, generations, static_cast<cudaStream_t>(stream));
+}
+
+int life_dev_packed_run_pair(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width,
+                             int64_t height, int64_t generations, int32_t depth,
+                             int32_t* result_in_b, void* stream) {
+  if (!pair_eligible(width))
+    return set_error(LIFE_ERR_CONFIG, "the pair layout needs W %% 64 == 0, got %lld",
+                     static_cast<long long>(width));
+  int flip = 0;
+  LIFE_TRY(packed_run(buf_a, buf_b, pitch, width, height, generations, depth,
+                      static_cast<cudaStream_t>(stream), nullptr, &flip, /*pair=*/true));
+  if (result_in_b) *result_in_b = flip;
+  return LIFE_OK;
+}
+
+int life_dev_packed_step_pair_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
+                                   const uint32_t* down, int64_t down_rows, int64_t pitch,
+                                   int64_t band_rows, uint32_t* out, int64_t out_row0,
+                                   int64_t out_rows, int64_t width, int32_t generations,
+                                   void* stream) {
+  return packed_pair_step_peer(in, up, up_rows, down, down_rows, pitch, band_rows, out, out_row0,
+                               out_rows, width, generations, static_cast<cudaStream_t>(stream));
+}
+
 int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
                               const uint32_t* down, int64_t down_rows, int64_t pitch,
                               int64_t band_rows, uint32_t* out, int64_t out_row0,
@@ -1211,13 +1246,6 @@ constexpr int64_t kResidentAutoCells = int64_t(1) << 22;
 // 8.1 / 8.8 / 8.1.)
 int byte_auto_depth(int64_t w, int64_t h) { return w * h >= (int64_t(1) << 26) ? 8 : 4; }
 
-// temporal_depth 0 on W % 64 == 0 tori: the interleaved-pair kernel at this
-// depth (0: keep the plain-layout kernels).
-int pair_auto_depth(int64_t w, int64_t h) {
-  if (!pair_eligible(w)) return 0;
-  return w * h >= (int64_t(1) << 30) ? 10 : 0;
-}
-
 bool resident_auto(int64_t w, int64_t h) {
   return w % 32 == 0 && w * h <= kResidentAutoCells && life_resident_cluster_size(w, h) > 0;
 }
@@ -1228,6 +1256,13 @@ bool resident_auto(int64_t w, int64_t h) {
 // passes run as one all-paths launch (W % 32 != 0, less than ~3 block waves
 // deep), where K = 12 fits 12 warps per SM instead of 8 (config 4: 37.5 ->
 // 38.6 T/s; kbench depth sweep).
+// temporal_depth 0 on W % 64 == 0 tori (or row bands of them, h rows tall):
+// the interleaved-pair kernel at this depth (0: keep the plain-layout kernels).
+int lifegpu::detail::pair_auto_depth(int64_t w, int64_t h) {
+  if (!pair_eligible(w)) return 0;
+  return w * h >= (int64_t(1) << 30) ? 10 : 0;
+}
+
 int lifegpu::detail::packed_auto_depth(int64_t w, int64_t h) {
   const int64_t strips = ceil_div(nw32(w) + 1, kStripStride);
   return (w % 32 != 0 && strips * h < 2000000) ? 12 : LIFE_MAX_TEMPORAL_DEPTH;
@@ -1238,6 +1273,11 @@ extern "C" {
 int life_packed_auto_depth(int64_t width, int64_t height) {
   if (width < 1 || height < 1) return LIFE_MAX_TEMPORAL_DEPTH;
   return packed_auto_depth(width, height);
+}
+
+int life_pair_auto_depth(int64_t width, int64_t height) {
+  if (width < 1 || height < 1) return 0;
+  return pair_auto_depth(width, height);
 }
 
 int life_packed_launch_kind(int64_t width, int64_t out_rows, int32_t generations) {
@@ -1823,8 +1863,8 @@ namespace {
 // download (8 GiB each at config 5) are exposed.  The first and last grid of
 // a batch are instead cut into kTrapChunks row chunks.  Chunk c's TRAPEZOID
 // runs all P passes on its own rows only, pass p producing the rows
-// [start + kShrink*(p+1), end - kShrink*(p+1)) (each pass loses at most
-// kShrink = 16 >= K rows per side of valid data), so it starts as soon as
+// [start + kShrink*(p+1), end - kShrink*(p+1)) (each pass loses kShrink = K,
+// the pass depth, rows per side of valid data), so it starts as soon as
 // chunk c has arrived and its interior can leave as soon as it is done.  The
 // TRIANGLE at the boundary row B between chunks c-1 and c then runs the P
 // passes on [B - kShrink*(p+1), B + kShrink*(p+1)), reading the trapezoids'
@@ -1841,11 +1881,11 @@ constexpr int kTrapChunks = LIFE_TRAP_CHUNKS;
 #define LIFE_TRAP_MIN_ROWS 8192
 #endif
 constexpr int64_t kTrapMinChunkRows = LIFE_TRAP_MIN_ROWS;
-constexpr int64_t kShrink = 16;
 
 struct BatchGeom {
   int64_t width, height, wpr, words_per_row, pitch, generations;
   int depth, passes;
+  bool pair;  // passes on the interleaved-pair layout (zip after upload, unzip before download)
   int64_t bounds[kTrapChunks + 1];
 };
 
@@ -1857,8 +1897,27 @@ int pass_rows(const BatchGeom& g, uint32_t* const* buf, int p, int64_t r0, int64
   if (r0 < 0) r0 += g.height;
   while (rows > 0) {
     const int64_t piece = std::min(rows, g.height - r0);
-    LIFE_TRY(packed_step(buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch, r0,
-                         g.width, piece, k, s, ss));
+    if (g.pair) {
+      LIFE_TRY(packed_pair_step(buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch, r0,
+                                g.width, piece, k, s));
+    } else {
+      LIFE_TRY(packed_step(buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch, r0,
+                           g.width, piece, k, s, ss));
+    }
+    rows -= piece;
+    r0 = 0;
+  }
+  return LIFE_OK;
+}
+
+// Layout conversion of rows [r0, r0 + rows) (mod H) of a batch buffer.
+int zip_rows(const BatchGeom& g, uint32_t* buf, int64_t r0, int64_t rows, bool unzip,
+             cudaStream_t s) {
+  r0 %= g.height;
+  if (r0 < 0) r0 += g.height;
+  while (rows > 0) {
+    const int64_t piece = std::min(rows, g.height - r0);
+    LIFE_TRY(packed_zip(buf, g.pitch, g.width, r0, piece, unzip, s));
     rows -= piece;
     r0 = 0;
   }
@@ -1904,6 +1963,19 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   if (depth < 1 || depth > LIFE_MAX_TEMPORAL_DEPTH)
     return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [0, %d], got %d",
                      LIFE_MAX_TEMPORAL_DEPTH, temporal_depth);
+  // temporal_depth 0 on a small W % 32 == 0 torus: the cluster-resident engine
+  // (as life_run's auto mode), one launch per grid.
+  const bool resident = temporal_depth == 0 && resident_auto(width, height);
+  // Interleaved-pair kernel (W % 64 == 0), chosen as in life_run: the grids are
+  // converted on the device after their upload and before their download.
+  int pair = 0;
+  if (!resident && pair_eligible(width) && generations > 0) {
+    if (c->pair_depth > 0)
+      pair = c->pair_depth;
+    else if (c->pair_depth < 0 && temporal_depth == 0)
+      pair = pair_auto_depth(width, height);
+    if (pair > 0) depth = pair;
+  }
   const int64_t wpr = ceil_div(width, 64);
   if (words_per_row < wpr) return set_error(LIFE_ERR_CONFIG, "words_per_row < ceil(W/64)");
   if (n == 0) return LIFE_OK;
@@ -1933,6 +2005,7 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   g.pitch = pitch;
   g.generations = generations;
   g.depth = depth;
+  g.pair = pair > 0;
   g.passes = static_cast<int>(ceil_div(generations, depth));
   // Chunked first/last grid when every chunk outlives its shrinking
   // trapezoid with room to spare and the chunks are tall enough for their
@@ -1940,12 +2013,10 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   // per pass): measured e2e / device value, 3 grids, with / without it:
   // config 5 (16384-row chunks) 0.965 / 0.882, config 3 (4096-row chunks)
   // 0.850 / 0.945.  LIFE_OPT_BATCH_TRAPEZOID 0 / 1 forces it off / on (when it fits).
+  const int64_t kShrink = depth;  // rows per side a pass gives up
   const int trap_env = c->batch_trap;
   const bool fits = n >= 1 && generations > 0 &&
                     height / kTrapChunks >= 2 * kShrink * g.passes + 1024;
-  // temporal_depth 0 on a small W % 32 == 0 torus: the cluster-resident engine
-  // (as life_run's auto mode), one launch per grid.
-  const bool resident = temporal_depth == 0 && resident_auto(width, height);
   const bool trap = !resident && fits &&
                     (trap_env == 1 || (trap_env != 0 && height / kTrapChunks >= kTrapMinChunkRows));
   if (trap) {
@@ -2005,7 +2076,9 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
         rc = life_dev_packed_run_resident(buf[0], buf[1], pitch, width, height, generations,
                                           c->stream);
       } else {
+        if (g.pair) LIFE_TRY(zip_rows(g, buf[0], 0, height, /*unzip=*/false, c->stream));
         for (int p = 0; p < P && rc == LIFE_OK; ++p) rc = pass_rows(g, buf, p, 0, height, c->stream, &c->split[0]);
+        if (g.pair && rc == LIFE_OK) rc = zip_rows(g, buf[P & 1], 0, height, /*unzip=*/true, c->stream);
       }
       LIFE_CUDA(cudaEventRecord(comp[i], c->stream));
       // Download on the D2H stream.
@@ -2034,9 +2107,15 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
       packed_mask_tail_kernel<<<grid_stride_blocks(mask_n, 256), 256, 0, st>>>(
           buf[0] + y0 * pitch, pitch, nw, tail_mask(width), rows);
       LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
+      if (g.pair) LIFE_TRY(zip_rows(g, buf[0], y0, rows, /*unzip=*/false, st));
       for (int p = 0; p < P && rc == LIFE_OK; ++p)
         rc = pass_rows(g, buf, p, y0 + kShrink * (p + 1), rows - 2 * kShrink * (p + 1), st,
                        &c->split[1 + ch % 2]);
+      // The interior leaves in the plain layout; the triangles never read
+      // these rows of the final buffer (their last read of it, pass P-2,
+      // stays within kShrink * P rows of the boundary).
+      if (g.pair && rc == LIFE_OK)
+        rc = zip_rows(g, buf[P & 1], y0 + shrink, rows - 2 * shrink, /*unzip=*/true, st);
       LIFE_CUDA(cudaEventRecord(trap_done[ch], st));
     }
     // Triangles at boundary b (row bounds[b]) between chunks b-1 and b.
@@ -2048,6 +2127,8 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
       for (int p = 0; p < P && rc == LIFE_OK; ++p)
         rc = pass_rows(g, buf, p, g.bounds[b] - kShrink * (p + 1), 2 * kShrink * (p + 1), st,
                        &c->split[3 + bi % 2]);
+      if (g.pair && rc == LIFE_OK)
+        rc = zip_rows(g, buf[P & 1], g.bounds[b] - shrink, 2 * shrink, /*unzip=*/true, st);
       LIFE_CUDA(cudaEventRecord(tri_done[b], st));
     }
     // Downloads: each chunk's interior when its trapezoid is done, then the

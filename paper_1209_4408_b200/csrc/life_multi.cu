@@ -79,6 +79,11 @@ struct MultiState {
   bool loaded = false;
   int64_t W = 0, H = 0, pitch = 0;
   int cur = 0;
+  // The resident bands buf[cur] are in the interleaved-pair layout
+  // (kernels_pair.cuh): left so by multi_run between runs; every reader of
+  // the plain layout calls to_plain() first.
+  bool pair = false;
+  int pair_depth = -1;  // LIFE_OPT_PAIR_DEPTH
   int64_t batch_bytes_total = 0;
 };
 
@@ -149,6 +154,7 @@ int set_dims(MultiState* m, int64_t w, int64_t h) {
     }
   }
   m->cur = 0;
+  m->pair = false;
   return LIFE_OK;
 }
 
@@ -182,6 +188,26 @@ int check_loaded(const MultiState* m) {
 
 // Rows [r0, r0 + rows) of a packed host grid (uint64 rows of wpr words)
 // <-> the same rows of band buffer `dev` (pitch words), on stream s.
+// Layout conversion of the resident bands, in place on each band's stream.
+int to_plain(MultiState* m) {
+  if (!m->pair) return LIFE_OK;
+  for (Band& b : m->bands) {
+    LIFE_TRY(use(b));
+    LIFE_TRY(packed_zip(b.buf[m->cur], m->pitch, m->W, 0, b.rows, /*unzip=*/true, b.main));
+  }
+  m->pair = false;
+  return LIFE_OK;
+}
+int to_pair(MultiState* m) {
+  if (m->pair) return LIFE_OK;
+  for (Band& b : m->bands) {
+    LIFE_TRY(use(b));
+    LIFE_TRY(packed_zip(b.buf[m->cur], m->pitch, m->W, 0, b.rows, /*unzip=*/false, b.main));
+  }
+  m->pair = true;
+  return LIFE_OK;
+}
+
 int copy_band_rows(const MultiState* m, void* host, int64_t words_per_row, uint32_t* dev,
                    int64_t rows, bool h2d, cudaStream_t s) {
   const int64_t wpr = ceil_div(m->W, 64);
@@ -199,7 +225,25 @@ int copy_band_rows(const MultiState* m, void* host, int64_t words_per_row, uint3
 // One pass of depth k (the previous pass had depth kprev; 0 = none) over every
 // band: src[b] -> dst[b].  Pass index p selects the event slots.
 int issue_pass(MultiState* m, uint32_t* const* src, uint32_t* const* dst, int64_t p, int k,
-               int kprev) {
+               int kprev, bool pair) {
+  // One torus / interior launch and one edge-strip launch on either layout.
+  auto step = [&](const uint32_t* in, int64_t in_row0, int64_t in_rows, uint32_t* out,
+                  int64_t out_rows, cudaStream_t s, SplitStreams* ss) -> int {
+    if (pair)
+      return packed_pair_step(in, m->pitch, in_row0, in_rows, out, m->pitch, in_row0, m->W,
+                              out_rows, k, s);
+    return packed_step(in, m->pitch, in_row0, in_rows, out, m->pitch, in_row0, m->W, out_rows, k,
+                       s, ss);
+  };
+  auto step_peer = [&](const uint32_t* in, const uint32_t* up, int64_t up_rows,
+                       const uint32_t* down, int64_t down_rows, int64_t band_rows, uint32_t* out,
+                       int64_t out_row0, int64_t out_rows, cudaStream_t s) -> int {
+    if (pair)
+      return packed_pair_step_peer(in, up, up_rows, down, down_rows, m->pitch, band_rows, out,
+                                   out_row0, out_rows, m->W, k, s);
+    return life_dev_packed_step_peer(in, up, up_rows, down, down_rows, m->pitch, band_rows, out,
+                                     out_row0, out_rows, m->W, k, static_cast<void*>(s));
+  };
   const int n = nbands(m);
   const int now = static_cast<int>(p & 1), prev = now ^ 1;
   auto prof_event = [&](std::vector<cudaEvent_t>& v, cudaStream_t s) -> int {
@@ -213,8 +257,7 @@ int issue_pass(MultiState* m, uint32_t* const* src, uint32_t* const* dst, int64_
     Band& b = m->bands[0];
     LIFE_TRY(use(b));
     if (m->profile) LIFE_TRY(prof_event(b.prof_int, b.main));
-    LIFE_TRY(packed_step(src[0], m->pitch, 0, b.rows, dst[0], m->pitch, 0, m->W, b.rows, k, b.main,
-                         &b.split));
+    LIFE_TRY(step(src[0], 0, b.rows, dst[0], b.rows, b.main, &b.split));
     if (m->profile) LIFE_TRY(prof_event(b.prof_int, b.main));
     LIFE_CUDA(cudaEventRecord(b.ev_int[now], b.main));
     LIFE_CUDA(cudaEventRecord(b.ev_edge[now], b.main));
@@ -232,8 +275,7 @@ int issue_pass(MultiState* m, uint32_t* const* src, uint32_t* const* dst, int64_
     }
     if (b.rows > 2 * k) {
       if (m->profile) LIFE_TRY(prof_event(b.prof_int, b.main));
-      LIFE_TRY(packed_step(src[i], m->pitch, k, b.rows, dst[i], m->pitch, k, m->W, b.rows - 2 * k,
-                           k, b.main, &b.split));
+      LIFE_TRY(step(src[i], k, b.rows, dst[i], b.rows - 2 * k, b.main, &b.split));
       if (m->profile) LIFE_TRY(prof_event(b.prof_int, b.main));
     }
     LIFE_CUDA(cudaEventRecord(b.ev_int[now], b.main));
@@ -264,15 +306,12 @@ int issue_pass(MultiState* m, uint32_t* const* src, uint32_t* const* dst, int64_
       down = b.ghost[1];
       up_rows = down_rows = k;
     }
-    void* es = static_cast<void*>(b.edge);
     if (b.rows > 2 * k) {
-      LIFE_TRY(life_dev_packed_step_peer(src[i], up, up_rows, down, down_rows, m->pitch, b.rows,
-                                         dst[i], 0, k, m->W, k, es));
-      LIFE_TRY(life_dev_packed_step_peer(src[i], up, up_rows, down, down_rows, m->pitch, b.rows,
-                                         dst[i], b.rows - k, k, m->W, k, es));
+      LIFE_TRY(step_peer(src[i], up, up_rows, down, down_rows, b.rows, dst[i], 0, k, b.edge));
+      LIFE_TRY(step_peer(src[i], up, up_rows, down, down_rows, b.rows, dst[i], b.rows - k, k,
+                         b.edge));
     } else {
-      LIFE_TRY(life_dev_packed_step_peer(src[i], up, up_rows, down, down_rows, m->pitch, b.rows,
-                                         dst[i], 0, b.rows, m->W, k, es));
+      LIFE_TRY(step_peer(src[i], up, up_rows, down, down_rows, b.rows, dst[i], 0, b.rows, b.edge));
     }
     if (m->profile) LIFE_TRY(prof_event(b.prof_edge, b.edge));
     LIFE_CUDA(cudaEventRecord(b.ev_edge[now], b.edge));
@@ -328,7 +367,7 @@ int check_packed_engine(int engine) {
 
 // Depth of a run: the auto rule on the tallest band, capped by the thinnest
 // band (a band feeds its neighbours K rows per pass).
-int run_depth(const MultiState* m, int temporal_depth, int* depth) {
+int run_depth(const MultiState* m, int temporal_depth, int* depth, bool* pair) {
   if (temporal_depth < 0 || temporal_depth > LIFE_MAX_TEMPORAL_DEPTH)
     return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [0, %d], got %d",
                      LIFE_MAX_TEMPORAL_DEPTH, temporal_depth);
@@ -338,8 +377,19 @@ int run_depth(const MultiState* m, int temporal_depth, int* depth) {
     max_rows = std::max(max_rows, b.rows);
   }
   int k = temporal_depth == 0 ? packed_auto_depth(m->W, max_rows) : temporal_depth;
+  // Interleaved-pair kernel (W % 64 == 0), chosen as in life_run: forced by
+  // LIFE_OPT_PAIR_DEPTH, or the auto rule on the tallest band.
+  int pk = 0;
+  if (pair_eligible(m->W)) {
+    if (m->pair_depth > 0)
+      pk = m->pair_depth;
+    else if (m->pair_depth < 0 && temporal_depth == 0)
+      pk = pair_auto_depth(m->W, max_rows);
+  }
+  if (pk > 0) k = pk;
   if (nbands(m) > 1) k = static_cast<int>(std::min<int64_t>(k, min_rows));
   *depth = std::max(k, 1);
+  *pair = pk > 0;
   return LIFE_OK;
 }
 
@@ -447,6 +497,12 @@ int multi_set_option(MultiState* m, int option, int64_t value) {
       return LIFE_OK;
     case LIFE_OPT_BATCH_TRAPEZOID:
       return LIFE_OK;  // the multi-device batch has no chunk schedule
+    case LIFE_OPT_PAIR_DEPTH:
+      if (value < -1 || value > kPairMaxDepthHost)
+        return set_error(LIFE_ERR_CONFIG, "LIFE_OPT_PAIR_DEPTH must be in [-1, %d]",
+                         kPairMaxDepthHost);
+      m->pair_depth = static_cast<int>(value);
+      return LIFE_OK;
     default:
       return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
   }
@@ -457,6 +513,7 @@ int multi_get_option(MultiState* m, int option, int64_t* value) {
     case LIFE_OPT_PROFILE: *value = m->profile ? 1 : 0; return LIFE_OK;
     case LIFE_OPT_HALO: *value = m->halo; return LIFE_OK;
     case LIFE_OPT_BATCH_TRAPEZOID: *value = 0; return LIFE_OK;
+    case LIFE_OPT_PAIR_DEPTH: *value = m->pair_depth; return LIFE_OK;
     default: return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
   }
 }
@@ -508,6 +565,7 @@ int multi_upload_packed(MultiState* m, const uint64_t* words, int64_t w, int64_t
   LIFE_TRY(set_dims(m, w, h));
   if (wpr < ceil_div(w, 64)) return set_error(LIFE_ERR_CONFIG, "words_per_row < ceil(W/64)");
   m->cur = 0;
+  m->pair = false;
   for (Band& b : m->bands) {
     LIFE_TRY(use(b));
     LIFE_TRY(copy_band_rows(m, const_cast<uint64_t*>(words) + b.y0 * wpr, wpr, b.buf[0], b.rows,
@@ -526,6 +584,7 @@ int multi_upload_u8(MultiState* m, const uint8_t* cells, int64_t w, int64_t h, i
   const int64_t bp = life_byte_pitch(w);
   const int64_t chunk = std::max<int64_t>(1, kScratchBytes / bp);
   m->cur = 0;
+  m->pair = false;
   for (Band& b : m->bands) {
     LIFE_TRY(use(b));
     LIFE_TRY(ensure_scratch(b, std::min(chunk, b.rows) * bp));
@@ -547,6 +606,7 @@ int multi_init_random(MultiState* m, int64_t w, int64_t h, double density, uint6
     return set_error(LIFE_ERR_CONFIG, "density must be in [0, 1], got %f", density);
   LIFE_TRY(set_dims(m, w, h));
   m->cur = 0;
+  m->pair = false;
   for (Band& b : m->bands) {  // band rows y0.. of random_fill's row-major stream
     LIFE_TRY(use(b));
     LIFE_TRY(life_dev_packed_random(b.buf[0], m->pitch, w, b.y0, b.rows, density, seed, b.main));
@@ -580,6 +640,7 @@ int multi_init_soup(MultiState* m, int64_t w, int64_t h, double coverage, int32_
 int multi_place_u8(MultiState* m, const uint8_t* pattern, int64_t pw, int64_t ph, int64_t x0,
                    int64_t y0) {
   LIFE_TRY(check_loaded(m));
+  LIFE_TRY(to_plain(m));
   if (pw < 0 || ph < 0 || (pw * ph > 0 && !pattern))
     return set_error(LIFE_ERR_CONFIG, "bad pattern buffer");
   if (x0 < 0 || y0 < 0 || x0 + pw > m->W || y0 + ph > m->H)
@@ -606,6 +667,7 @@ int multi_place_u8(MultiState* m, const uint8_t* pattern, int64_t pw, int64_t ph
 
 int multi_download_packed(MultiState* m, uint64_t* words, int64_t wpr) {
   LIFE_TRY(check_loaded(m));
+  LIFE_TRY(to_plain(m));
   if (!words || wpr < ceil_div(m->W, 64)) return set_error(LIFE_ERR_CONFIG, "bad output buffer");
   for (Band& b : m->bands) {
     LIFE_TRY(use(b));
@@ -616,6 +678,7 @@ int multi_download_packed(MultiState* m, uint64_t* words, int64_t wpr) {
 
 int multi_download_u8(MultiState* m, uint8_t* cells, int64_t stride) {
   LIFE_TRY(check_loaded(m));
+  LIFE_TRY(to_plain(m));
   if (!cells || stride < m->W) return set_error(LIFE_ERR_CONFIG, "bad output buffer");
   const int64_t bp = life_byte_pitch(m->W);
   const int64_t chunk = std::max<int64_t>(1, kScratchBytes / bp);
@@ -635,6 +698,7 @@ int multi_download_u8(MultiState* m, uint8_t* cells, int64_t stride) {
 
 int multi_window_u8(MultiState* m, int64_t x0, int64_t y0, int64_t w, int64_t h, uint8_t* out) {
   LIFE_TRY(check_loaded(m));
+  LIFE_TRY(to_plain(m));
   if (w < 0 || h < 0 || !out) return set_error(LIFE_ERR_CONFIG, "bad window");
   if (w * h == 0) return LIFE_OK;
   // Window rows j map to torus row (y0 + j) mod H; cut them into runs that
@@ -682,6 +746,7 @@ int multi_population(MultiState* m, uint64_t* out) {
 
 int multi_hash(MultiState* m, uint64_t* out) {
   LIFE_TRY(check_loaded(m));
+  LIFE_TRY(to_plain(m));
   if (!out) return set_error(LIFE_ERR_CONFIG, "null output pointer");
   std::vector<uint64_t> rows(static_cast<size_t>(m->H));
   for (Band& b : m->bands) {  // row hashes of the bands, concatenated in row order
@@ -709,7 +774,9 @@ int multi_run(MultiState* m, int64_t generations, int engine, int temporal_depth
   LIFE_TRY(check_run_args(generations, checkpoints, n_checkpoints, populations));
   LIFE_TRY(check_loaded(m));
   int depth = 0;
-  LIFE_TRY(run_depth(m, temporal_depth, &depth));
+  bool pair = false;
+  LIFE_TRY(run_depth(m, temporal_depth, &depth, &pair));
+  if (generations > 0) LIFE_TRY(pair ? to_pair(m) : to_plain(m));
   if (m->halo == LIFE_HALO_COPY) LIFE_TRY(ensure_ghosts(m));
   const int n = nbands(m);
   for (Band& b : m->bands) {
@@ -749,7 +816,7 @@ int multi_run(MultiState* m, int64_t generations, int engine, int temporal_depth
       src[i] = m->bands[i].buf[m->cur];
       dst[i] = m->bands[i].buf[m->cur ^ 1];
     }
-    LIFE_TRY(issue_pass(m, src.data(), dst.data(), p, k, kprev));
+    LIFE_TRY(issue_pass(m, src.data(), dst.data(), p, k, kprev, m->pair));
     m->cur ^= 1;
     done += k;
     kprev = k;
@@ -801,7 +868,9 @@ int multi_run_batch(MultiState* m, const uint64_t* const* inputs, uint64_t* cons
     return set_error(LIFE_ERR_CONFIG, "words_per_row < ceil(W/64)");
   LIFE_TRY(set_dims(m, width, height));  // band layout (the resident grid is not used)
   int depth = 0;
-  LIFE_TRY(run_depth(m, temporal_depth, &depth));
+  bool pair = false;
+  LIFE_TRY(run_depth(m, temporal_depth, &depth, &pair));
+  if (generations == 0) pair = false;
   if (n == 0) return LIFE_OK;
   if (m->halo == LIFE_HALO_COPY) LIFE_TRY(ensure_ghosts(m));
   const int nb = nbands(m);
@@ -868,6 +937,9 @@ int multi_run_batch(MultiState* m, const uint64_t* const* inputs, uint64_t* cons
       LIFE_TRY(copy_band_rows(m, const_cast<uint64_t*>(inputs[i]) + bd.y0 * words_per_row,
                               words_per_row, bd.batch[2 * slot], bd.rows, true, bd.h2d));
       LIFE_TRY(launch_mask_tail(bd.batch[2 * slot], m->pitch, width, bd.rows, bd.h2d));
+      if (pair)  // the band's rows into the interleaved-pair layout, behind their copy
+        LIFE_TRY(packed_zip(bd.batch[2 * slot], m->pitch, width, 0, bd.rows, /*unzip=*/false,
+                            bd.h2d));
       LIFE_CUDA(cudaEventRecord(up[b][i], bd.h2d));
     }
     // Every band's compute and edge streams start grid i once the band and
@@ -889,7 +961,7 @@ int multi_run_batch(MultiState* m, const uint64_t* const* inputs, uint64_t* cons
         src[b] = m->bands[b].batch[2 * slot + (p & 1)];
         dst[b] = m->bands[b].batch[2 * slot + ((p & 1) ^ 1)];
       }
-      LIFE_TRY(issue_pass(m, src.data(), dst.data(), p_global, k, kprev));
+      LIFE_TRY(issue_pass(m, src.data(), dst.data(), p_global, k, kprev, pair));
       kprev = k;
       ++p_global;
     }
@@ -899,6 +971,9 @@ int multi_run_batch(MultiState* m, const uint64_t* const* inputs, uint64_t* cons
       LIFE_TRY(use(bd));
       LIFE_CUDA(cudaEventRecord(comp[b][i], bd.main));
       LIFE_CUDA(cudaStreamWaitEvent(bd.d2h, comp[b][i], 0));
+      if (pair)  // back to the plain layout (only this band's kernels wrote the result buffer)
+        LIFE_TRY(packed_zip(bd.batch[2 * slot + (passes & 1)], m->pitch, width, 0, bd.rows,
+                            /*unzip=*/true, bd.d2h));
       LIFE_TRY(copy_band_rows(m, outputs[i] + bd.y0 * words_per_row, words_per_row,
                               bd.batch[2 * slot + (passes & 1)], bd.rows, false, bd.d2h));
       LIFE_CUDA(cudaEventRecord(down[b][i], bd.d2h));

@@ -30,6 +30,10 @@ __global__ void k(uint32_t* sink, int iters, uint32_t seed) {
       if (MODE == 8) { if ((j & 3) == 0) MADHI(a, a, m, b); else if ((j & 3) == 1) MAD(a, a, m, b); else L3(a, a, b, c, 0x96); }
       if (MODE == 9) { uint32_t lo; MADW(lo, a, m); a ^= lo; }
       if (MODE == 10) { if (j < 10) L3(a, a, b, c, 0x96); else if (j < 12) { uint32_t lo, t = a; MADW(lo, t, m); a = lo + t; } else MAD(a, a, m, b); }
+      if (MODE == 11) { if (j == 3 || j == 11) { uint32_t lo, t = a; MADW(lo, t, m); a = lo; r[(j + 1) & 15] ^= t; } else if (j == 7) { MAD(a, a, m, b); } else L3(a, a, b, c, 0x96); }
+      if (MODE == 12) { if (j == 3 || j == 11) SHF(a, a, b); else if (j == 7) {} else L3(a, a, b, c, 0x96); }
+      if (MODE == 13) { if (j == 7) {} else L3(a, a, b, c, 0x96); }
+      if (MODE == 14) { if (j == 3 || j == 11) { MADHI(a, a, m, b); } else if (j == 7) { MAD(a, a, m, b); } else L3(a, a, b, c, 0x96); }
       if (MODE == 5) { if ((j & 3) == 0) MAD(a, a, m, b); else L3(a, a, b, c, 0x96); }
     }
   }
@@ -52,7 +56,7 @@ void run(const char* name) {
   cudaEventSynchronize(b);
   float ms; cudaEventElapsedTime(&ms, a, b);
   double ops = double(blocks) * threads * iters * 16;
-  printf("%-22s %8.2f Tops/s (lane-ops)\n", name, ops / ms / 1e9);
+  printf("%-26s %8.2f Tops/s (lane-ops at 16 per iteration) %8.3f ms\n", name, ops / ms / 1e9, ms);
   cudaFree(sink);
 }
 
@@ -65,6 +69,10 @@ int main() {
   run<5>("lop3/imad 3:1");
   run<9>("imad.wide(+lop)");
   run<10>("10lop:2wide:4imad");
+  run<13>("15 lop3 (of 16 slots)");
+  run<12>("13lop:2shf (of 16)");
+  run<11>("13lop+2x(wide+xor):1imad");
+  run<14>("13lop:2imad.hi:1imad");
   run<6>("imad.hi");
   run<7>("lop3/imad.hi 1:1");
   run<8>("lop3:imad:imad.hi 2:1:1");
