@@ -32,23 +32,25 @@ METRIC = "cell-updates/sec (GCUPS) at 1/2/4/8 B200 and % of HBM/int roofline"
 UNIT = "GCUPS"
 OPS_PER_WORD = 11            # bit-sliced rule network (2 SHF + 9 LOP3), csrc/kernels.cuh
 OPS_PER_UPDATE = OPS_PER_WORD / 32.0
-PAIR_OPS_PER_WORD = 10       # interleaved-pair layout (1 SHF + 9 LOP3), csrc/kernels_pair.cuh
-PAIR_OPS_PER_UPDATE = PAIR_OPS_PER_WORD / 32.0
+# interleaved layouts (csrc/kernels_pair.cuh): pair = 1 SHF + 9 LOP3 per word,
+# quad = 2 SHF + 36 LOP3 per 4 words
+IL_OPS_PER_UPDATE = {0: OPS_PER_UPDATE, 2: 10 / 32.0, 4: 9.5 / 32.0}
+IL_NAME = {0: "plain", 2: "interleaved-pair", 4: "interleaved-quad"}
 
 
 def pick_depth(L, args, W: int, rows: int):
-    """(depth, pair) as life_run picks them for `--depth` / `--pair-depth` on
-    a W-wide torus (or band) of `rows` rows: the interleaved-pair kernel when
-    forced, or when both are left to the engine and life_pair_auto_depth says
-    so; else the plain-layout kernels at --depth or life_packed_auto_depth."""
-    pair = 0
-    if W % 64 == 0:
-        if args.pair_depth > 0:
-            pair = args.pair_depth
-        elif args.pair_depth < 0 and args.depth == 0:
-            pair = int(L.life_pair_auto_depth(W, rows))
-    depth = pair or args.depth or int(L.life_packed_auto_depth(W, rows))
-    return depth, bool(pair)
+    """(depth, il) as life_run picks them for `--depth` / `--pair-depth` /
+    `--quad-depth` on a W-wide torus (or band) of `rows` rows
+    (life_interleave_auto: the quad or pair layout when forced, or when
+    everything is left to the engine and the torus is large; else the
+    plain-layout kernels at --depth or life_packed_auto_depth)."""
+    import ctypes as C
+    d = C.c_int32(0)
+    il = int(L.life_interleave_auto(W, rows, args.pair_depth, args.quad_depth, args.depth,
+                                    C.byref(d)))
+    depth = d.value if il else (args.depth or int(L.life_packed_auto_depth(W, rows)))
+    return depth, il
+
 
 CONFIGS = {
     1: dict(w=1024, h=1024, p=0.5, gens=100,
@@ -65,6 +67,14 @@ CONFIGS = {
                  "row bands over the GPUs"),
 }
 L2_BYTES = 126 * 2 ** 20
+
+
+def set_il_options(eng, args) -> None:
+    from paper_1209_4408_b200 import capi
+    if args.pair_depth >= 0:
+        eng.set_option(capi.OPT_PAIR_DEPTH, args.pair_depth)
+    if args.quad_depth >= 0:
+        eng.set_option(capi.OPT_QUAD_DEPTH, args.quad_depth)
 
 
 def measured_peaks() -> dict:
@@ -473,9 +483,9 @@ def run_gpu_arm(args) -> None:
     W, H, gens = cfg["w"], cfg["h"], args.gens or cfg["gens"]
     bounds0 = [H * r // world for r in range(world + 1)]
     band_rows_max = max(b - a for a, b in zip(bounds0, bounds0[1:])) + 1
-    # depth 0: the engine's own auto rule (life_pair_auto_depth / life_packed_auto_depth)
-    depth, pair = pick_depth(L, args, W, H if world == 1 else band_rows_max)
-    ops_per_update = PAIR_OPS_PER_UPDATE if pair else OPS_PER_UPDATE
+    # depth 0: the engine's own auto rule (life_interleave_auto / life_packed_auto_depth)
+    depth, il = pick_depth(L, args, W, H if world == 1 else band_rows_max)
+    ops_per_update = IL_OPS_PER_UPDATE[il]
 
     def barrier():
         if world > 1:
@@ -495,13 +505,13 @@ def run_gpu_arm(args) -> None:
     if L.life_measure_int_peak(local, 4000, C.byref(o), C.byref(s)) == 0:
         int_ops = o.value
 
-    geo = make_geometry(W, H, rank, world, depth, pair)
+    geo = make_geometry(W, H, rank, world, depth, il)
     # Per-launch CUDA events are recorded only in one extra PROFILED step after
     # the timed region (events between launches serialise programmatic
     # dependent launch, so the timed steps carry none).
     launches = []
     from paper_1209_4408_b200.bands import cuda_stepper
-    base_step = cuda_stepper(W, pair)
+    base_step = cuda_stepper(W, il)
     record = {"on": False}
 
     def timed_step(inp, in_row0, in_rows, out, out_row0, out_rows, k):
@@ -653,10 +663,10 @@ def run_gpu_arm(args) -> None:
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     alg_bytes_per_update = 0.25 / depth
     hbm_achieved = kern_cells * alg_bytes_per_update / (kern_ms * 1e-3) / 1e9 if kern_ms else 0.0
-    traffic = ncu_traffic(args.config, depth, "pair" if pair else "")
-    kind = -2 if pair else int(L.life_packed_launch_kind(W, geo.band_rows if world > 1 else H,
-                                                         depth))
-    kname = {-2: f"packed_pair_kernel<{depth}>",
+    traffic = ncu_traffic(args.config, depth, {0: "", 2: "pair", 4: "quad"}[il])
+    kind = -2 if il else int(L.life_packed_launch_kind(W, geo.band_rows if world > 1 else H,
+                                                       depth))
+    kname = {-2: f"packed_il_kernel<{depth}, {il}>",
              capi.LAUNCH_STEP1: "packed_step1_kernel",
              capi.LAUNCH_FAST: f"packed_tb_fast_kernel<{depth}>",
              capi.LAUNCH_ALL_PATHS: f"packed_tb_kernel<{depth}>",
@@ -712,8 +722,7 @@ def run_gpu_arm(args) -> None:
             # memory, runs the generations and downloads the result; step i's
             # copies overlap step i+-1's compute (copy engines).
             eng = Engine(local)
-            if args.pair_depth >= 0:
-                eng.set_option(capi.OPT_PAIR_DEPTH, args.pair_depth)
+            set_il_options(eng, args)
             api_depth = args.depth  # 0: the engine's auto rule (the same choice as `depth`)
             wpr = math.ceil(W / 64)
             host_in = torch.empty((H, wpr), dtype=torch.int64, pin_memory=True)
@@ -790,7 +799,7 @@ def run_gpu_arm(args) -> None:
             "scaling": "strong", "vs_baseline": None,
             "dtype": "u32 bit-sliced (32 cells/word, exact integer)", "data": "synthetic",
             "config": {"workload": cfg["desc"], "width": W, "height": H, "generations": gens,
-                       "temporal_depth": depth, "layout": "interleaved-pair" if pair else "plain",
+                       "temporal_depth": depth, "layout": IL_NAME[il],
                        "global_cells": W * H,
                        "parallelism": f"rowbands{world}" if world > 1 else "single-gpu",
                        "halo": {"peer": "in-kernel NVLink peer reads (CUDA IPC) + "
@@ -910,8 +919,7 @@ def run_ctx_arm(args) -> None:
     int_ops = o.value if L.life_measure_int_peak(devices[0], 4000, C.byref(o), C.byref(s)) == 0 \
         else 0.0
     e = Engine(devices=devices)
-    if args.pair_depth >= 0:
-        e.set_option(capi.OPT_PAIR_DEPTH, args.pair_depth)
+    set_il_options(e, args)
 
     def init():
         if cfg.get("soup"):
@@ -975,8 +983,8 @@ def run_ctx_arm(args) -> None:
                       "every band, run, D2H; copies overlapped with the neighbouring steps)",
                "steps": steps_e2e}
     e.close()
-    eff_depth, pair = pick_depth(L, args, W, max(y - x for x, y in zip(b["bounds"], b["bounds"][1:])))
-    ops_per_update = PAIR_OPS_PER_UPDATE if pair else OPS_PER_UPDATE
+    eff_depth, il = pick_depth(L, args, W, max(y - x for x, y in zip(b["bounds"], b["bounds"][1:])))
+    ops_per_update = IL_OPS_PER_UPDATE[il]
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sum(ms) / args.steps, "higher_is_better": True,
@@ -984,7 +992,7 @@ def run_ctx_arm(args) -> None:
         "dtype": "u32 bit-sliced (32 cells/word, exact integer)", "data": "synthetic",
         "config": {"workload": cfg["desc"], "width": W, "height": H, "generations": gens,
                    "temporal_depth": eff_depth,
-                   "layout": "interleaved-pair" if pair else "plain",
+                   "layout": IL_NAME[il],
                    "parallelism": f"rowbands{n} (one process, "
                    "multi-device C-ABI context)", "devices": devices,
                    "bounds": b["bounds"], "halo": {0: "peer", 1: "copy"}.get(b["halo"], "none"),
@@ -1393,8 +1401,11 @@ def main() -> None:
                     help="generations per packed pass; 0 = the engine's auto rule (16; 12 for "
                          "one-launch W %% 32 != 0 tori such as config 4)")
     ap.add_argument("--pair-depth", type=int, default=-1,
-                    help="interleaved-pair kernel (W %% 64 == 0 tori): -1 = the engine's auto "
+                    help="pair-layout kernel (W %% 64 == 0 tori): -1 = the engine's auto "
                          "rule when --depth is 0 too, 0 = off, 1..12 = forced depth")
+    ap.add_argument("--quad-depth", type=int, default=-1,
+                    help="quad-layout kernel (W %% 128 == 0 tori): -1 = auto, 0 = off, "
+                         "1..6 = forced depth")
     ap.add_argument("--gens", type=int, default=0, help="override the config's generations")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

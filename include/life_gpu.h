@@ -100,7 +100,8 @@ int life_ctx_bands(life_ctx* ctx, int32_t* n, int64_t* bounds, int32_t* devices,
 #define LIFE_OPT_PROFILE 1         /* 1: CUDA events around every pass of life_run (band stats) */
 #define LIFE_OPT_BATCH_TRAPEZOID 2 /* life_run_batch first/last-grid chunk schedule: -1 auto, 0, 1 */
 #define LIFE_OPT_HALO 3            /* multi-device halo scheme: LIFE_HALO_PEER / LIFE_HALO_COPY */
-#define LIFE_OPT_PAIR_DEPTH 4      /* interleaved-pair kernel (W % 64 == 0): -1 auto, 0 off, 1..12 forced depth */
+#define LIFE_OPT_PAIR_DEPTH 4      /* pair-layout kernel (W % 64 == 0): -1 auto, 0 off, 1..12 forced depth */
+#define LIFE_OPT_QUAD_DEPTH 5      /* quad-layout kernel (W % 128 == 0): -1 auto, 0 off, 1..6 forced depth */
 #define LIFE_HALO_PEER 0           /* edge-strip kernels read neighbour rows over NVLink (P2P) */
 #define LIFE_HALO_COPY 1           /* neighbour rows copied into local ghost rows, then computed */
 int life_ctx_set_option(life_ctx* ctx, int32_t option, int64_t value);
@@ -195,11 +196,19 @@ int life_run_batch(life_ctx* ctx, const uint64_t* const* inputs, uint64_t* const
  * engine (16; 12 for W % 32 != 0 tori less than ~3 block waves deep). */
 int life_packed_auto_depth(int64_t width, int64_t height);
 
-/* The depth life_run / life_run_batch use for temporal_depth 0 on the
- * interleaved-pair kernel (packed_pair_kernel<K>: W % 64 == 0 tori of 2^30
- * cells or more, 10 instead of 11 integer ops per 32 cell-updates), or 0 when
- * the plain-layout kernels run (LIFE_OPT_PAIR_DEPTH overrides per context). */
-int life_pair_auto_depth(int64_t width, int64_t height);
+/* The interleaved layout life_run / life_run_batch pick for a W x H packed
+ * torus (or a row band of it), given a context's LIFE_OPT_PAIR_DEPTH and
+ * LIFE_OPT_QUAD_DEPTH values (-1 = the defaults) and the call's
+ * temporal_depth: returns the interleave order -- 4 = the quad layout
+ * (packed_il_kernel<K, 4>: W % 128 == 0, 9.5 integer ops per 32 cell-updates,
+ * K <= 6), 2 = the pair layout (packed_il_kernel<K, 2>: W % 64 == 0, 10 ops,
+ * K <= 12), 0 = the plain-layout kernels (11 ops) -- and writes the pass depth
+ * to *depth (0 with order 0: life_packed_auto_depth applies).  With both
+ * options at -1 and temporal_depth 0, tori of 2^30 cells or more run quad at
+ * K = 6 (W % 128 == 0) or pair at K = 10; an explicit temporal_depth keeps the
+ * plain kernels unless an option forces a layout. */
+int life_interleave_auto(int64_t width, int64_t height, int32_t pair_option, int32_t quad_option,
+                         int32_t temporal_depth, int32_t* depth);
 
 /* Which kernel(s) one torus pass of `generations` over `out_rows` rows of a
  * W-wide packed grid launches (device-buffer layer and life_run alike):
@@ -261,27 +270,29 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
                               int64_t band_rows, uint32_t* out, int64_t out_row0,
                               int64_t out_rows, int64_t width, int32_t generations,
                               void* stream);
-/* ---- the interleaved-pair layout at the device-buffer layer (W % 64 == 0):
- * each uint64 group of a packed row kept as (even columns, odd columns), the
- * layout packed_pair_kernel<K> steps at 10 integer ops per 32 cell-updates.
- * life_dev_packed_zip converts rows [row0, row0 + rows) in place (to_pair 1:
- * plain -> pair, 0: pair -> plain).  The _pair step / run / step_peer calls
- * are life_dev_packed_step / _run / _step_peer on buffers in that layout,
- * `generations` / `depth` in 1..12.  Populations (popcounts) are layout-
- * independent; everything else reads the plain layout. */
+/* ---- interleaved layouts at the device-buffer layer: `order` 2 = the pair
+ * layout (W % 64 == 0: each uint64 group of a packed row kept as even columns
+ * | odd columns), 4 = the quad layout (W % 128 == 0: 128-column groups as
+ * four words, word r bit j = column 4j + r), the layouts packed_il_kernel<K,
+ * N> steps at 10 / 9.5 integer ops per 32 cell-updates.  life_dev_packed_zip
+ * converts rows [row0, row0 + rows) in place (to_interleaved 1: plain ->
+ * interleaved, 0: back).  The _il step / run / step_peer calls are
+ * life_dev_packed_step / _run / _step_peer on buffers in that layout,
+ * `generations` / `depth` in 1..12 (pair) or 1..6 (quad).  Populations
+ * (popcounts) are layout-independent; everything else reads the plain layout. */
 int life_dev_packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
-                        int32_t to_pair, void* stream);
-int life_dev_packed_step_pair(const uint32_t* in, int64_t in_pitch, int64_t in_row0,
-                              int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0,
-                              int64_t width, int64_t out_rows, int32_t generations, void* stream);
-int life_dev_packed_run_pair(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width,
-                             int64_t height, int64_t generations, int32_t depth,
-                             int32_t* result_in_b, void* stream);
-int life_dev_packed_step_pair_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
-                                   const uint32_t* down, int64_t down_rows, int64_t pitch,
-                                   int64_t band_rows, uint32_t* out, int64_t out_row0,
-                                   int64_t out_rows, int64_t width, int32_t generations,
-                                   void* stream);
+                        int32_t order, int32_t to_interleaved, void* stream);
+int life_dev_packed_step_il(int32_t order, const uint32_t* in, int64_t in_pitch, int64_t in_row0,
+                            int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0,
+                            int64_t width, int64_t out_rows, int32_t generations, void* stream);
+int life_dev_packed_run_il(int32_t order, uint32_t* buf_a, uint32_t* buf_b, int64_t pitch,
+                           int64_t width, int64_t height, int64_t generations, int32_t depth,
+                           int32_t* result_in_b, void* stream);
+int life_dev_packed_step_il_peer(int32_t order, const uint32_t* in, const uint32_t* up,
+                                 int64_t up_rows, const uint32_t* down, int64_t down_rows,
+                                 int64_t pitch, int64_t band_rows, uint32_t* out, int64_t out_row0,
+                                 int64_t out_rows, int64_t width, int32_t generations,
+                                 void* stream);
 /* `generations` packed generations of a whole W x H torus (rows of `pitch`
  * words, in == out allowed) through the cluster-resident engine
  * (LIFE_ENGINE_RESIDENT), one launch per 2^30 generations. */

@@ -84,10 +84,11 @@ class BandGeometry:
     y0: int
     y1: int
     pitch: int  # uint32 words per row
-    # Passes run packed_pair_kernel on the interleaved-pair layout (W % 64 == 0,
-    # depth <= 12; kernels_pair.cuh): the drivers convert their band in place
-    # before the first pass and back before anything reads the plain words.
-    pair: bool = False
+    # Interleave order of the passes' layout (kernels_pair.cuh): 0 = plain,
+    # 2 = pair (W % 64 == 0, depth <= 12), 4 = quad (W % 128 == 0, depth <= 6).
+    # The drivers convert their band in place before the first pass and back
+    # before anything reads the plain words.
+    il: int = 0
 
     @property
     def band_rows(self) -> int:
@@ -102,37 +103,44 @@ class BandGeometry:
         return self.band_rows + 2 * self.ghost
 
 
+def il_max_depth(il: int) -> int:
+    return {0: capi.MAX_TEMPORAL_DEPTH, 2: capi.PAIR_MAX_DEPTH, 4: capi.QUAD_MAX_DEPTH}[il]
+
+
 def make_geometry(width: int, height: int, rank: int, world: int, depth: int,
-                  pair: bool = False) -> BandGeometry:
+                  il: int = 0) -> BandGeometry:
     if width < 3 or height < 3:
         raise ConfigError(f"grid dimensions must be at least 3x3, got {width}x{height}")
     if not 1 <= depth <= capi.MAX_TEMPORAL_DEPTH:
         raise ConfigError(f"temporal depth must be in [1, {capi.MAX_TEMPORAL_DEPTH}]")
-    if pair and (width % 64 != 0 or depth > capi.PAIR_MAX_DEPTH):
-        raise ConfigError(f"the pair layout needs W % 64 == 0 and depth <= {capi.PAIR_MAX_DEPTH}, "
-                          f"got W = {width}, depth {depth}")
+    if il not in (0, 2, 4):
+        raise ConfigError(f"interleave order must be 0 (plain), 2 (pair) or 4 (quad), got {il}")
+    if il and (width % (32 * il) != 0 or depth > il_max_depth(il)):
+        raise ConfigError(f"interleave order {il} needs W % {32 * il} == 0 and depth <= "
+                          f"{il_max_depth(il)}, got W = {width}, depth {depth}")
     bounds = band_bounds(height, world)  # TooManyParts like partition_rows
     y0, y1 = bounds[rank], bounds[rank + 1]
     if world > 1 and (y1 - y0) < depth:
         raise TooManyParts(f"band of {y1 - y0} rows is thinner than the temporal depth {depth}")
     return BandGeometry(width, height, rank, world, depth, y0, y1,
-                        int(capi.lib().life_packed_pitch_words(width)), pair)
+                        int(capi.lib().life_packed_pitch_words(width)), il)
 
 
 class PairLayout:
     """Mixin of the band drivers: which layout the current band is in.  A
     driver names its band rows with _band_raw() (a view of `band_rows` rows of
     `pitch` words); passes call _to_pair() first when the geometry asks for
-    the pair kernel, readers of the plain layout call _to_plain()."""
+    the pair / quad kernel (geo.il), readers of the plain layout call
+    _to_plain()."""
 
-    in_pair = False
+    in_pair = False  # the band is in the geometry's interleaved layout
 
     def _zip(self, to_pair: bool) -> None:
         g = self.geo
         raw = self._band_raw()
         stream = torch.cuda.current_stream(self.device).cuda_stream
         check(capi.lib().life_dev_packed_zip(raw.data_ptr(), g.pitch, g.width, 0, g.band_rows,
-                                             1 if to_pair else 0, stream))
+                                             g.il, 1 if to_pair else 0, stream))
 
     def set_band(self, rows: torch.Tensor) -> None:
         """Overwrites the band with `rows` (plain packed layout)."""
@@ -140,7 +148,7 @@ class PairLayout:
         self._band_raw().copy_(rows)
 
     def _to_pair(self) -> None:
-        if self.geo.pair and not self.in_pair:
+        if self.geo.il and not self.in_pair:
             self._zip(True)
             self.in_pair = True
 
@@ -155,15 +163,15 @@ class PairLayout:
 Stepper = Callable[[torch.Tensor, int, int, torch.Tensor, int, int, int], None]
 
 
-def cuda_stepper(width: int, pair: bool = False) -> Stepper:
+def cuda_stepper(width: int, il: int = 0) -> Stepper:
     L = capi.lib()
-    fn = L.life_dev_packed_step_pair if pair else L.life_dev_packed_step
 
     def step(inp, in_row0, in_rows, out, out_row0, out_rows, k):
         pitch = inp.shape[1]
         stream = torch.cuda.current_stream(inp.device).cuda_stream
-        check(fn(inp.data_ptr(), pitch, in_row0, in_rows, out.data_ptr(), out.shape[1], out_row0,
-                 width, out_rows, k, stream))
+        args = (inp.data_ptr(), pitch, in_row0, in_rows, out.data_ptr(), out.shape[1], out_row0,
+                width, out_rows, k, stream)
+        check(L.life_dev_packed_step_il(il, *args) if il else L.life_dev_packed_step(*args))
     return step
 
 
@@ -177,9 +185,9 @@ class BandDriver(PairLayout):
         self.device = device
         self.group = group
         self.overlap = overlap
-        if geo.pair and stepper is not None:
-            raise ConfigError("the pair layout runs on the CUDA stepper")
-        self.stepper = stepper or cuda_stepper(geo.width, geo.pair)
+        if geo.il and stepper is not None:
+            raise ConfigError("the interleaved layouts run on the CUDA stepper")
+        self.stepper = stepper or cuda_stepper(geo.width, geo.il)
         self.counter = counter  # test hook: band rows -> live cells (default: CUDA popcount)
         shape = (geo.buf_rows, geo.pitch)
         self.buf = [torch.zeros(shape, dtype=torch.int32, device=device) for _ in range(2)]
@@ -371,9 +379,9 @@ class TorusDriver(PairLayout):
         flip = C.c_int32(0)
         stream = torch.cuda.current_stream(self.device).cuda_stream
         L = capi.lib()
-        fn = L.life_dev_packed_run_pair if g.pair else L.life_dev_packed_run
-        check(fn(a.data_ptr(), b.data_ptr(), g.pitch, g.width, g.height, gens, g.depth,
-                 C.byref(flip), stream))
+        args = (a.data_ptr(), b.data_ptr(), g.pitch, g.width, g.height, gens, g.depth,
+                C.byref(flip), stream)
+        check(L.life_dev_packed_run_il(g.il, *args) if g.il else L.life_dev_packed_run(*args))
         self.cur ^= flip.value
         self.generations += gens
 
@@ -383,9 +391,9 @@ class TorusDriver(PairLayout):
         a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
         stream = torch.cuda.current_stream(self.device).cuda_stream
         L = capi.lib()
-        fn = L.life_dev_packed_step_pair if g.pair else L.life_dev_packed_step
-        check(fn(a.data_ptr(), g.pitch, 0, g.height, b.data_ptr(), g.pitch, 0, g.width, g.height,
-                 k, stream))
+        args = (a.data_ptr(), g.pitch, 0, g.height, b.data_ptr(), g.pitch, 0, g.width, g.height,
+                k, stream)
+        check(L.life_dev_packed_step_il(g.il, *args) if g.il else L.life_dev_packed_step(*args))
         self.cur ^= 1
         self.generations += k
 
@@ -435,8 +443,8 @@ class LocalBands:
     (no rank ever waits on another)."""
 
     def __init__(self, width: int, height: int, parts: int, depth: int, device: torch.device,
-                 overlap: bool = True, pair: bool = False):
-        self.drivers = [BandDriver(make_geometry(width, height, r, parts, depth, pair), device,
+                 overlap: bool = True, il: int = 0):
+        self.drivers = [BandDriver(make_geometry(width, height, r, parts, depth, il), device,
                                    overlap=overlap) for r in range(parts)]
 
     def init_random(self, density: float, seed: int) -> None:
@@ -527,15 +535,20 @@ def open_peer(handle: bytes) -> int:
 def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows: int,
               pitch: int, band_rows: int, dst: int, k: int, device: torch.device,
               edge_stream: Optional["torch.cuda.Stream"] = None,
-              interior_done: Optional["torch.cuda.Event"] = None, pair: bool = False) -> None:
+              interior_done: Optional["torch.cuda.Event"] = None, il: int = 0) -> None:
     """One depth-k pass of a band with in-kernel NVLink halos: the interior
     rows [k, band-k) read only the band's own rows (the branch-free kernel
     path); the two k-row edge strips read the neighbours' rows through peer
     pointers and run on `edge_stream` (if given) beside the interior.
-    `pair`: every buffer is in the interleaved-pair layout (packed_pair_kernel)."""
+    `il` 2 / 4: every buffer is in the pair / quad layout (packed_il_kernel)."""
     L = capi.lib()
-    step = L.life_dev_packed_step_pair if pair else L.life_dev_packed_step
-    step_peer = L.life_dev_packed_step_pair_peer if pair else L.life_dev_packed_step_peer
+
+    def step(*args):
+        return L.life_dev_packed_step_il(il, *args) if il else L.life_dev_packed_step(*args)
+
+    def step_peer(*args):
+        return (L.life_dev_packed_step_il_peer(il, *args) if il
+                else L.life_dev_packed_step_peer(*args))
     main = torch.cuda.current_stream(device)
     if band_rows <= 2 * k:
         check(step_peer(src, up, up_rows, down, down_rows, pitch, band_rows, dst, 0, band_rows,
@@ -655,14 +668,14 @@ class PeerBandDriver(PairLayout):
         peer_pass(g.width, self.buf[c].ptr.value, self.up_ptrs[c], self.up_rows,
                   self.down_ptrs[c], self.down_rows, g.pitch, g.band_rows,
                   self.buf[c ^ 1].ptr.value, k, self.device, self.edge_stream,
-                  interior_done=interior_done, pair=g.pair)
+                  interior_done=interior_done, il=g.il)
 
     def pass_(self, k: int) -> None:
         g = self.geo
         if not 1 <= k <= g.depth:
             raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
-        if g.pair and not self.in_pair:
-            raise ConfigError("band in the plain layout: pair-layout passes start through run() "
+        if g.il and not self.in_pair:
+            raise ConfigError("band in the plain layout: interleaved passes start through run() "
                               "(conversion, then a barrier with the neighbours)")
         if self.profile:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -742,11 +755,11 @@ class LocalPeerBands:
     cross-GPU waits."""
 
     def __init__(self, width: int, height: int, parts: int, depth: int, device: torch.device,
-                 pair: bool = False):
+                 il: int = 0):
         if parts < 2:
             raise ConfigError("LocalPeerBands needs at least two bands")
-        self.geos = [make_geometry(width, height, r, parts, depth, pair) for r in range(parts)]
-        self.pair = pair
+        self.geos = [make_geometry(width, height, r, parts, depth, il) for r in range(parts)]
+        self.il = il
         self.in_pair = False
         self.device = device
         self.bufs = [[torch.zeros((g.band_rows, g.pitch), dtype=torch.int32, device=device)
@@ -765,12 +778,13 @@ class LocalPeerBands:
         stream = torch.cuda.current_stream(self.device).cuda_stream
         for g, b in zip(self.geos, self.bufs):
             check(capi.lib().life_dev_packed_zip(b[self.cur].data_ptr(), g.pitch, g.width, 0,
-                                                 g.band_rows, 1 if to_pair else 0, stream))
+                                                 g.band_rows, self.il, 1 if to_pair else 0,
+                                                 stream))
         self.in_pair = to_pair
 
     def pass_(self, k: int) -> None:
         p = len(self.geos)
-        if self.pair and not self.in_pair:
+        if self.il and not self.in_pair:
             self._zip(True)
         c = self.cur
         for r, g in enumerate(self.geos):
@@ -779,7 +793,7 @@ class LocalPeerBands:
                       self.geos[up].band_rows, self.bufs[down][c].data_ptr(),
                       self.geos[down].band_rows, g.pitch, g.band_rows,
                       self.bufs[r][c ^ 1].data_ptr(), k, self.device, self.edge_stream,
-                      pair=self.pair)
+                      il=self.il)
         self.cur ^= 1
 
     def run(self, generations: int) -> None:

@@ -26,13 +26,15 @@ ENGINE_PACKED = 0
 ENGINE_BYTE = 1
 ENGINE_RESIDENT = 2
 MAX_TEMPORAL_DEPTH = 16
-PAIR_MAX_DEPTH = 12  # packed_pair_kernel<K> (W % 64 == 0)
+PAIR_MAX_DEPTH = 12  # packed_il_kernel<K, 2> (W % 64 == 0)
+QUAD_MAX_DEPTH = 6   # packed_il_kernel<K, 4> (W % 128 == 0)
 MAX_BYTE_DEPTH = 8
 
 OPT_PROFILE = 1
 OPT_BATCH_TRAPEZOID = 2
 OPT_HALO = 3
 OPT_PAIR_DEPTH = 4
+OPT_QUAD_DEPTH = 5
 HALO_PEER = 0
 HALO_COPY = 1
 
@@ -95,14 +97,14 @@ SIGNATURES = [
                                        _vp]),
     ("life_dev_packed_step_peer", C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp, _i64,
                                             _i64, _i64, _i32, _vp]),
-    ("life_pair_auto_depth", C.c_int, [_i64, _i64]),
-    ("life_dev_packed_zip", C.c_int, [_vp, _i64, _i64, _i64, _i64, _i32, _vp]),
-    ("life_dev_packed_step_pair", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64,
-                                            _i32, _vp]),
-    ("life_dev_packed_run_pair", C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32,
-                                           C.POINTER(_i32), _vp]),
-    ("life_dev_packed_step_pair_peer", C.c_int, [_vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp,
-                                                 _i64, _i64, _i64, _i32, _vp]),
+    ("life_interleave_auto", C.c_int, [_i64, _i64, _i32, _i32, _i32, C.POINTER(_i32)]),
+    ("life_dev_packed_zip", C.c_int, [_vp, _i64, _i64, _i64, _i64, _i32, _i32, _vp]),
+    ("life_dev_packed_step_il", C.c_int, [_i32, _vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64,
+                                          _i64, _i32, _vp]),
+    ("life_dev_packed_run_il", C.c_int, [_i32, _vp, _vp, _i64, _i64, _i64, _i64, _i32,
+                                         C.POINTER(_i32), _vp]),
+    ("life_dev_packed_step_il_peer", C.c_int, [_i32, _vp, _vp, _i64, _vp, _i64, _i64, _i64, _vp,
+                                               _i64, _i64, _i64, _i32, _vp]),
     ("life_dev_packed_run_resident", C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     ("life_resident_cluster_size", C.c_int, [_i64, _i64]),
     ("life_dev_alloc", C.c_int, [_i64, C.POINTER(_vp)]),

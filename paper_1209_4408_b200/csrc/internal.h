@@ -87,26 +87,43 @@ int packed_auto_depth(int64_t width, int64_t height);
 // buf_b: whole passes of `depth`, then the remainder; *result_in_b = 1 if the result is in buf_b.
 int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, int64_t height,
                int64_t generations, int32_t depth, cudaStream_t stream, SplitStreams* ss,
-               int* result_in_b, bool pair = false);
+               int* result_in_b, int il = 0);
 
-// ---- interleaved-pair layout (life_pair.cu, kernels_pair.cuh) ---------------
-// W % 64 == 0 tori: each uint64 group of a packed row kept as (even columns,
-// odd columns); passes of up to kPairMaxDepth generations at 10 instead of 11
-// integer ops per 32 cell-updates.  packed_zip converts rows in place.
+// ---- interleaved layouts (life_pair.cu, kernels_pair.cuh) -------------------
+// Order 2, the PAIR layout (W % 64 == 0): each uint64 group of a packed row
+// kept as (even columns, odd columns); passes of up to 12 generations at 10
+// instead of 11 integer ops per 32 cell-updates.  Order 4, the QUAD layout
+// (W % 128 == 0): 128-column groups as four words of every 4th column; up to
+// 6 generations per pass at 9.5 ops.  Order 0 = the plain layout.
+// packed_zip converts rows in place.
 constexpr int kPairMaxDepthHost = 12;
-inline bool pair_eligible(int64_t width) { return width >= 64 && width % 64 == 0; }
-int packed_pair_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
-                     uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
-                     int64_t out_rows, int32_t generations, cudaStream_t stream);
-int packed_pair_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
-                          const uint32_t* down, int64_t down_rows, int64_t pitch,
-                          int64_t band_rows, uint32_t* out, int64_t out_row0, int64_t out_rows,
-                          int64_t width, int32_t generations, cudaStream_t stream);
-int packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
+constexpr int kQuadMaxDepthHost = 6;
+inline bool il_eligible(int il, int64_t width) {
+  return (il == 2 || il == 4) && width >= 32 * il && width % (32 * il) == 0;
+}
+inline int il_max_depth(int il) {
+  return il == 4 ? kQuadMaxDepthHost : il == 2 ? kPairMaxDepthHost : LIFE_MAX_TEMPORAL_DEPTH;
+}
+int packed_il_step(int il, const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                   uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                   int64_t out_rows, int32_t generations, cudaStream_t stream);
+int packed_il_step_peer(int il, const uint32_t* in, const uint32_t* up, int64_t up_rows,
+                        const uint32_t* down, int64_t down_rows, int64_t pitch,
+                        int64_t band_rows, uint32_t* out, int64_t out_row0, int64_t out_rows,
+                        int64_t width, int32_t generations, cudaStream_t stream);
+int packed_zip(int il, uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
                bool unzip, cudaStream_t stream);
-// temporal_depth 0: the pair kernel's depth for a W-wide torus (or band) of
-// `height` rows, 0 = keep the plain-layout kernels (exported as life_pair_auto_depth).
-int pair_auto_depth(int64_t width, int64_t height);
+// The layout and depth a run uses on a W-wide torus (or band) of `height`
+// rows: a forced LIFE_OPT_QUAD_DEPTH / LIFE_OPT_PAIR_DEPTH (> 0) where the
+// width allows it; else, when the caller left the depth to the engine
+// (temporal_depth 0), the auto rule over the layouts whose option is -1
+// (exported as life_interleave_auto); else order 0 (the plain kernels at
+// temporal_depth or packed_auto_depth).
+struct IlChoice {
+  int il = 0;
+  int depth = 0;
+};
+IlChoice il_choose(int64_t width, int64_t height, int pair_opt, int quad_opt, int temporal_depth);
 
 // Small kernels the multi-device context launches on band buffers.
 int launch_mask_tail(uint32_t* words, int64_t pitch, int64_t width, int64_t rows,

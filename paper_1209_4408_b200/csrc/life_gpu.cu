@@ -516,10 +516,10 @@ int packed_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t i
 
 int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, int64_t height,
                int64_t generations, int32_t depth, cudaStream_t stream, SplitStreams* ss,
-               int* result_in_b, bool pair) {
-  if (depth < 1 || depth > (pair ? kPairMaxDepthHost : LIFE_MAX_TEMPORAL_DEPTH))
+               int* result_in_b, int il) {
+  if (depth < 1 || depth > il_max_depth(il))
     return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [1, %d], got %d",
-                     pair ? kPairMaxDepthHost : LIFE_MAX_TEMPORAL_DEPTH, depth);
+                     il_max_depth(il), depth);
   if (generations < 0) return set_error(LIFE_ERR_CONFIG, "generations must be >= 0");
   if (width < 1 || height < 1 || pitch < 2 * ceil_div(width, 64) || buf_a == buf_b)
     return set_error(LIFE_ERR_CONFIG, "bad packed run geometry");
@@ -529,8 +529,8 @@ int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, i
   const int64_t full = generations / depth;
   const int rem = static_cast<int>(generations % depth);
   auto pass = [&](int k) -> int {
-    if (pair)  // buffers in the interleaved-pair layout (kernels_pair.cuh)
-      return packed_pair_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, k, stream);
+    if (il != 0)  // buffers in the pair / quad layout (kernels_pair.cuh)
+      return packed_il_step(il, cur, pitch, 0, height, nxt, pitch, 0, width, height, k, stream);
     return packed_step(cur, pitch, 0, height, nxt, pitch, 0, width, height, k, stream, ss);
   };
   for (int64_t i = 0; i < full; ++i) {
@@ -568,38 +568,39 @@ int life_dev_packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t
 }
 
 int life_dev_packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
-                        int32_t to_pair, void* stream) {
-  return packed_zip(words, pitch, width, row0, rows, /*unzip=*/to_pair == 0,
+                        int32_t order, int32_t to_interleaved, void* stream) {
+  return packed_zip(order, words, pitch, width, row0, rows, /*unzip=*/to_interleaved == 0,
                     static_cast<cudaStream_t>(stream));
 }
 
-int life_dev_packed_step_pair(const uint32_t* in, int64_t in_pitch, int64_t in_row0,
-                              int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0,
-                              int64_t width, int64_t out_rows, int32_t generations, void* stream) {
-  return packed_pair_step(in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
-                          out_rows, generations, static_cast<cudaStream_t>(stream));
+int life_dev_packed_step_il(int32_t order, const uint32_t* in, int64_t in_pitch, int64_t in_row0,
+                            int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0,
+                            int64_t width, int64_t out_rows, int32_t generations, void* stream) {
+  return packed_il_step(order, in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
+                        out_rows, generations, static_cast<cudaStream_t>(stream));
 }
 
-int life_dev_packed_run_pair(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width,
-                             int64_t height, int64_t generations, int32_t depth,
-                             int32_t* result_in_b, void* stream) {
-  if (!pair_eligible(width))
-    return set_error(LIFE_ERR_CONFIG, "the pair layout needs W %% 64 == 0, got %lld",
-                     static_cast<long long>(width));
+int life_dev_packed_run_il(int32_t order, uint32_t* buf_a, uint32_t* buf_b, int64_t pitch,
+                           int64_t width, int64_t height, int64_t generations, int32_t depth,
+                           int32_t* result_in_b, void* stream) {
+  if (!il_eligible(order, width))
+    return set_error(LIFE_ERR_CONFIG, "interleave order %d needs W %% %d == 0, got %lld", order,
+                     32 * order, static_cast<long long>(width));
   int flip = 0;
   LIFE_TRY(packed_run(buf_a, buf_b, pitch, width, height, generations, depth,
-                      static_cast<cudaStream_t>(stream), nullptr, &flip, /*pair=*/true));
+                      static_cast<cudaStream_t>(stream), nullptr, &flip, order));
   if (result_in_b) *result_in_b = flip;
   return LIFE_OK;
 }
 
-int life_dev_packed_step_pair_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
-                                   const uint32_t* down, int64_t down_rows, int64_t pitch,
-                                   int64_t band_rows, uint32_t* out, int64_t out_row0,
-                                   int64_t out_rows, int64_t width, int32_t generations,
-                                   void* stream) {
-  return packed_pair_step_peer(in, up, up_rows, down, down_rows, pitch, band_rows, out, out_row0,
-                               out_rows, width, generations, static_cast<cudaStream_t>(stream));
+int life_dev_packed_step_il_peer(int32_t order, const uint32_t* in, const uint32_t* up,
+                                 int64_t up_rows, const uint32_t* down, int64_t down_rows,
+                                 int64_t pitch, int64_t band_rows, uint32_t* out, int64_t out_row0,
+                                 int64_t out_rows, int64_t width, int32_t generations,
+                                 void* stream) {
+  return packed_il_step_peer(order, in, up, up_rows, down, down_rows, pitch, band_rows, out,
+                             out_row0, out_rows, width, generations,
+                             static_cast<cudaStream_t>(stream));
 }
 
 int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
@@ -1080,7 +1081,7 @@ struct life_ctx {
   int pk_cur = 0;
   // pk[pk_cur] is in the interleaved-pair layout (kernels_pair.cuh): left so by
   // life_run between runs; every reader of the plain layout calls pk_plain().
-  bool pk_pair = false;
+  int pk_il = 0;  // 0 plain, 2 pair, 4 quad
   uint8_t* by[2] = {nullptr, nullptr};
   int64_t by_pitch = 0;  // bytes
   int by_cur = 0;
@@ -1101,6 +1102,7 @@ struct life_ctx {
   int batch_trap = -1;   // LIFE_OPT_BATCH_TRAPEZOID
   bool profile = false;  // LIFE_OPT_PROFILE
   int pair_depth = -1;   // LIFE_OPT_PAIR_DEPTH
+  int quad_depth = -1;   // LIFE_OPT_QUAD_DEPTH
   // Statistics of the last life_run (life_ctx_band_stats, band 0).
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   double run_ms = 0.0, pass_ms = 0.0;
@@ -1130,7 +1132,7 @@ void free_buffers(life_ctx* c) {
 
 int set_dims(life_ctx* c, int64_t w, int64_t h) {
   LIFE_TRY(check_dims(w, h));
-  c->pk_pair = false;  // callers overwrite the whole grid in the plain layout
+  c->pk_il = 0;  // callers overwrite the whole grid in the plain layout
   if (w != c->W || h != c->H) {
     LIFE_CUDA(cudaStreamSynchronize(c->stream));
     free_buffers(c);
@@ -1180,17 +1182,19 @@ int ensure_counts(life_ctx* c, int64_t n) {
 // reads or edits the plain packed words converts it back first (in place,
 // one HBM read + write of the grid).
 int pk_plain(life_ctx* c) {
-  if (c->layout == kPacked && c->pk_pair) {
-    LIFE_TRY(packed_zip(c->pk[c->pk_cur], c->pk_pitch, c->W, 0, c->H, /*unzip=*/true, c->stream));
+  if (c->layout == kPacked && c->pk_il != 0) {
+    LIFE_TRY(packed_zip(c->pk_il, c->pk[c->pk_cur], c->pk_pitch, c->W, 0, c->H, /*unzip=*/true,
+                        c->stream));
   }
-  c->pk_pair = false;
+  c->pk_il = 0;
   return LIFE_OK;
 }
-int pk_to_pair(life_ctx* c) {
-  if (c->layout == kPacked && !c->pk_pair) {
-    LIFE_TRY(packed_zip(c->pk[c->pk_cur], c->pk_pitch, c->W, 0, c->H, /*unzip=*/false, c->stream));
-    c->pk_pair = true;
-  }
+int pk_to_il(life_ctx* c, int il) {
+  if (c->layout != kPacked || c->pk_il == il) return LIFE_OK;
+  LIFE_TRY(pk_plain(c));
+  LIFE_TRY(packed_zip(il, c->pk[c->pk_cur], c->pk_pitch, c->W, 0, c->H, /*unzip=*/false,
+                      c->stream));
+  c->pk_il = il;
   return LIFE_OK;
 }
 
@@ -1256,11 +1260,35 @@ bool resident_auto(int64_t w, int64_t h) {
 // passes run as one all-paths launch (W % 32 != 0, less than ~3 block waves
 // deep), where K = 12 fits 12 warps per SM instead of 8 (config 4: 37.5 ->
 // 38.6 T/s; kbench depth sweep).
-// temporal_depth 0 on W % 64 == 0 tori (or row bands of them, h rows tall):
-// the interleaved-pair kernel at this depth (0: keep the plain-layout kernels).
-int lifegpu::detail::pair_auto_depth(int64_t w, int64_t h) {
-  if (!pair_eligible(w)) return 0;
-  return w * h >= (int64_t(1) << 30) ? 10 : 0;
+// temporal_depth 0 on W % 64 == 0 tori (or row bands of them, h rows tall) of
+// 2^30 cells or more: the quad layout at K = 6 where W % 128 == 0 (kbench,
+// T cell-updates/s, quad K = 4 / 5 / 6 vs pair K = 10 vs plain K = 16:
+// 262144^2 50.3 / 52.4 / 52.6 vs 49.8 vs 47.1; 65536^2 49.3 / 50.6 / 51.3 vs
+// 46.8 vs 44.5), else the pair layout at K = 10.  Smaller tori keep the plain
+// kernels (16384^2: quad 35.1, pair 35.9, plain 37.3: fewer, wider strips
+// waste more lanes and the one-wave tiles gain nothing from fewer ops).
+namespace {
+constexpr int64_t kIlAutoCells = int64_t(1) << 30;
+}
+lifegpu::detail::IlChoice lifegpu::detail::il_choose(int64_t w, int64_t h, int pair_opt,
+                                                     int quad_opt, int temporal_depth) {
+  IlChoice c;
+  if (quad_opt > 0 && il_eligible(4, w)) {
+    c.il = 4;
+    c.depth = quad_opt;
+  } else if (pair_opt > 0 && il_eligible(2, w)) {
+    c.il = 2;
+    c.depth = pair_opt;
+  } else if (temporal_depth == 0 && w * h >= kIlAutoCells) {
+    if (quad_opt < 0 && il_eligible(4, w)) {
+      c.il = 4;
+      c.depth = 6;
+    } else if (pair_opt < 0 && il_eligible(2, w)) {
+      c.il = 2;
+      c.depth = 10;
+    }
+  }
+  return c;
 }
 
 int lifegpu::detail::packed_auto_depth(int64_t w, int64_t h) {
@@ -1275,9 +1303,13 @@ int life_packed_auto_depth(int64_t width, int64_t height) {
   return packed_auto_depth(width, height);
 }
 
-int life_pair_auto_depth(int64_t width, int64_t height) {
+int life_interleave_auto(int64_t width, int64_t height, int32_t pair_option, int32_t quad_option,
+                         int32_t temporal_depth, int32_t* depth) {
+  if (depth) *depth = 0;
   if (width < 1 || height < 1) return 0;
-  return pair_auto_depth(width, height);
+  const IlChoice c = il_choose(width, height, pair_option, quad_option, temporal_depth);
+  if (depth) *depth = c.depth;
+  return c.il;
 }
 
 int life_packed_launch_kind(int64_t width, int64_t out_rows, int32_t generations) {
@@ -1401,6 +1433,12 @@ int life_ctx_set_option(life_ctx* c, int32_t option, int64_t value) {
                          kPairMaxDepthHost);
       c->pair_depth = static_cast<int>(value);
       return LIFE_OK;
+    case LIFE_OPT_QUAD_DEPTH:
+      if (value < -1 || value > kQuadMaxDepthHost)
+        return set_error(LIFE_ERR_CONFIG, "LIFE_OPT_QUAD_DEPTH must be in [-1, %d]",
+                         kQuadMaxDepthHost);
+      c->quad_depth = static_cast<int>(value);
+      return LIFE_OK;
     default:
       return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
   }
@@ -1413,6 +1451,7 @@ int life_ctx_get_option(life_ctx* c, int32_t option, int64_t* value) {
     case LIFE_OPT_PROFILE: *value = c->profile ? 1 : 0; return LIFE_OK;
     case LIFE_OPT_BATCH_TRAPEZOID: *value = c->batch_trap; return LIFE_OK;
     case LIFE_OPT_PAIR_DEPTH: *value = c->pair_depth; return LIFE_OK;
+    case LIFE_OPT_QUAD_DEPTH: *value = c->quad_depth; return LIFE_OK;
     default: return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
   }
 }
@@ -1717,7 +1756,7 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
   LIFE_TRY(check_engine(engine));
   LIFE_TRY(check_run_args(generations, checkpoints, n_checkpoints, populations));
   int depth = temporal_depth;
-  int pair = 0;  // > 0: passes of that depth on the interleaved-pair layout
+  int il = 0;  // 2 / 4: passes on the pair / quad layout
   if (engine != LIFE_ENGINE_BYTE) {
     if (depth < 0 || depth > LIFE_MAX_TEMPORAL_DEPTH)
       return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [0, %d], got %d",
@@ -1731,14 +1770,14 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
                        "(needs W %% 32 == 0 and every band in one CTA's shared memory)",
                        static_cast<long long>(c->W), static_cast<long long>(c->H));
     if (depth == 0) depth = packed_auto_depth(c->W, c->H);
-    // Interleaved-pair kernel (W % 64 == 0): forced by LIFE_OPT_PAIR_DEPTH, or
-    // the auto rule's choice when the caller left the depth to the engine.
-    if (engine == LIFE_ENGINE_PACKED && pair_eligible(c->W)) {
-      if (c->pair_depth > 0)
-        pair = c->pair_depth;
-      else if (c->pair_depth < 0 && temporal_depth == 0)
-        pair = pair_auto_depth(c->W, c->H);
-      if (pair > 0) depth = pair;
+    // Pair / quad layout kernels: forced by LIFE_OPT_PAIR_DEPTH / _QUAD_DEPTH,
+    // or the auto rule's choice when the caller left the depth to the engine.
+    if (engine == LIFE_ENGINE_PACKED) {
+      const IlChoice ch = il_choose(c->W, c->H, c->pair_depth, c->quad_depth, temporal_depth);
+      if (ch.il != 0) {
+        il = ch.il;
+        depth = ch.depth;
+      }
     }
   } else {
     // Byte engine: K generations per pass (byte_tb2_kernel) when W % 16 == 0 or
@@ -1752,8 +1791,8 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
   }
   if (c->layout == kNone) return set_error(LIFE_ERR_STATE, "no grid loaded");
   LIFE_TRY(to_layout(c, engine_layout(engine)));
-  if (pair > 0 && generations > 0) {
-    LIFE_TRY(pk_to_pair(c));
+  if (il != 0 && generations > 0) {
+    LIFE_TRY(pk_to_il(c, il));
   } else if (generations > 0 || engine != LIFE_ENGINE_PACKED) {
     LIFE_TRY(pk_plain(c));
   }
@@ -1807,7 +1846,7 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
       // the remainder).
       int flip = 0;
       LIFE_TRY(packed_run(c->pk[c->pk_cur], c->pk[c->pk_cur ^ 1], c->pk_pitch, c->W, c->H,
-                          stop - done, depth, c->stream, &c->split[0], &flip, c->pk_pair));
+                          stop - done, depth, c->stream, &c->split[0], &flip, c->pk_il));
       c->pk_cur ^= flip;
       c->passes += ceil_div(stop - done, int64_t(depth));
       done = stop;
@@ -1818,9 +1857,9 @@ int life_run(life_ctx* c, int64_t generations, int engine, int temporal_depth,
     const int step = static_cast<int>(std::min<int64_t>(depth, stop - done));
     if (engine == LIFE_ENGINE_PACKED) {
       const int nxt = c->pk_cur ^ 1;
-      if (c->pk_pair) {
-        LIFE_TRY(packed_pair_step(c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt],
-                                  c->pk_pitch, 0, c->W, c->H, step, c->stream));
+      if (c->pk_il != 0) {
+        LIFE_TRY(packed_il_step(c->pk_il, c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt],
+                                c->pk_pitch, 0, c->W, c->H, step, c->stream));
       } else {
         LIFE_TRY(packed_step(c->pk[c->pk_cur], c->pk_pitch, 0, c->H, c->pk[nxt], c->pk_pitch, 0,
                              c->W, c->H, step, c->stream, &c->split[0]));
@@ -1885,7 +1924,7 @@ constexpr int64_t kTrapMinChunkRows = LIFE_TRAP_MIN_ROWS;
 struct BatchGeom {
   int64_t width, height, wpr, words_per_row, pitch, generations;
   int depth, passes;
-  bool pair;  // passes on the interleaved-pair layout (zip after upload, unzip before download)
+  int il;  // 2 / 4: passes on the pair / quad layout (zip after upload, unzip before download)
   int64_t bounds[kTrapChunks + 1];
 };
 
@@ -1897,9 +1936,9 @@ int pass_rows(const BatchGeom& g, uint32_t* const* buf, int p, int64_t r0, int64
   if (r0 < 0) r0 += g.height;
   while (rows > 0) {
     const int64_t piece = std::min(rows, g.height - r0);
-    if (g.pair) {
-      LIFE_TRY(packed_pair_step(buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch, r0,
-                                g.width, piece, k, s));
+    if (g.il != 0) {
+      LIFE_TRY(packed_il_step(g.il, buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch,
+                              r0, g.width, piece, k, s));
     } else {
       LIFE_TRY(packed_step(buf[p & 1], g.pitch, r0, g.height, buf[(p & 1) ^ 1], g.pitch, r0,
                            g.width, piece, k, s, ss));
@@ -1917,7 +1956,7 @@ int zip_rows(const BatchGeom& g, uint32_t* buf, int64_t r0, int64_t rows, bool u
   if (r0 < 0) r0 += g.height;
   while (rows > 0) {
     const int64_t piece = std::min(rows, g.height - r0);
-    LIFE_TRY(packed_zip(buf, g.pitch, g.width, r0, piece, unzip, s));
+    LIFE_TRY(packed_zip(g.il, buf, g.pitch, g.width, r0, piece, unzip, s));
     rows -= piece;
     r0 = 0;
   }
@@ -1966,15 +2005,15 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   // temporal_depth 0 on a small W % 32 == 0 torus: the cluster-resident engine
   // (as life_run's auto mode), one launch per grid.
   const bool resident = temporal_depth == 0 && resident_auto(width, height);
-  // Interleaved-pair kernel (W % 64 == 0), chosen as in life_run: the grids are
-  // converted on the device after their upload and before their download.
-  int pair = 0;
-  if (!resident && pair_eligible(width) && generations > 0) {
-    if (c->pair_depth > 0)
-      pair = c->pair_depth;
-    else if (c->pair_depth < 0 && temporal_depth == 0)
-      pair = pair_auto_depth(width, height);
-    if (pair > 0) depth = pair;
+  // Pair / quad layout kernels, chosen as in life_run: the grids are converted
+  // on the device after their upload and before their download.
+  int il = 0;
+  if (!resident && generations > 0) {
+    const IlChoice ch = il_choose(width, height, c->pair_depth, c->quad_depth, temporal_depth);
+    if (ch.il != 0) {
+      il = ch.il;
+      depth = ch.depth;
+    }
   }
   const int64_t wpr = ceil_div(width, 64);
   if (words_per_row < wpr) return set_error(LIFE_ERR_CONFIG, "words_per_row < ceil(W/64)");
@@ -2005,7 +2044,7 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   g.pitch = pitch;
   g.generations = generations;
   g.depth = depth;
-  g.pair = pair > 0;
+  g.il = il;
   g.passes = static_cast<int>(ceil_div(generations, depth));
   // Chunked first/last grid when every chunk outlives its shrinking
   // trapezoid with room to spare and the chunks are tall enough for their
@@ -2076,9 +2115,9 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
         rc = life_dev_packed_run_resident(buf[0], buf[1], pitch, width, height, generations,
                                           c->stream);
       } else {
-        if (g.pair) LIFE_TRY(zip_rows(g, buf[0], 0, height, /*unzip=*/false, c->stream));
+        if (g.il != 0) LIFE_TRY(zip_rows(g, buf[0], 0, height, /*unzip=*/false, c->stream));
         for (int p = 0; p < P && rc == LIFE_OK; ++p) rc = pass_rows(g, buf, p, 0, height, c->stream, &c->split[0]);
-        if (g.pair && rc == LIFE_OK) rc = zip_rows(g, buf[P & 1], 0, height, /*unzip=*/true, c->stream);
+        if (g.il != 0 && rc == LIFE_OK) rc = zip_rows(g, buf[P & 1], 0, height, /*unzip=*/true, c->stream);
       }
       LIFE_CUDA(cudaEventRecord(comp[i], c->stream));
       // Download on the D2H stream.
@@ -2107,14 +2146,14 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
       packed_mask_tail_kernel<<<grid_stride_blocks(mask_n, 256), 256, 0, st>>>(
           buf[0] + y0 * pitch, pitch, nw, tail_mask(width), rows);
       LIFE_CHECK_LAUNCH("packed_mask_tail_kernel");
-      if (g.pair) LIFE_TRY(zip_rows(g, buf[0], y0, rows, /*unzip=*/false, st));
+      if (g.il != 0) LIFE_TRY(zip_rows(g, buf[0], y0, rows, /*unzip=*/false, st));
       for (int p = 0; p < P && rc == LIFE_OK; ++p)
         rc = pass_rows(g, buf, p, y0 + kShrink * (p + 1), rows - 2 * kShrink * (p + 1), st,
                        &c->split[1 + ch % 2]);
       // The interior leaves in the plain layout; the triangles never read
       // these rows of the final buffer (their last read of it, pass P-2,
       // stays within kShrink * P rows of the boundary).
-      if (g.pair && rc == LIFE_OK)
+      if (g.il != 0 && rc == LIFE_OK)
         rc = zip_rows(g, buf[P & 1], y0 + shrink, rows - 2 * shrink, /*unzip=*/true, st);
       LIFE_CUDA(cudaEventRecord(trap_done[ch], st));
     }
@@ -2127,7 +2166,7 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
       for (int p = 0; p < P && rc == LIFE_OK; ++p)
         rc = pass_rows(g, buf, p, g.bounds[b] - kShrink * (p + 1), 2 * kShrink * (p + 1), st,
                        &c->split[3 + bi % 2]);
-      if (g.pair && rc == LIFE_OK)
+      if (g.il != 0 && rc == LIFE_OK)
         rc = zip_rows(g, buf[P & 1], g.bounds[b] - shrink, 2 * shrink, /*unzip=*/true, st);
       LIFE_CUDA(cudaEventRecord(tri_done[b], st));
     }

@@ -79,11 +79,12 @@ struct MultiState {
   bool loaded = false;
   int64_t W = 0, H = 0, pitch = 0;
   int cur = 0;
-  // The resident bands buf[cur] are in the interleaved-pair layout
-  // (kernels_pair.cuh): left so by multi_run between runs; every reader of
-  // the plain layout calls to_plain() first.
-  bool pair = false;
+  // Layout of the resident bands buf[cur]: 0 plain, 2 pair, 4 quad
+  // (kernels_pair.cuh); left interleaved by multi_run between runs; every
+  // reader of the plain layout calls to_plain() first.
+  int il = 0;
   int pair_depth = -1;  // LIFE_OPT_PAIR_DEPTH
+  int quad_depth = -1;  // LIFE_OPT_QUAD_DEPTH
   int64_t batch_bytes_total = 0;
 };
 
@@ -154,7 +155,7 @@ int set_dims(MultiState* m, int64_t w, int64_t h) {
     }
   }
   m->cur = 0;
-  m->pair = false;
+  m->il = 0;
   return LIFE_OK;
 }
 
@@ -190,21 +191,22 @@ int check_loaded(const MultiState* m) {
 // <-> the same rows of band buffer `dev` (pitch words), on stream s.
 // Layout conversion of the resident bands, in place on each band's stream.
 int to_plain(MultiState* m) {
-  if (!m->pair) return LIFE_OK;
+  if (m->il == 0) return LIFE_OK;
   for (Band& b : m->bands) {
     LIFE_TRY(use(b));
-    LIFE_TRY(packed_zip(b.buf[m->cur], m->pitch, m->W, 0, b.rows, /*unzip=*/true, b.main));
+    LIFE_TRY(packed_zip(m->il, b.buf[m->cur], m->pitch, m->W, 0, b.rows, /*unzip=*/true, b.main));
   }
-  m->pair = false;
+  m->il = 0;
   return LIFE_OK;
 }
-int to_pair(MultiState* m) {
-  if (m->pair) return LIFE_OK;
+int to_il(MultiState* m, int il) {
+  if (m->il == il) return LIFE_OK;
+  LIFE_TRY(to_plain(m));
   for (Band& b : m->bands) {
     LIFE_TRY(use(b));
-    LIFE_TRY(packed_zip(b.buf[m->cur], m->pitch, m->W, 0, b.rows, /*unzip=*/false, b.main));
+    LIFE_TRY(packed_zip(il, b.buf[m->cur], m->pitch, m->W, 0, b.rows, /*unzip=*/false, b.main));
   }
-  m->pair = true;
+  m->il = il;
   return LIFE_OK;
 }
 
@@ -225,22 +227,22 @@ int copy_band_rows(const MultiState* m, void* host, int64_t words_per_row, uint3
 // One pass of depth k (the previous pass had depth kprev; 0 = none) over every
 // band: src[b] -> dst[b].  Pass index p selects the event slots.
 int issue_pass(MultiState* m, uint32_t* const* src, uint32_t* const* dst, int64_t p, int k,
-               int kprev, bool pair) {
+               int kprev, int il) {
   // One torus / interior launch and one edge-strip launch on either layout.
   auto step = [&](const uint32_t* in, int64_t in_row0, int64_t in_rows, uint32_t* out,
                   int64_t out_rows, cudaStream_t s, SplitStreams* ss) -> int {
-    if (pair)
-      return packed_pair_step(in, m->pitch, in_row0, in_rows, out, m->pitch, in_row0, m->W,
-                              out_rows, k, s);
+    if (il != 0)
+      return packed_il_step(il, in, m->pitch, in_row0, in_rows, out, m->pitch, in_row0, m->W,
+                            out_rows, k, s);
     return packed_step(in, m->pitch, in_row0, in_rows, out, m->pitch, in_row0, m->W, out_rows, k,
                        s, ss);
   };
   auto step_peer = [&](const uint32_t* in, const uint32_t* up, int64_t up_rows,
                        const uint32_t* down, int64_t down_rows, int64_t band_rows, uint32_t* out,
                        int64_t out_row0, int64_t out_rows, cudaStream_t s) -> int {
-    if (pair)
-      return packed_pair_step_peer(in, up, up_rows, down, down_rows, m->pitch, band_rows, out,
-                                   out_row0, out_rows, m->W, k, s);
+    if (il != 0)
+      return packed_il_step_peer(il, in, up, up_rows, down, down_rows, m->pitch, band_rows, out,
+                                 out_row0, out_rows, m->W, k, s);
     return life_dev_packed_step_peer(in, up, up_rows, down, down_rows, m->pitch, band_rows, out,
                                      out_row0, out_rows, m->W, k, static_cast<void*>(s));
   };
@@ -367,7 +369,7 @@ int check_packed_engine(int engine) {
 
 // Depth of a run: the auto rule on the tallest band, capped by the thinnest
 // band (a band feeds its neighbours K rows per pass).
-int run_depth(const MultiState* m, int temporal_depth, int* depth, bool* pair) {
+int run_depth(const MultiState* m, int temporal_depth, int* depth, int* il) {
   if (temporal_depth < 0 || temporal_depth > LIFE_MAX_TEMPORAL_DEPTH)
     return set_error(LIFE_ERR_CONFIG, "temporal depth must be in [0, %d], got %d",
                      LIFE_MAX_TEMPORAL_DEPTH, temporal_depth);
@@ -377,19 +379,13 @@ int run_depth(const MultiState* m, int temporal_depth, int* depth, bool* pair) {
     max_rows = std::max(max_rows, b.rows);
   }
   int k = temporal_depth == 0 ? packed_auto_depth(m->W, max_rows) : temporal_depth;
-  // Interleaved-pair kernel (W % 64 == 0), chosen as in life_run: forced by
-  // LIFE_OPT_PAIR_DEPTH, or the auto rule on the tallest band.
-  int pk = 0;
-  if (pair_eligible(m->W)) {
-    if (m->pair_depth > 0)
-      pk = m->pair_depth;
-    else if (m->pair_depth < 0 && temporal_depth == 0)
-      pk = pair_auto_depth(m->W, max_rows);
-  }
-  if (pk > 0) k = pk;
+  // Pair / quad layout kernels, chosen as in life_run: forced by
+  // LIFE_OPT_PAIR_DEPTH / _QUAD_DEPTH, or the auto rule on the tallest band.
+  const IlChoice ch = il_choose(m->W, max_rows, m->pair_depth, m->quad_depth, temporal_depth);
+  if (ch.il != 0) k = ch.depth;
   if (nbands(m) > 1) k = static_cast<int>(std::min<int64_t>(k, min_rows));
   *depth = std::max(k, 1);
-  *pair = pk > 0;
+  *il = ch.il;
   return LIFE_OK;
 }
 
@@ -503,6 +499,12 @@ int multi_set_option(MultiState* m, int option, int64_t value) {
                          kPairMaxDepthHost);
       m->pair_depth = static_cast<int>(value);
       return LIFE_OK;
+    case LIFE_OPT_QUAD_DEPTH:
+      if (value < -1 || value > kQuadMaxDepthHost)
+        return set_error(LIFE_ERR_CONFIG, "LIFE_OPT_QUAD_DEPTH must be in [-1, %d]",
+                         kQuadMaxDepthHost);
+      m->quad_depth = static_cast<int>(value);
+      return LIFE_OK;
     default:
       return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
   }
@@ -514,6 +516,7 @@ int multi_get_option(MultiState* m, int option, int64_t* value) {
     case LIFE_OPT_HALO: *value = m->halo; return LIFE_OK;
     case LIFE_OPT_BATCH_TRAPEZOID: *value = 0; return LIFE_OK;
     case LIFE_OPT_PAIR_DEPTH: *value = m->pair_depth; return LIFE_OK;
+    case LIFE_OPT_QUAD_DEPTH: *value = m->quad_depth; return LIFE_OK;
     default: return set_error(LIFE_ERR_CONFIG, "unknown option %d", option);
   }
 }
@@ -565,7 +568,7 @@ int multi_upload_packed(MultiState* m, const uint64_t* words, int64_t w, int64_t
   LIFE_TRY(set_dims(m, w, h));
   if (wpr < ceil_div(w, 64)) return set_error(LIFE_ERR_CONFIG, "words_per_row < ceil(W/64)");
   m->cur = 0;
-  m->pair = false;
+  m->il = 0;
   for (Band& b : m->bands) {
     LIFE_TRY(use(b));
     LIFE_TRY(copy_band_rows(m, const_cast<uint64_t*>(words) + b.y0 * wpr, wpr, b.buf[0], b.rows,
@@ -584,7 +587,7 @@ int multi_upload_u8(MultiState* m, const uint8_t* cells, int64_t w, int64_t h, i
   const int64_t bp = life_byte_pitch(w);
   const int64_t chunk = std::max<int64_t>(1, kScratchBytes / bp);
   m->cur = 0;
-  m->pair = false;
+  m->il = 0;
   for (Band& b : m->bands) {
     LIFE_TRY(use(b));
     LIFE_TRY(ensure_scratch(b, std::min(chunk, b.rows) * bp));
@@ -606,7 +609,7 @@ int multi_init_random(MultiState* m, int64_t w, int64_t h, double density, uint6
     return set_error(LIFE_ERR_CONFIG, "density must be in [0, 1], got %f", density);
   LIFE_TRY(set_dims(m, w, h));
   m->cur = 0;
-  m->pair = false;
+  m->il = 0;
   for (Band& b : m->bands) {  // band rows y0.. of random_fill's row-major stream
     LIFE_TRY(use(b));
     LIFE_TRY(life_dev_packed_random(b.buf[0], m->pitch, w, b.y0, b.rows, density, seed, b.main));
@@ -774,9 +777,9 @@ int multi_run(MultiState* m, int64_t generations, int engine, int temporal_depth
   LIFE_TRY(check_run_args(generations, checkpoints, n_checkpoints, populations));
   LIFE_TRY(check_loaded(m));
   int depth = 0;
-  bool pair = false;
-  LIFE_TRY(run_depth(m, temporal_depth, &depth, &pair));
-  if (generations > 0) LIFE_TRY(pair ? to_pair(m) : to_plain(m));
+  int il = 0;
+  LIFE_TRY(run_depth(m, temporal_depth, &depth, &il));
+  if (generations > 0) LIFE_TRY(il != 0 ? to_il(m, il) : to_plain(m));
   if (m->halo == LIFE_HALO_COPY) LIFE_TRY(ensure_ghosts(m));
   const int n = nbands(m);
   for (Band& b : m->bands) {
@@ -816,7 +819,7 @@ int multi_run(MultiState* m, int64_t generations, int engine, int temporal_depth
       src[i] = m->bands[i].buf[m->cur];
       dst[i] = m->bands[i].buf[m->cur ^ 1];
     }
-    LIFE_TRY(issue_pass(m, src.data(), dst.data(), p, k, kprev, m->pair));
+    LIFE_TRY(issue_pass(m, src.data(), dst.data(), p, k, kprev, m->il));
     m->cur ^= 1;
     done += k;
     kprev = k;
@@ -868,9 +871,9 @@ int multi_run_batch(MultiState* m, const uint64_t* const* inputs, uint64_t* cons
     return set_error(LIFE_ERR_CONFIG, "words_per_row < ceil(W/64)");
   LIFE_TRY(set_dims(m, width, height));  // band layout (the resident grid is not used)
   int depth = 0;
-  bool pair = false;
-  LIFE_TRY(run_depth(m, temporal_depth, &depth, &pair));
-  if (generations == 0) pair = false;
+  int il = 0;
+  LIFE_TRY(run_depth(m, temporal_depth, &depth, &il));
+  if (generations == 0) il = 0;
   if (n == 0) return LIFE_OK;
   if (m->halo == LIFE_HALO_COPY) LIFE_TRY(ensure_ghosts(m));
   const int nb = nbands(m);
@@ -937,8 +940,8 @@ int multi_run_batch(MultiState* m, const uint64_t* const* inputs, uint64_t* cons
       LIFE_TRY(copy_band_rows(m, const_cast<uint64_t*>(inputs[i]) + bd.y0 * words_per_row,
                               words_per_row, bd.batch[2 * slot], bd.rows, true, bd.h2d));
       LIFE_TRY(launch_mask_tail(bd.batch[2 * slot], m->pitch, width, bd.rows, bd.h2d));
-      if (pair)  // the band's rows into the interleaved-pair layout, behind their copy
-        LIFE_TRY(packed_zip(bd.batch[2 * slot], m->pitch, width, 0, bd.rows, /*unzip=*/false,
+      if (il != 0)  // the band's rows into the pair / quad layout, behind their copy
+        LIFE_TRY(packed_zip(il, bd.batch[2 * slot], m->pitch, width, 0, bd.rows, /*unzip=*/false,
                             bd.h2d));
       LIFE_CUDA(cudaEventRecord(up[b][i], bd.h2d));
     }
@@ -961,7 +964,7 @@ int multi_run_batch(MultiState* m, const uint64_t* const* inputs, uint64_t* cons
         src[b] = m->bands[b].batch[2 * slot + (p & 1)];
         dst[b] = m->bands[b].batch[2 * slot + ((p & 1) ^ 1)];
       }
-      LIFE_TRY(issue_pass(m, src.data(), dst.data(), p_global, k, kprev, pair));
+      LIFE_TRY(issue_pass(m, src.data(), dst.data(), p_global, k, kprev, il));
       kprev = k;
       ++p_global;
     }
@@ -971,8 +974,8 @@ int multi_run_batch(MultiState* m, const uint64_t* const* inputs, uint64_t* cons
       LIFE_TRY(use(bd));
       LIFE_CUDA(cudaEventRecord(comp[b][i], bd.main));
       LIFE_CUDA(cudaStreamWaitEvent(bd.d2h, comp[b][i], 0));
-      if (pair)  // back to the plain layout (only this band's kernels wrote the result buffer)
-        LIFE_TRY(packed_zip(bd.batch[2 * slot + (passes & 1)], m->pitch, width, 0, bd.rows,
+      if (il != 0)  // back to the plain layout (only this band's kernels wrote the result buffer)
+        LIFE_TRY(packed_zip(il, bd.batch[2 * slot + (passes & 1)], m->pitch, width, 0, bd.rows,
                             /*unzip=*/true, bd.d2h));
       LIFE_TRY(copy_band_rows(m, outputs[i] + bd.y0 * words_per_row, words_per_row,
                               bd.batch[2 * slot + (passes & 1)], bd.rows, false, bd.d2h));

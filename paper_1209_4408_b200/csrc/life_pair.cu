@@ -1,5 +1,5 @@
-// life_pair.cu -- launchers of the interleaved-pair packed kernels
-// (kernels_pair.cuh): packed_pair_kernel<K> passes, the peer-mode edge strips
+// life_pair.cu -- launchers of the interleaved-layout packed kernels
+// (kernels_pair.cuh): packed_il_kernel<K, N> passes (N = 2 pair, 4 quad), the peer-mode edge strips
 // of multi-GPU row bands, and the in-place layout conversion.  Its own
 // translation unit so the K instantiations compile beside life_gpu.cu.
 #include <algorithm>
@@ -12,7 +12,8 @@
 using namespace lifegpu;
 using namespace lifegpu::detail;
 
-static_assert(kPairMaxDepth == kPairMaxDepthHost, "internal.h and kernels_pair.cuh disagree");
+static_assert(kPairMaxDepth == kPairMaxDepthHost && kQuadMaxDepth == kQuadMaxDepthHost,
+              "internal.h and kernels_pair.cuh disagree");
 
 namespace {
 
@@ -40,12 +41,12 @@ int launch_pdl_pair(Kernel kernel, unsigned blocks, unsigned threads, size_t sme
 // warp, kWarps warps per block, one block per SM; the segment count minimises
 // (block waves) x (rows per tile + pipeline fill), the cost model of
 // launch_packed_kernel (life_gpu.cu).
-template <int K, bool PEER>
+template <int K, int N, bool PEER>
 int launch_pair(PackedStepArgs a, cudaStream_t s) {
-  using T = PairTraits<K>;
+  using T = PairTraits<K, N>;
   // Peer-mode edge strips are 2K rows: always the single-loop-body variant.
-  const auto kernel = packed_pair_kernel<K, PEER, PEER>;
-  const auto kernel_uni = packed_pair_kernel<K, true, PEER>;
+  const auto kernel = packed_il_kernel<K, N, PEER, PEER>;
+  const auto kernel_uni = packed_il_kernel<K, N, true, PEER>;
   static DeviceCache ready;  // per instantiation
   int dev = 0;
   cudaGetDevice(&dev);
@@ -57,7 +58,7 @@ int launch_pair(PackedStepArgs a, cudaStream_t s) {
                                    T::kWarps * T::kRingBytes));
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, 32 * T::kWarps,
                                                             T::kWarps * T::kRingBytes));
-    if (bps < 1) return set_error(LIFE_ERR_CUDA, "packed_pair_kernel<%d> does not fit an SM", K);
+    if (bps < 1) return set_error(LIFE_ERR_CUDA, "packed_il_kernel<%d, %d> does not fit an SM", K, N);
     ready.put(dev, bps);
   }
   int wpb = static_cast<int>(std::min<int64_t>(knob("LIFE_PAIR_WPB", T::kWarps), T::kWarps));
@@ -96,7 +97,7 @@ int launch_pair(PackedStepArgs a, cudaStream_t s) {
   LIFE_TRY(launch_pdl_pair(a.seg_rows <= kUniMaxRows ? kernel_uni : kernel,
                            static_cast<unsigned>(blocks), 32 * wpb,
                            static_cast<size_t>(wpb) * T::kRingBytes, s, a));
-  LIFE_CHECK_LAUNCH("packed_pair_kernel");
+  LIFE_CHECK_LAUNCH("packed_il_kernel");
   return LIFE_OK;
 }
 
@@ -104,25 +105,35 @@ using PairLauncher = int (*)(PackedStepArgs, cudaStream_t);
 template <bool PEER>
 struct PairTable {
   static constexpr PairLauncher v[kPairMaxDepth + 1] = {
-      nullptr,              launch_pair<1, PEER>,  launch_pair<2, PEER>,  launch_pair<3, PEER>,
-      launch_pair<4, PEER>, launch_pair<5, PEER>,  launch_pair<6, PEER>,  launch_pair<7, PEER>,
-      launch_pair<8, PEER>, launch_pair<9, PEER>,  launch_pair<10, PEER>, launch_pair<11, PEER>,
-      launch_pair<12, PEER>};
+      nullptr,                 launch_pair<1, 2, PEER>,  launch_pair<2, 2, PEER>,
+      launch_pair<3, 2, PEER>, launch_pair<4, 2, PEER>,  launch_pair<5, 2, PEER>,
+      launch_pair<6, 2, PEER>, launch_pair<7, 2, PEER>,  launch_pair<8, 2, PEER>,
+      launch_pair<9, 2, PEER>, launch_pair<10, 2, PEER>, launch_pair<11, 2, PEER>,
+      launch_pair<12, 2, PEER>};
+};
+template <bool PEER>
+struct QuadTable {
+  static constexpr PairLauncher v[kQuadMaxDepth + 1] = {
+      nullptr,                 launch_pair<1, 4, PEER>, launch_pair<2, 4, PEER>,
+      launch_pair<3, 4, PEER>, launch_pair<4, 4, PEER>, launch_pair<5, 4, PEER>,
+      launch_pair<6, 4, PEER>};
 };
 
-int fill_args(PackedStepArgs* a, const uint32_t* in, int64_t in_pitch, int64_t in_row0,
+int fill_args(int il, PackedStepArgs* a, const uint32_t* in, int64_t in_pitch, int64_t in_row0,
               int64_t in_rows, uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
               int64_t out_rows, int32_t generations) {
-  if (generations < 1 || generations > kPairMaxDepth)
-    return set_error(LIFE_ERR_CONFIG, "pair-layout temporal depth must be in [1, %d], got %d",
-                     kPairMaxDepth, generations);
-  if (width < 64 || width % 64 != 0)
-    return set_error(LIFE_ERR_CONFIG, "the pair layout needs W %% 64 == 0, got %lld",
-                     static_cast<long long>(width));
+  if (il != 2 && il != 4)
+    return set_error(LIFE_ERR_CONFIG, "interleave order must be 2 (pair) or 4 (quad), got %d", il);
+  if (generations < 1 || generations > il_max_depth(il))
+    return set_error(LIFE_ERR_CONFIG, "%s-layout temporal depth must be in [1, %d], got %d",
+                     il == 4 ? "quad" : "pair", il_max_depth(il), generations);
+  if (!il_eligible(il, width))
+    return set_error(LIFE_ERR_CONFIG, "the %s layout needs W %% %d == 0, got %lld",
+                     il == 4 ? "quad" : "pair", 32 * il, static_cast<long long>(width));
   if (in_rows < 1 || out_rows < 0 || in_pitch < width / 32 || out_pitch < width / 32 ||
-      in_pitch % 2 != 0 || out_pitch % 2 != 0 || reinterpret_cast<uintptr_t>(in) % 8 != 0 ||
-      reinterpret_cast<uintptr_t>(out) % 8 != 0)
-    return set_error(LIFE_ERR_CONFIG, "bad pair step geometry");
+      in_pitch % il != 0 || out_pitch % il != 0 || reinterpret_cast<uintptr_t>(in) % (4 * il) != 0 ||
+      reinterpret_cast<uintptr_t>(out) % (4 * il) != 0)
+    return set_error(LIFE_ERR_CONFIG, "bad interleaved step geometry");
   *a = PackedStepArgs{};
   a->in = in;
   a->in_pitch = in_pitch;
@@ -133,7 +144,7 @@ int fill_args(PackedStepArgs* a, const uint32_t* in, int64_t in_pitch, int64_t i
   a->out_row0 = out_row0;
   a->width = width;
   a->out_rows = out_rows;
-  a->nw = static_cast<int32_t>(width / 64);  // groups
+  a->nw = static_cast<int32_t>(width / (32 * il));  // groups
   a->n_strips = static_cast<int32_t>(ceil_div(a->nw + 1, kStripStride));
   a->strips_total = a->n_strips;
   a->tail_mask = 0xffffffffu;
@@ -145,51 +156,59 @@ int fill_args(PackedStepArgs* a, const uint32_t* in, int64_t in_pitch, int64_t i
 namespace lifegpu {
 namespace detail {
 
-int packed_pair_step(const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
-                     uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
-                     int64_t out_rows, int32_t generations, cudaStream_t stream) {
+int packed_il_step(int il, const uint32_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
+                   uint32_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
+                   int64_t out_rows, int32_t generations, cudaStream_t stream) {
   PackedStepArgs a;
-  LIFE_TRY(fill_args(&a, in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
+  LIFE_TRY(fill_args(il, &a, in, in_pitch, in_row0, in_rows, out, out_pitch, out_row0, width,
                      out_rows, generations));
   if (out_rows == 0) return LIFE_OK;
-  return PairTable<false>::v[generations](a, stream);
+  return il == 4 ? QuadTable<false>::v[generations](a, stream)
+                 : PairTable<false>::v[generations](a, stream);
 }
 
-int packed_pair_step_peer(const uint32_t* in, const uint32_t* up, int64_t up_rows,
-                          const uint32_t* down, int64_t down_rows, int64_t pitch,
-                          int64_t band_rows, uint32_t* out, int64_t out_row0, int64_t out_rows,
-                          int64_t width, int32_t generations, cudaStream_t stream) {
+int packed_il_step_peer(int il, const uint32_t* in, const uint32_t* up, int64_t up_rows,
+                        const uint32_t* down, int64_t down_rows, int64_t pitch,
+                        int64_t band_rows, uint32_t* out, int64_t out_row0, int64_t out_rows,
+                        int64_t width, int32_t generations, cudaStream_t stream) {
   if (!up || !down) return set_error(LIFE_ERR_CONFIG, "bad peer step geometry");
   if (band_rows < generations || up_rows < generations || down_rows < generations)
     return set_error(LIFE_ERR_TOO_MANY_PARTS, "bands must be at least %d rows", generations);
   if (out_row0 < 0 || out_rows < 0 || out_row0 + out_rows > band_rows)
     return set_error(LIFE_ERR_CONFIG, "output rows outside the band");
   PackedStepArgs a;
-  LIFE_TRY(fill_args(&a, in, pitch, out_row0, band_rows, out, pitch, out_row0, width, out_rows,
-                     generations));
+  LIFE_TRY(fill_args(il, &a, in, pitch, out_row0, band_rows, out, pitch, out_row0, width,
+                     out_rows, generations));
   if (out_rows == 0) return LIFE_OK;
   a.up = up;
   a.down = down;
   a.up_rows = up_rows;
   a.down_rows = down_rows;
   a.peer = 1;
-  return PairTable<true>::v[generations](a, stream);
+  return il == 4 ? QuadTable<true>::v[generations](a, stream)
+                 : PairTable<true>::v[generations](a, stream);
 }
 
-int packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
+int packed_zip(int il, uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
                bool unzip, cudaStream_t stream) {
-  if (width < 64 || width % 64 != 0 || pitch < width / 32 || pitch % 2 != 0 ||
-      reinterpret_cast<uintptr_t>(words) % 8 != 0 || rows < 0 || row0 < 0)
-    return set_error(LIFE_ERR_CONFIG, "bad pair layout conversion geometry");
+  if (!il_eligible(il, width) || pitch < width / 32 || pitch % il != 0 ||
+      reinterpret_cast<uintptr_t>(words) % (4 * il) != 0 || rows < 0 || row0 < 0)
+    return set_error(LIFE_ERR_CONFIG, "bad layout conversion geometry");
   if (rows == 0) return LIFE_OK;
-  const int64_t groups = width / 64;
+  const int64_t groups = width / (32 * il);
   const int64_t bx = ceil_div(groups, 256);
   const int64_t by = std::max<int64_t>(1, std::min<int64_t>(rows, (int64_t(sm_count()) * 64) / bx));
   const dim3 grid(static_cast<unsigned>(bx), static_cast<unsigned>(std::min<int64_t>(by, 65535)));
-  if (unzip)
-    packed_zip_kernel<true><<<grid, 256, 0, stream>>>(words, pitch, groups, row0, rows);
-  else
-    packed_zip_kernel<false><<<grid, 256, 0, stream>>>(words, pitch, groups, row0, rows);
+  if (il == 4) {
+    if (unzip)
+      packed_zip_kernel<true, 4><<<grid, 256, 0, stream>>>(words, pitch, groups, row0, rows);
+    else
+      packed_zip_kernel<false, 4><<<grid, 256, 0, stream>>>(words, pitch, groups, row0, rows);
+  } else if (unzip) {
+    packed_zip_kernel<true, 2><<<grid, 256, 0, stream>>>(words, pitch, groups, row0, rows);
+  } else {
+    packed_zip_kernel<false, 2><<<grid, 256, 0, stream>>>(words, pitch, groups, row0, rows);
+  }
   LIFE_CHECK_LAUNCH("packed_zip_kernel");
   return LIFE_OK;
 }

@@ -79,7 +79,7 @@ def test_local_peer_bands_match_oracle(oracle, W, H, P, depth, gens):
     assert np.array_equal(got, want)
 
 
-def _ipc_worker(rank, world, port, W, H, depth, gens, q, pair=False):
+def _ipc_worker(rank, world, port, W, H, depth, gens, q, il=0):
     import os
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -92,7 +92,7 @@ def _ipc_worker(rank, world, port, W, H, depth, gens, q, pair=False):
         from paper_1209_4408_b200.bands import PeerBandDriver, make_geometry
         dev = torch.device("cuda", 0)
         torch.cuda.set_device(dev)
-        drv = PeerBandDriver(make_geometry(W, H, rank, world, depth, pair), dev)
+        drv = PeerBandDriver(make_geometry(W, H, rank, world, depth, il), dev)
         drv.init_random(0.4, 5)
         # gloo => host barrier per pass: no kernel waits on another
         cps = drv.run(gens, checkpoints=[0, 5, 11, gens])  # passes split at 5 and 11
@@ -107,21 +107,22 @@ def _ipc_worker(rank, world, port, W, H, depth, gens, q, pair=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("W,pair", [(500, False), (512, True)], ids=["plain", "pair"])
-def test_peer_driver_ipc_two_processes_one_gpu(oracle, W, pair):
+@pytest.mark.parametrize("W,depth,il", [(500, 8, 0), (576, 8, 2), (512, 6, 4)],
+                         ids=["plain", "pair", "quad"])
+def test_peer_driver_ipc_two_processes_one_gpu(oracle, W, depth, il):
     """PeerBandDriver across two processes sharing cuda:0 through CUDA IPC
     handles (host barrier between passes, so no kernel waits on another); also
-    on the interleaved-pair layout (bands converted before the first barrier)."""
+    on the pair and quad layouts (bands converted before the first barrier)."""
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
     s.close()
-    H, depth, gens = 90, 8, 27
+    H, gens = 90, 27
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, W, H, depth, gens, q, pair))
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, W, H, depth, gens, q, il))
              for r in range(2)]
     for p in procs:
         p.start()

@@ -1,4 +1,5 @@
-"""The interleaved-pair kernel (kernels_pair.cuh, W % 64 == 0) behind every
+"""The pair- and quad-layout kernels (kernels_pair.cuh; interleave order 2: W %
+64 == 0, order 4: W % 128 == 0) behind every
 caller of the packed step besides life_run: life_run_batch (whole-grid and
 trapezoid schedules), the multi-device context (row bands, peer and copy
 halos, run and run_batch) and the device-buffer band drivers of
@@ -18,6 +19,8 @@ from paper_1209_4408_b200 import capi, life
 pytestmark = pytest.mark.gpu
 
 PACKED = capi.ENGINE_PACKED
+OPT = {2: capi.OPT_PAIR_DEPTH, 4: capi.OPT_QUAD_DEPTH}
+MAXK = {2: capi.PAIR_MAX_DEPTH, 4: capi.QUAD_MAX_DEPTH}
 
 
 def fnv(oracle, a) -> str:
@@ -31,17 +34,20 @@ def words_to_cells(words: np.ndarray, width: int) -> np.ndarray:
 
 
 # ---- life_run_batch ---------------------------------------------------------
-@pytest.mark.parametrize("W,H,G,pair", [(64, 50, 7, 3), (2048, 600, 25, 10), (1984, 333, 24, 12),
-                                        (128, 4099, 0, 8), (640, 1030, 5, 5),
-                                        (64, 33280, 8, 4),      # trapezoids + triangles
-                                        (128, 70000, 30, 10),   # ... 3 passes of 10
-                                        (192, 40000, 17, 7)])   # ... with a remainder pass
-def test_run_batch_pair(oracle, W, H, G, pair):
-    """life_run_batch with LIFE_OPT_PAIR_DEPTH forced: grids zipped after the
-    upload and unzipped before the download, also chunk by chunk on the
-    trapezoid schedule (forced on for the tall shapes) and in place."""
+@pytest.mark.parametrize("il,W,H,G,depth", [
+    (2, 64, 50, 7, 3), (2, 2048, 600, 25, 10), (2, 1984, 333, 24, 12), (2, 128, 4099, 0, 8),
+    (2, 640, 1030, 5, 5),
+    (2, 64, 33280, 8, 4),      # trapezoids + triangles
+    (2, 128, 70000, 30, 10),   # ... 3 passes of 10
+    (2, 192, 40000, 17, 7),    # ... with a remainder pass
+    (4, 128, 50, 7, 3), (4, 2048, 600, 25, 6), (4, 3968, 333, 24, 5), (4, 1280, 1030, 5, 4),
+    (4, 128, 33280, 8, 4), (4, 256, 70000, 30, 6), (4, 384, 40000, 17, 5)])
+def test_run_batch_pair(oracle, il, W, H, G, depth):
+    """life_run_batch with LIFE_OPT_PAIR_DEPTH / _QUAD_DEPTH forced: grids
+    zipped after the upload and unzipped before the download, also chunk by
+    chunk on the trapezoid schedule (forced on for the tall shapes) and in place."""
     with life.Engine(0) as e:
-        e.set_option(capi.OPT_PAIR_DEPTH, pair)
+        e.set_option(OPT[il], depth)
         if H >= 32768:
             e.set_option(capi.OPT_BATCH_TRAPEZOID, 1)
         grids = [oracle.random_fill(W, H, 0.35, 300 + i) for i in range(3)]
@@ -57,29 +63,30 @@ def test_run_batch_pair(oracle, W, H, G, pair):
 
 
 # ---- multi-device context ---------------------------------------------------
-def multi(n: int, halo_mode: int, pair: int) -> life.Engine:
+def multi(n: int, halo_mode: int, il: int, depth: int) -> life.Engine:
     e = life.Engine(devices=[0] * n)
     e.set_option(capi.OPT_HALO, halo_mode)
-    e.set_option(capi.OPT_PAIR_DEPTH, pair)
+    e.set_option(OPT[il], depth)
     return e
 
 
+@pytest.mark.parametrize("il", [2, 4], ids=["pair", "quad"])
 @pytest.mark.parametrize("halo_mode", [capi.HALO_PEER, capi.HALO_COPY], ids=["peer", "copy"])
 @pytest.mark.parametrize("n", [1, 2, 3, 8])
-def test_multi_pair_matches_oracle(oracle, halo_mode, n):
-    """Row bands on the pair layout: random W % 64 == 0 shapes, pair depths
-    1..12, checkpoint splits; grid, uint64 populations, windows across band
-    seams, hash and place on a grid left in the pair layout."""
-    rng = np.random.default_rng(500 + n)
+def test_multi_pair_matches_oracle(oracle, halo_mode, n, il):
+    """Row bands on the pair / quad layout: random shapes, every pass depth,
+    checkpoint splits; grid, uint64 populations, windows across band seams,
+    hash and place on a grid left in the interleaved layout."""
+    rng = np.random.default_rng(500 + n + il)
     for case in range(5):
-        w = 64 * int(rng.integers(1, 70))
+        w = 32 * il * int(rng.integers(1, 70))
         h = int(rng.integers(max(3, n), 220))
-        pair = int(rng.integers(1, 13))
+        pair = int(rng.integers(1, MAXK[il] + 1))
         gens = int(rng.integers(1, 50))
         g = oracle.random_fill(w, h, 0.35, int(rng.integers(1 << 30)))
         cps = sorted({0, gens, *[int(x) for x in rng.integers(0, gens + 1, 2)]})
         want, pops = oracle.run(g, gens, cps)
-        with multi(n, halo_mode, pair) as e, life.Engine(0) as one:
+        with multi(n, halo_mode, il, pair) as e, life.Engine(0) as one:
             e.upload(g)
             assert e.run(gens, PACKED, 0, cps) == pops, (w, h, gens, pair, n)
             assert e.population() == int(want.sum())
@@ -106,8 +113,9 @@ def test_multi_pair_run_batch(oracle):
     ins = [oracle.pack(g) for g in grids]
     outs = [np.zeros_like(p) for p in ins]
     wants = [oracle.run(g, G)[0] for g in grids]
-    for halo_mode in (capi.HALO_PEER, capi.HALO_COPY):
-        with multi(3, halo_mode, 9) as e:
+    for halo_mode, il, depth in ((capi.HALO_PEER, 2, 9), (capi.HALO_COPY, 2, 9),
+                                 (capi.HALO_PEER, 4, 5), (capi.HALO_COPY, 4, 6)):
+        with multi(3, halo_mode, il, depth) as e:
             assert e.run_batch(ins, outs, W, G, 0) > 0
             for want, out in zip(wants, outs):
                 assert np.array_equal(oracle.unpack(out, W), want)
@@ -116,10 +124,13 @@ def test_multi_pair_run_batch(oracle):
 
 
 def test_multi_pair_option(oracle):
-    with multi(2, capi.HALO_PEER, 5) as e:
+    with multi(2, capi.HALO_PEER, 2, 5) as e:
         assert e.get_option(capi.OPT_PAIR_DEPTH) == 5
+        assert e.get_option(capi.OPT_QUAD_DEPTH) == -1
         with pytest.raises(life.ConfigError):
             e.set_option(capi.OPT_PAIR_DEPTH, 13)
+        with pytest.raises(life.ConfigError):
+            e.set_option(capi.OPT_QUAD_DEPTH, 7)
         # W % 64 != 0: ignored, the plain kernels run
         g = oracle.random_fill(100, 40, 0.4, 3)
         e.upload(g)
@@ -128,14 +139,19 @@ def test_multi_pair_option(oracle):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("n", [2, 8])
-def test_cfg5_pair_band_seam_windows(oracle, n):
+@pytest.mark.parametrize("n,quad", [(2, -1), (8, -1), (8, 0)])
+def test_cfg5_pair_band_seam_windows(oracle, n, quad):
     """Config 5 as n bands at the engine's own choice (temporal_depth 0: the
-    pair kernel at K = 10): the reference's light-cone windows at T = 500,
-    including every band seam and both wrap corners."""
+    quad kernel at K = 6; with the quad layout off, the pair kernel at K =
+    10): the reference's light-cone windows at T = 500, including every band
+    seam and both wrap corners."""
+    import ctypes as C
     gold = load_golden("golden_cfg5_windows.json")
-    assert capi.lib().life_pair_auto_depth(262144, 262144 // n) == 10
+    d = C.c_int32(0)
+    il = capi.lib().life_interleave_auto(262144, 262144 // n, -1, quad, 0, C.byref(d))
+    assert (il, d.value) == ((4, 6) if quad < 0 else (2, 10))
     with life.Engine(devices=[0] * n) as e:
+        e.set_option(capi.OPT_QUAD_DEPTH, quad)
         e.init_random(262144, 262144, 0.4, 42)
         e.run(500, PACKED, 0)
         for w in gold["windows_500"]:
@@ -143,13 +159,14 @@ def test_cfg5_pair_band_seam_windows(oracle, n):
 
 
 # ---- device-buffer band drivers (bands.py) ----------------------------------
-@pytest.mark.parametrize("W,H,depth,gens", [(64, 37, 4, 13), (1984, 97, 12, 50),
-                                            (4096, 1025, 10, 100), (2112, 300, 1, 9)])
-def test_torus_driver_pair(oracle, W, H, depth, gens):
+@pytest.mark.parametrize("il,W,H,depth,gens", [
+    (2, 64, 37, 4, 13), (2, 1984, 97, 12, 50), (2, 4096, 1025, 10, 100), (2, 2112, 300, 1, 9),
+    (4, 128, 37, 4, 13), (4, 3968, 97, 6, 50), (4, 4096, 1025, 5, 100), (4, 4224, 300, 1, 9)])
+def test_torus_driver_pair(oracle, il, W, H, depth, gens):
     import torch
     from paper_1209_4408_b200.bands import TorusDriver, make_geometry
     dev = torch.device("cuda", 0)
-    drv = TorusDriver(make_geometry(W, H, 0, 1, depth, pair=True), dev)
+    drv = TorusDriver(make_geometry(W, H, 0, 1, depth, il), dev)
     drv.init_random(0.4, 9)
     g0 = oracle.random_fill(W, H, 0.4, 9)
     pops = drv.run(gens, checkpoints=[0, gens // 2, gens])
@@ -163,14 +180,16 @@ def test_torus_driver_pair(oracle, W, H, depth, gens):
     assert np.array_equal(words_to_cells(drv.band().cpu().numpy(), W), want)
 
 
-@pytest.mark.parametrize("W,H,P,depth,gens,overlap", [
-    (64, 37, 2, 4, 13, True), (1984, 97, 3, 12, 50, True), (1984, 97, 3, 12, 50, False),
-    (4096, 1025, 8, 10, 100, True), (40960, 12289 // 16, 8, 7, 30, True)])
-def test_local_bands_pair(oracle, W, H, P, depth, gens, overlap):
-    """Ghost-row bands (the NCCL scheme's addressing) on the pair layout."""
+@pytest.mark.parametrize("il,W,H,P,depth,gens,overlap", [
+    (2, 64, 37, 2, 4, 13, True), (2, 1984, 97, 3, 12, 50, True), (2, 1984, 97, 3, 12, 50, False),
+    (2, 4096, 1025, 8, 10, 100, True), (2, 40960, 12289 // 16, 8, 7, 30, True),
+    (4, 128, 37, 2, 4, 13, True), (4, 3968, 97, 3, 6, 50, True), (4, 3968, 97, 3, 6, 50, False),
+    (4, 4096, 1025, 8, 5, 100, True), (4, 40960, 12289 // 16, 8, 3, 30, True)])
+def test_local_bands_pair(oracle, il, W, H, P, depth, gens, overlap):
+    """Ghost-row bands (the NCCL scheme's addressing) on the pair / quad layout."""
     import torch
     from paper_1209_4408_b200.bands import LocalBands
-    lb = LocalBands(W, H, P, depth, torch.device("cuda", 0), overlap=overlap, pair=True)
+    lb = LocalBands(W, H, P, depth, torch.device("cuda", 0), overlap=overlap, il=il)
     lb.init_random(0.4, 9)
     lb.run(gens)
     torch.cuda.synchronize()
@@ -179,14 +198,16 @@ def test_local_bands_pair(oracle, W, H, P, depth, gens, overlap):
     assert np.array_equal(got, want)
 
 
-@pytest.mark.parametrize("W,H,P,depth,gens", [
-    (64, 37, 2, 4, 13), (1984, 97, 3, 12, 50), (4096, 1025, 8, 10, 100),
-    (40960, 12289 // 16, 8, 7, 30), (128, 40, 2, 12, 48), (2048, 300, 3, 1, 9)])
-def test_local_peer_bands_pair(oracle, W, H, P, depth, gens):
-    """In-kernel peer halos on the pair layout (life_dev_packed_step_pair_peer)."""
+@pytest.mark.parametrize("il,W,H,P,depth,gens", [
+    (2, 64, 37, 2, 4, 13), (2, 1984, 97, 3, 12, 50), (2, 4096, 1025, 8, 10, 100),
+    (2, 40960, 12289 // 16, 8, 7, 30), (2, 128, 40, 2, 12, 48), (2, 2048, 300, 3, 1, 9),
+    (4, 128, 37, 2, 4, 13), (4, 3968, 97, 3, 6, 50), (4, 4096, 1025, 8, 5, 100),
+    (4, 40960, 12289 // 16, 8, 3, 30), (4, 256, 40, 2, 6, 48), (4, 2048, 300, 3, 1, 9)])
+def test_local_peer_bands_pair(oracle, il, W, H, P, depth, gens):
+    """In-kernel peer halos on the pair / quad layout (life_dev_packed_step_il_peer)."""
     import torch
     from paper_1209_4408_b200.bands import LocalPeerBands
-    lb = LocalPeerBands(W, H, P, depth, torch.device("cuda", 0), pair=True)
+    lb = LocalPeerBands(W, H, P, depth, torch.device("cuda", 0), il=il)
     lb.init_random(0.4, 9)
     lb.run(gens)
     torch.cuda.synchronize()
@@ -198,6 +219,12 @@ def test_local_peer_bands_pair(oracle, W, H, P, depth, gens):
 def test_pair_geometry_errors():
     from paper_1209_4408_b200.bands import make_geometry
     with pytest.raises(life.ConfigError):
-        make_geometry(100, 50, 0, 1, 8, pair=True)   # W % 64 != 0
+        make_geometry(100, 50, 0, 1, 8, il=2)    # W % 64 != 0
     with pytest.raises(life.ConfigError):
-        make_geometry(128, 50, 0, 1, 13, pair=True)  # deeper than the pair kernel goes
+        make_geometry(128, 50, 0, 1, 13, il=2)   # deeper than the pair kernel goes
+    with pytest.raises(life.ConfigError):
+        make_geometry(192, 50, 0, 1, 4, il=4)    # W % 128 != 0
+    with pytest.raises(life.ConfigError):
+        make_geometry(256, 50, 0, 1, 7, il=4)    # deeper than the quad kernel goes
+    with pytest.raises(life.ConfigError):
+        make_geometry(256, 50, 0, 1, 4, il=3)
