@@ -41,10 +41,13 @@ constexpr int kQuadMaxDepth = 6;
 // and Q3's right neighbour need a funnel shift and a shuffle, so a group
 // costs 2 SHF + 2 SHFL + 36 LOP3 per 128 cell-updates: 9.5 integer ops per
 // 32.  Four words per stage halve the depth the registers allow (K <= 6).
+#ifndef LIFE_IL_PF
+#define LIFE_IL_PF 6
+#endif
 template <int K, int N>
 struct PairTraits {
   static_assert(N == 2 || N == 4, "two or four words per lane");
-  static constexpr int kPrefetch = 6;  // rows per loop trip (fetched that far ahead)
+  static constexpr int kPrefetch = LIFE_IL_PF;  // rows per loop trip (fetched that far ahead)
   // Warps per SM the registers allow (N words x K stages x 6 registers of
   // state per lane: N x K = 16 156 registers, 20 194, 24 234, no spills).
   static constexpr int kWarps = N * K <= 16 ? 12 : 8;
@@ -57,7 +60,7 @@ struct PairTraits {
 #define LIFE_PAIR_GROUP 2
 #endif
 #ifndef LIFE_QUAD_GROUP
-#define LIFE_QUAD_GROUP 1
+#define LIFE_QUAD_GROUP 2
 #endif
 // stages issued level by level together (N words each)
 template <int N>

@@ -15,6 +15,8 @@ engine = int(sys.argv[4]) if len(sys.argv) > 4 else capi.ENGINE_PACKED
 eng = life.Engine(0)
 if os.environ.get("KB_PAIR") is not None:  # LIFE_OPT_PAIR_DEPTH: -1 auto, 0 off, 1..12 forced
     eng.set_option(capi.OPT_PAIR_DEPTH, int(os.environ["KB_PAIR"]))
+if os.environ.get("KB_QUAD") is not None:  # LIFE_OPT_QUAD_DEPTH: -1 auto, 0 off, 1..6 forced
+    eng.set_option(capi.OPT_QUAD_DEPTH, int(os.environ["KB_QUAD"]))
 for (w, h) in shapes:
     eng.init_random(w, h, 0.4, 42)
     eng.run(max(depth, 1), engine, depth)
@@ -26,4 +28,4 @@ for (w, h) in shapes:
         eng.sync()
         best = min(best, time.perf_counter() - t)
     print(json.dumps({"lib": os.path.basename(os.environ.get("LIFE_GPU_LIB", "default")), "w": w, "h": h,
-                      "depth": depth, "pair": os.environ.get("KB_PAIR"), "engine": engine, "gcups": round(w * h * gens / best / 1e9, 1)}))
+                      "depth": depth, "pair": os.environ.get("KB_PAIR"), "quad": os.environ.get("KB_QUAD"), "engine": engine, "gcups": round(w * h * gens / best / 1e9, 1)}))
