@@ -166,7 +166,10 @@ int life_grid_hash(life_ctx* ctx, uint64_t* out);
 /* ---- the step loop ------------------------------------------------------ */
 /* Replaces run(Grid&&, RunConfig, checkpoints) (engine.cpp:162-214):
  *   `generations` >= 0 (ConfigError otherwise, engine.cpp:133-136);
- *   `temporal_depth`: generations per kernel pass, 0 = auto; packed 1..16,
+ *   `temporal_depth`: generations per kernel pass, 0 = auto (the
+ *     cluster-resident engine for small tori; the quad / pair layout kernels
+ *     for W % 128 / 64 == 0 tori of 2^30 cells or more, life_interleave_auto;
+ *     else life_packed_auto_depth); packed 1..16,
  *     byte 1..8 (W % 16 == 0 or W >= 33; narrower tori run one generation per pass);
  *   `checkpoints`: strictly ascending in [0, generations] (engine.cpp:137-147);
  *     `populations[i]` receives the population after checkpoints[i]
