@@ -1260,16 +1260,29 @@ bool resident_auto(int64_t w, int64_t h) {
 // passes run as one all-paths launch (W % 32 != 0, less than ~3 block waves
 // deep), where K = 12 fits 12 warps per SM instead of 8 (config 4: 37.5 ->
 // 38.6 T/s; kbench depth sweep).
-// temporal_depth 0 on W % 64 == 0 tori (or row bands of them, h rows tall) of
-// 2^30 cells or more: the quad layout at K = 6 where W % 128 == 0 (kbench,
-// T cell-updates/s, quad K = 4 / 5 / 6 vs pair K = 10 vs plain K = 16:
-// 262144^2 50.3 / 52.4 / 52.6 vs 49.8 vs 47.1; 65536^2 49.3 / 50.6 / 51.3 vs
-// 46.8 vs 44.5), else the pair layout at K = 10.  Smaller tori keep the plain
-// kernels (16384^2: quad 35.1, pair 35.9, plain 37.3: fewer, wider strips
-// waste more lanes and the one-wave tiles gain nothing from fewer ops).
+// temporal_depth 0 on tori (or row bands of them, h rows tall) of 2^29 cells
+// or more: the layout with the best lanes-per-op figure -- the share of a
+// strip's 32 lanes that hold cells (groups / (32 x strips), strips of 32
+// groups advancing by 31) over the network's ops per word (11 plain, 10 pair,
+// 9.5 quad).  Wide tori fill their strips in every layout and take quad at
+// K = 6; narrower ones waste the last strip of the wider groups and keep pair
+// (K = 10) or the plain kernels.  kbench, T cell-updates/s, plain K = 16 /
+// pair K = 10 / quad K = 6:
+//   262144^2      47.1 / 49.8 / 53.1     65536^2        44.5 / 46.8 / 51.5
+//   131072 x 8192 39.9 / 45.3 / 48.0     49152^2        44.2 / 47.0 / 50.0
+//   32768 x 65536 43.4 / 47.5 / 47.5     32768 x 16384  39.3 / 42.2 / 42.1
+//   16384 x 65536 42.2 / 43.2 / 40.9     8192 x 131072  40.4 / 39.3 / 34.9
+// Smaller tori keep the plain kernels (16384^2: 37.3 / 35.9 / 34.0: their
+// one-wave tiles are bounded by pipeline fill, not by the op count).
 namespace {
-constexpr int64_t kIlAutoCells = int64_t(1) << 30;
+constexpr int64_t kIlAutoCells = int64_t(1) << 29;
+double lanes_per_op(int il, int64_t w) {
+  const int64_t groups = il == 0 ? nw32(w) : w / (32 * il);
+  const int64_t strips = ceil_div(groups + 1, kStripStride);
+  const double ops = il == 4 ? 9.5 : il == 2 ? 10.0 : 11.0;
+  return static_cast<double>(groups) / static_cast<double>(32 * strips) / ops;
 }
+}  // namespace
 lifegpu::detail::IlChoice lifegpu::detail::il_choose(int64_t w, int64_t h, int pair_opt,
                                                      int quad_opt, int temporal_depth) {
   IlChoice c;
@@ -1280,12 +1293,15 @@ lifegpu::detail::IlChoice lifegpu::detail::il_choose(int64_t w, int64_t h, int p
     c.il = 2;
     c.depth = pair_opt;
   } else if (temporal_depth == 0 && w * h >= kIlAutoCells) {
-    if (quad_opt < 0 && il_eligible(4, w)) {
-      c.il = 4;
-      c.depth = 6;
-    } else if (pair_opt < 0 && il_eligible(2, w)) {
+    double best = lanes_per_op(0, w);
+    if (pair_opt < 0 && il_eligible(2, w) && lanes_per_op(2, w) > best) {
+      best = lanes_per_op(2, w);
       c.il = 2;
       c.depth = 10;
+    }
+    if (quad_opt < 0 && il_eligible(4, w) && lanes_per_op(4, w) > best) {
+      c.il = 4;
+      c.depth = 6;
     }
   }
   return c;

@@ -72,9 +72,9 @@ enum class Engine { Packed = LIFE_ENGINE_PACKED, Byte = LIFE_ENGINE_BYTE, Reside
 struct RunConfig {
   Engine engine = Engine::Packed;
   // Generations per kernel pass; 0 = auto: the cluster-resident engine for
-  // small W % 32 == 0 tori (<= 2^22 cells, one GPU); tori of 2^30 cells or
-  // more in the quad layout at 6 (W % 128 == 0) or the pair layout at 10
-  // (W % 64 == 0) (life_interleave_auto); else 16 -- 12 for W % 32 != 0 tori
+  // small W % 32 == 0 tori (<= 2^22 cells, one GPU); tori of 2^29 cells or
+  // more in the quad layout at 6 (W % 128 == 0, wide) or the pair layout at
+  // 10 (W % 64 == 0) (life_interleave_auto); else 16 -- 12 for W % 32 != 0 tori
   // less than ~3 block waves deep (life_packed_auto_depth).
   int temporal_depth = 0;
   int workers = 1;  // validated like the reference (>= 1, <= rows)

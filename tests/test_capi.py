@@ -97,3 +97,36 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".hpp", ".cpp")):
                 text = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", text).replace("oracle/", ""), f
+
+
+def test_interleave_auto_rule(lib):
+    """life_interleave_auto (host logic): the layout and depth temporal_depth 0
+    picks by width and size, the LIFE_OPT_PAIR_DEPTH / _QUAD_DEPTH overrides,
+    and that an explicit temporal_depth keeps the plain kernels."""
+    def pick(w, h, pair=-1, quad=-1, td=0):
+        d = C.c_int32(-1)
+        il = lib.life_interleave_auto(w, h, pair, quad, td, C.byref(d))
+        return il, d.value
+    # wide tori: quad K = 6; 16384..32768 columns: pair K = 10; narrow or small: plain
+    assert pick(262144, 262144) == (4, 6)           # config 5
+    assert pick(262144, 32768) == (4, 6)            # ... one of 8 row bands
+    assert pick(65536, 65536) == (4, 6)             # config 3
+    assert pick(49152, 49152) == (4, 6)
+    assert pick(32768, 32768) == (2, 10)
+    assert pick(16384, 65536) == (2, 10)
+    assert pick(8192, 131072) == (0, 0)
+    assert pick(16384, 16384) == (0, 0)             # config 2: below 2^29 cells
+    assert pick(40961, 12289) == (0, 0)             # config 4: W % 64 != 0
+    assert pick(262208, 262144) == (2, 10)          # W % 128 != 0, W % 64 == 0
+    # options: 0 disables a layout, > 0 forces it where the width allows
+    assert pick(262144, 262144, quad=0) == (2, 10)
+    assert pick(262144, 262144, pair=0, quad=0) == (0, 0)
+    assert pick(1024, 100, quad=3) == (4, 3)
+    assert pick(1024, 100, pair=7) == (2, 7)
+    assert pick(1024, 100, pair=7, quad=3) == (4, 3)
+    assert pick(192, 100, pair=7, quad=3) == (2, 7)  # W % 128 != 0: the quad option is skipped
+    assert pick(100, 100, pair=7, quad=3) == (0, 0)
+    # explicit depth: plain kernels unless forced
+    assert pick(262144, 262144, td=16) == (0, 0)
+    assert pick(262144, 262144, quad=5, td=16) == (4, 5)
+    assert pick(0, 10) == (0, 0)
