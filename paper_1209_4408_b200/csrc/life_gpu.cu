@@ -1928,19 +1928,66 @@ namespace {
 // B - kShrink*(p+2), exactly where triangle pass p stops reading; triangles
 // run after both neighbouring trapezoids.  Middle grids keep whole-grid
 // passes (their copies overlap the neighbouring grids' compute anyway).
+//
+// Chunk heights (round 2): only the chunks whose own copy is exposed need to
+// be small -- the first ones of a grid no earlier grid computes behind, the
+// last ones of a grid no later grid computes behind.  A chunk computes
+// `growth` times longer than it takes to copy (generations x ~0.009: PCIe
+// moves ~4e11 cells/s, the kernels ~4.5e13 cell-updates/s), so each chunk may
+// be up to that much taller than the one before it and still find its rows
+// arrived: heights grow geometrically from the exposed end(s) and the rest
+// of the grid is one chunk -- 7 chunks for one config-5 grid instead of 32
+// equal ones, a quarter of the launches, and most rows run in tall
+// trapezoids at whole-grid speed.  (32 equal chunks, the round-1 schedule:
+// e2e / value 0.967 at K = 16 but 0.936 at the quad kernel's K = 6, whose 84
+// passes make 5376 small launches per chunked grid.)  Few generations per
+// byte copied (growth < 1.5) keep equal chunks.
 #ifndef LIFE_TRAP_CHUNKS
-#define LIFE_TRAP_CHUNKS 32  // e2e / value on config 5: 8 chunks 0.945, 16 0.953, 32 0.967, 48 0.955, 64 0.940
+#define LIFE_TRAP_CHUNKS 32  // most chunks per grid (equal chunks: 8 0.945, 16 0.953, 32 0.967, 48 0.955)
 #endif
 constexpr int kTrapChunks = LIFE_TRAP_CHUNKS;
 #ifndef LIFE_TRAP_MIN_ROWS
-#define LIFE_TRAP_MIN_ROWS 8192
+#define LIFE_TRAP_MIN_ROWS 8192  // equal chunks shorter than this run their passes too slowly
 #endif
 constexpr int64_t kTrapMinChunkRows = LIFE_TRAP_MIN_ROWS;
+constexpr int kSmallFirst = 1, kSmallLast = 2;
+
+// Cut points of a chunked grid into bounds[0..n]; returns n (0: does not fit).
+// min_rows: the shortest chunk (its trapezoid must survive every pass).
+int plan_chunks(int64_t height, int64_t min_rows, double growth, int profile, int64_t* bounds) {
+  std::vector<int64_t> head, tail;
+  int64_t rem = height, cur = min_rows;
+  while (true) {
+    const int64_t last = head.empty() ? (tail.empty() ? 0 : tail.back()) : head.back();
+    const int64_t need = ((profile & kSmallFirst) ? cur : 0) + ((profile & kSmallLast) ? cur : 0);
+    if (last > 0 && static_cast<double>(rem) <= growth * static_cast<double>(last)) break;
+    if (rem - need < min_rows || static_cast<int>(head.size() + tail.size()) + 3 > kTrapChunks) break;
+    if (profile & kSmallFirst) head.push_back(cur);
+    if (profile & kSmallLast) tail.push_back(cur);
+    rem -= need;
+    cur = static_cast<int64_t>(std::min(static_cast<double>(cur) * growth, 4e18));
+  }
+  if (head.empty() && tail.empty()) return 0;
+  int n = 0;
+  bounds[0] = 0;
+  for (int64_t v : head) {
+    bounds[n + 1] = bounds[n] + v;
+    ++n;
+  }
+  bounds[n + 1] = bounds[n] + rem;  // the rest of the grid: one chunk
+  ++n;
+  for (auto it = tail.rbegin(); it != tail.rend(); ++it) {
+    bounds[n + 1] = bounds[n] + *it;
+    ++n;
+  }
+  return n;
+}
 
 struct BatchGeom {
   int64_t width, height, wpr, words_per_row, pitch, generations;
   int depth, passes;
   int il;  // 2 / 4: passes on the pair / quad layout (zip after upload, unzip before download)
+  int nchunks;  // chunks of the grid being scheduled
   int64_t bounds[kTrapChunks + 1];
 };
 
@@ -2063,19 +2110,25 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   g.il = il;
   g.passes = static_cast<int>(ceil_div(generations, depth));
   // Chunked first/last grid when every chunk outlives its shrinking
-  // trapezoid with room to spare and the chunks are tall enough for their
-  // passes to run near full speed (the schedule launches 2 x 16 small passes
-  // per pass): measured e2e / device value, 3 grids, with / without it:
-  // config 5 (16384-row chunks) 0.965 / 0.882, config 3 (4096-row chunks)
-  // 0.850 / 0.945.  LIFE_OPT_BATCH_TRAPEZOID 0 / 1 forces it off / on (when it fits).
+  // trapezoid with room to spare.  LIFE_OPT_BATCH_TRAPEZOID 0 / 1 forces it
+  // off / on (when it fits); auto: grids of 32768 rows or more.
   const int64_t kShrink = depth;  // rows per side a pass gives up
   const int trap_env = c->batch_trap;
-  const bool fits = n >= 1 && generations > 0 &&
-                    height / kTrapChunks >= 2 * kShrink * g.passes + 1024;
-  const bool trap = !resident && fits &&
-                    (trap_env == 1 || (trap_env != 0 && height / kTrapChunks >= kTrapMinChunkRows));
+  const int64_t min_chunk = std::max<int64_t>(2 * kShrink * g.passes + 1024, 2048);
+  const double growth = std::min(std::max(double(generations) * 0.007, 1.0), 6.0);
+  const bool geometric = growth >= 1.5;
+  // Plans for a grid that is first, last, or both: the chunk count of the
+  // most demanding one decides whether the schedule fits.
+  auto plan = [&](int profile, int64_t* bounds) -> int {
+    if (geometric) return plan_chunks(height, min_chunk, growth, profile, bounds);
+    if (height / kTrapChunks < min_chunk) return 0;
+    return life_band_bounds(height, kTrapChunks, bounds) == LIFE_OK ? kTrapChunks : 0;
+  };
+  const bool fits = n >= 1 && generations > 0 && !resident &&
+                    plan(n == 1 ? (kSmallFirst | kSmallLast) : kSmallFirst, g.bounds) >= 2;
+  const bool tall = geometric ? height >= 32768 : height / kTrapChunks >= kTrapMinChunkRows;
+  const bool trap = fits && (trap_env == 1 || (trap_env != 0 && tall));
   if (trap) {
-    LIFE_TRY(life_band_bounds(height, kTrapChunks, g.bounds));
     for (auto& st : c->cs)
       if (!st) LIFE_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   }
@@ -2097,14 +2150,24 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
     LIFE_TRY(mk(&comp[i]));
     LIFE_TRY(mk(&down[i]));
   }
-  cudaEvent_t chunk_up[kTrapChunks], trap_done[kTrapChunks], tri_done[kTrapChunks];
+  // LIFE_BATCH_TRACE (debug builds): timed chunk events of the last chunked grid on stderr.
+  static const bool trace_chunks = knob("LIFE_BATCH_TRACE", 0) != 0;
+  const unsigned chunk_flags = trace_chunks ? cudaEventDefault : cudaEventDisableTiming;
+  cudaEvent_t chunk_up[kTrapChunks], trap_done[kTrapChunks], tri_done[kTrapChunks],
+      chunk_down[kTrapChunks], strip_down[kTrapChunks];
   if (trap) {
     for (int i = 0; i < kTrapChunks; ++i) {
-      LIFE_TRY(mk(&chunk_up[i]));
-      LIFE_TRY(mk(&trap_done[i]));
-      LIFE_TRY(mk(&tri_done[i]));
+      LIFE_TRY(mk(&chunk_up[i], chunk_flags));
+      LIFE_TRY(mk(&trap_done[i], chunk_flags));
+      LIFE_TRY(mk(&tri_done[i], chunk_flags));
+      if (trace_chunks) {
+        LIFE_TRY(mk(&chunk_down[i], chunk_flags));
+        LIFE_TRY(mk(&strip_down[i], chunk_flags));
+      }
     }
   }
+  int traced_nc = 0;
+  int64_t traced_bounds[kTrapChunks + 1] = {0};
   cudaEvent_t t0, t1;
   LIFE_TRY(mk(&t0, cudaEventDefault));
   LIFE_TRY(mk(&t1, cudaEventDefault));
@@ -2112,17 +2175,35 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   const int P = g.passes;
   LIFE_CUDA(cudaEventRecord(t0, c->h2d));
   int rc = LIFE_OK;
+  // The passes of consecutive grids run one grid after another: each grid
+  // fills the GPU by itself, and passes of two grids launched side by side
+  // (programmatic dependent launch) park early blocks of the one on the SMs
+  // the other could be using (config 5, 3 grids: 2.17 s side by side, against
+  // 1.94 s of passes).  main_done: the previous grid's whole-grid passes, or
+  // its trapezoids and triangles, are complete.  (Triangles left running
+  // beside the next grid's passes get an SM only at its block-wave
+  // boundaries: their 84 small launches then outlast it, and the grid after
+  // it, which reuses the chunked grid's buffers, uploads late.)
+  cudaEvent_t main_done = nullptr;
+  cudaEvent_t tri_join[2] = {nullptr, nullptr};
+  if (trap)
+    for (auto& e : tri_join) LIFE_TRY(mk(&e));
   for (int32_t i = 0; i < n && rc == LIFE_OK; ++i) {
     uint32_t* buf[2] = {c->batch[2 * (i & 1)], c->batch[2 * (i & 1) + 1]};
     // Upload grid i into its slot once grid i-2 has left it.
     if (i >= 2) LIFE_CUDA(cudaStreamWaitEvent(c->h2d, down[i - 2], 0));
-    const bool chunked = trap && (i == 0 || i == n - 1);
+    // Chunk plan of a first / last grid (small chunks where its own copy is exposed).
+    const int nc = trap && (i == 0 || i == n - 1)
+                       ? plan((i == 0 ? kSmallFirst : 0) | (i == n - 1 ? kSmallLast : 0), g.bounds)
+                       : 0;
+    const bool chunked = nc >= 2;
     if (!chunked) {
       LIFE_CUDA(cudaMemcpy2DAsync(buf[0], pitch * 4, inputs[i], words_per_row * 8, wpr * 8, height,
                                   cudaMemcpyHostToDevice, c->h2d));
       LIFE_CUDA(cudaEventRecord(up[i], c->h2d));
       // Compute on the context stream.
       LIFE_CUDA(cudaStreamWaitEvent(c->stream, up[i], 0));
+      if (main_done) LIFE_CUDA(cudaStreamWaitEvent(c->stream, main_done, 0));
       const int64_t mask_n = height * (pitch - nw + 1);
       packed_mask_tail_kernel<<<grid_stride_blocks(mask_n, 256), 256, 0, c->stream>>>(
           buf[0], pitch, nw, tail_mask(width), height);
@@ -2136,6 +2217,7 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
         if (g.il != 0 && rc == LIFE_OK) rc = zip_rows(g, buf[P & 1], 0, height, /*unzip=*/true, c->stream);
       }
       LIFE_CUDA(cudaEventRecord(comp[i], c->stream));
+      main_done = comp[i];
       // Download on the D2H stream.
       LIFE_CUDA(cudaStreamWaitEvent(c->d2h, comp[i], 0));
       LIFE_CUDA(cudaMemcpy2DAsync(outputs[i], words_per_row * 8, buf[resident ? 1 : (P & 1)],
@@ -2143,19 +2225,20 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
       LIFE_CUDA(cudaEventRecord(down[i], c->d2h));
       continue;
     }
-    const int nc = kTrapChunks;
+    g.nchunks = nc;
     const int64_t shrink = kShrink * P;  // rows per side the trapezoid gives up
     for (int ch = 0; ch < nc; ++ch) {
       const int64_t y0 = g.bounds[ch], rows = g.bounds[ch + 1] - y0;
       LIFE_TRY(copy_rows(g, const_cast<uint64_t*>(inputs[i]), buf[0], y0, rows, true, c->h2d));
       LIFE_CUDA(cudaEventRecord(chunk_up[ch], c->h2d));
     }
-    // Trapezoids in chunk order on two streams (so they finish one after
+    // Trapezoids in chunk order on one stream (so they finish one after
     // another and their interiors leave early), each as soon as its chunk has
-    // arrived; triangles on the other two streams, each as soon as its two
+    // arrived; triangles on two other streams, each as soon as its two
     // trapezoids are done.
+    if (main_done) LIFE_CUDA(cudaStreamWaitEvent(c->cs[0], main_done, 0));
     for (int ch = 0; ch < nc && rc == LIFE_OK; ++ch) {
-      cudaStream_t st = c->cs[ch % 2];
+      cudaStream_t st = c->cs[0];  // one after another: a chunk's rows leave as early as possible
       const int64_t y0 = g.bounds[ch], rows = g.bounds[ch + 1] - y0;
       LIFE_CUDA(cudaStreamWaitEvent(st, chunk_up[ch], 0));
       const int64_t mask_n = rows * (pitch - nw + 1);
@@ -2165,7 +2248,7 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
       if (g.il != 0) LIFE_TRY(zip_rows(g, buf[0], y0, rows, /*unzip=*/false, st));
       for (int p = 0; p < P && rc == LIFE_OK; ++p)
         rc = pass_rows(g, buf, p, y0 + kShrink * (p + 1), rows - 2 * kShrink * (p + 1), st,
-                       &c->split[1 + ch % 2]);
+                       &c->split[1]);
       // The interior leaves in the plain layout; the triangles never read
       // these rows of the final buffer (their last read of it, pass P-2,
       // stays within kShrink * P rows of the boundary).
@@ -2186,22 +2269,38 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
         rc = zip_rows(g, buf[P & 1], g.bounds[b] - shrink, 2 * shrink, /*unzip=*/true, st);
       LIFE_CUDA(cudaEventRecord(tri_done[b], st));
     }
-    // Downloads: each chunk's interior when its trapezoid is done, then the
-    // boundary strips.
-    for (int ch = 0; ch <= nc; ++ch) {
-      if (ch < nc) {
-        const int64_t y0 = g.bounds[ch], rows = g.bounds[ch + 1] - y0;
-        LIFE_CUDA(cudaStreamWaitEvent(c->d2h, trap_done[ch], 0));
-        LIFE_TRY(
-            copy_rows(g, outputs[i], buf[P & 1], y0 + shrink, rows - 2 * shrink, false, c->d2h));
-      }
-      if (ch >= 1) {  // boundary ch (ch == nc: the seam, boundary 0)
-        const int b = ch % nc;
-        LIFE_CUDA(cudaStreamWaitEvent(c->d2h, tri_done[b], 0));
-        LIFE_TRY(copy_rows(g, outputs[i], buf[P & 1], g.bounds[b] - shrink, 2 * shrink, false,
-                           c->d2h));
-      }
+    // The next grid's passes start when this grid's launches are all done:
+    // join the triangle streams into the trapezoid stream.
+    for (int k = 0; k < 2; ++k) {
+      LIFE_CUDA(cudaEventRecord(tri_join[k], c->cs[2 + k]));
+      LIFE_CUDA(cudaStreamWaitEvent(c->cs[0], tri_join[k], 0));
     }
+    LIFE_CUDA(cudaEventRecord(comp[i], c->cs[0]));
+    main_done = comp[i];
+    // Downloads: each chunk's interior as soon as its trapezoid is done, on
+    // the D2H stream; the boundary strips on a second copy stream (cs[1]), so
+    // a triangle still running -- its small launches wait for the trapezoid
+    // passes to free SM slots -- never holds up the interiors behind it.
+    cudaStream_t strips = c->cs[1];
+    for (int ch = 0; ch < nc; ++ch) {
+      const int64_t y0 = g.bounds[ch], rows = g.bounds[ch + 1] - y0;
+      LIFE_CUDA(cudaStreamWaitEvent(c->d2h, trap_done[ch], 0));
+      LIFE_TRY(copy_rows(g, outputs[i], buf[P & 1], y0 + shrink, rows - 2 * shrink, false, c->d2h));
+      if (trace_chunks) LIFE_CUDA(cudaEventRecord(chunk_down[ch], c->d2h));
+    }
+    for (int bi = 1; bi <= nc; ++bi) {  // the order the triangles were launched in
+      const int b = bi % nc;
+      LIFE_CUDA(cudaStreamWaitEvent(strips, tri_done[b], 0));
+      LIFE_TRY(copy_rows(g, outputs[i], buf[P & 1], g.bounds[b] - shrink, 2 * shrink, false,
+                         strips));
+      if (trace_chunks) LIFE_CUDA(cudaEventRecord(strip_down[b], strips));
+    }
+    cudaEvent_t strips_done;
+    LIFE_TRY(mk(&strips_done));
+    LIFE_CUDA(cudaEventRecord(strips_done, strips));
+    LIFE_CUDA(cudaStreamWaitEvent(c->d2h, strips_done, 0));
+    traced_nc = nc;
+    for (int ch = 0; ch <= nc; ++ch) traced_bounds[ch] = g.bounds[ch];
     LIFE_CUDA(cudaEventRecord(down[i], c->d2h));
   }
   LIFE_CUDA(cudaEventRecord(t1, c->d2h));
@@ -2212,6 +2311,19 @@ int life_run_batch(life_ctx* c, const uint64_t* const* inputs, uint64_t* const* 
   float ms = 0;
   LIFE_CUDA(cudaEventElapsedTime(&ms, t0, t1));
   if (elapsed_ms) *elapsed_ms = ms;
+  if (trace_chunks && traced_nc > 0 && rc == LIFE_OK) {
+    std::fprintf(stderr, "life_run_batch trace (n = %d, total %.1f ms): chunk rows  up  trap  down | boundary tri  strip-down\n", n, ms);
+    for (int ch = 0; ch < traced_nc; ++ch) {
+      float a = 0, b = 0, d = 0, e = 0, f = 0;
+      cudaEventElapsedTime(&a, t0, chunk_up[ch]);
+      cudaEventElapsedTime(&b, t0, trap_done[ch]);
+      cudaEventElapsedTime(&d, t0, chunk_down[ch]);
+      cudaEventElapsedTime(&e, t0, tri_done[ch]);
+      cudaEventElapsedTime(&f, t0, strip_down[ch]);
+      std::fprintf(stderr, "  %2d %7lld  %7.1f %7.1f %7.1f | %7.1f %7.1f\n", ch,
+                   static_cast<long long>(traced_bounds[ch + 1] - traced_bounds[ch]), a, b, d, e, f);
+    }
+  }
   return rc;
 }
 

@@ -228,3 +228,27 @@ def test_pair_geometry_errors():
         make_geometry(256, 50, 0, 1, 7, il=4)    # deeper than the quad kernel goes
     with pytest.raises(life.ConfigError):
         make_geometry(256, 50, 0, 1, 4, il=3)
+
+
+@pytest.mark.parametrize("il,W,H,G,depth", [(0, 96, 60000, 260, 16), (2, 64, 50000, 240, 10),
+                                            (4, 128, 60000, 300, 6), (4, 128, 40000, 215, 5)])
+def test_run_batch_geometric_chunks(oracle, il, W, H, G, depth):
+    """Enough generations per byte copied for the geometric chunk plan of the
+    trapezoid schedule (growth >= 1.5): small chunks first in the first grid,
+    last in the last grid, at both ends of a single grid; in place too."""
+    with life.Engine(0) as e:
+        if il:
+            e.set_option(OPT[il], depth)
+        e.set_option(capi.OPT_BATCH_TRAPEZOID, 1)
+        grids = [oracle.random_fill(W, H, 0.35, 700 + i) for i in range(3)]
+        wants = [oracle.run(g, G)[0] for g in grids]
+        for n in (1, 2, 3):
+            ins = [oracle.pack(g) for g in grids[:n]]
+            outs = [np.zeros_like(p) for p in ins]
+            e.run_batch(ins, outs, W, G, 0 if il else depth)
+            for want, out in zip(wants, outs):
+                assert np.array_equal(oracle.unpack(out, W), want), (n,)
+        ins = [oracle.pack(g) for g in grids]
+        e.run_batch(ins, ins, W, G, 0 if il else depth)
+        for want, out in zip(wants, ins):
+            assert np.array_equal(oracle.unpack(out, W), want)
