@@ -1405,7 +1405,7 @@ def main() -> None:
                          "rule when --depth is 0 too, 0 = off, 1..12 = forced depth")
     ap.add_argument("--quad-depth", type=int, default=-1,
                     help="quad-layout kernel (W %% 128 == 0 tori): -1 = auto, 0 = off, "
-                         "1..6 = forced depth")
+                         "1..7 = forced depth")
     ap.add_argument("--gens", type=int, default=0, help="override the config's generations")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

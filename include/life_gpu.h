@@ -101,7 +101,7 @@ int life_ctx_bands(life_ctx* ctx, int32_t* n, int64_t* bounds, int32_t* devices,
 #define LIFE_OPT_BATCH_TRAPEZOID 2 /* life_run_batch first/last-grid chunk schedule: -1 auto, 0, 1 */
 #define LIFE_OPT_HALO 3            /* multi-device halo scheme: LIFE_HALO_PEER / LIFE_HALO_COPY */
 #define LIFE_OPT_PAIR_DEPTH 4      /* pair-layout kernel (W % 64 == 0): -1 auto, 0 off, 1..12 forced depth */
-#define LIFE_OPT_QUAD_DEPTH 5      /* quad-layout kernel (W % 128 == 0): -1 auto, 0 off, 1..6 forced depth */
+#define LIFE_OPT_QUAD_DEPTH 5      /* quad-layout kernel (W % 128 == 0): -1 auto, 0 off, 1..7 forced depth */
 #define LIFE_HALO_PEER 0           /* edge-strip kernels read neighbour rows over NVLink (P2P) */
 #define LIFE_HALO_COPY 1           /* neighbour rows copied into local ghost rows, then computed */
 int life_ctx_set_option(life_ctx* ctx, int32_t option, int64_t value);
@@ -204,7 +204,7 @@ int life_packed_auto_depth(int64_t width, int64_t height);
  * LIFE_OPT_QUAD_DEPTH values (-1 = the defaults) and the call's
  * temporal_depth: returns the interleave order -- 4 = the quad layout
  * (packed_il_kernel<K, 4>: W % 128 == 0, 9.5 integer ops per 32 cell-updates,
- * K <= 6), 2 = the pair layout (packed_il_kernel<K, 2>: W % 64 == 0, 10 ops,
+ * K <= 7), 2 = the pair layout (packed_il_kernel<K, 2>: W % 64 == 0, 10 ops,
  * K <= 12), 0 = the plain-layout kernels (11 ops) -- and writes the pass depth
  * to *depth (0 with order 0: life_packed_auto_depth applies).  With both
  * options at -1 and temporal_depth 0, tori of 2^29 cells or more run the
@@ -284,7 +284,7 @@ int life_dev_packed_step_peer(const uint32_t* in, const uint32_t* up, int64_t up
  * converts rows [row0, row0 + rows) in place (to_interleaved 1: plain ->
  * interleaved, 0: back).  The _il step / run / step_peer calls are
  * life_dev_packed_step / _run / _step_peer on buffers in that layout,
- * `generations` / `depth` in 1..12 (pair) or 1..6 (quad).  Populations
+ * `generations` / `depth` in 1..12 (pair) or 1..7 (quad).  Populations
  * (popcounts) are layout-independent; everything else reads the plain layout. */
 int life_dev_packed_zip(uint32_t* words, int64_t pitch, int64_t width, int64_t row0, int64_t rows,
                         int32_t order, int32_t to_interleaved, void* stream);

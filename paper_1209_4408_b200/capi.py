@@ -27,7 +27,7 @@ ENGINE_BYTE = 1
 ENGINE_RESIDENT = 2
 MAX_TEMPORAL_DEPTH = 16
 PAIR_MAX_DEPTH = 12  # packed_il_kernel<K, 2> (W % 64 == 0)
-QUAD_MAX_DEPTH = 6   # packed_il_kernel<K, 4> (W % 128 == 0)
+QUAD_MAX_DEPTH = 7   # packed_il_kernel<K, 4> (W % 128 == 0)
 MAX_BYTE_DEPTH = 8
 
 OPT_PROFILE = 1

@@ -97,7 +97,7 @@ int packed_run(uint32_t* buf_a, uint32_t* buf_b, int64_t pitch, int64_t width, i
 // 6 generations per pass at 9.5 ops.  Order 0 = the plain layout.
 // packed_zip converts rows in place.
 constexpr int kPairMaxDepthHost = 12;
-constexpr int kQuadMaxDepthHost = 6;
+constexpr int kQuadMaxDepthHost = 7;
 inline bool il_eligible(int il, int64_t width) {
   return (il == 2 || il == 4) && width >= 32 * il && width % (32 * il) == 0;
 }

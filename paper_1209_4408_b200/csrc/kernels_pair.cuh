@@ -32,7 +32,7 @@
 namespace lifegpu {
 
 constexpr int kPairMaxDepth = 12;
-constexpr int kQuadMaxDepth = 6;
+constexpr int kQuadMaxDepth = 7;
 
 // N = words per lane: 2 = the pair layout above; 4 = the QUAD layout, the same
 // idea one level further: a group is 128 columns (two uint64 of the exchange
@@ -40,7 +40,7 @@ constexpr int kQuadMaxDepth = 6;
 // Q1 and Q2 find both neighbours aligned in Q0/Q2 and Q1/Q3; only Q0's left
 // and Q3's right neighbour need a funnel shift and a shuffle, so a group
 // costs 2 SHF + 2 SHFL + 36 LOP3 per 128 cell-updates: 9.5 integer ops per
-// 32.  Four words per stage halve the depth the registers allow (K <= 6).
+// 32.  Four words per stage halve the depth the registers allow (K <= 7).
 #ifndef LIFE_IL_PF
 #define LIFE_IL_PF 6
 #endif
@@ -79,8 +79,8 @@ __device__ __forceinline__ void cp_async_lane(uint32_t* smem_dst, const void* gm
 // The pair store of one output row: lanes 1..30 one 8-byte vector, the two
 // shared lanes the 16-bit halves they own -- predicates, no branch.
 __device__ __forceinline__ void st_pair_if(char* p, uint32_t e, uint32_t o, bool mid, bool edge,
-                                           uint32_t eoff, uint32_t esh) {
-  char* q = p + eoff;
+                                           uint32_t esh) {
+  char* q = p;  // edge lanes: p already points at the half they own
   asm volatile(
       "{\n .reg .pred a, b;\n setp.ne.u32 a, %3, 0;\n setp.ne.u32 b, %4, 0;\n"
       " @a st.global.v2.u32 [%0], {%1, %2};\n"
@@ -91,8 +91,8 @@ __device__ __forceinline__ void st_pair_if(char* p, uint32_t e, uint32_t o, bool
 }
 
 __device__ __forceinline__ void st_quad_if(char* p, const uint32_t (&w)[4], bool mid, bool edge,
-                                           uint32_t eoff, uint32_t esh) {
-  char* q = p + eoff;
+                                           uint32_t esh) {
+  char* q = p;  // edge lanes: p already points at the half they own
   asm volatile(
       "{\n .reg .pred a, b;\n setp.ne.u32 a, %5, 0;\n setp.ne.u32 b, %6, 0;\n"
       " @a st.global.v4.u32 [%0], {%1, %2, %3, %4};\n"
@@ -160,17 +160,37 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
     ++lrow;
   };
 
+  // The PF rows of one loop trip, one commit group each, into ring slots
+  // slot0 .. slot0 + PF - 1.  The torus row wrap is tested once per trip
+  // (warp-uniform): a trip that does not cross it takes its rows at constant
+  // offsets from one address.
+  auto issue_trip = [&](int slot0) {
+    if (!PEER && lrow + PF <= in_rows) {
+      const char* p0 = row_addr(in_lane, static_cast<uint32_t>(lrow), in_pitch_b);
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        cp_async_lane<N>(ring + (slot0 + u) * LW, p0 + static_cast<size_t>(u) * in_pitch_b);
+        cp_async_commit();
+      }
+      lrow = (lrow + PF == in_rows) ? 0 : lrow + PF;
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) issue(slot0 + u);
+  };
+
   const bool in_grid = gi >= 0 && gi < a.nw;
   const bool st_mid = in_grid && lane >= 1 && lane <= 30;
   const bool st_edge = in_grid && (lane == 0 || lane == 31);
-  const uint32_t eoff = lane == 0 ? 2u : 0u;   // lane 0 owns the group's upper half: the high halves
+  // lane 0 owns the group's upper half: the high halves of its words, two
+  // bytes into each -- folded into the lane's output base once
   const uint32_t esh = lane == 0 ? 16u : 0u;
   char* const out_seg =
-      reinterpret_cast<char*>(a.out + (a.out_row0 + y) * a.out_pitch + N * (in_grid ? gi : 0));
+      reinterpret_cast<char*>(a.out + (a.out_row0 + y) * a.out_pitch + N * (in_grid ? gi : 0)) +
+      (lane == 0 ? 2 : 0);
   const uint32_t out_pitch_b = static_cast<uint32_t>(a.out_pitch * 4);
 
-#pragma unroll
-  for (int u = 0; u < PF; ++u) issue(u);
+  issue_trip(0);
 
   HSum sa[K][N], sb[K][N];
   uint32_t self[K][N], x[K][N];
@@ -188,10 +208,12 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
   auto trip = [&](const int t, auto kind_tag) {
     constexpr int KIND = decltype(kind_tag)::value;
     constexpr bool FILL = KIND == kFill;
+    issue_trip(half ^ PF);  // the next trip's rows
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
-      issue((half ^ PF) + u);
-      cp_async_wait<PF>();
+      // row u of this trip: issued one trip ago, PF - 1 - u rows of that trip
+      // and the PF just issued may still be in flight
+      cp_async_wait_dyn<2 * PF - 1>(u);
       if constexpr (N == 2) {
         const uint2 v = *reinterpret_cast<const uint2*>(ring + (half + u) * LW);
         x[0][0] = v.x;
@@ -261,9 +283,9 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
           const bool ok = static_cast<unsigned>(j) < static_cast<unsigned>(n);
           char* p = const_cast<char*>(row_addr(out_seg, static_cast<uint32_t>(j), out_pitch_b));
           if constexpr (N == 2) {
-            st_pair_if(p, y_last[0], y_last[1], st_mid && ok, st_edge && ok, eoff, esh);
+            st_pair_if(p, y_last[0], y_last[1], st_mid && ok, st_edge && ok, esh);
           } else {
-            st_quad_if(p, y_last, st_mid && ok, st_edge && ok, eoff, esh);
+            st_quad_if(p, y_last, st_mid && ok, st_edge && ok, esh);
           }
         } else if (KIND == kSteady || static_cast<unsigned>(j) < static_cast<unsigned>(n)) {
           char* p = const_cast<char*>(row_addr(out_seg, static_cast<uint32_t>(j), out_pitch_b));
@@ -276,7 +298,7 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
           if (st_edge) {
 #pragma unroll
             for (int r = 0; r < N; ++r)
-              *reinterpret_cast<uint16_t*>(p + eoff + 4 * r) = static_cast<uint16_t>(y_last[r] >> esh);
+              *reinterpret_cast<uint16_t*>(p + 4 * r) = static_cast<uint16_t>(y_last[r] >> esh);
           }
         }
       }

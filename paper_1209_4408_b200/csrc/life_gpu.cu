@@ -1265,13 +1265,13 @@ bool resident_auto(int64_t w, int64_t h) {
 // strip's 32 lanes that hold cells (groups / (32 x strips), strips of 32
 // groups advancing by 31) over the network's ops per word (11 plain, 10 pair,
 // 9.5 quad).  Wide tori fill their strips in every layout and take quad at
-// K = 6; narrower ones waste the last strip of the wider groups and keep pair
-// (K = 10) or the plain kernels.  kbench, T cell-updates/s, plain K = 16 /
-// pair K = 10 / quad K = 6:
-//   262144^2      47.1 / 49.8 / 53.1     65536^2        44.5 / 46.8 / 51.5
-//   131072 x 8192 39.9 / 45.3 / 48.0     49152^2        44.2 / 47.0 / 50.0
-//   32768 x 65536 43.4 / 47.5 / 47.5     32768 x 16384  39.3 / 42.2 / 42.1
-//   16384 x 65536 42.2 / 43.2 / 40.9     8192 x 131072  40.4 / 39.3 / 34.9
+// K = 7 (2^31 cells or more) or 6; narrower ones waste the last strip of the
+// wider groups and keep pair (K = 10) or the plain kernels.  kbench, T
+// cell-updates/s, plain K = 16 / pair K = 10 / quad K = 6 / quad K = 7:
+//   262144^2      47.1 / 51.1 / 53.1 / 54.0   65536^2       44.5 / 48.1 / 52.2 / 52.8
+//   131072 x 8192 39.9 / 45.3 / 48.7 / 48.1   32768^2       41.7 / 46.4 / 46.0 / 45.6
+//   32768 x 65536 43.4 / 47.5 / 47.5          32768 x 16384 39.3 / 42.2 / 42.1
+//   16384 x 65536 42.2 / 43.2 / 40.9          8192 x 131072 40.4 / 39.3 / 34.9
 // Smaller tori keep the plain kernels (16384^2: 37.3 / 35.9 / 34.0: their
 // one-wave tiles are bounded by pipeline fill, not by the op count).
 namespace {
@@ -1300,8 +1300,8 @@ lifegpu::detail::IlChoice lifegpu::detail::il_choose(int64_t w, int64_t h, int p
       c.depth = 10;
     }
     if (quad_opt < 0 && il_eligible(4, w) && lanes_per_op(4, w) > best) {
-      c.il = 4;
-      c.depth = 6;
+      c.il = 4;  // K = 7 (243 registers) pays on the largest tori only
+      c.depth = w * h >= (int64_t(1) << 31) ? 7 : 6;
     }
   }
   return c;

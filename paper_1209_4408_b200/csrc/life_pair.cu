@@ -116,7 +116,7 @@ struct QuadTable {
   static constexpr PairLauncher v[kQuadMaxDepth + 1] = {
       nullptr,                 launch_pair<1, 4, PEER>, launch_pair<2, 4, PEER>,
       launch_pair<3, 4, PEER>, launch_pair<4, 4, PEER>, launch_pair<5, 4, PEER>,
-      launch_pair<6, 4, PEER>};
+      launch_pair<6, 4, PEER>, launch_pair<7, 4, PEER>};
 };
 
 int fill_args(int il, PackedStepArgs* a, const uint32_t* in, int64_t in_pitch, int64_t in_row0,

@@ -102,5 +102,22 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// cp.async.wait_group (MAX - u) for a loop index u the unroller has made a
+// constant (the operand must be an immediate).
+template <int MAX>
+__device__ __forceinline__ void cp_async_wait_dyn(int u) {
+  switch (u) {
+    case 0: cp_async_wait<MAX>(); break;
+    case 1: cp_async_wait<(MAX > 1 ? MAX - 1 : 0)>(); break;
+    case 2: cp_async_wait<(MAX > 2 ? MAX - 2 : 0)>(); break;
+    case 3: cp_async_wait<(MAX > 3 ? MAX - 3 : 0)>(); break;
+    case 4: cp_async_wait<(MAX > 4 ? MAX - 4 : 0)>(); break;
+    case 5: cp_async_wait<(MAX > 5 ? MAX - 5 : 0)>(); break;
+    case 6: cp_async_wait<(MAX > 6 ? MAX - 6 : 0)>(); break;
+    case 7: cp_async_wait<(MAX > 7 ? MAX - 7 : 0)>(); break;
+    default: cp_async_wait<0>(); break;
+  }
+}
+
 
 }  // namespace lifegpu

@@ -108,10 +108,11 @@ def test_interleave_auto_rule(lib):
         il = lib.life_interleave_auto(w, h, pair, quad, td, C.byref(d))
         return il, d.value
     # wide tori: quad K = 6; 16384..32768 columns: pair K = 10; narrow or small: plain
-    assert pick(262144, 262144) == (4, 6)           # config 5
-    assert pick(262144, 32768) == (4, 6)            # ... one of 8 row bands
-    assert pick(65536, 65536) == (4, 6)             # config 3
-    assert pick(49152, 49152) == (4, 6)
+    assert pick(262144, 262144) == (4, 7)           # config 5
+    assert pick(262144, 32768) == (4, 7)            # ... one of 8 row bands
+    assert pick(65536, 65536) == (4, 7)             # config 3
+    assert pick(49152, 49152) == (4, 7)
+    assert pick(65536, 16384) == (4, 6)             # below 2^31 cells
     assert pick(32768, 32768) == (2, 10)
     assert pick(16384, 65536) == (2, 10)
     assert pick(8192, 131072) == (0, 0)

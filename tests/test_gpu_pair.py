@@ -41,7 +41,7 @@ SHAPES = [(64, 3), (64, 40), (128, 33), (192, 100), (1920, 50), (1984, 77), (204
 
 
 @pytest.mark.parametrize("layout,depth", [(PAIR, d) for d in (1, 2, 3, 5, 8, 10, 12)] +
-                         [(QUAD, d) for d in (1, 2, 3, 4, 5, 6)],
+                         [(QUAD, d) for d in (1, 2, 3, 4, 5, 6, 7)],
                          ids=lambda v: v if isinstance(v, int) else f"order{v[0]}")
 def test_pair_depths_match_oracle(pair_engine, oracle, layout, depth):
     e = pair_engine
@@ -123,7 +123,7 @@ def test_pair_option_validation(pair_engine):
     with pytest.raises(life.ConfigError):
         e.set_option(capi.OPT_PAIR_DEPTH, -2)
     with pytest.raises(life.ConfigError):
-        e.set_option(capi.OPT_QUAD_DEPTH, 7)
+        e.set_option(capi.OPT_QUAD_DEPTH, 8)
     # W % 128 != 0 with both forced: the quad option is skipped, pair runs
     e.set_option(capi.OPT_QUAD_DEPTH, 4)
     e.set_option(capi.OPT_PAIR_DEPTH, 8)
@@ -148,7 +148,7 @@ def _check_schedule(e, oracle, gold):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("layout,depth", [(PAIR, 8), (PAIR, 10), (QUAD, 5), (QUAD, 6)],
+@pytest.mark.parametrize("layout,depth", [(PAIR, 8), (PAIR, 10), (QUAD, 5), (QUAD, 6), (QUAD, 7)],
                          ids=lambda v: v if isinstance(v, int) else f"order{v[0]}")
 def test_pair_cfg2_golden(pair_engine, oracle, layout, depth):
     """Config 2 (16384^2, 1000 generations) on the pair / quad kernel against
@@ -162,11 +162,11 @@ def test_pair_cfg2_golden(pair_engine, oracle, layout, depth):
 
 @pytest.mark.slow
 def test_pair_cfg3_golden(pair_engine, oracle):
-    """Config 3 (65536^2) at the auto rule's choice (temporal_depth 0: quad, K = 6),
+    """Config 3 (65536^2) at the auto rule's choice (temporal_depth 0: quad, K = 7),
     then with the quad layout off (pair, K = 10)."""
     import ctypes as C
     d = C.c_int32(0)
-    assert capi.lib().life_interleave_auto(65536, 65536, -1, -1, 0, C.byref(d)) == 4 and d.value == 6
+    assert capi.lib().life_interleave_auto(65536, 65536, -1, -1, 0, C.byref(d)) == 4 and d.value == 7
     assert capi.lib().life_interleave_auto(65536, 65536, -1, 0, 0, C.byref(d)) == 2 and d.value == 10
     assert capi.lib().life_interleave_auto(65536, 65536, -1, -1, 16, C.byref(d)) == 0
     assert capi.lib().life_interleave_auto(16384, 16384, -1, -1, 0, C.byref(d)) == 0

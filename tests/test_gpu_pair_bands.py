@@ -130,7 +130,7 @@ def test_multi_pair_option(oracle):
         with pytest.raises(life.ConfigError):
             e.set_option(capi.OPT_PAIR_DEPTH, 13)
         with pytest.raises(life.ConfigError):
-            e.set_option(capi.OPT_QUAD_DEPTH, 7)
+            e.set_option(capi.OPT_QUAD_DEPTH, 8)
         # W % 64 != 0: ignored, the plain kernels run
         g = oracle.random_fill(100, 40, 0.4, 3)
         e.upload(g)
@@ -142,14 +142,14 @@ def test_multi_pair_option(oracle):
 @pytest.mark.parametrize("n,quad", [(2, -1), (8, -1), (8, 0)])
 def test_cfg5_pair_band_seam_windows(oracle, n, quad):
     """Config 5 as n bands at the engine's own choice (temporal_depth 0: the
-    quad kernel at K = 6; with the quad layout off, the pair kernel at K =
+    quad kernel at K = 7; with the quad layout off, the pair kernel at K =
     10): the reference's light-cone windows at T = 500, including every band
     seam and both wrap corners."""
     import ctypes as C
     gold = load_golden("golden_cfg5_windows.json")
     d = C.c_int32(0)
     il = capi.lib().life_interleave_auto(262144, 262144 // n, -1, quad, 0, C.byref(d))
-    assert (il, d.value) == ((4, 6) if quad < 0 else (2, 10))
+    assert (il, d.value) == ((4, 7) if quad < 0 else (2, 10))
     with life.Engine(devices=[0] * n) as e:
         e.set_option(capi.OPT_QUAD_DEPTH, quad)
         e.init_random(262144, 262144, 0.4, 42)
@@ -225,7 +225,7 @@ def test_pair_geometry_errors():
     with pytest.raises(life.ConfigError):
         make_geometry(192, 50, 0, 1, 4, il=4)    # W % 128 != 0
     with pytest.raises(life.ConfigError):
-        make_geometry(256, 50, 0, 1, 7, il=4)    # deeper than the quad kernel goes
+        make_geometry(256, 50, 0, 1, 8, il=4)    # deeper than the quad kernel goes
     with pytest.raises(life.ConfigError):
         make_geometry(256, 50, 0, 1, 4, il=3)
 

@@ -15,7 +15,7 @@ engine = int(sys.argv[4]) if len(sys.argv) > 4 else capi.ENGINE_PACKED
 eng = life.Engine(0)
 if os.environ.get("KB_PAIR") is not None:  # LIFE_OPT_PAIR_DEPTH: -1 auto, 0 off, 1..12 forced
     eng.set_option(capi.OPT_PAIR_DEPTH, int(os.environ["KB_PAIR"]))
-if os.environ.get("KB_QUAD") is not None:  # LIFE_OPT_QUAD_DEPTH: -1 auto, 0 off, 1..6 forced
+if os.environ.get("KB_QUAD") is not None:  # LIFE_OPT_QUAD_DEPTH: -1 auto, 0 off, 1..7 forced
     eng.set_option(capi.OPT_QUAD_DEPTH, int(os.environ["KB_QUAD"]))
 for (w, h) in shapes:
     eng.init_random(w, h, 0.4, 42)
