@@ -251,7 +251,13 @@ constexpr int kPathFast = 0, kPathSeam = 1, kPathGeneral = 2;
 // row test as a store predicate): short tiles no longer run the cold check-
 // trip copies (16384^2 +1.4 %, 8192^2 +3.8 %; 65536^2 -0.5 %, so long tiles
 // keep the steady/check split).
-template <int K, int PATH, int PF = PackedTraits<K>::kPrefetch, bool UNI = false>
+// TRIP: the PF rows of a loop trip are requested together at its start (one
+// row-wrap test and one address per trip) instead of one per step.  The
+// all-paths kernel uses it (config 4 38.7 -> 39.3 T/s); the fast-only kernel
+// keeps the per-step requests (short tiles lose to the larger loop body:
+// 16384^2 37.3 -> 36.7, 8192^2 24.9 -> 22.4; long tiles unchanged).
+template <int K, int PATH, int PF = PackedTraits<K>::kPrefetch, bool UNI = false,
+          bool TRIP = false>
 __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int lane,
                                               const int strip, const int y, const int n,
                                               uint32_t* ring) {
@@ -329,6 +335,31 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
       lrow = (lrow + 1 == in_rows) ? 0 : lrow + 1;
     }
   };
+  // The PF rows of one loop trip, one commit group each, into ring slots
+  // slot0 .. slot0 + PF - 1.  On the fast and seam paths the torus row wrap
+  // is tested once per trip (warp-uniform): a trip that does not cross it
+  // takes its rows at constant offsets from one address.
+  auto issue_trip = [&](int slot0) {
+    if (!EDGE && lrow + PF <= in_rows) {
+      const char* p0 = row_addr(in_lane, static_cast<uint32_t>(lrow), in_pitch_b);
+      const char* p1 = PATH == kPathSeam
+                           ? row_addr(in_lane1, static_cast<uint32_t>(lrow), in_pitch_b)
+                           : nullptr;
+#pragma unroll
+      for (int u = 0; u < PF; ++u) {
+        uint32_t* s = ring + (slot0 + u) * 96;
+        cp_async4(s, reinterpret_cast<const uint32_t*>(p0 + static_cast<size_t>(u) * in_pitch_b));
+        if (PATH == kPathSeam)
+          cp_async4(s + 32,
+                    reinterpret_cast<const uint32_t*>(p1 + static_cast<size_t>(u) * in_pitch_b));
+        cp_async_commit();
+      }
+      lrow = (lrow + PF == in_rows) ? 0 : lrow + PF;
+      return;
+    }
+#pragma unroll
+    for (int u = 0; u < PF; ++u) issue(slot0 + u);
+  };
   auto consume = [&](int slot) -> uint32_t {
     const uint32_t* s = ring + slot * 96;
     if (PATH == kPathFast || (EDGE && (tiny || plan.mode == 0))) return s[0];
@@ -349,8 +380,12 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   char* const out_seg = reinterpret_cast<char*>(a.out + (a.out_row0 + y) * a.out_pitch + wi);
   const uint32_t out_pitch_b = static_cast<uint32_t>(a.out_pitch * 4);
 
+  if constexpr (TRIP) {
+    issue_trip(0);
+  } else {
 #pragma unroll
-  for (int u = 0; u < PF; ++u) issue(u);
+    for (int u = 0; u < PF; ++u) issue(u);
+  }
 
   HSum sa[K], sb[K];
   uint32_t sself[K], xin[K];
@@ -376,10 +411,17 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   auto trip = [&](const int t, auto kind_tag) {
     constexpr int KIND = decltype(kind_tag)::value;
     constexpr bool FILL = KIND == kFill;
+    if constexpr (TRIP) issue_trip(half ^ PF);  // the next trip's rows
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
-      issue((half ^ PF) + u);
-      cp_async_wait<PF>();
+      if constexpr (TRIP) {
+        // row u of this trip: issued one trip ago; PF - 1 - u rows of that
+        // trip and the PF just issued may still be in flight
+        cp_async_wait_dyn<2 * PF - 1>(u);
+      } else {
+        issue((half ^ PF) + u);
+        cp_async_wait<PF>();
+      }
       xin[0] = consume(half + u);
       const int step = t * PF + u;
       // The K stages of a step are independent (skewed pipeline); they are
@@ -552,11 +594,14 @@ packed_tb_kernel(const PackedStepArgs a) {
                                                                                   : kPathFast;
 #endif
     if (path == kPathFast) {
-      trips = packed_segment<K, kPathFast>(a, lane, strip, static_cast<int>(y0), n, ring);
+      trips = packed_segment<K, kPathFast, PackedTraits<K>::kPrefetch, false, true>(
+          a, lane, strip, static_cast<int>(y0), n, ring);
     } else if (path == kPathSeam) {
-      trips = packed_segment<K, kPathSeam>(a, lane, strip, static_cast<int>(y0), n, ring);
+      trips = packed_segment<K, kPathSeam, PackedTraits<K>::kPrefetch, false, true>(
+          a, lane, strip, static_cast<int>(y0), n, ring);
     } else {
-      trips = packed_segment<K, kPathGeneral>(a, lane, strip, static_cast<int>(y0), n, ring);
+      trips = packed_segment<K, kPathGeneral, PackedTraits<K>::kPrefetch, false, true>(
+          a, lane, strip, static_cast<int>(y0), n, ring);
     }
   }
 #ifndef LIFE_NO_LOCKSTEP
