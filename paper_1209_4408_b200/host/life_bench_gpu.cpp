@@ -18,6 +18,7 @@
 #include <iostream>
 #include <map>
 #include <set>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -46,38 +47,45 @@ class ByteGrid {
   std::vector<uint8_t> c_;
 };
 
+// Fields of a separator-joined list; an empty input is one empty field.
 std::vector<std::string> split(const std::string& text, char sep) {
-  std::vector<std::string> out;
-  size_t start = 0;
-  for (;;) {
-    const size_t end = text.find(sep, start);
-    out.push_back(text.substr(start, end == std::string::npos ? std::string::npos : end - start));
-    if (end == std::string::npos) break;
-    start = end + 1;
+  std::vector<std::string> fields(1);
+  for (const char ch : text) {
+    if (ch == sep) {
+      fields.emplace_back();
+    } else {
+      fields.back().push_back(ch);
+    }
   }
-  return out;
+  return fields;
+}
+
+// Whole-token numeric conversion: trailing junk, overflow and empty tokens
+// are all the same configuration error.
+template <class T, class Convert>
+T parse_number(const std::string& token, const std::string& what, Convert convert) {
+  size_t consumed = 0;
+  bool good = !token.empty();
+  T v{};
+  if (good) {
+    try {
+      v = static_cast<T>(convert(token, &consumed));
+    } catch (const std::logic_error&) {  // invalid_argument / out_of_range
+      good = false;
+    }
+  }
+  if (!good || consumed != token.size()) throw ConfigError("invalid " + what + " '" + token + "'");
+  return v;
 }
 
 int64_t to_int(const std::string& token, const std::string& what) {
-  try {
-    size_t used = 0;
-    const long long v = std::stoll(token, &used);
-    if (used != token.size()) throw std::invalid_argument(token);
-    return v;
-  } catch (const std::exception&) {
-    throw ConfigError("invalid " + what + " '" + token + "'");
-  }
+  return parse_number<int64_t>(token, what,
+                               [](const std::string& t, size_t* n) { return std::stoll(t, n); });
 }
 
 double to_double(const std::string& token, const std::string& what) {
-  try {
-    size_t used = 0;
-    const double v = std::stod(token, &used);
-    if (used != token.size()) throw std::invalid_argument(token);
-    return v;
-  } catch (const std::exception&) {
-    throw ConfigError("invalid " + what + " '" + token + "'");
-  }
+  return parse_number<double>(token, what,
+                              [](const std::string& t, size_t* n) { return std::stod(t, n); });
 }
 
 std::vector<int64_t> int_list(const std::string& arg, const std::string& what) {
@@ -87,13 +95,15 @@ std::vector<int64_t> int_list(const std::string& arg, const std::string& what) {
   return out;
 }
 
+// An empty path means standard output.
 void write_output(const std::string& path, const std::string& payload) {
-  if (path.empty()) {
-    std::cout << payload;
-    return;
-  }
-  std::ofstream out(path, std::ios::binary);
-  if (!out || !(out << payload)) throw ConfigError("cannot write output file '" + path + "'");
+  const bool to_file = !path.empty();
+  std::ofstream file;
+  if (to_file) file.open(path, std::ios::out | std::ios::binary | std::ios::trunc);
+  std::ostream& sink = to_file ? static_cast<std::ostream&>(file) : std::cout;
+  sink.write(payload.data(), static_cast<std::streamsize>(payload.size()));
+  if (to_file && (!file.is_open() || file.fail()))
+    throw ConfigError("cannot write output file '" + path + "'");
 }
 
 // --name value options of one subcommand; unknown names are configuration errors.

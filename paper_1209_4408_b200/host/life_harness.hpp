@@ -120,11 +120,16 @@ struct BenchRecord {
 };
 
 inline BenchRecord time_run(const TimingSpec& spec) {
-  if (spec.repetitions < 1) throw ConfigError("repetitions must be at least 1");
-  if (spec.warmup_runs < 0) throw ConfigError("warmup runs must be non-negative");
-  if (spec.iterations < 1) throw ConfigError("iteration count must be at least 1");
-  if (!(spec.density >= 0.0 && spec.density <= 1.0))
-    throw ConfigError("density must be in [0, 1]");
+  // Same order of checks (and messages) as the reference harness: the first
+  // violated rule is the one reported.
+  const std::pair<bool, const char*> rules[] = {
+      {spec.repetitions >= 1, "repetitions must be at least 1"},
+      {spec.warmup_runs >= 0, "warmup runs must be non-negative"},
+      {spec.iterations >= 1, "iteration count must be at least 1"},
+      {spec.density >= 0.0 && spec.density <= 1.0, "density must be in [0, 1]"},
+  };
+  for (const auto& [holds, message] : rules)
+    if (!holds) throw ConfigError(message);
   const Engine e = spec.strategy.engine;
   Context ctx(spec.device);
   // The seeded soup, once, on the device; kept on the host for the re-uploads.
@@ -258,12 +263,22 @@ inline std::string fixed(double v, int decimals) {
 }
 
 inline std::string csv_row_prefix(const BenchRecord& r) {
-  std::ostringstream row;
-  row << r.width << ',' << r.height << ',' << r.iterations << ',' << to_string(r.strategy) << ','
-      << r.workers << ',' << r.seed << ',' << r.density << ',' << r.repetitions << ','
-      << fixed(r.median_s, 3) << ',' << fixed(r.speedup, 2) << ',' << r.hardware_threads << ','
-      << r.final_population;
-  return row.str();
+  // The twelve pinned columns, in header order, joined by commas.
+  std::ostringstream num;
+  num << r.density;  // default ostream formatting, as the reference prints it
+  const std::string fields[] = {
+      std::to_string(r.width),       std::to_string(r.height),
+      std::to_string(r.iterations),  to_string(r.strategy),
+      std::to_string(r.workers),     std::to_string(r.seed),
+      num.str(),                     std::to_string(r.repetitions),
+      fixed(r.median_s, 3),          fixed(r.speedup, 2),
+      std::to_string(r.hardware_threads), std::to_string(r.final_population)};
+  std::string row;
+  for (const std::string& f : fields) {
+    if (!row.empty()) row.push_back(',');
+    row.append(f);
+  }
+  return row;
 }
 
 // The reference's pinned CSV (bench.hpp:90-97).

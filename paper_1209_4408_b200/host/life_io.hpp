@@ -23,6 +23,7 @@
 #include <cctype>
 #include <cstdint>
 #include <fstream>
+#include <iterator>
 #include <sstream>
 #include <string>
 #include <string_view>
@@ -61,9 +62,13 @@ struct Pattern {
   std::vector<Coord> live_cells;
 
   void normalize() {
-    std::sort(live_cells.begin(), live_cells.end(),
-              [](const Coord& a, const Coord& b) { return a.y != b.y ? a.y < b.y : a.x < b.x; });
-    live_cells.erase(std::unique(live_cells.begin(), live_cells.end()), live_cells.end());
+    // row-major order: (y, x) pairs compared as tuples, duplicates dropped
+    auto& v = live_cells;
+    std::stable_sort(v.begin(), v.end(), [](const Coord& lhs, const Coord& rhs) {
+      return std::make_pair(lhs.y, lhs.x) < std::make_pair(rhs.y, rhs.x);
+    });
+    const auto tail = std::unique(v.begin(), v.end());
+    v.resize(static_cast<size_t>(tail - v.begin()));
   }
   friend bool operator==(const Pattern&, const Pattern&) = default;
 };
@@ -224,15 +229,20 @@ inline Pattern parse_rle(std::string_view text) {
 }
 
 inline std::string serialize_rle(const Pattern& pattern) {
-  Pattern p = pattern;
+  Pattern p{pattern.width, pattern.height, pattern.live_cells};
   p.normalize();
-  for (const Coord& c : p.live_cells)
-    if (c.x < 0 || c.x >= p.width || c.y < 0 || c.y >= p.height)
-      throw ConfigError("pattern has live cells outside its declared bounds");
-  std::string out = "x = " + std::to_string(p.width) + ", y = " + std::to_string(p.height) + "\n";
-  auto put = [&out](long n, char tag) {
-    if (n > 1) out += std::to_string(n);
-    out += tag;
+  const auto inside = [&p](const Coord& c) {
+    return 0 <= c.x && c.x < p.width && 0 <= c.y && c.y < p.height;
+  };
+  if (!std::all_of(p.live_cells.begin(), p.live_cells.end(), inside))
+    throw ConfigError("pattern has live cells outside its declared bounds");
+  std::ostringstream header;
+  header << "x = " << p.width << ", y = " << p.height << '\n';
+  std::string out = header.str();
+  // One RLE item: the count is written only for runs longer than one.
+  const auto put = [&out](long run, char tag) {
+    if (run >= 2) out.append(std::to_string(run));
+    out.push_back(tag);
   };
   int row = 0, col = 0;
   for (size_t i = 0; i < p.live_cells.size();) {
@@ -287,26 +297,35 @@ inline Pattern parse_plaintext(std::string_view text) {
 }
 
 inline Pattern load_pattern_file(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw ConfigError("cannot read pattern file '" + path + "'");
-  std::ostringstream body;
-  body << in.rdbuf();
-  const size_t dot = path.rfind('.');
-  const std::string ext = dot == std::string::npos ? "" : detail::lowered(path.substr(dot));
-  if (ext == ".rle") return parse_rle(body.str());
-  if (ext == ".cells") return parse_plaintext(body.str());
-  throw ConfigError("unsupported pattern extension '" + ext + "' (expected .rle or .cells)");
+  std::string text;
+  {
+    std::ifstream file(path, std::ios::in | std::ios::binary);
+    if (!file.is_open()) throw ConfigError("cannot read pattern file '" + path + "'");
+    text.assign(std::istreambuf_iterator<char>(file), std::istreambuf_iterator<char>());
+  }
+  // The format is picked by the (case-insensitive) file extension alone.
+  std::string ext;
+  if (const auto at = path.find_last_of('.'); at != std::string::npos)
+    ext = detail::lowered(path.substr(at));
+  const bool rle = ext == ".rle", cells = ext == ".cells";
+  if (!rle && !cells)
+    throw ConfigError("unsupported pattern extension '" + ext + "' (expected .rle or .cells)");
+  return rle ? parse_rle(text) : parse_plaintext(text);
 }
 
 // place_pattern on a host grid (any GridT with width()/height()/data()).
 template <class GridT>
 GridT place_pattern(const GridT& grid, const Pattern& pattern, Coord origin) {
-  if (origin.x < 0 || origin.y < 0 || origin.x + pattern.width > grid.width() ||
-      origin.y + pattern.height > grid.height())
-    throw OutOfBounds("pattern footprint " + std::to_string(pattern.width) + "x" +
-                      std::to_string(pattern.height) + " at (" + std::to_string(origin.x) + ", " +
-                      std::to_string(origin.y) + ") exceeds grid " +
-                      std::to_string(grid.width()) + "x" + std::to_string(grid.height()));
+  const int64_t gw = grid.width(), gh = grid.height();
+  const bool fits = origin.x >= 0 && origin.y >= 0 &&
+                    int64_t{origin.x} + pattern.width <= gw &&
+                    int64_t{origin.y} + pattern.height <= gh;
+  if (!fits) {
+    std::ostringstream why;  // no wrap-around: the whole footprint must lie on the grid
+    why << "pattern footprint " << pattern.width << 'x' << pattern.height << " at (" << origin.x
+        << ", " << origin.y << ") exceeds grid " << gw << 'x' << gh;
+    throw OutOfBounds(why.str());
+  }
   GridT out = grid;
   uint8_t* cells = out.data();
   const int64_t w = out.width();
