@@ -168,7 +168,7 @@ int life_grid_hash(life_ctx* ctx, uint64_t* out);
  *   `generations` >= 0 (ConfigError otherwise, engine.cpp:133-136);
  *   `temporal_depth`: generations per kernel pass, 0 = auto (the
  *     cluster-resident engine for small tori; the quad / pair layout kernels
- *     for W % 128 / 64 == 0 tori of 2^29 cells or more, life_interleave_auto;
+ *     for W % 128 / 64 == 0 tori of 2^29 / 2^27 cells or more, life_interleave_auto;
  *     else life_packed_auto_depth); packed 1..16,
  *     byte 1..8 (W % 16 == 0 or W >= 33; narrower tori run one generation per pass);
  *   `checkpoints`: strictly ascending in [0, generations] (engine.cpp:137-147);
@@ -207,10 +207,11 @@ int life_packed_auto_depth(int64_t width, int64_t height);
  * K <= 7), 2 = the pair layout (packed_il_kernel<K, 2>: W % 64 == 0, 10 ops,
  * K <= 12), 0 = the plain-layout kernels (11 ops) -- and writes the pass depth
  * to *depth (0 with order 0: life_packed_auto_depth applies).  With both
- * options at -1 and temporal_depth 0, tori of 2^29 cells or more run the
+ * options at -1 and temporal_depth 0, tori of 2^27 cells or more run the
  * layout that keeps most lanes per integer op busy at their width (strips of
- * 32 groups advancing by 31): quad at K = 6 for wide tori (W >= 49152 or so),
- * pair at K = 10 for 16384..32768 columns, the plain kernels below; an
+ * 32 groups advancing by 31): quad (2^29 cells or more) at K = 7 / 6 for wide
+ * tori (W >= 49152 or so), pair at K = 10 for 12288..32768 columns, the plain
+ * kernels below and for narrower or smaller tori; an
  * explicit temporal_depth keeps the plain kernels unless an option forces a
  * layout. */
 int life_interleave_auto(int64_t width, int64_t height, int32_t pair_option, int32_t quad_option,

@@ -117,6 +117,7 @@ struct PackedTraits {
 #ifndef LIFE_GROUP
 #define LIFE_GROUP 4
 #endif
+
 constexpr int kGroup = LIFE_GROUP;  // stages issued level by level together
 
 // How a lane fetches its 32-cell word of a row.  The column is the same for
@@ -256,11 +257,29 @@ constexpr int kPathFast = 0, kPathSeam = 1, kPathGeneral = 2;
 // all-paths kernel uses it (config 4 38.7 -> 39.3 T/s); the fast-only kernel
 // keeps the per-step requests (short tiles lose to the larger loop body:
 // 16384^2 37.3 -> 36.7, 8192^2 24.9 -> 22.4; long tiles unchanged).
+// LIFE_TIMELINE builds (tools/r5_timeline.py): lane 0 of every warp of the
+// fast-only kernel stamps %clock64 at the phases of its tile.
+#ifdef LIFE_TIMELINE
+#define LIFE_TL(i)                                                   \
+  do {                                                               \
+    if (tl != nullptr && lane == 0) {                                \
+      unsigned long long c_;                                         \
+      asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_)::"memory");   \
+      tl[i] = c_;                                                    \
+    }                                                                \
+  } while (0)
+#else
+#define LIFE_TL(i) \
+  do {             \
+  } while (0)
+#endif
+
 template <int K, int PATH, int PF = PackedTraits<K>::kPrefetch, bool UNI = false,
           bool TRIP = false>
 __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int lane,
                                               const int strip, const int y, const int n,
-                                              uint32_t* ring) {
+                                              uint32_t* ring, unsigned long long* tl = nullptr) {
+  (void)tl;
   constexpr int kLag = PackedTraits<K>::kLag;
   constexpr bool EDGE = PATH == kPathGeneral;
   const bool tiny = a.width < 32;  // warp-uniform (general path only)
@@ -407,10 +426,13 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   // Trip kinds: kFill (no output yet; lower stage groups skipped), kCheck
   // (per-step test whether the output row is inside the segment), kSteady
   // (every step stores: no per-step test, no branch).
-  constexpr int kFill = 0, kCheck = 1, kSteady = 2;
+  constexpr int kFill = 0, kCheck = 1, kSteady = 2, kFillPhase = 16;
   auto trip = [&](const int t, auto kind_tag) {
     constexpr int KIND = decltype(kind_tag)::value;
-    constexpr bool FILL = KIND == kFill;
+    // KIND >= kFillPhase: a fill trip whose active stage groups are known at
+    // compile time (groups below (KIND - kFillPhase) * kGroup), no branch.
+    constexpr bool FILL = KIND == kFill || KIND >= kFillPhase;
+    constexpr int kActive = KIND >= kFillPhase ? (KIND - kFillPhase) * kGroup : K;
     if constexpr (TRIP) issue_trip(half ^ PF);  // the next trip's rows
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
@@ -434,7 +456,11 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
       uint32_t y_last = 0;
 #pragma unroll
       for (int g0 = ((K - 1) / kGroup) * kGroup; g0 >= 0; g0 -= kGroup) {
-        if (FILL && step < 3 * g0) continue;
+        if constexpr (KIND >= kFillPhase) {
+          if (g0 >= kActive) continue;  // compile time
+        } else {
+          if (FILL && step < 3 * g0) continue;
+        }
         uint32_t xl[kGroup], xr[kGroup];
         HSum c[kGroup];
 #pragma unroll
@@ -502,7 +528,43 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
   const int steady_begin = (kLag + PF - 1) / PF;
   const int steady_end = (n + kLag) / PF;
   int t = 0;
-  for (; t < fill_trips; ++t) trip(t, std::integral_constant<int, kFill>{});
+  LIFE_TL(2);  // prologue done, first PF rows requested
+  // Fill as phases of 3 * kGroup steps: phase p runs groups 0..p-1 from a
+  // straight-line body with no per-group branch (LIFE_FILL_PHASES 1: the
+  // short-tile UNI variant only, 2: every variant, 0: the branchy fill body).
+  // The all-paths kernel (TRIP) carries both fills and takes the phased one
+  // on short tiles (config 4: +1 %, 16383^2: +3 %; long tiles and the split
+  // launch's seam strips lose 1 % to the extra hot code, so they keep the
+  // branchy body, as does the long-tile fast kernel).
+  constexpr bool kPhased =
+      (LIFE_FILL_PHASES == 2 || (LIFE_FILL_PHASES == 1 && (UNI || TRIP))) &&
+      (3 * kGroup) % PF == 0 && kTopG0 > 0;
+  const bool phased_now = true;  // (a run-time choice by tile length gave the gain back: both bodies hot)
+  if constexpr (kPhased) {
+    constexpr int kTripsPerPhase = 3 * kGroup / PF;
+    constexpr int kPhases = kTopG0 / kGroup;
+    static_assert(kPhases * kTripsPerPhase == kFillTrips, "phases cover the fill trips");
+    auto phases = [&](auto self, auto p_tag) {
+      constexpr int P = decltype(p_tag)::value;  // groups active in this phase
+      if constexpr (P <= kPhases) {
+#pragma unroll 1
+        for (int r = 0; r < kTripsPerPhase; ++r, ++t) {
+          trip(t, std::integral_constant<int, kFillPhase + P>{});
+          if (t == 0) LIFE_TL(3);
+        }
+        self(self, std::integral_constant<int, P + 1>{});
+      }
+    };
+    if (phased_now) phases(phases, std::integral_constant<int, 1>{});
+  }
+  (void)phased_now;
+  if constexpr (!kPhased) {
+    for (; t < fill_trips; ++t) {  // not phased: one body, a warp-uniform branch per group
+      trip(t, std::integral_constant<int, kFill>{});
+      if (t == 0) LIFE_TL(3);  // first trip: first rows have arrived
+    }
+  }
+  LIFE_TL(4);  // fill trips done
   if constexpr (UNI) {
     (void)steady_begin;
     (void)steady_end;
@@ -515,6 +577,7 @@ __device__ __forceinline__ int packed_segment(const PackedStepArgs& a, const int
     for (; t < trips; ++t) trip(t, std::integral_constant<int, kCheck>{});
   }
   cp_async_wait<0>();
+  LIFE_TL(5);  // last row stored
   return trips;
 }
 
@@ -647,10 +710,29 @@ packed_tb_fast_kernel(const PackedStepArgs a) {
   extern __shared__ uint32_t ring_fast_smem[];
   uint32_t* ring =
       ring_fast_smem + (threadIdx.x >> 5) * (2 * PackedTraits<K>::kPrefetchFast * 96) + lane;
+#ifdef LIFE_TIMELINE
+  unsigned long long* tl =
+      a.trace ? reinterpret_cast<unsigned long long*>(a.trace) + 8 * tile : nullptr;
+  LIFE_TL(0);  // block resident
+#endif
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: previous pass complete
   asm volatile("griddepcontrol.launch_dependents;");
+#ifdef LIFE_TIMELINE
+  LIFE_TL(1);  // previous pass complete
+  if (tl != nullptr && lane == 0) {
+    unsigned long long g_;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    tl[6] = g_;
+    tl[7] = smid;
+  }
+  packed_segment<K, kPathFast, PackedTraits<K>::kPrefetchFast, UNI>(
+      a, lane, strip, static_cast<int>(y0), n, ring, tl);
+#else
   packed_segment<K, kPathFast, PackedTraits<K>::kPrefetchFast, UNI>(a, lane, strip,
                                                                    static_cast<int>(y0), n, ring);
+#endif
 }
 
 // ---------------------------------------------------------------------------

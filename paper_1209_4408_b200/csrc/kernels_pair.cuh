@@ -204,10 +204,13 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
   }
 
   int half = 0;
-  constexpr int kFill = 0, kCheck = 1, kSteady = 2;
+  constexpr int kFill = 0, kCheck = 1, kSteady = 2, kFillPhase = 16;
   auto trip = [&](const int t, auto kind_tag) {
     constexpr int KIND = decltype(kind_tag)::value;
-    constexpr bool FILL = KIND == kFill;
+    // KIND >= kFillPhase: a fill trip with (KIND - kFillPhase) stage groups
+    // active, known at compile time (no per-group branch).
+    constexpr bool FILL = KIND == kFill || KIND >= kFillPhase;
+    constexpr int kActive = KIND >= kFillPhase ? (KIND - kFillPhase) * G : K;
     issue_trip(half ^ PF);  // the next trip's rows
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
@@ -231,7 +234,11 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
       for (int r = 0; r < N; ++r) y_last[r] = 0;
 #pragma unroll
       for (int g0 = ((K - 1) / G) * G; g0 >= 0; g0 -= G) {
-        if (FILL && step < 3 * g0) continue;
+        if constexpr (KIND >= kFillPhase) {
+          if (g0 >= kActive) continue;  // compile time
+        } else {
+          if (FILL && step < 3 * g0) continue;
+        }
         uint32_t lu[G], rd[G];
         HSum c[G][N];
 #pragma unroll
@@ -316,6 +323,24 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
   const int steady_begin = (kLag + PF - 1) / PF;
   const int steady_end = (n + kLag) / PF;
   int t = 0;
+  // Fill as phases of 3 * G steps with groups 0..p-1 active (kernels.cuh,
+  // LIFE_FILL_PHASES); a fill cut short by kLag ends in the branchy body.
+  constexpr bool kPhased =
+      (LIFE_FILL_PHASES == 2 || (LIFE_FILL_PHASES == 1 && UNI)) && (3 * G) % PF == 0 && kTopG0 > 0;
+  if constexpr (kPhased) {
+    constexpr int kTripsPerPhase = 3 * G / PF;
+    constexpr int kPhases = (kFillTrips / kTripsPerPhase) < (kTopG0 / G) ? (kFillTrips / kTripsPerPhase)
+                                                                         : (kTopG0 / G);
+    auto phases = [&](auto self, auto p_tag) {
+      constexpr int P = decltype(p_tag)::value;  // groups active in this phase
+      if constexpr (P <= kPhases) {
+#pragma unroll 1
+        for (int r = 0; r < kTripsPerPhase; ++r, ++t) trip(t, std::integral_constant<int, kFillPhase + P>{});
+        self(self, std::integral_constant<int, P + 1>{});
+      }
+    };
+    phases(phases, std::integral_constant<int, 1>{});
+  }
   for (; t < fill_trips; ++t) trip(t, std::integral_constant<int, kFill>{});
   if constexpr (UNI) {
     (void)steady_begin;

@@ -182,7 +182,7 @@ int peer_sync_trips() {
 }
 
 // Tiles up to this many rows run the fast kernel's single-loop-body variant.
-constexpr int64_t kUniMaxRows = 1024;
+constexpr int64_t kUniMaxRows = kShortTileRows;  // tiles up to this many rows: the single-loop-body variant
 // One-wave fast-kernel tiles shorter than this run at half the warps per SM.
 constexpr int64_t kShortTileRows = 128;
 
@@ -337,7 +337,11 @@ int thread_split_streams(SplitStreams** out) {
 // one-wave grids (config 4, 16383^2) keep the single all-paths launch.
 template <int K>
 int launch_packed_deep(PackedStepArgs a, cudaStream_t s, SplitStreams* ss) {
+  #ifdef LIFE_TIMELINE
+  const bool fast_ok = !a.peer && a.width >= 64;  // the fast kernel carries the phase stamps
+#else
   const bool fast_ok = !a.peer && a.width >= 64 && !a.trace;
+#endif
   if (fast_ok && a.width % 32 == 0) return launch_packed_kernel<K, true>(a, s);
   const int32_t total = a.n_strips;
   // Strip s holds words [31s - 1, 31s + 30]: s_last is the first strip
@@ -1260,8 +1264,8 @@ bool resident_auto(int64_t w, int64_t h) {
 // passes run as one all-paths launch (W % 32 != 0, less than ~3 block waves
 // deep), where K = 12 fits 12 warps per SM instead of 8 (config 4: 37.5 ->
 // 38.6 T/s; kbench depth sweep).
-// temporal_depth 0 on tori (or row bands of them, h rows tall) of 2^29 cells
-// or more: the layout with the best lanes-per-op figure -- the share of a
+// temporal_depth 0 on tori (or row bands of them, h rows tall) of 2^27 cells
+// or more (quad: 2^29): the layout with the best lanes-per-op figure -- the share of a
 // strip's 32 lanes that hold cells (groups / (32 x strips), strips of 32
 // groups advancing by 31) over the network's ops per word (11 plain, 10 pair,
 // 9.5 quad).  Wide tori fill their strips in every layout and take quad at
@@ -1272,10 +1276,18 @@ bool resident_auto(int64_t w, int64_t h) {
 //   131072 x 8192 39.9 / 45.3 / 48.7 / 48.1   32768^2       41.7 / 46.4 / 46.0 / 45.6
 //   32768 x 65536 43.4 / 47.5 / 47.5          32768 x 16384 39.3 / 42.2 / 42.1
 //   16384 x 65536 42.2 / 43.2 / 40.9          8192 x 131072 40.4 / 39.3 / 34.9
-// Smaller tori keep the plain kernels (16384^2: 37.3 / 35.9 / 34.0: their
-// one-wave tiles are bounded by pipeline fill, not by the op count).
+// With the phased pipeline fill (LIFE_FILL_PHASES, packed_common.cuh) the
+// pair layout also pays on one-wave tori down to 2^27 cells (plain K = 16 /
+// pair K = 10 / quad K = 7, tools/r5_rule.sh):
+//   16384^2 (config 2) 38.8 / 40.8 / 38.2   20480^2      41.5 / 43.9 / 41.5
+//   32768 x 8192       38.9 / 42.6 / 41.2   12288^2      34.8 / 36.3 / 30.1
+//   16384 x 8192       34.2 / 34.5 / 29.7   8192 x 16384 32.8 / 32.2 / 26.8
+//   8192^2             28.2 / 26.3 / 22.3   4096^2       14.4 / 11.5 /  8.5
+// Quad stays with tori of 2^29 cells or more; smaller tori keep the plain
+// kernels (their tiles are too short for the wider groups' fewer strips).
 namespace {
-constexpr int64_t kIlAutoCells = int64_t(1) << 29;
+constexpr int64_t kIlAutoCells = int64_t(1) << 27;      // pair layout from here
+constexpr int64_t kIlAutoCellsQuad = int64_t(1) << 29;  // quad layout from here
 double lanes_per_op(int il, int64_t w) {
   const int64_t groups = il == 0 ? nw32(w) : w / (32 * il);
   const int64_t strips = ceil_div(groups + 1, kStripStride);
@@ -1299,7 +1311,8 @@ lifegpu::detail::IlChoice lifegpu::detail::il_choose(int64_t w, int64_t h, int p
       c.il = 2;
       c.depth = 10;
     }
-    if (quad_opt < 0 && il_eligible(4, w) && lanes_per_op(4, w) > best) {
+    if (quad_opt < 0 && w * h >= kIlAutoCellsQuad && il_eligible(4, w) &&
+        lanes_per_op(4, w) > best) {
       c.il = 4;  // K = 7 (243 registers) pays on the largest tori only
       c.depth = w * h >= (int64_t(1) << 31) ? 7 : 6;
     }

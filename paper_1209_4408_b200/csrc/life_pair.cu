@@ -17,7 +17,7 @@ static_assert(kPairMaxDepth == kPairMaxDepthHost && kQuadMaxDepth == kQuadMaxDep
 
 namespace {
 
-constexpr int64_t kUniMaxRows = 1024;  // tiles up to this many rows: the single-loop-body variant
+constexpr int64_t kUniMaxRows = kShortTileRows;  // tiles up to this many rows: the single-loop-body variant
 
 template <typename Kernel>
 int launch_pdl_pair(Kernel kernel, unsigned blocks, unsigned threads, size_t smem, cudaStream_t s,

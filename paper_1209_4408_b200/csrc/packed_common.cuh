@@ -9,6 +9,18 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
+// Pipeline fill of the temporal-blocked kernels as compile-time phases (one
+// straight-line trip body per number of active stage groups) instead of one
+// fill body with a warp-uniform branch per group: 0 = off, 1 = the short-tile
+// (UNI) variants, 2 = every variant.  Timeline of a config-2 tile
+// (tools/r5_timeline.py): fill 12.6 -> 6.7 us of a 114 us tile.
+#ifndef LIFE_FILL_PHASES
+#define LIFE_FILL_PHASES 1
+#endif
+// Tiles up to this many rows are "short": the single-loop-body (UNI) kernel
+// variants and the phased fill of the all-paths kernel.
+constexpr long long kShortTileRows = 1024;
+
 namespace lifegpu {
 
 constexpr unsigned kFull = 0xffffffffu;

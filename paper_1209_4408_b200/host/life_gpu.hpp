@@ -73,8 +73,8 @@ struct RunConfig {
   Engine engine = Engine::Packed;
   // Generations per kernel pass; 0 = auto: the cluster-resident engine for
   // small W % 32 == 0 tori (<= 2^22 cells, one GPU); tori of 2^29 cells or
-  // more in the quad layout at 6 (W % 128 == 0, wide) or the pair layout at
-  // 10 (W % 64 == 0) (life_interleave_auto); else 16 -- 12 for W % 32 != 0 tori
+  // more in the quad layout at 7 / 6 (W % 128 == 0, wide), of 2^27 or more in
+  // the pair layout at 10 (W % 64 == 0) (life_interleave_auto); else 16 -- 12 for W % 32 != 0 tori
   // less than ~3 block waves deep (life_packed_auto_depth).
   int temporal_depth = 0;
   int workers = 1;  // validated like the reference (>= 1, <= rows)

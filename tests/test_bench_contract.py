@@ -113,7 +113,7 @@ def test_single_process_multi_device_context_line():
 def test_one_gpu_line_carries_parity():
     j = run_bench("--config", "2", "--steps", "3", "--warmup", "3", "--no-cpu", "--no-e2e")
     assert j["parity"]["ok"] is True and j["n_gpus"] == 1
-    assert j["roofline"]["kernel"].startswith("packed_tb_")
+    assert j["roofline"]["kernel"].startswith("packed_")  # config 2: the pair layout (auto rule)
     assert 0.5 < j["roofline"]["step_frac"] <= j["roofline"]["frac"] * 1.05
 
 

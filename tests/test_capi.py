@@ -116,7 +116,12 @@ def test_interleave_auto_rule(lib):
     assert pick(32768, 32768) == (2, 10)
     assert pick(16384, 65536) == (2, 10)
     assert pick(8192, 131072) == (0, 0)
-    assert pick(16384, 16384) == (0, 0)             # config 2: below 2^29 cells
+    assert pick(16384, 16384) == (2, 10)            # config 2: pair from 2^27 cells
+    assert pick(12288, 12288) == (2, 10)
+    assert pick(16384, 8192) == (2, 10)             # 2^27 cells
+    assert pick(65536, 4096) == (2, 10)             # quad only from 2^29 cells
+    assert pick(8192, 8192) == (0, 0)               # below 2^27 cells
+    assert pick(8192, 32768) == (0, 0)              # 8192 columns: plain fills its strips best
     assert pick(40961, 12289) == (0, 0)             # config 4: W % 64 != 0
     assert pick(262208, 262144) == (2, 10)          # W % 128 != 0, W % 64 == 0
     # options: 0 disables a layout, > 0 forces it where the width allows

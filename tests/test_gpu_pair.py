@@ -169,7 +169,8 @@ def test_pair_cfg3_golden(pair_engine, oracle):
     assert capi.lib().life_interleave_auto(65536, 65536, -1, -1, 0, C.byref(d)) == 4 and d.value == 7
     assert capi.lib().life_interleave_auto(65536, 65536, -1, 0, 0, C.byref(d)) == 2 and d.value == 10
     assert capi.lib().life_interleave_auto(65536, 65536, -1, -1, 16, C.byref(d)) == 0
-    assert capi.lib().life_interleave_auto(16384, 16384, -1, -1, 0, C.byref(d)) == 0
+    assert capi.lib().life_interleave_auto(16384, 16384, -1, -1, 0, C.byref(d)) == 2 and d.value == 10
+    assert capi.lib().life_interleave_auto(8192, 8192, -1, -1, 0, C.byref(d)) == 0
     gold = load_golden("golden_cfg3.json")
     e = pair_engine
     e.init_random(gold["w"], gold["h"], gold["density"], gold["seed"], PACKED)

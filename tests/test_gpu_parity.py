@@ -219,7 +219,11 @@ def _check_schedule(engine, oracle, gold, eng, depth, init):
 @pytest.mark.slow
 def test_cfg2_16384_1000_generations(engine, oracle):
     gold = load_golden("golden_cfg2.json")
-    # depth 0 = what life_run / bench.py run: byte auto K=6, packed auto K=16
+    # depth 0 = what life_run / bench.py run: byte auto K=6, packed auto = the
+    # pair layout at K=10 (2^27 cells or more; plain K=16 with an explicit depth)
+    import ctypes as C
+    d = C.c_int32(0)
+    assert capi.lib().life_interleave_auto(16384, 16384, -1, -1, 0, C.byref(d)) == 2 and d.value == 10
     assert capi.lib().life_packed_auto_depth(16384, 16384) == 16
     for eng, depth in [(BYTE, 1), (BYTE, 4), (BYTE, 0), (BYTE, 6), (PACKED, 16), (PACKED, 8),
                        (PACKED, 0)]:
