@@ -204,13 +204,18 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
   }
 
   int half = 0;
-  constexpr int kFill = 0, kCheck = 1, kSteady = 2, kFillPhase = 16;
+  constexpr int kFill = 0, kCheck = 1, kSteady = 2, kFillPhase = 16, kDrainPhase = 32;
   auto trip = [&](const int t, auto kind_tag) {
     constexpr int KIND = decltype(kind_tag)::value;
-    // KIND >= kFillPhase: a fill trip with (KIND - kFillPhase) stage groups
-    // active, known at compile time (no per-group branch).
-    constexpr bool FILL = KIND == kFill || KIND >= kFillPhase;
-    constexpr int kActive = KIND >= kFillPhase ? (KIND - kFillPhase) * G : K;
+    // kFillPhase <= KIND < kDrainPhase: a fill trip with (KIND - kFillPhase)
+    // stage groups active, known at compile time (no per-group branch).
+    // KIND >= kDrainPhase: one of a tile's last trips, the (KIND -
+    // kDrainPhase) lowest groups skipped -- stage g's output is last needed at
+    // step n + 2K - 1 + g -- otherwise a check trip.
+    constexpr bool DRAIN = KIND >= kDrainPhase;
+    constexpr bool FILL = KIND == kFill || (KIND >= kFillPhase && !DRAIN);
+    constexpr int kActive = (KIND >= kFillPhase && !DRAIN) ? (KIND - kFillPhase) * G : K;
+    constexpr int kSkipLow = DRAIN ? (KIND - kDrainPhase) * G : 0;
     issue_trip(half ^ PF);  // the next trip's rows
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
@@ -234,7 +239,9 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
       for (int r = 0; r < N; ++r) y_last[r] = 0;
 #pragma unroll
       for (int g0 = ((K - 1) / G) * G; g0 >= 0; g0 -= G) {
-        if constexpr (KIND >= kFillPhase) {
+        if constexpr (DRAIN) {
+          if (g0 < kSkipLow) continue;  // compile time
+        } else if constexpr (KIND >= kFillPhase) {
           if (g0 >= kActive) continue;  // compile time
         } else {
           if (FILL && step < 3 * g0) continue;
@@ -286,7 +293,7 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
       }
       const int j = step - kLag;  // output row j of the segment leaves the pipeline at step j + kLag
       if (!FILL) {
-        if (UNI && KIND == kCheck) {
+        if (UNI && (KIND == kCheck || DRAIN)) {
           const bool ok = static_cast<unsigned>(j) < static_cast<unsigned>(n);
           char* p = const_cast<char*>(row_addr(out_seg, static_cast<uint32_t>(j), out_pitch_b));
           if constexpr (N == 2) {
@@ -345,8 +352,33 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
   if constexpr (UNI) {
     (void)steady_begin;
     (void)steady_end;
+#if LIFE_DRAIN_PHASES
+    // The last two trips skip the stage groups whose outputs nothing needs
+    // any more (a trip starting at step s skips group g0 if s >= n + 2K + g0
+    // + G - 1), from bodies specialised on the number of skipped groups.
+    constexpr int kMaxD = (kTopG0 / G) < 3 ? (kTopG0 / G) : 3;
+    auto drain_trip = [&](const int tt) {
+      const int x = tt * PF - (n + 2 * K + G - 1);
+      const int d = x < 0 ? 0 : (x / G + 1 < kMaxD ? x / G + 1 : kMaxD);
+      if constexpr (kMaxD >= 3) {
+        if (d == 3) return trip(tt, std::integral_constant<int, kDrainPhase + 3>{});
+      }
+      if constexpr (kMaxD >= 2) {
+        if (d == 2) return trip(tt, std::integral_constant<int, kDrainPhase + 2>{});
+      }
+      if constexpr (kMaxD >= 1) {
+        if (d == 1) return trip(tt, std::integral_constant<int, kDrainPhase + 1>{});
+      }
+      return trip(tt, std::integral_constant<int, kCheck>{});
+    };
+#pragma unroll 1
+    for (; t < trips - 2; ++t) trip(t, std::integral_constant<int, kCheck>{});
+#pragma unroll 1
+    for (; t < trips; ++t) drain_trip(t);
+#else
 #pragma unroll 1
     for (; t < trips; ++t) trip(t, std::integral_constant<int, kCheck>{});
+#endif
   } else {
     for (; t < trips && (t < steady_begin || t >= steady_end); ++t)
       trip(t, std::integral_constant<int, kCheck>{});

@@ -66,6 +66,8 @@ int launch_pair(PackedStepArgs a, cudaStream_t s) {
   if (wpb != T::kWarps)
     LIFE_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kernel, 32 * wpb,
                                                             wpb * T::kRingBytes));
+  static const int64_t forced_bps = knob("LIFE_PAIR_BPS", 0);  // debug builds: blocks per SM the plan assumes
+  if (forced_bps > 0) bps = static_cast<int>(forced_bps);
   if (a.out_rows >= (int64_t(1) << 31) || a.in_rows >= (int64_t(1) << 31) ||
       a.in_pitch * 4 >= (int64_t(1) << 32) || a.out_pitch * 4 >= (int64_t(1) << 32))
     return set_error(LIFE_ERR_CONFIG, "grid too large for one packed pass");

@@ -17,6 +17,10 @@
 #ifndef LIFE_FILL_PHASES
 #define LIFE_FILL_PHASES 1
 #endif
+// Drain of short tiles as specialised last trips (kernels_pair.cuh): 0 = off.
+#ifndef LIFE_DRAIN_PHASES
+#define LIFE_DRAIN_PHASES 0
+#endif
 // Tiles up to this many rows are "short": the single-loop-body (UNI) kernel
 // variants and the phased fill of the all-paths kernel.
 constexpr long long kShortTileRows = 1024;
