@@ -219,7 +219,7 @@ def _check_schedule(engine, oracle, gold, eng, depth, init):
 @pytest.mark.slow
 def test_cfg2_16384_1000_generations(engine, oracle):
     gold = load_golden("golden_cfg2.json")
-    # depth 0 = what life_run / bench.py run: byte auto K=6, packed auto = the
+    # depth 0 = what life_run / bench.py run: byte auto K=8, packed auto = the
     # pair layout at K=10 (2^27 cells or more; plain K=16 with an explicit depth)
     import ctypes as C
     d = C.c_int32(0)
