@@ -89,14 +89,22 @@ class BandGeometry:
     # The drivers convert their band in place before the first pass and back
     # before anything reads the plain words.
     il: int = 0
+    # world == 1 only: run the halo exchange anyway, the rank being its own
+    # neighbour above and below (the torus wrap as a self send / receive).
+    # This is how the NCCL halo path runs on a single GPU (tests).
+    self_exchange: bool = False
 
     @property
     def band_rows(self) -> int:
         return self.y1 - self.y0
 
     @property
+    def exchanges(self) -> bool:
+        return self.world > 1 or self.self_exchange
+
+    @property
     def ghost(self) -> int:
-        return 0 if self.world == 1 else self.depth
+        return self.depth if self.exchanges else 0
 
     @property
     def buf_rows(self) -> int:
@@ -108,7 +116,7 @@ def il_max_depth(il: int) -> int:
 
 
 def make_geometry(width: int, height: int, rank: int, world: int, depth: int,
-                  il: int = 0) -> BandGeometry:
+                  il: int = 0, self_exchange: bool = False) -> BandGeometry:
     if width < 3 or height < 3:
         raise ConfigError(f"grid dimensions must be at least 3x3, got {width}x{height}")
     if not 1 <= depth <= capi.MAX_TEMPORAL_DEPTH:
@@ -120,10 +128,12 @@ def make_geometry(width: int, height: int, rank: int, world: int, depth: int,
                           f"{il_max_depth(il)}, got W = {width}, depth {depth}")
     bounds = band_bounds(height, world)  # TooManyParts like partition_rows
     y0, y1 = bounds[rank], bounds[rank + 1]
-    if world > 1 and (y1 - y0) < depth:
+    if (world > 1 or self_exchange) and (y1 - y0) < depth:
         raise TooManyParts(f"band of {y1 - y0} rows is thinner than the temporal depth {depth}")
+    if self_exchange and world != 1:
+        raise ConfigError("self_exchange is the one-rank form of the halo exchange")
     return BandGeometry(width, height, rank, world, depth, y0, y1,
-                        int(capi.lib().life_packed_pitch_words(width)), il)
+                        int(capi.lib().life_packed_pitch_words(width)), il, self_exchange)
 
 
 class PairLayout:
@@ -228,7 +238,7 @@ class BandDriver(PairLayout):
     def post_exchange(self, k: int):
         """Sends my top/bottom k rows, receives k ghost rows on each side."""
         g = self.geo
-        if g.world == 1:
+        if not g.exchanges:
             return None
         up, down = self._peers()
         top, bottom, ghost_top, ghost_bottom = self.halo_views(k)
@@ -279,7 +289,7 @@ class BandDriver(PairLayout):
         if not 1 <= k <= g.depth:
             raise ConfigError(f"pass depth {k} outside [1, {g.depth}]")
         self._to_pair()
-        if g.world == 1:
+        if not g.exchanges:
             a, b = self.buf[self.cur], self.buf[self.cur ^ 1]
             self.stepper(a, 0, g.height, b, 0, g.height, k)
         elif self.edge_stream is None:
@@ -602,7 +612,7 @@ class PeerBandDriver(PairLayout):
 
     def __init__(self, geo: BandGeometry, device: torch.device, group=None,
                  sync: str = "neighbour", profile: bool = False):
-        if geo.world < 2:
+        if geo.world < 2 and not geo.self_exchange:
             raise ConfigError("PeerBandDriver needs at least two ranks")
         self.geo = geo
         self.device = device
