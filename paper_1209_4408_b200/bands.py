@@ -545,12 +545,16 @@ def open_peer(handle: bytes) -> int:
 def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows: int,
               pitch: int, band_rows: int, dst: int, k: int, device: torch.device,
               edge_stream: Optional["torch.cuda.Stream"] = None,
-              interior_done: Optional["torch.cuda.Event"] = None, il: int = 0) -> None:
+              interior_done: Optional["torch.cuda.Event"] = None, il: int = 0,
+              before_edges: Optional[Callable[[], None]] = None) -> None:
     """One depth-k pass of a band with in-kernel NVLink halos: the interior
     rows [k, band-k) read only the band's own rows (the branch-free kernel
     path); the two k-row edge strips read the neighbours' rows through peer
     pointers and run on `edge_stream` (if given) beside the interior.
-    `il` 2 / 4: every buffer is in the pair / quad layout (packed_il_kernel)."""
+    `il` 2 / 4: every buffer is in the pair / quad layout (packed_il_kernel).
+    `before_edges` (needs `edge_stream`, band taller than 2k): called with the
+    edge stream current, after it has joined the compute stream and before the
+    edge strips -- where the overlapped pass sync waits for the neighbours."""
     L = capi.lib()
 
     def step(*args):
@@ -573,6 +577,9 @@ def peer_pass(width: int, src: int, up: int, up_rows: int, down: int, down_rows:
     if interior_done is not None:
         interior_done.record(main)
     es = edge_stream.cuda_stream if edge_stream is not None else main.cuda_stream
+    if before_edges is not None:
+        with torch.cuda.stream(edge_stream):
+            before_edges()
     for r0 in (0, band_rows - k):
         check(step_peer(src, up, up_rows, down, down_rows, pitch, band_rows, dst, r0, k, width,
                         k, es))
@@ -605,7 +612,13 @@ class PeerBandDriver(PairLayout):
     4-byte token sent to and received from the bands above and below,
     stream-ordered on the compute stream (the reference's per-generation
     barrier, engine.cpp:79-96, narrowed to the two ranks whose rows a band
-    touches); "allreduce" -- a 1-element NCCL all-reduce over every rank;
+    touches); "neighbour_overlap" (opt-in, NCCL only) -- the same token, but
+    exchanged on the EDGE stream before a pass's edge strips instead of on the
+    compute stream after the pass: the token of pass p-1 only guards pass p's
+    edge strips (they read the neighbours' rows and overwrite the rows the
+    neighbours read), while pass p's interior reads the band's own rows and
+    writes rows no neighbour reads, so it starts without waiting and hides the
+    exchange; "allreduce" -- a 1-element NCCL all-reduce over every rank;
     "host" (forced with non-NCCL groups) -- synchronize + dist.barrier.
     With `profile` on, CUDA events around each pass's interior launch and
     barrier give per-rank interior / barrier times (stats())."""
@@ -646,12 +659,14 @@ class PeerBandDriver(PairLayout):
         self._flag = torch.zeros(1, dtype=torch.int32, device=device)
         self._tok_in = torch.zeros(2, dtype=torch.int32, device=device)
         self._nccl = dist.get_backend(group) == "nccl"
-        if sync not in ("neighbour", "allreduce", "host"):
+        if sync not in ("neighbour", "neighbour_overlap", "allreduce", "host"):
             raise ConfigError(f"unknown pass sync {sync!r}")
         self.sync = sync if self._nccl else "host"
         self.edge_stream = torch.cuda.Stream(device)
         self.profile = profile
         self._events = []  # (start, interior done, pass done, barrier done) per pass
+        self._passes_since_sync = 0  # neighbour_overlap: passes whose token is still owed
+        self._last_k = 0             # ... and the depth of the previous pass
 
     def _band_raw(self) -> torch.Tensor:
         return self.buf[self.cur].tensor
@@ -663,7 +678,7 @@ class PeerBandDriver(PairLayout):
         return self.buf[self.cur].tensor
 
     def barrier(self) -> None:
-        if self.sync == "neighbour":
+        if self.sync in ("neighbour", "neighbour_overlap"):
             neighbour_token(self._flag, self._tok_in, self.geo.rank, self.geo.world, self.group)
         elif self.sync == "allreduce":
             dist.all_reduce(self._flag, group=self.group)  # ordered on the current stream
@@ -671,14 +686,14 @@ class PeerBandDriver(PairLayout):
             torch.cuda.synchronize(self.device)
             dist.barrier(group=self.group)
 
-    def compute(self, k: int, interior_done=None) -> None:
+    def compute(self, k: int, interior_done=None, before_edges=None) -> None:
         """The pass's kernels (interior + peer edge strips), no barrier."""
         g = self.geo
         c = self.cur
         peer_pass(g.width, self.buf[c].ptr.value, self.up_ptrs[c], self.up_rows,
                   self.down_ptrs[c], self.down_rows, g.pitch, g.band_rows,
                   self.buf[c ^ 1].ptr.value, k, self.device, self.edge_stream,
-                  interior_done=interior_done, il=g.il)
+                  interior_done=interior_done, il=g.il, before_edges=before_edges)
 
     def pass_(self, k: int) -> None:
         g = self.geo
@@ -687,7 +702,23 @@ class PeerBandDriver(PairLayout):
         if g.il and not self.in_pair:
             raise ConfigError("band in the plain layout: interleaved passes start through run() "
                               "(conversion, then a barrier with the neighbours)")
-        if self.profile:
+        if self.sync == "neighbour_overlap":
+            # run() has exchanged the "initial band in place" token; from then
+            # on each pass waits for "previous pass done" on its edge stream.
+            # The interior writes rows [k, band - k) of the buffer the previous
+            # pass read; the neighbours read that buffer's outer k_prev rows, so
+            # the interior may run ahead of the token only if k >= k_prev (a
+            # shallower remainder pass after a full one waits like the rest).
+            owed = self._passes_since_sync > 0
+            if g.band_rows > 2 * k and k >= self._last_k:
+                self.compute(k, before_edges=self.barrier if owed else None)
+            else:  # thin band (one peer-mode launch) or a shallower pass: token first
+                if owed:
+                    self.barrier()
+                self.compute(k)
+            self._passes_since_sync += 1
+            self._last_k = k
+        elif self.profile:
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
             ev[0].record()
             self.compute(k, interior_done=ev[1])
@@ -723,7 +754,13 @@ class PeerBandDriver(PairLayout):
             checkpoints: Sequence[int] = ()) -> list[int]:
         self._to_pair()  # before the barrier: the neighbours read this band in that layout
         self.barrier()  # every rank's initial band is in place
-        return run_schedule(self, generations, checkpoints, on_pass)
+        self._passes_since_sync = 0
+        self._last_k = 0
+        pops = run_schedule(self, generations, checkpoints, on_pass)
+        if self.sync == "neighbour_overlap" and self._passes_since_sync:
+            self.barrier()  # the last pass's token: nobody reads this band's old rows any more
+            self._passes_since_sync = 0
+        return pops
 
     def init_random(self, density: float, seed: int) -> None:
         g = self.geo
