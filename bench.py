@@ -1417,7 +1417,7 @@ def main() -> None:
                     help="byte engine generations per pass (0 = auto, 1 = HBM-bound single step)")
     ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
                     help="multi-GPU halo: in-kernel NVLink peer reads or NCCL send/recv")
-    ap.add_argument("--pass-sync", choices=["neighbour", "neighbour_overlap", "allreduce"], default="neighbour",
+    ap.add_argument("--pass-sync", choices=["neighbour", "neighbour_overlap", "flag", "flag_overlap", "allreduce"], default="neighbour",
                     help="peer halo: order passes by a token with the two neighbour ranks "
                          "(default) or by an all-rank NCCL all-reduce")
     ap.add_argument("--single-process", action="store_true",

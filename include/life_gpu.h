@@ -316,6 +316,15 @@ int life_dev_free(void* dev_ptr);
 int life_ipc_get_handle(void* dev_ptr, void* handle_out);
 int life_ipc_open(const void* handle, void** out);
 int life_ipc_close(void* dev_ptr);
+/* Pass ordering between neighbouring bands without a kernel: a 32-bit flag in
+ * a life_dev_alloc'd buffer (the band's own, or a neighbour's opened with
+ * life_ipc_open) written / awaited by stream memory operations
+ * (cuStreamWriteValue32 / cuStreamWaitValue32, >= comparison), ordered on
+ * `stream` like a kernel but using no SM.  The cross-device form of the
+ * reference's per-generation barrier (WorkerTeam, engine.cpp:79-96), narrowed
+ * to the two bands a band touches.  LIFE_ERR_CUDA if the driver lacks them. */
+int life_dev_flag_write(void* flag, uint32_t value, void* stream);
+int life_dev_flag_wait_geq(void* flag, uint32_t value, void* stream);
 /* One byte-engine generation with the same row addressing (pitches in bytes). */
 int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
                        uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,

@@ -618,7 +618,12 @@ class PeerBandDriver(PairLayout):
     edge strips (they read the neighbours' rows and overwrite the rows the
     neighbours read), while pass p's interior reads the band's own rows and
     writes rows no neighbour reads, so it starts without waiting and hides the
-    exchange; "allreduce" -- a 1-element NCCL all-reduce over every rank;
+    exchange; "flag" / "flag_overlap" (opt-in) -- the same two orders with no
+    kernel at all: each rank owns two 32-bit flags in a CUDA-IPC buffer, the
+    neighbours bump them with stream memory operations
+    (life_dev_flag_write) and the rank waits for both on its stream
+    (life_dev_flag_wait_geq): no SM slot, no NCCL launch;
+    "allreduce" -- a 1-element NCCL all-reduce over every rank;
     "host" (forced with non-NCCL groups) -- synchronize + dist.barrier.
     With `profile` on, CUDA events around each pass's interior launch and
     barrier give per-rank interior / barrier times (stats())."""
@@ -631,10 +636,15 @@ class PeerBandDriver(PairLayout):
         self.device = device
         self.group = group
         self.buf = [DeviceBuffer(geo.band_rows, geo.pitch, device) for _ in range(2)]
+        # Pass-ordering flags (sync "flag"): word 0 is bumped by the band above,
+        # word 1 by the band below (zeroed by life_dev_alloc).
+        self.flags = DeviceBuffer(1, 32, device)
+        self._epoch = 0
+        torch.cuda.synchronize(device)
         self.cur = 0
         self.generations = 0
         # Exchange IPC handles and band heights with every rank.
-        mine = (geo.band_rows, [b.handle() for b in self.buf])
+        mine = (geo.band_rows, [b.handle() for b in self.buf] + [self.flags.handle()])
         allinfo = [None] * geo.world
         dist.all_gather_object(allinfo, mine, group=group)
         up, down = (geo.rank - 1) % geo.world, (geo.rank + 1) % geo.world
@@ -645,7 +655,7 @@ class PeerBandDriver(PairLayout):
             ptrs = []
             for i, h in enumerate(handles):
                 if r == geo.rank:
-                    ptrs.append(self.buf[i].ptr.value)
+                    ptrs.append((self.buf + [self.flags])[i].ptr.value)
                 else:
                     p = open_peer(h)
                     self._opened.append(p)
@@ -659,9 +669,11 @@ class PeerBandDriver(PairLayout):
         self._flag = torch.zeros(1, dtype=torch.int32, device=device)
         self._tok_in = torch.zeros(2, dtype=torch.int32, device=device)
         self._nccl = dist.get_backend(group) == "nccl"
-        if sync not in ("neighbour", "neighbour_overlap", "allreduce", "host"):
+        if sync not in ("neighbour", "neighbour_overlap", "flag", "flag_overlap", "allreduce",
+                        "host"):
             raise ConfigError(f"unknown pass sync {sync!r}")
-        self.sync = sync if self._nccl else "host"
+        # flags need no collective backend; the NCCL orders fall back to host barriers
+        self.sync = sync if (self._nccl or sync.startswith("flag")) else "host"
         self.edge_stream = torch.cuda.Stream(device)
         self.profile = profile
         self._events = []  # (start, interior done, pass done, barrier done) per pass
@@ -678,7 +690,17 @@ class PeerBandDriver(PairLayout):
         return self.buf[self.cur].tensor
 
     def barrier(self) -> None:
-        if self.sync in ("neighbour", "neighbour_overlap"):
+        if self.sync in ("flag", "flag_overlap"):
+            # "I am past this point" into the neighbours' flags, then wait for
+            # theirs: up's word 1 (I am its band below), down's word 0.
+            L = capi.lib()
+            s = torch.cuda.current_stream(self.device).cuda_stream
+            self._epoch += 1
+            check(L.life_dev_flag_write(self.up_ptrs[2] + 4, self._epoch, s))
+            check(L.life_dev_flag_write(self.down_ptrs[2], self._epoch, s))
+            check(L.life_dev_flag_wait_geq(self.flags.ptr.value, self._epoch, s))
+            check(L.life_dev_flag_wait_geq(self.flags.ptr.value + 4, self._epoch, s))
+        elif self.sync in ("neighbour", "neighbour_overlap"):
             neighbour_token(self._flag, self._tok_in, self.geo.rank, self.geo.world, self.group)
         elif self.sync == "allreduce":
             dist.all_reduce(self._flag, group=self.group)  # ordered on the current stream
@@ -702,7 +724,7 @@ class PeerBandDriver(PairLayout):
         if g.il and not self.in_pair:
             raise ConfigError("band in the plain layout: interleaved passes start through run() "
                               "(conversion, then a barrier with the neighbours)")
-        if self.sync == "neighbour_overlap":
+        if self.sync in ("neighbour_overlap", "flag_overlap"):
             # run() has exchanged the "initial band in place" token; from then
             # on each pass waits for "previous pass done" on its edge stream.
             # The interior writes rows [k, band - k) of the buffer the previous
@@ -757,7 +779,7 @@ class PeerBandDriver(PairLayout):
         self._passes_since_sync = 0
         self._last_k = 0
         pops = run_schedule(self, generations, checkpoints, on_pass)
-        if self.sync == "neighbour_overlap" and self._passes_since_sync:
+        if self.sync in ("neighbour_overlap", "flag_overlap") and self._passes_since_sync:
             self.barrier()  # the last pass's token: nobody reads this band's old rows any more
             self._passes_since_sync = 0
         return pops
@@ -791,7 +813,7 @@ class PeerBandDriver(PairLayout):
         for p in self._opened:
             capi.lib().life_ipc_close(p)
         self._opened = []
-        for b in self.buf:
+        for b in self.buf + [self.flags]:
             b.free()
 
 

@@ -112,6 +112,8 @@ SIGNATURES = [
     ("life_ipc_get_handle", C.c_int, [_vp, _vp]),
     ("life_ipc_open", C.c_int, [_vp, C.POINTER(_vp)]),
     ("life_ipc_close", C.c_int, [_vp]),
+    ("life_dev_flag_write", C.c_int, [_vp, C.c_uint32, _vp]),
+    ("life_dev_flag_wait_geq", C.c_int, [_vp, C.c_uint32, _vp]),
     ("life_dev_byte_step", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _vp]),
     ("life_dev_byte_pass", C.c_int, [_vp, _i64, _i64, _i64, _vp, _i64, _i64, _i64, _i64, _i32,
                                      _vp]),

@@ -816,6 +816,52 @@ int life_ipc_close(void* dev_ptr) {
   return LIFE_OK;
 }
 
+// Stream memory operations through the driver entry points (the library links
+// cudart statically and not libcuda): cuStreamWriteValue32(stream, addr, value,
+// flags) and cuStreamWaitValue32(stream, addr, value, CU_STREAM_WAIT_VALUE_GEQ).
+namespace {
+using StreamMemOp = int (*)(cudaStream_t, unsigned long long, uint32_t, unsigned int);
+struct StreamMemOps {
+  StreamMemOp write = nullptr, wait = nullptr;
+  StreamMemOps() {
+    void* w = nullptr;
+    void* q = nullptr;
+    cudaDriverEntryPointQueryResult rw, rq;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &w, cudaEnableDefault, &rw) == cudaSuccess &&
+        rw == cudaDriverEntryPointSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWaitValue32", &q, cudaEnableDefault, &rq) == cudaSuccess &&
+        rq == cudaDriverEntryPointSuccess) {
+      write = reinterpret_cast<StreamMemOp>(w);
+      wait = reinterpret_cast<StreamMemOp>(q);
+    }
+  }
+};
+int stream_mem_op(bool wait, void* flag, uint32_t value, void* stream) {
+  static const StreamMemOps ops;  // thread-safe initialisation
+  if (!flag || (reinterpret_cast<uintptr_t>(flag) & 3))
+    return set_error(LIFE_ERR_CONFIG, "flag must be a 4-byte aligned device pointer");
+  if (!ops.write || !ops.wait)
+    return set_error(LIFE_ERR_CUDA, "the driver exports no stream memory operations");
+  constexpr unsigned int kGeq = 0x0;  // CU_STREAM_WAIT_VALUE_GEQ: (int32_t)(*addr - value) >= 0
+  const int rc = wait ? ops.wait(static_cast<cudaStream_t>(stream),
+                                 reinterpret_cast<unsigned long long>(flag), value, kGeq)
+                      : ops.write(static_cast<cudaStream_t>(stream),
+                                  reinterpret_cast<unsigned long long>(flag), value, 0u);
+  if (rc != 0)
+    return set_error(LIFE_ERR_CUDA, "%s failed (CUresult %d)",
+                     wait ? "cuStreamWaitValue32" : "cuStreamWriteValue32", rc);
+  return LIFE_OK;
+}
+}  // namespace
+
+int life_dev_flag_write(void* flag, uint32_t value, void* stream) {
+  return stream_mem_op(false, flag, value, stream);
+}
+
+int life_dev_flag_wait_geq(void* flag, uint32_t value, void* stream) {
+  return stream_mem_op(true, flag, value, stream);
+}
+
 int life_dev_byte_step(const uint8_t* in, int64_t in_pitch, int64_t in_row0, int64_t in_rows,
                        uint8_t* out, int64_t out_pitch, int64_t out_row0, int64_t width,
                        int64_t out_rows, void* stream) {

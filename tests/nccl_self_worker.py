@@ -61,7 +61,10 @@ def main() -> None:
                                                (1024, 300, 10, 2, 33, [0, 33], "neighbour"),
                                                (333, 257, 7, 0, 40, [0, 13, 40], "neighbour_overlap"),
                                                (1024, 300, 7, 4, 30, [0, 9, 30], "neighbour_overlap"),
-                                               (1024, 21, 10, 2, 33, [0, 33], "neighbour_overlap")]:
+                                               (1024, 21, 10, 2, 33, [0, 33], "neighbour_overlap"),
+                                               (333, 257, 7, 0, 40, [0, 13, 40], "flag"),
+                                               (1024, 300, 7, 4, 30, [0, 9, 30], "flag_overlap"),
+                                               (1024, 21, 10, 2, 33, [0, 33], "flag_overlap")]:
         geo = make_geometry(W, H, 0, 1, depth, il, self_exchange=True)
         drv = PeerBandDriver(geo, dev, sync=sync, profile=True)
         drv.init_random(0.4, 9)

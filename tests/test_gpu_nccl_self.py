@@ -37,9 +37,9 @@ def test_nccl_halo_and_token_single_rank():
     for c in out["cases"]:
         assert c["grid"] and c["pops"], c
         assert c["exchange_bytes"] > 0, c   # the halos really went through send / recv
-    assert len(out["peer_cases"]) == 7
+    assert len(out["peer_cases"]) == 10
     for c in out["peer_cases"]:
         assert c["grid"] and c["pops"], c
-        assert c["passes"] > 0 or c["case"][5] == "neighbour_overlap", c  # (its passes carry no events)
+        assert c["passes"] > 0 or c["case"][5].endswith("_overlap"), c  # (those passes carry no events)
         assert c["sync"] == c["case"][5], c   # NCCL group: the stream-ordered sync, not the host barrier
     assert out["tokens"] == [[1, 1], [2, 2], [3, 3]]

@@ -60,6 +60,8 @@ geo = make_geometry(W, H, 0, 1, depth, il, self_exchange=True)
 for name, make in [("peer_neighbour_token", lambda: PeerBandDriver(geo, dev, sync="neighbour")),
                    ("peer_neighbour_token_overlapped",
                     lambda: PeerBandDriver(geo, dev, sync="neighbour_overlap")),
+                   ("peer_flag", lambda: PeerBandDriver(geo, dev, sync="flag")),
+                   ("peer_flag_overlapped", lambda: PeerBandDriver(geo, dev, sync="flag_overlap")),
                    ("peer_allreduce", lambda: PeerBandDriver(geo, dev, sync="allreduce")),
                    ("nccl_sendrecv_halo", lambda: BandDriver(geo, dev))]:
     drv = make()
