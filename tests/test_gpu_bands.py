@@ -79,7 +79,7 @@ def test_local_peer_bands_match_oracle(oracle, W, H, P, depth, gens):
     assert np.array_equal(got, want)
 
 
-def _ipc_worker(rank, world, port, W, H, depth, gens, q, il=0):
+def _ipc_worker(rank, world, port, W, H, depth, gens, q, il=0, sync="neighbour"):
     import os
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -92,9 +92,10 @@ def _ipc_worker(rank, world, port, W, H, depth, gens, q, il=0):
         from paper_1209_4408_b200.bands import PeerBandDriver, make_geometry
         dev = torch.device("cuda", 0)
         torch.cuda.set_device(dev)
-        drv = PeerBandDriver(make_geometry(W, H, rank, world, depth, il), dev)
+        drv = PeerBandDriver(make_geometry(W, H, rank, world, depth, il), dev, sync=sync)
         drv.init_random(0.4, 5)
-        # gloo => host barrier per pass: no kernel waits on another
+        # gloo => host barrier per pass (sync "neighbour"), or stream-memory-operation
+        # flags in the other process's IPC buffer: either way no kernel waits on another
         cps = drv.run(gens, checkpoints=[0, 5, 11, gens])  # passes split at 5 and 11
         band = drv.band().cpu().numpy()
         pop = drv.population()
@@ -107,12 +108,18 @@ def _ipc_worker(rank, world, port, W, H, depth, gens, q, il=0):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("W,depth,il", [(500, 8, 0), (576, 8, 2), (512, 6, 4)],
-                         ids=["plain", "pair", "quad"])
-def test_peer_driver_ipc_two_processes_one_gpu(oracle, W, depth, il):
+@pytest.mark.parametrize("W,depth,il,sync", [(500, 8, 0, "neighbour"), (576, 8, 2, "neighbour"),
+                                             (512, 6, 4, "neighbour"), (500, 8, 0, "flag"),
+                                             (512, 6, 4, "flag_overlap")],
+                         ids=["plain", "pair", "quad", "plain-flag", "quad-flag-overlap"])
+def test_peer_driver_ipc_two_processes_one_gpu(oracle, W, depth, il, sync):
     """PeerBandDriver across two processes sharing cuda:0 through CUDA IPC
     handles (host barrier between passes, so no kernel waits on another); also
-    on the pair and quad layouts (bands converted before the first barrier)."""
+    on the pair and quad layouts (bands converted before the first barrier),
+    and with the passes ordered by flags each process bumps in the OTHER
+    process's IPC-mapped buffer with stream memory operations (a waiting
+    stream holds no SM, so two processes time-sliced on one GPU cannot
+    starve each other)."""
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -122,14 +129,20 @@ def test_peer_driver_ipc_two_processes_one_gpu(oracle, W, depth, il):
     H, gens = 90, 27
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, W, H, depth, gens, q, il))
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, W, H, depth, gens, q, il, sync),
+                         daemon=True)
              for r in range(2)]
     for p in procs:
         p.start()
-    parts = q.get(timeout=300)
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    try:
+        parts = q.get(timeout=120)
+        for p in procs:
+            p.join(timeout=60)
+            assert p.exitcode == 0
+    finally:
+        for p in procs:
+            if p.is_alive():
+                p.kill()
     parts.sort(key=lambda t: t[0])
     got = words_to_cells(np.concatenate([b for _, b, _, _ in parts], axis=0), W)
     want, pops = oracle.run(oracle.random_fill(W, H, 0.4, 5), gens, [0, 5, 11, gens])
