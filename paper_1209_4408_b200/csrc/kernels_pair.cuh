@@ -332,8 +332,8 @@ __device__ __forceinline__ void pair_segment(const PackedStepArgs& a, const int 
   int t = 0;
   // Fill as phases of 3 * G steps with groups 0..p-1 active (kernels.cuh,
   // LIFE_FILL_PHASES); a fill cut short by kLag ends in the branchy body.
-  constexpr bool kPhased =
-      (LIFE_FILL_PHASES == 2 || (LIFE_FILL_PHASES == 1 && UNI)) && (3 * G) % PF == 0 && kTopG0 > 0;
+  constexpr bool kPhased = (LIFE_FILL_PHASES_IL == 2 || (LIFE_FILL_PHASES_IL == 1 && UNI)) &&
+                           (3 * G) % PF == 0 && kTopG0 > 0;
   if constexpr (kPhased) {
     constexpr int kTripsPerPhase = 3 * G / PF;
     constexpr int kPhases = (kFillTrips / kTripsPerPhase) < (kTopG0 / G) ? (kFillTrips / kTripsPerPhase)

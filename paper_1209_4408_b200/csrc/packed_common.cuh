@@ -17,6 +17,12 @@
 #ifndef LIFE_FILL_PHASES
 #define LIFE_FILL_PHASES 1
 #endif
+// The interleaved kernels take the phased fill in every variant: their long
+// tiles gain too (config 5 53.95 -> 54.26 T/s, 131072^2 52.0 -> 52.3, one of
+// config 5's 8 bands 51.15 -> 51.46; tools/r5_il2.sh, three runs each).
+#ifndef LIFE_FILL_PHASES_IL
+#define LIFE_FILL_PHASES_IL 2
+#endif
 // Drain of short tiles as specialised last trips (kernels_pair.cuh): 0 = off.
 #ifndef LIFE_DRAIN_PHASES
 #define LIFE_DRAIN_PHASES 0
