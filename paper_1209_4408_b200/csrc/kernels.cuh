@@ -1276,8 +1276,11 @@ __device__ __forceinline__ void byte_tb2_body(const ByteStepArgs& a, const int l
 
   const int trips = (nA + kLag + PF - 1) / PF;
   int half = 0;
-  auto trip = [&](const int t, auto steady_tag) {
+  // ACTIVE < K: a fill trip that runs stages 0..ACTIVE-1 only and stores
+  // nothing (stage g sees valid input from step 3g on; LIFE_BYTE_FILL_PHASES).
+  auto trip = [&](const int t, auto steady_tag, auto active_tag) {
     constexpr bool STEADY = decltype(steady_tag)::value;
+    constexpr int ACTIVE = decltype(active_tag)::value;
 #pragma unroll
     for (int u = 0; u < PF; ++u) {
       issue((half ^ PF) + u);
@@ -1294,6 +1297,7 @@ __device__ __forceinline__ void byte_tb2_body(const ByteStepArgs& a, const int l
       uint32_t y_last[4];
 #pragma unroll
       for (int g = K - 1; g >= 0; --g) {
+        if (g >= ACTIVE) continue;  // compile time
         const uint32_t lw = __shfl_up_sync(kFull, xin[g][3], 1);
         const uint32_t rw = __shfl_down_sync(kFull, xin[g][0], 1);
         uint32_t h[4], hn[4];
@@ -1312,6 +1316,7 @@ __device__ __forceinline__ void byte_tb2_body(const ByteStepArgs& a, const int l
           }
         }
       }
+      if constexpr (ACTIVE < K) continue;  // fill phase: no output row yet
       const int j = t * PF + u - kLag;
       uint32_t ya[4], yb[4];
 #pragma unroll
@@ -1338,10 +1343,23 @@ __device__ __forceinline__ void byte_tb2_body(const ByteStepArgs& a, const int l
   };
   const int steady_begin = (kLag + PF - 1) / PF;
   const int steady_end = (nA + kLag) / PF;
+  using AllStages = std::integral_constant<int, K>;
   int t = 0;
-  for (; t < trips && (t < steady_begin || t >= steady_end); ++t) trip(t, std::false_type{});
-  for (; t < steady_end; ++t) trip(t, std::true_type{});
-  for (; t < trips; ++t) trip(t, std::false_type{});
+#if LIFE_BYTE_FILL_PHASES
+  // Two coarse fill phases of 8 steps (PF = 4): steps 0..7 need stages 0..2,
+  // steps 8..15 stages 0..5; both end before the first output (step 3K - 1).
+  static_assert(PF == 4, "fill phases assume 4 rows per trip");
+  if constexpr (K > 3) {
+    for (int r = 0; r < 2; ++r, ++t) trip(t, std::false_type{}, std::integral_constant<int, 3>{});
+  }
+  if constexpr (K > 6) {
+    for (int r = 0; r < 2; ++r, ++t) trip(t, std::false_type{}, std::integral_constant<int, 6>{});
+  }
+#endif
+  for (; t < trips && (t < steady_begin || t >= steady_end); ++t)
+    trip(t, std::false_type{}, AllStages{});
+  for (; t < steady_end; ++t) trip(t, std::true_type{}, AllStages{});
+  for (; t < trips; ++t) trip(t, std::false_type{}, AllStages{});
   cp_async_wait<0>();
 }
 

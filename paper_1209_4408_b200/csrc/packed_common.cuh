@@ -23,6 +23,10 @@
 #ifndef LIFE_FILL_PHASES_IL
 #define LIFE_FILL_PHASES_IL 2
 #endif
+// Byte engine (byte_tb2_kernel): two coarse compile-time fill phases; 0 = off.
+#ifndef LIFE_BYTE_FILL_PHASES
+#define LIFE_BYTE_FILL_PHASES 0
+#endif
 // Drain of short tiles as specialised last trips (kernels_pair.cuh): 0 = off.
 #ifndef LIFE_DRAIN_PHASES
 #define LIFE_DRAIN_PHASES 0
