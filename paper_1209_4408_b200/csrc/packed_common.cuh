@@ -12,8 +12,9 @@
 // Pipeline fill of the temporal-blocked kernels as compile-time phases (one
 // straight-line trip body per number of active stage groups) instead of one
 // fill body with a warp-uniform branch per group: 0 = off, 1 = the short-tile
-// (UNI) variants, 2 = every variant.  Timeline of a config-2 tile
-// (tools/r5_timeline.py): fill 12.6 -> 6.7 us of a 114 us tile.
+// (UNI) variant of the fast kernel and the all-paths kernel, 2 = the long-tile
+// fast kernel too.  Timeline of a config-2 tile (tools/r5_timeline.py): fill
+// 12.6 -> 6.7 us of a 114 us tile.
 #ifndef LIFE_FILL_PHASES
 #define LIFE_FILL_PHASES 1
 #endif
@@ -31,8 +32,8 @@
 #ifndef LIFE_DRAIN_PHASES
 #define LIFE_DRAIN_PHASES 0
 #endif
-// Tiles up to this many rows are "short": the single-loop-body (UNI) kernel
-// variants and the phased fill of the all-paths kernel.
+// Tiles up to this many rows are "short": they run the single-loop-body (UNI)
+// kernel variants.
 constexpr long long kShortTileRows = 1024;
 
 namespace lifegpu {
